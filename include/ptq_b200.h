@@ -1,0 +1,144 @@
+/*
+ * ptq_b200.h -- C ABI of the B200 PTQ-configuration evaluator.
+ *
+ * Drop-in boundary for the reference's evaluator plug point
+ *   Evaluator = Callable[[QuantConfig], float]            (ptqtune/tuner.py:44)
+ *   make_accuracy_evaluator(g, d, seed, profile)          (ptqtune/tuner.py:434-444)
+ * ("ptqtune/" = /root/reference/pkg/src/ptqtune/).  The reference is pure
+ * Python, so the binding a maintainer adds is a ctypes stub;
+ * paper_2202_05048_b200/_lib.py is exactly that stub.
+ *
+ * Conventions: plain C types only, host pointers in and out, caller owns all
+ * host buffers; every entry point returns 0 on success or a negative
+ * PTQ_E* status and never throws across the boundary; ptq_last_error()
+ * describes the most recent failure of the calling thread.  One context is
+ * bound to one CUDA device and is not safe for concurrent calls (the Python
+ * wrapper serialises calls with a lock, tuner.py:192-203 may call from
+ * threads).
+ */
+#ifndef PTQ_B200_H
+#define PTQ_B200_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define PTQ_OK 0
+#define PTQ_EINVAL (-1)   /* bad argument / unsupported graph (GraphError, ValueError) */
+#define PTQ_ECUDA (-2)    /* CUDA runtime or kernel failure */
+#define PTQ_ESTATE (-3)   /* call out of order (e.g. eval before ranges are set) */
+#define PTQ_ENOMEM (-4)   /* device allocation failed */
+
+#define PTQ_NBINS 2048
+#define PTQ_NWINDOWS 1921 /* KL candidate windows i = 128..2048 (clipping.py:78) */
+
+/* node kinds: the reference IR vocabulary (ptqtune/ir.py:31-33) */
+enum ptq_node_kind {
+  PTQ_CONV = 0, PTQ_DWCONV = 1, PTQ_PWCONV = 2, PTQ_FC = 3, PTQ_RELU = 4,
+  PTQ_MAXPOOL = 5, PTQ_AVGPOOL = 6, PTQ_ADD = 7, PTQ_CONCAT = 8, PTQ_SOFTMAX = 9
+};
+
+#define PTQ_MAX_INPUTS 8
+
+/* One IR node (ptqtune/ir.py:40-64).  Tensor ids: 0 = graph input, i+1 = output
+ * of node i (so tensor ids equal the calibration-cache order, calibration.py:81). */
+typedef struct {
+  int32_t kind;
+  int32_t n_inputs;                 /* data inputs */
+  int32_t inputs[PTQ_MAX_INPUTS];   /* tensor ids */
+  int32_t weight;                   /* index into weights[] or -1 */
+  int32_t bias;                     /* index into weights[] or -1 */
+  int32_t kernel, stride, pad;      /* conv/pool attributes (ir.py:119-150) */
+} ptq_node_desc;
+
+typedef struct {
+  const float* data;                /* host fp32, reference layout (OIHW / (O, F) / (O,)) */
+  int64_t shape[4];
+  int32_t ndim;
+} ptq_weight_desc;
+
+typedef struct {
+  int32_t n_nodes;
+  const ptq_node_desc* nodes;
+  int32_t n_weights;
+  const ptq_weight_desc* weights;
+  int32_t in_c, in_h, in_w;         /* Graph.input_shape */
+  int32_t n_classes;                /* Graph.output_classes */
+} ptq_graph_desc;
+
+/* QuantConfig (ptqtune/quantize.py:54-84) as small integers, in the reference's
+ * enumeration order: cache {S1,S2,S3}, scheme {Asymmetric, Symmetric,
+ * SymmetricUint8, SymmetricPower2}, clipping {Max, KL}, granularity {Tensor,
+ * Channel}, mixed {Off, FirstLastFp32}, fusion {0,1} (numerically neutral). */
+typedef struct {
+  int32_t cache, scheme, clipping, granularity, mixed, fusion;
+} ptq_config;
+
+typedef struct ptq_ctx ptq_ctx;
+
+const char* ptq_last_error(void);
+int ptq_version(void);
+
+/* Upload graph, images (N, C, H, W fp32, calibration pool first) and the eval
+ * labels (n_images - n_calib int64) to device `device`.  Replaces the state the
+ * reference builds inside make_accuracy_evaluator (tuner.py:434-438). */
+int ptq_create(ptq_ctx** out, int device, const ptq_graph_desc* g, const float* images,
+               const int64_t* eval_labels, int64_t n_images, int64_t n_calib);
+int ptq_destroy(ptq_ctx* ctx);
+
+/* Number of histogram tensors T (graph input + one per node). */
+int ptq_num_tensors(const ptq_ctx* ctx, int32_t* T);
+
+/* Calibrate the three caches (calibration.py:57-112 with select_images ids
+ * supplied by the host, tuner.py:438): one fp32 forward over the union of the
+ * image ids, exact per-tensor min/max, 2048-bin histograms.  ids: concatenated
+ * calibration-pool indices of cache 0..n_caches-1, sizes in cache_sizes.
+ * Outputs (may be NULL): ranges [n_caches][T][2] fp32 (min_seen, max_seen),
+ * counts [n_caches][T][2048] int64, n_samples [n_caches][T]. */
+int ptq_calibrate(ptq_ctx* ctx, int32_t n_caches, const int32_t* cache_sizes, const int64_t* ids,
+                  float* ranges, int64_t* counts, int64_t* n_samples);
+
+/* KL sweep (clipping.py:55-86): kl[h][w] for window width 128+w of histogram h;
+ * +inf for infeasible windows and for histograms the reference does not sweep
+ * (min == max or empty).  counts [n_hist][2048], ranges [n_hist][2] as above. */
+int ptq_kl_sweep(ptq_ctx* ctx, int32_t n_hist, const int64_t* counts, const float* ranges,
+                 double* kl);
+
+/* Install the clipped ranges (clipped_range, clipping.py:89-96) for
+ * (cache, clipping): ranges [T][2] fp64 (lo, hi). */
+int ptq_set_clip_ranges(ptq_ctx* ctx, int32_t cache, int32_t clipping, const double* ranges);
+
+/* Device-side preparation that every config shares: activation params for all
+ * 24 (cache, scheme, clipping) variants, the 8 (scheme, granularity) weight
+ * variants and, for FirstLastFp32, the config-invariant fp32 first layer of the
+ * eval set.  Called implicitly by ptq_eval_configs when needed. */
+int ptq_prepare(ptq_ctx* ctx);
+
+/* Evaluate configs (quantize_model + evaluate_quantized, quantize.py:133-211,
+ * intexec.py:337-366): correct[i] = number of eval images whose top-1 matches. */
+int ptq_eval_configs(ptq_ctx* ctx, const ptq_config* cfgs, int32_t n_cfg, int64_t* correct);
+
+/* Parity probes (tests): int8 codes of tensor `tensor` for one config over the
+ * eval set in NCHW order [n_eval][C][H][W] (fp32-domain tensors return
+ * PTQ_EINVAL).  Returns the element count through *n_out when out == NULL. */
+int ptq_probe_codes(ptq_ctx* ctx, const ptq_config* cfg, int32_t tensor, int8_t* out,
+                    int64_t* n_out);
+/* Activation params the device derived for one variant: scale/zp [T]. */
+int ptq_probe_act_params(ptq_ctx* ctx, int32_t cache, int32_t scheme, int32_t clipping,
+                         float* scale, int32_t* zp);
+/* Histogram a host array exactly like np.histogram(x.astype(f64), 2048, (lo, hi)). */
+int ptq_histogram_host(ptq_ctx* ctx, const float* x, int64_t n, float lo, float hi,
+                       int64_t* counts);
+/* Runtime options: "conv_ref" (1 = CUDA-core reference conv instead of tcgen05,
+ * tests only), "fusion" (0 = materialise every tensor so each can be probed),
+ * "eval_chunk" (images per eval pass; default = whole eval set). */
+int ptq_set_option(ptq_ctx* ctx, const char* key, int64_t value);
+/* Launch-count / timing statistics of the last ptq_eval_configs call. */
+int ptq_last_stats(const ptq_ctx* ctx, int64_t* kernel_launches, double* conv_ms_event);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* PTQ_B200_H */

@@ -1,0 +1,336 @@
+// F1: calibration reductions.  F2: KL-divergence threshold sweep.
+//
+// F1 restates the reference's two-pass calibration
+// (/root/reference/pkg/src/ptqtune/calibration.py:57-106): exact fp32
+// min/max per tensor, then np.histogram(x.astype(f64), 2048, range=(lo, hi))
+// with numpy's uniform-bin index rule (numpy lib/_histograms_impl.py: fp64
+// (x-lo)/(hi-lo)*2048, truncate, one-step decrement/increment fixup against
+// the np.linspace edges).  lo == hi puts every value in bin 0 (:86-87).
+//
+// F2 restates clip_range_kl / _window_kl (clipping.py:38-86): 1921 candidate
+// windows per histogram, one CTA per (histogram, window).  The KL sum is
+// accumulated over the compacted P>0 sequence in numpy's pairwise-summation
+// order (8 strided accumulators per <=128-element leaf, halving splits rounded
+// to multiples of 8), so it is bit-identical to numpy whenever the log values
+// agree; the host re-ranks near-ties with numpy (evaluator.py).
+#include "common.cuh"
+#include "kernels.h"
+
+namespace ptq {
+
+// ---------------------------------------------------------------- F1a: per-image min/max
+// x: [n_img][elems] fp32.  out_ord: [n_img][2] ordered-uint (min, max), pre-initialised.
+__global__ void k_minmax_per_image(const float* __restrict__ x, int64_t elems,
+                                   unsigned int* __restrict__ out_ord) {
+  const int img = blockIdx.y;
+  const float* p = x + (int64_t)img * elems;
+  float lo = INFINITY, hi = -INFINITY;
+  // 16-byte vector body when the per-image slice is 16B aligned
+  const bool vec = ((((uintptr_t)p) & 15) == 0);
+  int64_t n4 = vec ? (elems >> 2) : 0;
+  const float4* p4 = reinterpret_cast<const float4*>(p);
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n4;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    float4 v = __ldg(p4 + i);
+    lo = fminf(lo, fminf(fminf(v.x, v.y), fminf(v.z, v.w)));
+    hi = fmaxf(hi, fmaxf(fmaxf(v.x, v.y), fmaxf(v.z, v.w)));
+  }
+  for (int64_t i = (n4 << 2) + blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < elems;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    float v = __ldg(p + i);
+    lo = fminf(lo, v);
+    hi = fmaxf(hi, v);
+  }
+  // warp shuffle reduction, then one atomic per warp
+  for (int o = 16; o > 0; o >>= 1) {
+    lo = fminf(lo, __shfl_xor_sync(0xffffffffu, lo, o));
+    hi = fmaxf(hi, __shfl_xor_sync(0xffffffffu, hi, o));
+  }
+  __shared__ float slo[32], shi[32];
+  int w = threadIdx.x >> 5, l = threadIdx.x & 31;
+  if (l == 0) { slo[w] = lo; shi[w] = hi; }
+  __syncthreads();
+  if (w == 0) {
+    int nw = blockDim.x >> 5;
+    lo = l < nw ? slo[l] : INFINITY;
+    hi = l < nw ? shi[l] : -INFINITY;
+    for (int o = 16; o > 0; o >>= 1) {
+      lo = fminf(lo, __shfl_xor_sync(0xffffffffu, lo, o));
+      hi = fmaxf(hi, __shfl_xor_sync(0xffffffffu, hi, o));
+    }
+    if (l == 0 && elems > 0) {
+      atomicMin(out_ord + 2 * img, f2ord(lo));
+      atomicMax(out_ord + 2 * img + 1, f2ord(hi));
+    }
+  }
+}
+
+__global__ void k_fill_u32(unsigned int* p, int64_t n, unsigned int a, unsigned int b) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+    p[i] = (i & 1) ? b : a;
+}
+
+// per-cache reduction of per-image (min,max): slots[j] are image slots of the cache
+__global__ void k_minmax_reduce_cache(const unsigned int* __restrict__ per_img, int n_tensors,
+                                      int n_img_total, const int* __restrict__ slots, int n_slots,
+                                      float* __restrict__ ranges /*[T][2]*/) {
+  int t = blockIdx.x * blockDim.x + threadIdx.x;
+  if (t >= n_tensors) return;
+  unsigned int lo = 0xffffffffu, hi = 0u;
+  for (int j = 0; j < n_slots; ++j) {
+    const unsigned int* q = per_img + ((int64_t)t * n_img_total + slots[j]) * 2;
+    lo = min(lo, q[0]);
+    hi = max(hi, q[1]);
+  }
+  ranges[2 * t] = ord2f(lo);
+  ranges[2 * t + 1] = ord2f(hi);
+}
+
+// ---------------------------------------------------------------- F1b: histogram
+// numpy uniform-bin index for x in [lo, hi] (lo < hi), exact.
+__device__ __forceinline__ int np_bin(double x, double lo, double hi, double denom) {
+  double f = __dmul_rn(__ddiv_rn(__dsub_rn(x, lo), denom), (double)PTQ_NBINS);
+  int idx = (int)f;
+  if (idx >= PTQ_NBINS) idx = PTQ_NBINS - 1;
+  if (x < hist_edge(lo, hi, idx)) idx -= 1;
+  if (idx != PTQ_NBINS - 1 && x >= hist_edge(lo, hi, idx + 1)) idx += 1;
+  return idx;
+}
+
+// x: [n_img_total][elems]; slots: image slots of this cache; range: lo, hi (fp32 values).
+// counts: [2048] int64 (accumulated).
+__global__ void __launch_bounds__(512) k_histogram(const float* __restrict__ x, int64_t elems,
+                                                   const int* __restrict__ slots, int n_slots,
+                                                   const float* __restrict__ range,
+                                                   unsigned long long* __restrict__ counts) {
+  __shared__ unsigned int sh[PTQ_NBINS];
+  for (int i = threadIdx.x; i < PTQ_NBINS; i += blockDim.x) sh[i] = 0;
+  __syncthreads();
+  const double lo = (double)range[0], hi = (double)range[1];
+  const double denom = __dsub_rn(hi, lo);
+  const bool degenerate = !(lo < hi);
+  const int64_t total = elems * n_slots;
+  const int lane = threadIdx.x & 31;
+  for (int64_t base = blockIdx.x * (int64_t)blockDim.x; base < total;
+       base += (int64_t)gridDim.x * blockDim.x) {
+    int64_t i = base + threadIdx.x;
+    bool valid = i < total;
+    int bin = 0;
+    if (valid && !degenerate) {
+      int j = (int)(i / elems);
+      int64_t off = i - (int64_t)j * elems;
+      float v = __ldg(x + (int64_t)slots[j] * elems + off);
+      bin = np_bin((double)v, lo, hi, denom);
+    }
+    // warp-aggregated increments: post-ReLU tensors pile up in bin 0
+    unsigned int act = __ballot_sync(0xffffffffu, valid);
+    if (valid) {
+      unsigned int peers = __match_any_sync(act, bin);
+      if (lane == __ffs(peers) - 1) atomicAdd(&sh[bin], __popc(peers));
+    }
+  }
+  __syncthreads();
+  for (int i = threadIdx.x; i < PTQ_NBINS; i += blockDim.x)
+    if (sh[i]) atomicAdd(counts + i, (unsigned long long)sh[i]);
+}
+
+// ---------------------------------------------------------------- F2: KL sweep
+// Per histogram h we precompute (k_kl_prep): cum[j] = sum counts[0..j] (fp64, exact
+// integers), nzc[j] = #(counts[0..j] > 0), logc[j] = log(counts[j]) (0 where empty).
+__global__ void k_kl_prep(const long long* __restrict__ counts, int n_hist,
+                          double* __restrict__ cum, int* __restrict__ nzc, double* __restrict__ logc) {
+  int h = blockIdx.x;
+  if (h >= n_hist || threadIdx.x != 0) return;
+  const long long* c = counts + (int64_t)h * PTQ_NBINS;
+  double acc = 0.0;
+  int nz = 0;
+  for (int j = 0; j < PTQ_NBINS; ++j) {
+    double v = (double)c[j];
+    acc = __dadd_rn(acc, v);
+    nz += (c[j] > 0);
+    cum[(int64_t)h * PTQ_NBINS + j] = acc;
+    nzc[(int64_t)h * PTQ_NBINS + j] = nz;
+    logc[(int64_t)h * PTQ_NBINS + j] = c[j] > 0 ? log(v) : 0.0;
+  }
+}
+
+// numpy pairwise sum of t[0..n) (numpy loops_utils.h pairwise_sum, PW_BLOCKSIZE 128),
+// evaluated from the per-leaf partial sums computed in parallel.
+__device__ double pw_leaf(const double* t, int n) {
+  if (n < 8) {
+    double r = 0.0;
+    for (int i = 0; i < n; ++i) r = __dadd_rn(r, t[i]);
+    return r;
+  }
+  double r[8];
+#pragma unroll
+  for (int j = 0; j < 8; ++j) r[j] = t[j];
+  int i = 8;
+  for (; i < n - (n % 8); i += 8) {
+#pragma unroll
+    for (int j = 0; j < 8; ++j) r[j] = __dadd_rn(r[j], t[i + j]);
+  }
+  double res = __dadd_rn(__dadd_rn(__dadd_rn(r[0], r[1]), __dadd_rn(r[2], r[3])),
+                         __dadd_rn(__dadd_rn(r[4], r[5]), __dadd_rn(r[6], r[7])));
+  for (; i < n; ++i) res = __dadd_rn(res, t[i]);
+  return res;
+}
+
+// leaves of the pairwise recursion over [0, n): enumerate in order
+__device__ int pw_leaves(int n, int* lstart, int* llen) {
+  // iterative DFS with an explicit stack; depth <= 6 for n <= 2048
+  int stack_s[16], stack_n[16], sp = 0, cnt = 0;
+  stack_s[sp] = 0; stack_n[sp] = n; ++sp;
+  while (sp) {
+    --sp;
+    int s = stack_s[sp], m = stack_n[sp];
+    if (m <= 128) { lstart[cnt] = s; llen[cnt] = m; ++cnt; continue; }
+    int m2 = m / 2; m2 -= m2 % 8;
+    // push right then left so left is processed first
+    stack_s[sp] = s + m2; stack_n[sp] = m - m2; ++sp;
+    stack_s[sp] = s; stack_n[sp] = m2; ++sp;
+  }
+  return cnt;
+}
+
+__device__ double pw_combine(int n, const double* leafsum, int* leaf_idx) {
+  if (n <= 128) return leafsum[(*leaf_idx)++];
+  int m2 = n / 2; m2 -= m2 % 8;
+  double a = pw_combine(m2, leafsum, leaf_idx);
+  double b = pw_combine(n - m2, leafsum, leaf_idx);
+  return __dadd_rn(a, b);
+}
+
+// grid: (1921 windows, n_hist); block 128 threads (one per quantization level / group)
+// out: kl[h][w] (inf when infeasible or not applicable)
+__global__ void __launch_bounds__(128) k_kl_sweep(const long long* __restrict__ counts,
+                                                  const float* __restrict__ ranges,
+                                                  const double* __restrict__ cum_all,
+                                                  const int* __restrict__ nzc_all,
+                                                  const double* __restrict__ logc_all,
+                                                  double* __restrict__ kl_out) {
+  __shared__ double terms[PTQ_NBINS];
+  __shared__ int gcount[PTQ_LEVELS + 1];
+  __shared__ double leafsum[40];
+  __shared__ int lstart[40], llen[40], nleaves;
+  __shared__ int infeasible;
+
+  const int w = blockIdx.x, h = blockIdx.y, g = threadIdx.x;
+  const int i = w + PTQ_LEVELS;                    // window width in bins
+  const long long* c = counts + (int64_t)h * PTQ_NBINS;
+  const double* cum = cum_all + (int64_t)h * PTQ_NBINS;
+  const int* nzc = nzc_all + (int64_t)h * PTQ_NBINS;
+  const double* logc = logc_all + (int64_t)h * PTQ_NBINS;
+  const double lo = (double)ranges[2 * h], hi = (double)ranges[2 * h + 1];
+  const double total = cum[PTQ_NBINS - 1];
+  double* out = kl_out + (int64_t)h * PTQ_NWIN + w;
+  if (!(lo < hi) || !(total > 0.0)) {              // clip_range_kl early returns (:63-69)
+    if (g == 0) *out = INFINITY;
+    return;
+  }
+  const bool is_signed = lo < 0.0;
+  int zero_bin = 0;
+  if (is_signed) {
+    double width = __ddiv_rn(__dsub_rn(hi, lo), (double)PTQ_NBINS);
+    zero_bin = (int)__ddiv_rn(-lo, width);         // int((0.0 - lo) / width), lo < 0
+  }
+  int start = 0;
+  if (is_signed) {
+    start = zero_bin - i / 2;
+    start = start < 0 ? 0 : start;
+    start = start > PTQ_NBINS - i ? PTQ_NBINS - i : start;
+  }
+  const int end = start + i;
+  // merged reference P: outliers folded into the window edge bins (:77-80)
+  const double ref_first = (double)c[start] + (start > 0 ? cum[start - 1] : 0.0);
+  const double ref_last_add = __dsub_rn(total, cum[end - 1]);
+  // group layout: m = i // 128, group g covers [g*m, (g+1)*m), last absorbs remainder
+  const int m = i / PTQ_LEVELS;
+  const int gs = g * m, ge = (g == PTQ_LEVELS - 1) ? i : (g + 1) * m;
+  auto refv = [&](int j) -> double {               // ref value at window-relative bin j
+    double v = (double)c[start + j];
+    if (j == 0) v = ref_first;
+    if (j == i - 1) v = __dadd_rn(v, ref_last_add);
+    return v;
+  };
+  // unmerged group sum (exact integer arithmetic in fp64) and P>0 count
+  double gsum = __dsub_rn(cum[start + ge - 1], (start + gs > 0) ? cum[start + gs - 1] : 0.0);
+  int gnz = nzc[start + ge - 1] - ((start + gs > 0) ? nzc[start + gs - 1] : 0);
+  // the two edge bins use the merged flags
+  if (gs == 0) gnz += (refv(0) > 0.0) - (c[start] > 0);
+  if (ge == i && i - 1 != 0) gnz += (refv(i - 1) > 0.0) - (c[start + i - 1] > 0);
+  if (g == 0) infeasible = 0;
+  gcount[g + 1] = gnz;
+  __syncthreads();
+  if (gnz > 0 && gsum == 0.0) infeasible = 1;      // Q = 0 under P > 0 -> inf (:49-50)
+  // exclusive scan of gnz over groups (128 entries, one thread)
+  if (g == 0) {
+    gcount[0] = 0;
+    for (int k = 1; k <= PTQ_LEVELS; ++k) gcount[k] += gcount[k - 1];
+  }
+  __syncthreads();
+  if (infeasible) {
+    if (g == 0) *out = INFINITY;
+    return;
+  }
+  // terms p * (log p - log q) written at their compacted positions
+  if (gnz > 0) {
+    double q = __ddiv_rn(gsum, (double)gnz);
+    double lq = log(q);
+    int pos = gcount[g];
+    for (int j = gs; j < ge; ++j) {
+      double p = refv(j);
+      if (p > 0.0) {
+        bool edge = (j == 0) || (j == i - 1);
+        double lp = edge ? log(p) : logc[start + j];
+        terms[pos++] = __dmul_rn(p, __dsub_rn(lp, lq));
+      }
+    }
+  }
+  const int n = gcount[PTQ_LEVELS];
+  if (g == 0) nleaves = pw_leaves(n, lstart, llen);
+  __syncthreads();
+  if (g < nleaves) leafsum[g] = pw_leaf(terms + lstart[g], llen[g]);
+  __syncthreads();
+  if (g == 0) {
+    int li = 0;
+    double s = (n == 0) ? 0.0 : __dadd_rn(0.0, pw_combine(n, leafsum, &li));
+    *out = __ddiv_rn(s, total);                    // / ref.sum() == total (:52)
+  }
+}
+
+// ---------------------------------------------------------------- launch wrappers
+static inline int nblocks(int64_t n, int t, int cap) {
+  int64_t b = (n + t - 1) / t;
+  return (int)(b < 1 ? 1 : (b > cap ? cap : b));
+}
+void launch_fill_minmax(unsigned int* p, int64_t n_pairs, cudaStream_t s) {
+  k_fill_u32<<<nblocks(2 * n_pairs, 256, 4096), 256, 0, s>>>(p, 2 * n_pairs, 0xffffffffu, 0u);
+}
+void launch_minmax_per_image(const float* x, int64_t elems, int n_img, unsigned int* out_ord,
+                             cudaStream_t s) {
+  int bx = nblocks(elems / 4 + 1, 256, 512);
+  int want = (148 * 8 + n_img - 1) / n_img;
+  if (bx > want) bx = want < 1 ? 1 : want;
+  dim3 g(bx, n_img);
+  k_minmax_per_image<<<g, 256, 0, s>>>(x, elems, out_ord);
+}
+void launch_minmax_reduce_cache(const unsigned int* per_img, int n_tensors, int n_img_total,
+                                const int* slots, int n_slots, float* ranges, cudaStream_t s) {
+  k_minmax_reduce_cache<<<(n_tensors + 127) / 128, 128, 0, s>>>(per_img, n_tensors, n_img_total,
+                                                               slots, n_slots, ranges);
+}
+void launch_histogram(const float* x, int64_t elems, const int* slots, int n_slots,
+                      const float* range, unsigned long long* counts, cudaStream_t s) {
+  int64_t total = elems * n_slots;
+  k_histogram<<<nblocks(total, 512, 148 * 4), 512, 0, s>>>(x, elems, slots, n_slots, range, counts);
+}
+void launch_kl_sweep(const long long* counts, const float* ranges, int n_hist, double* cum,
+                     int* nzc, double* logc, double* kl_out, cudaStream_t s) {
+  if (n_hist <= 0) return;
+  k_kl_prep<<<n_hist, 32, 0, s>>>(counts, n_hist, cum, nzc, logc);
+  dim3 g(PTQ_NWIN, n_hist);
+  k_kl_sweep<<<g, 128, 0, s>>>(counts, ranges, cum, nzc, logc, kl_out);
+}
+
+}  // namespace ptq

@@ -1,0 +1,337 @@
+// F4: int8 implicit-GEMM convolution on the 5th-generation tensor cores.
+//
+// Restates the reference's integer conv/fc branch (/root/reference/pkg/src/
+// ptqtune/intexec.py:170-211, _int_conv :95-105): acc = sum (x-zx)(w-zw) with
+// zero padding in the shifted domain, + int32 bias, saturate to int32, then
+// requantize with m = (sx*sw)/sy and round-half-up, optional relu / residual
+// add on codes.  The contraction runs as D[s32] = A[s8] x B[s8] with
+//   sum (x-zx)(w-zw) = sum x*w - zw*sum x - zx*sum w + K*zx*zw
+// where the halo of the NHWC input holds the zero-point code (so padded taps
+// contribute exactly 0), sum w is per output channel (precomputed) and sum x is
+// per output pixel (from per-pixel channel sums P, only when some zw != 0).
+//
+// Kernel anatomy (one 128 x BN output tile per CTA, 192 threads):
+//   warps 0-3  A producers: one output pixel (GEMM row) per thread; gather the
+//              row's 16-byte K chunks with cp.async into the UMMA K-major
+//              no-swizzle canonical layout; completion signalled with
+//              cp.async.mbarrier.arrive.noinc on the stage's full barrier.
+//   warp 4     B producer: one cp.async.bulk (TMA bulk engine) per stage from
+//              the pre-tiled weight image, complete_tx on the same barrier.
+//   warp 5     TMEM allocator + single-thread tcgen05.mma.kind::i8 issuer
+//              (M=128, N=BN, K=32 per instruction, 4 per 128-byte stage);
+//              tcgen05.commit frees a stage / signals the accumulator.
+//   warps 0-3  epilogue: tcgen05.ld 32x32b (thread = TMEM lane = output row),
+//              zero-point correction, bias, int32 clip, fp64 requant, relu /
+//              fused add, 16-byte stores of int8 codes.
+#include <climits>
+
+#include "common.cuh"
+#include "kernels.h"
+
+namespace ptq {
+
+constexpr int TC_BM = 128;
+constexpr int TC_STAGES = 4;
+constexpr int TC_THREADS = 192;
+constexpr int TC_A_STAGE = TC_BM * 128;  // 16 KB: 8 chunks x 128 rows x 16 B
+
+__device__ __forceinline__ uint64_t umma_desc(uint32_t saddr, uint32_t lbo, uint32_t sbo) {
+  uint64_t d = 0;
+  d |= (uint64_t)((saddr >> 4) & 0x3FFFu);
+  d |= (uint64_t)((lbo >> 4) & 0x3FFFu) << 16;
+  d |= (uint64_t)((sbo >> 4) & 0x3FFFu) << 32;
+  d |= (uint64_t)1 << 46;  // descriptor version 1 (sm_100); base offset 0; SWIZZLE_NONE
+  return d;
+}
+
+// instruction descriptor: D=s32, A=s8, B=s8, both K-major, N=BN, M=128
+template <int BN>
+__device__ __forceinline__ uint32_t idesc_i8() {
+  return (2u << 4) | (1u << 7) | (1u << 10) | ((uint32_t)(BN >> 3) << 17) |
+         ((uint32_t)(TC_BM >> 4) << 24);
+}
+
+__device__ __forceinline__ void mma_i8(uint32_t tmem_d, uint64_t adesc, uint64_t bdesc,
+                                       uint32_t idesc, uint32_t accumulate) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %4, 0;\n\t"
+      "tcgen05.mma.cta_group::1.kind::i8 [%0], %1, %2, %3, p;\n\t}" ::"r"(tmem_d),
+      "l"(adesc), "l"(bdesc), "r"(idesc), "r"(accumulate));
+}
+__device__ __forceinline__ void mma_commit(uint64_t* bar) {
+  asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(
+                   smem_u32(bar))
+               : "memory");
+}
+__device__ __forceinline__ void tc_fence_before() {
+  asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+}
+__device__ __forceinline__ void tc_fence_after() {
+  asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+}
+__device__ __forceinline__ void tmem_ld16(uint32_t taddr, uint32_t (&v)[16]) {
+  asm volatile(
+      "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15}, [%16];"
+      : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]), "=r"(v[6]),
+        "=r"(v[7]), "=r"(v[8]), "=r"(v[9]), "=r"(v[10]), "=r"(v[11]), "=r"(v[12]), "=r"(v[13]),
+        "=r"(v[14]), "=r"(v[15])
+      : "r"(taddr));
+  asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+}
+
+__device__ __forceinline__ int64_t vpix(const View& v, int n, int h, int w) {
+  const int Hp = v.H + 2 * v.halo, Wp = v.W + 2 * v.halo;
+  return ((int64_t)n * Hp + h + v.halo) * Wp + w + v.halo;
+}
+
+// shared epilogue math for one output element (used by the tensor-core kernel
+// and by the CUDA-core reference kernel).  `dot` = sum x*w over the padded K.
+__device__ __forceinline__ int epi_code(long long dot, int c, long long rowsum, const ConvTcArgs& a,
+                                        const LayerRt& rt, int skip_code) {
+  long long zw = a.wzp[c];
+  long long acc = dot - zw * rowsum - (long long)rt.zx * a.wsum[c] + (long long)a.kreal * rt.zx * zw;
+  acc = clip32(acc + a.L.biasq[c]);
+  int q = requant1(acc, a.L.mult[c], rt.zy);
+  if (q < rt.relu_zp) q = rt.relu_zp;
+  if (a.skip.p) {
+    int xa = a.conv_is_a ? q : skip_code, xb = a.conv_is_a ? skip_code : q;
+    double s = __dadd_rn(__dmul_rn((double)(xa - rt.za), rt.ra), __dmul_rn((double)(xb - rt.zb), rt.rb));
+    q = clip8(rhu(s) + (double)rt.zo);
+    if (q < rt.add_relu_zp) q = rt.add_relu_zp;
+  }
+  return q;
+}
+
+__device__ __forceinline__ long long pixel_rowsum(const ConvTcArgs& a, int n, int ih0, int iw0) {
+  if (!a.has_wzp) return 0;
+  const int Wp = a.in.W + 2 * a.in.halo, Hp = a.in.H + 2 * a.in.halo;
+  long long s = 0;
+  for (int kh = 0; kh < a.k; ++kh)
+    for (int kw = 0; kw < a.k; ++kw) s += a.P[((int64_t)n * Hp + ih0 + kh) * Wp + iw0 + kw];
+  return s;
+}
+
+template <int BN>
+__global__ void __launch_bounds__(TC_THREADS, 1) k_conv_tc(const ConvTcArgs a) {
+  extern __shared__ __align__(1024) uint8_t smem[];
+  uint8_t* sA = smem;
+  uint8_t* sB = smem + TC_STAGES * TC_A_STAGE;
+  uint64_t* full = reinterpret_cast<uint64_t*>(sB + TC_STAGES * BN * 128);
+  uint64_t* empty = full + TC_STAGES;
+  uint64_t* accb = empty + TC_STAGES;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(accb + 1);
+  constexpr uint32_t TMEM_COLS = BN < 32 ? 32 : BN;
+
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int64_t M = (int64_t)a.in.N * a.OH * a.OW;
+  const int64_t m0 = (int64_t)blockIdx.x * TC_BM;
+  const int nt = blockIdx.y;
+
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < TC_STAGES; ++s) {
+      mbar_init(&full[s], 128 + 1);
+      mbar_init(&empty[s], 1);
+    }
+    mbar_init(accb, 1);
+    fence_mbar_init();
+  }
+  if (warp == 5) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
+                     smem_u32(tmem_slot)),
+                 "r"(TMEM_COLS));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+  }
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = *tmem_slot;
+
+  // per-row geometry (warps 0-3: row r = threadIdx.x)
+  const int r = threadIdx.x;
+  const int64_t m = m0 + r;
+  const bool row_ok = (warp < 4) && (m < M);
+  int n_img = 0, oh = 0, ow = 0;
+  if (row_ok) {
+    ow = (int)(m % a.OW);
+    int64_t t = m / a.OW;
+    oh = (int)(t % a.OH);
+    n_img = (int)(t / a.OH);
+  }
+  const int Wp = a.in.W + 2 * a.in.halo, Hp = a.in.H + 2 * a.in.halo;
+  const int ih0 = oh * a.stride - a.pad + a.in.halo, iw0 = ow * a.stride - a.pad + a.in.halo;
+
+  if (warp < 4) {
+    // ------------------------------------------------ A producer (implicit im2col gather)
+    const int Cp = a.in.Cp, cpc = Cp >> 4;
+    const int8_t* base = a.in.p + (((int64_t)n_img * Hp + ih0) * Wp + iw0) * Cp;
+    int kh = 0, kw = 0, ch = 0, kk = 0;
+    for (int it = 0; it < a.n_kiter; ++it) {
+      const int s = it % TC_STAGES;
+      const uint32_t ph = (uint32_t)(it / TC_STAGES) & 1u;
+      mbar_wait(&empty[s], ph ^ 1u);
+      uint8_t* dst = sA + s * TC_A_STAGE + r * 16;
+#pragma unroll
+      for (int j = 0; j < 8; ++j) {
+        const bool v = row_ok && kk < a.n_chunks;
+        const int8_t* src = v ? base + ((int64_t)kh * Wp + kw) * Cp + ch * 16 : a.in.p;
+        cp_async16(dst + j * (TC_BM * 16), src, v ? 16u : 0u);
+        ++kk;
+        if (++ch == cpc) {
+          ch = 0;
+          if (++kw == a.k) { kw = 0; ++kh; }
+        }
+      }
+      cp_async_mbar_arrive_noinc(&full[s]);
+    }
+  } else if (warp == 4) {
+    // ------------------------------------------------ B producer (bulk copies of pre-tiled weights)
+    if (lane == 0) {
+      const int8_t* gB = a.wB + (int64_t)nt * a.n_kiter * BN * 128;
+      for (int it = 0; it < a.n_kiter; ++it) {
+        const int s = it % TC_STAGES;
+        const uint32_t ph = (uint32_t)(it / TC_STAGES) & 1u;
+        mbar_wait(&empty[s], ph ^ 1u);
+        mbar_arrive_expect_tx(&full[s], BN * 128);
+        bulk_g2s(sB + s * BN * 128, gB + (int64_t)it * BN * 128, BN * 128, &full[s]);
+      }
+    }
+  } else {
+    // ------------------------------------------------ MMA issuer
+    if (lane == 0) {
+      const uint32_t idesc = idesc_i8<BN>();
+      for (int it = 0; it < a.n_kiter; ++it) {
+        const int s = it % TC_STAGES;
+        const uint32_t ph = (uint32_t)(it / TC_STAGES) & 1u;
+        mbar_wait(&full[s], ph);
+        tc_fence_after();
+        fence_proxy_async();
+        const uint32_t a0 = smem_u32(sA + s * TC_A_STAGE), b0 = smem_u32(sB + s * BN * 128);
+#pragma unroll
+        for (int ks = 0; ks < 4; ++ks) {
+          const uint64_t ad = umma_desc(a0 + ks * 2 * (TC_BM * 16), TC_BM * 16, 128);
+          const uint64_t bd = umma_desc(b0 + ks * 2 * (BN * 16), BN * 16, 128);
+          mma_i8(tmem, ad, bd, idesc, (it | ks) != 0);
+        }
+        mma_commit(&empty[s]);
+      }
+      mma_commit(accb);
+    }
+    __syncwarp();
+  }
+
+  if (warp < 4) {
+    // ------------------------------------------------ epilogue
+    mbar_wait(accb, 0);
+    tc_fence_after();
+    const LayerRt rt = *a.L.rt;
+    const long long rowsum = row_ok ? pixel_rowsum(a, n_img, ih0, iw0) : 0;
+    const int Cout = a.L.cout;
+    int8_t* orow = row_ok ? a.out.p + vpix(a.out, n_img, oh, ow) * a.out.Cp : nullptr;
+    const int8_t* srow = (row_ok && a.skip.p) ? a.skip.p + vpix(a.skip, n_img, oh, ow) * a.skip.Cp : nullptr;
+#pragma unroll 1
+    for (int c0 = 0; c0 < BN; c0 += 16) {
+      uint32_t v[16];
+      tmem_ld16(tmem + ((uint32_t)(warp * 32) << 16) + (uint32_t)c0, v);
+      const int cb = nt * BN + c0;
+      if (!row_ok || cb >= a.out.Cp) continue;
+      alignas(16) int8_t codes[16];
+      alignas(16) int8_t sk[16];
+      if (srow) *reinterpret_cast<int4*>(sk) = *reinterpret_cast<const int4*>(srow + cb);
+#pragma unroll
+      for (int j = 0; j < 16; ++j) {
+        const int c = cb + j;
+        codes[j] = c < Cout ? (int8_t)epi_code((long long)(int)v[j], c, rowsum, a, rt, srow ? sk[j] : 0) : (int8_t)0;
+      }
+      *reinterpret_cast<int4*>(orow + cb) = *reinterpret_cast<int4*>(codes);
+    }
+  }
+
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 5) {
+    tc_fence_after();
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(TMEM_COLS));
+  }
+}
+
+// ---------------------------------------------------------------- CUDA-core reference
+// Same contract, direct sum over the tiled weight image (tests / cross-checks only).
+template <int BN>
+__global__ void k_conv_i8_ref(const ConvTcArgs a) {
+  const int64_t M = (int64_t)a.in.N * a.OH * a.OW;
+  const int Cout = a.L.cout;
+  const int64_t total = M * a.out.Cp;
+  const LayerRt rt = *a.L.rt;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < total;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    const int c = (int)(i % a.out.Cp);
+    const int64_t m = i / a.out.Cp;
+    const int ow = (int)(m % a.OW);
+    const int64_t t = m / a.OW;
+    const int oh = (int)(t % a.OH), n = (int)(t / a.OH);
+    int8_t* orow = a.out.p + vpix(a.out, n, oh, ow) * a.out.Cp;
+    if (c >= Cout) { orow[c] = 0; continue; }
+    const int Wp = a.in.W + 2 * a.in.halo, Hp = a.in.H + 2 * a.in.halo;
+    const int ih0 = oh * a.stride - a.pad + a.in.halo, iw0 = ow * a.stride - a.pad + a.in.halo;
+    const int cpc = a.in.Cp >> 4;
+    const int ntile = c / BN, row = c % BN;
+    long long dot = 0;
+    for (int kk = 0; kk < a.n_chunks; ++kk) {
+      const int tap = kk / cpc, ch = kk % cpc;
+      const int kh = tap / a.k, kw = tap % a.k;
+      const int8_t* xs = a.in.p + (((int64_t)n * Hp + ih0 + kh) * Wp + iw0 + kw) * a.in.Cp + ch * 16;
+      const int8_t* ws = a.wB + (((int64_t)ntile * a.n_kiter + kk / 8) * 8 + kk % 8) * BN * 16 + row * 16;
+      for (int b = 0; b < 16; ++b) dot += (long long)xs[b] * ws[b];
+    }
+    const long long rowsum = pixel_rowsum(a, n, ih0, iw0);
+    const int sk = a.skip.p ? a.skip.p[vpix(a.skip, n, oh, ow) * a.skip.Cp + c] : 0;
+    orow[c] = (int8_t)epi_code(dot, c, rowsum, a, rt, sk);
+  }
+}
+
+int conv_tc_bn_for(int cout) {
+  if (cout <= 16) return 16;
+  if (cout <= 32) return 32;
+  if (cout <= 64) return 64;
+  if (cout <= 128) return 128;
+  return 256;
+}
+
+template <int BN>
+static void launch_bn(const ConvTcArgs& a, cudaStream_t s) {
+  const size_t smem = (size_t)TC_STAGES * TC_A_STAGE + (size_t)TC_STAGES * BN * 128 +
+                      (2 * TC_STAGES + 1) * 8 + 16;
+  static bool configured = false;
+  if (!configured) {
+    cudaFuncSetAttribute(k_conv_tc<BN>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    configured = true;
+  }
+  const int64_t M = (int64_t)a.in.N * a.OH * a.OW;
+  dim3 g((unsigned)((M + TC_BM - 1) / TC_BM), (unsigned)((a.L.cout + BN - 1) / BN));
+  k_conv_tc<BN><<<g, TC_THREADS, smem, s>>>(a);
+}
+
+void launch_conv_tc(const ConvTcArgs& a, int bn, cudaStream_t s) {
+  switch (bn) {
+    case 16: launch_bn<16>(a, s); break;
+    case 32: launch_bn<32>(a, s); break;
+    case 64: launch_bn<64>(a, s); break;
+    case 128: launch_bn<128>(a, s); break;
+    default: launch_bn<256>(a, s); break;
+  }
+}
+
+void launch_conv_i8_ref(const ConvTcArgs& a, int bn, cudaStream_t s) {
+  const int64_t total = (int64_t)a.in.N * a.OH * a.OW * a.out.Cp;
+  int64_t b = (total + 255) / 256;
+  int blocks = (int)(b > 148 * 64 ? 148 * 64 : (b < 1 ? 1 : b));
+  switch (bn) {
+    case 16: k_conv_i8_ref<16><<<blocks, 256, 0, s>>>(a); break;
+    case 32: k_conv_i8_ref<32><<<blocks, 256, 0, s>>>(a); break;
+    case 64: k_conv_i8_ref<64><<<blocks, 256, 0, s>>>(a); break;
+    case 128: k_conv_i8_ref<128><<<blocks, 256, 0, s>>>(a); break;
+    default: k_conv_i8_ref<256><<<blocks, 256, 0, s>>>(a); break;
+  }
+}
+
+}  // namespace ptq

@@ -1,0 +1,242 @@
+// fp32 forward kernels (calibration observer pass and mixed-precision
+// FirstLastFp32 layers).  Layout NHWC, batch-major.  These restate the
+// reference's fp32 interpreter (/root/reference/pkg/src/ptqtune/fp32.py:41-114)
+// but accumulate in a different order than OpenBLAS sgemm, so activations
+// agree to ~1e-6 relative, not bitwise (SURVEY.md 8(c) staged parity).
+#include "common.cuh"
+#include "kernels.h"
+
+namespace ptq {
+
+// images NCHW (host layout) -> NHWC, gathering image ids
+__global__ void k_nchw_to_nhwc(const float* __restrict__ src, const int* __restrict__ ids, int n,
+                               int C, int H, int W, float* __restrict__ dst) {
+  int64_t total = (int64_t)n * C * H * W;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < total;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    int c = i % C;
+    int64_t r = i / C;
+    int w = r % W; r /= W;
+    int h = r % H;
+    int img = (int)(r / H);
+    int64_t sid = ids ? ids[img] : img;
+    dst[i] = __ldg(src + ((sid * C + c) * H + h) * W + w);
+  }
+}
+
+// Implicit-GEMM direct conv, fp32 SIMT.
+// out[m][co] = bias[co] + sum_k A[m][k] * Bw[k][co];  m = (n, oh, ow); k = (kh, kw, ci).
+// Bw is [K][Cout] (prepared on device).  Also used for fully-connected layers
+// (1x1 "image" whose channel axis is the NHWC-flattened feature vector).
+constexpr int CF_BM = 128, CF_BN = 64, CF_BK = 8;
+__global__ void __launch_bounds__(256) k_conv_f32(const float* __restrict__ x, int N, int H, int W,
+                                                  int Cin, const float* __restrict__ Bw,
+                                                  const float* __restrict__ bias, int Cout, int k,
+                                                  int stride, int pad, int OH, int OW,
+                                                  float* __restrict__ y) {
+  __shared__ float As[CF_BK][CF_BM + 4];
+  __shared__ float Bs[CF_BK][CF_BN];
+  const int tid = threadIdx.x;
+  const int64_t M = (int64_t)N * OH * OW;
+  const int K = k * k * Cin;
+  const int64_t m0 = (int64_t)blockIdx.x * CF_BM;
+  const int n0 = blockIdx.y * CF_BN;
+  // loader mapping: A: kk = tid % 8, rows r = tid/8 + 32*j
+  const int a_k = tid & 7;
+  int a_ih0[4], a_iw0[4];
+  int64_t a_base[4];
+  bool a_ok[4];
+#pragma unroll
+  for (int j = 0; j < 4; ++j) {
+    int64_t m = m0 + (tid >> 3) + 32 * j;
+    a_ok[j] = m < M;
+    int64_t mm = a_ok[j] ? m : 0;
+    int ow = mm % OW;
+    int64_t t = mm / OW;
+    int oh = t % OH;
+    int nimg = (int)(t / OH);
+    a_ih0[j] = oh * stride - pad;
+    a_iw0[j] = ow * stride - pad;
+    a_base[j] = (int64_t)nimg * H * W;
+  }
+  const int b_k = tid >> 5, b_n = (tid & 31) * 2;  // 8 x 64 tile, 2 per thread
+  const int tm = tid >> 4, tn = tid & 15;           // compute: rows tm*8.., cols tn*4..
+  float acc[8][4];
+#pragma unroll
+  for (int i = 0; i < 8; ++i)
+#pragma unroll
+    for (int j = 0; j < 4; ++j) acc[i][j] = 0.f;
+
+  for (int k0 = 0; k0 < K; k0 += CF_BK) {
+    {
+      int kk = k0 + a_k;
+      int tap = kk / Cin, ci = kk - tap * Cin;
+      int kh = tap / k, kw = tap - kh * k;
+#pragma unroll
+      for (int j = 0; j < 4; ++j) {
+        float v = 0.f;
+        int ih = a_ih0[j] + kh, iw = a_iw0[j] + kw;
+        if (a_ok[j] && kk < K && ih >= 0 && ih < H && iw >= 0 && iw < W)
+          v = __ldg(x + ((a_base[j] + (int64_t)ih * W + iw) * Cin + ci));
+        As[a_k][(tid >> 3) + 32 * j] = v;
+      }
+      int kb = k0 + b_k;
+#pragma unroll
+      for (int j = 0; j < 2; ++j) {
+        int nn = n0 + b_n + j;
+        Bs[b_k][b_n + j] = (kb < K && nn < Cout) ? __ldg(Bw + (int64_t)kb * Cout + nn) : 0.f;
+      }
+    }
+    __syncthreads();
+#pragma unroll
+    for (int kk = 0; kk < CF_BK; ++kk) {
+      float a[8], b[4];
+#pragma unroll
+      for (int i = 0; i < 8; ++i) a[i] = As[kk][tm * 8 + i];
+#pragma unroll
+      for (int j = 0; j < 4; ++j) b[j] = Bs[kk][tn * 4 + j];
+#pragma unroll
+      for (int i = 0; i < 8; ++i)
+#pragma unroll
+        for (int j = 0; j < 4; ++j) acc[i][j] = fmaf(a[i], b[j], acc[i][j]);
+    }
+    __syncthreads();
+  }
+#pragma unroll
+  for (int i = 0; i < 8; ++i) {
+    int64_t m = m0 + tm * 8 + i;
+    if (m >= M) continue;
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      int nn = n0 + tn * 4 + j;
+      if (nn < Cout) y[m * Cout + nn] = acc[i][j] + (bias ? __ldg(bias + nn) : 0.f);
+    }
+  }
+}
+
+// depthwise conv: w is [C][k*k]
+__global__ void k_dwconv_f32(const float* __restrict__ x, int N, int H, int W, int C,
+                             const float* __restrict__ w, const float* __restrict__ bias, int k,
+                             int stride, int pad, int OH, int OW, float* __restrict__ y) {
+  int64_t total = (int64_t)N * OH * OW * C;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < total;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    int c = i % C;
+    int64_t r = i / C;
+    int ow = r % OW; r /= OW;
+    int oh = r % OH;
+    int n = (int)(r / OH);
+    float acc = 0.f;
+    for (int kh = 0; kh < k; ++kh) {
+      int ih = oh * stride - pad + kh;
+      if (ih < 0 || ih >= H) continue;
+      for (int kw = 0; kw < k; ++kw) {
+        int iw = ow * stride - pad + kw;
+        if (iw < 0 || iw >= W) continue;
+        acc = fmaf(__ldg(x + (((int64_t)n * H + ih) * W + iw) * C + c), __ldg(w + c * k * k + kh * k + kw), acc);
+      }
+    }
+    y[i] = acc + (bias ? __ldg(bias + c) : 0.f);
+  }
+}
+
+__global__ void k_relu_f32(const float* __restrict__ x, float* __restrict__ y, int64_t n) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+    y[i] = fmaxf(x[i], 0.f);
+}
+
+__global__ void k_add_f32(const float* __restrict__ a, const float* __restrict__ b,
+                          float* __restrict__ y, int64_t n) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+    y[i] = a[i] + b[i];
+}
+
+// mode 0 = max, 1 = avg (sum in fp32 then / area)
+__global__ void k_pool_f32(const float* __restrict__ x, int N, int H, int W, int C, int k,
+                           int stride, int OH, int OW, int mode, float* __restrict__ y) {
+  int64_t total = (int64_t)N * OH * OW * C;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < total;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    int c = i % C;
+    int64_t r = i / C;
+    int ow = r % OW; r /= OW;
+    int oh = r % OH;
+    int n = (int)(r / OH);
+    float acc = mode ? 0.f : -INFINITY;
+    for (int kh = 0; kh < k; ++kh)
+      for (int kw = 0; kw < k; ++kw) {
+        float v = __ldg(x + (((int64_t)n * H + oh * stride + kh) * W + ow * stride + kw) * C + c);
+        acc = mode ? acc + v : fmaxf(acc, v);
+      }
+    y[i] = mode ? acc / (float)(k * k) : acc;
+  }
+}
+
+// copy x [n][HW][Cx] into y [n][HW][Cy] at channel offset coff
+__global__ void k_concat_f32(const float* __restrict__ x, int64_t npix, int Cx, int Cy, int coff,
+                             float* __restrict__ y) {
+  int64_t total = npix * Cx;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < total;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    int64_t p = i / Cx;
+    int c = i - p * Cx;
+    y[p * Cy + coff + c] = x[i];
+  }
+}
+
+// softmax over the last axis of [rows][C] (one warp per row)
+__global__ void k_softmax_f32(const float* __restrict__ x, int64_t rows, int C, float* __restrict__ y) {
+  int64_t r = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
+  int lane = threadIdx.x & 31;
+  if (r >= rows) return;
+  const float* p = x + r * C;
+  float mx = -INFINITY;
+  for (int c = lane; c < C; c += 32) mx = fmaxf(mx, p[c]);
+  for (int o = 16; o; o >>= 1) mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+  float s = 0.f;
+  for (int c = lane; c < C; c += 32) s += expf(p[c] - mx);
+  for (int o = 16; o; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+  for (int c = lane; c < C; c += 32) y[r * C + c] = expf(p[c] - mx) / s;
+}
+
+// ---------------------------------------------------------------- launch wrappers
+static inline int gblk(int64_t n) {
+  int64_t b = (n + 255) / 256;
+  return (int)(b < 1 ? 1 : (b > 148 * 32 ? 148 * 32 : b));
+}
+void launch_nchw_to_nhwc(const float* src, const int* ids, int n, int C, int H, int W, float* dst,
+                         cudaStream_t s) {
+  k_nchw_to_nhwc<<<gblk((int64_t)n * C * H * W), 256, 0, s>>>(src, ids, n, C, H, W, dst);
+}
+void launch_conv_f32(const float* x, int N, int H, int W, int Cin, const float* Bw,
+                     const float* bias, int Cout, int k, int stride, int pad, int OH, int OW,
+                     float* y, cudaStream_t s) {
+  int64_t M = (int64_t)N * OH * OW;
+  dim3 g((unsigned)((M + CF_BM - 1) / CF_BM), (unsigned)((Cout + CF_BN - 1) / CF_BN));
+  k_conv_f32<<<g, 256, 0, s>>>(x, N, H, W, Cin, Bw, bias, Cout, k, stride, pad, OH, OW, y);
+}
+void launch_dwconv_f32(const float* x, int N, int H, int W, int C, const float* w,
+                       const float* bias, int k, int stride, int pad, int OH, int OW, float* y,
+                       cudaStream_t s) {
+  k_dwconv_f32<<<gblk((int64_t)N * OH * OW * C), 256, 0, s>>>(x, N, H, W, C, w, bias, k, stride,
+                                                             pad, OH, OW, y);
+}
+void launch_relu_f32(const float* x, float* y, int64_t n, cudaStream_t s) {
+  k_relu_f32<<<gblk(n), 256, 0, s>>>(x, y, n);
+}
+void launch_add_f32(const float* a, const float* b, float* y, int64_t n, cudaStream_t s) {
+  k_add_f32<<<gblk(n), 256, 0, s>>>(a, b, y, n);
+}
+void launch_pool_f32(const float* x, int N, int H, int W, int C, int k, int stride, int OH, int OW,
+                     int mode, float* y, cudaStream_t s) {
+  k_pool_f32<<<gblk((int64_t)N * OH * OW * C), 256, 0, s>>>(x, N, H, W, C, k, stride, OH, OW, mode, y);
+}
+void launch_concat_f32(const float* x, int64_t npix, int Cx, int Cy, int coff, float* y,
+                       cudaStream_t s) {
+  k_concat_f32<<<gblk(npix * Cx), 256, 0, s>>>(x, npix, Cx, Cy, coff, y);
+}
+void launch_softmax_f32(const float* x, int64_t rows, int C, float* y, cudaStream_t s) {
+  k_softmax_f32<<<(int)((rows * 32 + 255) / 256), 256, 0, s>>>(x, rows, C, y);
+}
+
+}  // namespace ptq

@@ -1,0 +1,520 @@
+// F3: quantize / dequantize / requantize kernels and their parameter math.
+//
+// Every formula follows SURVEY.md App. A and cites the reference:
+//   params      schemes.py:81-131      (device fp64, explicit _rn intrinsics)
+//   quantize    schemes.py:145-150     clip(RHA(x64/s64 + zp), -128, 127)
+//   dequantize  schemes.py:153-155     f32((c - zp) * s64)
+//   bias        quantize.py:177-182    clip(RHA(b64 / (s_in * s_w)), int32)
+//   requant     intexec.py:72-85,:201  m = (s_x * s_w) / s_y; clip(RHU(acc*m) + zp)
+//   avgpool     intexec.py:225-244     requant(sum - zp*area, 1.0/area)
+//   add         intexec.py:245-276     clip(RHU(xs*(sa/so) + ys*(sb/so)) + zo)
+//   concat      intexec.py:115-129     requant(c - zs, ss/sd, zd) per input
+//   relu        intexec.py:212-216     max(c, zp)
+// Layout: NHWC int8 views (kernels.h View) with a zero-point-filled halo.
+#include <climits>
+
+#include "common.cuh"
+#include "kernels.h"
+
+namespace ptq {
+
+static inline int nblk(int64_t n, int t = 256, int cap = 148 * 32) {
+  int64_t b = (n + t - 1) / t;
+  return (int)(b < 1 ? 1 : (b > cap ? cap : b));
+}
+
+__device__ __forceinline__ int64_t voff(const View& v, int n, int h, int w) {
+  const int Hp = v.H + 2 * v.halo, Wp = v.W + 2 * v.halo;
+  return (((int64_t)n * Hp + h + v.halo) * Wp + w + v.halo) * v.Cp;
+}
+
+// ---------------------------------------------------------------- activation params
+__global__ void k_act_params(const double* __restrict__ ranges, const int* __restrict__ var_scheme,
+                             int n_var, int T, float* __restrict__ scale, int* __restrict__ zp) {
+  int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n_var * T) return;
+  int v = i / T;
+  params_for_range(var_scheme[v], ranges[2 * i], ranges[2 * i + 1], scale + i, zp + i);
+}
+void launch_act_params(const double* ranges, const int* var_scheme, int n_var, int T, float* scale,
+                       int* zp, cudaStream_t s) {
+  int n = n_var * T;
+  k_act_params<<<(n + 127) / 128, 128, 0, s>>>(ranges, var_scheme, n_var, T, scale, zp);
+}
+
+// ---------------------------------------------------------------- weights
+// F1 per-channel variant: one block per output channel (or grid-stride over the tensor)
+__global__ void k_weight_minmax(const float* __restrict__ w, int cout, int64_t per_ch,
+                                int per_channel, unsigned int* __restrict__ mnmx) {
+  float lo = INFINITY, hi = -INFINITY;
+  if (per_channel) {
+    const float* p = w + (int64_t)blockIdx.x * per_ch;
+    for (int64_t i = threadIdx.x; i < per_ch; i += blockDim.x) {
+      float v = __ldg(p + i);
+      lo = fminf(lo, v);
+      hi = fmaxf(hi, v);
+    }
+  } else {
+    int64_t n = per_ch * cout;
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
+         i += (int64_t)gridDim.x * blockDim.x) {
+      float v = __ldg(w + i);
+      lo = fminf(lo, v);
+      hi = fmaxf(hi, v);
+    }
+  }
+  for (int o = 16; o; o >>= 1) {
+    lo = fminf(lo, __shfl_xor_sync(0xffffffffu, lo, o));
+    hi = fmaxf(hi, __shfl_xor_sync(0xffffffffu, hi, o));
+  }
+  unsigned int* dst = mnmx + (per_channel ? 2 * blockIdx.x : 0);
+  if ((threadIdx.x & 31) == 0) {
+    atomicMin(dst, f2ord(lo));
+    atomicMax(dst + 1, f2ord(hi));
+  }
+}
+__global__ void k_init_minmax(unsigned int* p, int n) {
+  int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < n) { p[2 * i] = 0xffffffffu; p[2 * i + 1] = 0u; }
+}
+void launch_weight_minmax(const float* w, int cout, int64_t per_ch, int per_channel,
+                          unsigned int* mnmx, cudaStream_t s) {
+  int npairs = per_channel ? cout : 1;
+  k_init_minmax<<<(npairs + 255) / 256, 256, 0, s>>>(mnmx, npairs);
+  if (per_channel)
+    k_weight_minmax<<<cout, 256, 0, s>>>(w, cout, per_ch, 1, mnmx);
+  else
+    k_weight_minmax<<<nblk(per_ch * cout), 256, 0, s>>>(w, cout, per_ch, 0, mnmx);
+}
+
+// params per channel; per-tensor params are broadcast to every channel slot
+__global__ void k_weight_params(const unsigned int* __restrict__ mnmx, int cout, int per_channel,
+                                int scheme, float* __restrict__ scale, int* __restrict__ zp) {
+  int o = blockIdx.x * blockDim.x + threadIdx.x;
+  if (o >= cout) return;
+  const unsigned int* q = mnmx + (per_channel ? 2 * o : 0);
+  params_for_range(scheme, (double)ord2f(q[0]), (double)ord2f(q[1]), scale + o, zp + o);
+}
+void launch_weight_params(const unsigned int* mnmx, int cout, int per_channel, int scheme,
+                          float* scale, int* zp, cudaStream_t s) {
+  k_weight_params<<<(cout + 127) / 128, 128, 0, s>>>(mnmx, cout, per_channel, scheme, scale, zp);
+}
+
+// value of the weight element feeding GEMM column o, K byte position kb (padded layout)
+__device__ __forceinline__ bool wsrc(int o, int64_t kb, int cin, int k, int fc_hw, int cin_p,
+                                     int64_t* src_idx) {
+  if (fc_hw > 0) {                       // fc: kb = pix*cin_p + c  ->  ref index c*fc_hw + pix
+    int64_t pix = kb / cin_p;
+    int c = (int)(kb - pix * cin_p);
+    if (c >= cin || pix >= fc_hw) return false;
+    *src_idx = (int64_t)o * cin * fc_hw + (int64_t)c * fc_hw + pix;
+    return true;
+  }
+  int64_t tap = kb / cin_p;
+  int c = (int)(kb - tap * cin_p);
+  if (c >= cin || tap >= (int64_t)k * k) return false;
+  int kh = (int)(tap / k), kw = (int)(tap - (int64_t)kh * k);
+  *src_idx = (((int64_t)o * cin + c) * k + kh) * k + kw;
+  return true;
+}
+
+// tiled B operand: [nt][it][j(8)][row(bn)][16 bytes]
+__global__ void k_weight_quant_tc(const float* __restrict__ w, int cout, int cin, int k, int fc_hw,
+                                  int cin_p, const float* __restrict__ scale,
+                                  const int* __restrict__ zp, int bn, int n_kiter,
+                                  int8_t* __restrict__ out, int64_t total) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < total;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    int b = (int)(i & 15);
+    int64_t r = i >> 4;
+    int row = (int)(r % bn); r /= bn;
+    int j = (int)(r & 7); r >>= 3;
+    int it = (int)(r % n_kiter);
+    int nt = (int)(r / n_kiter);
+    int o = nt * bn + row;
+    int64_t kb = ((int64_t)it * 8 + j) * 16 + b;
+    int8_t code = 0;
+    int64_t si;
+    if (o < cout && wsrc(o, kb, cin, k, fc_hw, cin_p, &si))
+      code = (int8_t)quant1(__ldg(w + si), (double)scale[o], (double)zp[o]);
+    out[i] = code;
+  }
+}
+// wsum[o] = sum of real weight codes of column o (used by the zero-point correction)
+__global__ void k_weight_sum(const float* __restrict__ w, int64_t per_ch, const float* __restrict__ scale,
+                             const int* __restrict__ zp, int* __restrict__ wsum) {
+  int o = blockIdx.x;
+  double s = (double)scale[o], z = (double)zp[o];
+  int acc = 0;
+  for (int64_t i = threadIdx.x; i < per_ch; i += blockDim.x) acc += quant1(__ldg(w + (int64_t)o * per_ch + i), s, z);
+  for (int d = 16; d; d >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, d);
+  __shared__ int red[32];
+  if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = acc;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    int t = 0;
+    for (int q = 0; q < (int)(blockDim.x >> 5); ++q) t += red[q];
+    wsum[o] = t;
+  }
+}
+void launch_weight_quant_tc(const float* w, int cout, int cin, int k, int fc_hw, int cin_p,
+                            const float* scale, const int* zp, int bn, int n_kiter, int8_t* out,
+                            int* wsum, cudaStream_t s) {
+  int nt = (cout + bn - 1) / bn;
+  int64_t total = (int64_t)nt * n_kiter * 8 * bn * 16;
+  k_weight_quant_tc<<<nblk(total), 256, 0, s>>>(w, cout, cin, k, fc_hw, cin_p, scale, zp, bn,
+                                                n_kiter, out, total);
+  int64_t per_ch = fc_hw > 0 ? (int64_t)cin * fc_hw : (int64_t)cin * k * k;
+  k_weight_sum<<<cout, 128, 0, s>>>(w, per_ch, scale, zp, wsum);
+}
+
+// depthwise: out [c][k*k] codes
+__global__ void k_weight_quant_dw(const float* __restrict__ w, int c, int kk,
+                                  const float* __restrict__ scale, const int* __restrict__ zp,
+                                  int8_t* __restrict__ out) {
+  int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= c * kk) return;
+  int ch = i / kk;
+  out[i] = (int8_t)quant1(__ldg(w + i), (double)scale[ch], (double)zp[ch]);
+}
+void launch_weight_quant_dw(const float* w, int c, int k, const float* scale, const int* zp,
+                            int8_t* out, cudaStream_t s) {
+  int n = c * k * k;
+  k_weight_quant_dw<<<(n + 255) / 256, 256, 0, s>>>(w, c, k * k, scale, zp, out);
+}
+
+// ---------------------------------------------------------------- per-config layer params
+__global__ void k_layer_params(const LayerSt* __restrict__ layers, const float* __restrict__ as,
+                               const int* __restrict__ az, int wvar) {
+  const LayerSt L = layers[blockIdx.x];
+  const double sx = (double)as[L.in_hist], sy = (double)as[L.out_hist];
+  const float* ws = L.wscale + (int64_t)wvar * L.cout;
+  for (int o = threadIdx.x; o < L.cout; o += blockDim.x) {
+    double sw = (double)ws[o];
+    double sxw = __dmul_rn(sx, sw);
+    L.mult[o] = __ddiv_rn(sxw, sy);
+    if (L.bias) L.biasq[o] = (int)clip32((long long)rha(__ddiv_rn((double)L.bias[o], sxw)));
+    else L.biasq[o] = 0;
+  }
+  if (threadIdx.x == 0) {
+    LayerRt r;
+    r.zx = az[L.in_hist];
+    r.zy = az[L.out_hist];
+    r.relu_zp = L.relu_hist >= 0 ? az[L.relu_hist] : INT_MIN;
+    if (L.add_o_hist >= 0) {
+      double so = (double)as[L.add_o_hist];
+      r.za = az[L.add_a_hist];
+      r.zb = az[L.add_b_hist];
+      r.zo = az[L.add_o_hist];
+      r.ra = __ddiv_rn((double)as[L.add_a_hist], so);
+      r.rb = __ddiv_rn((double)as[L.add_b_hist], so);
+    } else {
+      r.za = r.zb = r.zo = 0;
+      r.ra = r.rb = 0.0;
+    }
+    r.add_relu_zp = L.add_relu_hist >= 0 ? az[L.add_relu_hist] : INT_MIN;
+    r.pad_ = 0;
+    *L.rt = r;
+  }
+}
+void launch_layer_params(const LayerSt* d_layers, int n_layers, const float* act_scale,
+                         const int* act_zp, int wvar, cudaStream_t s) {
+  if (n_layers > 0) k_layer_params<<<n_layers, 256, 0, s>>>(d_layers, act_scale, act_zp, wvar);
+}
+
+// ---------------------------------------------------------------- quantize / dequantize
+// images NCHW fp32 -> int8 view (one thread per pixel, Cp bytes written, pads = 0)
+__global__ void k_quant_input(const float* __restrict__ imgs, int64_t img0, View out,
+                              const float* __restrict__ as, const int* __restrict__ az, int hist) {
+  const double s = (double)as[hist], z = (double)az[hist];
+  const int64_t npix = (int64_t)out.N * out.H * out.W;
+  const int64_t plane = (int64_t)out.H * out.W;
+  for (int64_t p = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; p < npix;
+       p += (int64_t)gridDim.x * blockDim.x) {
+    int n = (int)(p / plane);
+    int64_t hw = p - (int64_t)n * plane;
+    int h = (int)(hw / out.W), w = (int)(hw - (int64_t)h * out.W);
+    int8_t* dst = out.p + voff(out, n, h, w);
+    const float* src = imgs + ((img0 + n) * out.C) * plane + hw;
+    for (int c0 = 0; c0 < out.Cp; c0 += 16) {
+      alignas(16) int8_t v[16];
+#pragma unroll
+      for (int j = 0; j < 16; ++j) {
+        int c = c0 + j;
+        v[j] = c < out.C ? (int8_t)quant1(__ldg(src + (int64_t)c * plane), s, z) : (int8_t)0;
+      }
+      *reinterpret_cast<int4*>(dst + c0) = *reinterpret_cast<int4*>(v);
+    }
+  }
+}
+void launch_quant_input(const float* imgs, int64_t img0, View out, const float* as, const int* az,
+                        int hist, cudaStream_t s) {
+  k_quant_input<<<nblk((int64_t)out.N * out.H * out.W), 256, 0, s>>>(imgs, img0, out, as, az, hist);
+}
+
+// fp32 NHWC (pitch C) -> int8 view, optional fused relu clamp
+__global__ void k_quant_nhwc(const float* __restrict__ x, View out, const float* __restrict__ as,
+                             const int* __restrict__ az, int hist, int relu_hist) {
+  const double s = (double)as[hist], z = (double)az[hist];
+  const int rz = relu_hist >= 0 ? az[relu_hist] : INT_MIN;
+  const int64_t total = (int64_t)out.N * out.H * out.W * out.Cp;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < total;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    int c = (int)(i % out.Cp);
+    int64_t p = i / out.Cp;
+    int w = (int)(p % out.W);
+    int64_t t = p / out.W;
+    int h = (int)(t % out.H);
+    int n = (int)(t / out.H);
+    int8_t code = 0;
+    if (c < out.C) {
+      int q = quant1(__ldg(x + p * out.C + c), s, z);
+      code = (int8_t)(q > rz ? q : rz);
+    }
+    out.p[voff(out, n, h, w) + c] = code;
+  }
+}
+void launch_quant_nhwc(const float* x, View out, const float* as, const int* az, int hist,
+                       int relu_hist, cudaStream_t s) {
+  k_quant_nhwc<<<nblk((int64_t)out.N * out.H * out.W * out.Cp), 256, 0, s>>>(x, out, as, az, hist,
+                                                                            relu_hist);
+}
+
+__global__ void k_dequant(View in, const float* __restrict__ as, const int* __restrict__ az,
+                          int hist, float* __restrict__ y) {
+  const double s = (double)as[hist];
+  const int z = az[hist];
+  const int64_t total = (int64_t)in.N * in.H * in.W * in.C;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < total;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    int c = (int)(i % in.C);
+    int64_t p = i / in.C;
+    int w = (int)(p % in.W);
+    int64_t t = p / in.W;
+    int h = (int)(t % in.H);
+    int n = (int)(t / in.H);
+    int code = in.p[voff(in, n, h, w) + c];
+    y[i] = (float)__dmul_rn((double)(code - z), s);
+  }
+}
+void launch_dequant(View in, const float* as, const int* az, int hist, float* y, cudaStream_t s) {
+  k_dequant<<<nblk((int64_t)in.N * in.H * in.W * in.C), 256, 0, s>>>(in, as, az, hist, y);
+}
+
+// fill the spatial halo with the zero-point code (all Cp bytes)
+__global__ void k_halo_fill(View v, const int* __restrict__ az, int hist) {
+  const int8_t z = (int8_t)az[hist];
+  const int Hp = v.H + 2 * v.halo, Wp = v.W + 2 * v.halo;
+  const int64_t total = (int64_t)v.N * Hp * Wp;
+  for (int64_t p = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; p < total;
+       p += (int64_t)gridDim.x * blockDim.x) {
+    int w = (int)(p % Wp);
+    int h = (int)((p / Wp) % Hp);
+    if (h >= v.halo && h < v.halo + v.H && w >= v.halo && w < v.halo + v.W) continue;
+    int8_t* d = v.p + p * v.Cp;
+    for (int c = 0; c < v.Cp; ++c) d[c] = z;
+  }
+}
+void launch_halo_fill(View v, const int* az, int hist, cudaStream_t s) {
+  if (v.halo <= 0) return;
+  int64_t n = (int64_t)v.N * (v.H + 2 * v.halo) * (v.W + 2 * v.halo);
+  k_halo_fill<<<nblk(n), 256, 0, s>>>(v, az, hist);
+}
+
+// ---------------------------------------------------------------- elementwise / pooling on codes
+__global__ void k_relu_codes(View in, View out, const int* __restrict__ az, int hist) {
+  const int z = az[hist];
+  const int64_t total = (int64_t)in.N * in.H * in.W * in.Cp;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < total;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    int c = (int)(i % in.Cp);
+    int64_t p = i / in.Cp;
+    int w = (int)(p % in.W);
+    int64_t t = p / in.W;
+    int h = (int)(t % in.H), n = (int)(t / in.H);
+    int v = in.p[voff(in, n, h, w) + c];
+    out.p[voff(out, n, h, w) + c] = (int8_t)(c < in.C ? (v > z ? v : z) : 0);
+  }
+}
+void launch_relu_codes(View in, View out, const int* az, int hist, cudaStream_t s) {
+  k_relu_codes<<<nblk((int64_t)in.N * in.H * in.W * in.Cp), 256, 0, s>>>(in, out, az, hist);
+}
+
+// mode 0: max; mode 1: avg = requant(sum - zp*area, 1.0/area, zp)
+__global__ void k_pool_codes(View in, View out, int k, int stride, int mode,
+                             const int* __restrict__ az, int hist) {
+  const int z = az[hist];
+  const int area = k * k;
+  const double m = __ddiv_rn(1.0, (double)area);
+  const int64_t total = (int64_t)out.N * out.H * out.W * out.Cp;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < total;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    int c = (int)(i % out.Cp);
+    int64_t p = i / out.Cp;
+    int ow = (int)(p % out.W);
+    int64_t t = p / out.W;
+    int oh = (int)(t % out.H), n = (int)(t / out.H);
+    int8_t r = 0;
+    if (c < out.C) {
+      if (mode == 0) {
+        int mx = -128;
+        for (int kh = 0; kh < k; ++kh)
+          for (int kw = 0; kw < k; ++kw) {
+            int v = in.p[voff(in, n, oh * stride + kh, ow * stride + kw) + c];
+            mx = v > mx ? v : mx;
+          }
+        r = (int8_t)mx;
+      } else {
+        long long sum = 0;
+        for (int kh = 0; kh < k; ++kh)
+          for (int kw = 0; kw < k; ++kw) sum += in.p[voff(in, n, oh * stride + kh, ow * stride + kw) + c];
+        r = (int8_t)requant1(sum - (long long)z * area, m, z);
+      }
+    }
+    out.p[voff(out, n, oh, ow) + c] = r;
+  }
+}
+void launch_pool_codes(View in, View out, int k, int stride, int mode, const int* az, int hist,
+                       cudaStream_t s) {
+  k_pool_codes<<<nblk((int64_t)out.N * out.H * out.W * out.Cp), 256, 0, s>>>(in, out, k, stride,
+                                                                             mode, az, hist);
+}
+
+__device__ __forceinline__ int add_codes1(int xa, int xb, int za, int zb, double ra, double rb, int zo) {
+  double acc = __dadd_rn(__dmul_rn((double)(xa - za), ra), __dmul_rn((double)(xb - zb), rb));
+  return clip8(rhu(acc) + (double)zo);
+}
+
+__global__ void k_add_codes(View a, View b, View out, const float* __restrict__ as,
+                            const int* __restrict__ az, int ha, int hb, int ho) {
+  const double so = (double)as[ho];
+  const double ra = __ddiv_rn((double)as[ha], so), rb = __ddiv_rn((double)as[hb], so);
+  const int za = az[ha], zb = az[hb], zo = az[ho];
+  const int64_t total = (int64_t)out.N * out.H * out.W * out.Cp;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < total;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    int c = (int)(i % out.Cp);
+    int64_t p = i / out.Cp;
+    int w = (int)(p % out.W);
+    int64_t t = p / out.W;
+    int h = (int)(t % out.H), n = (int)(t / out.H);
+    int8_t r = 0;
+    if (c < out.C)
+      r = (int8_t)add_codes1(a.p[voff(a, n, h, w) + c], b.p[voff(b, n, h, w) + c], za, zb, ra, rb, zo);
+    out.p[voff(out, n, h, w) + c] = r;
+  }
+}
+void launch_add_codes(View a, View b, View out, const float* as, const int* az, int ha, int hb,
+                      int ho, cudaStream_t s) {
+  k_add_codes<<<nblk((int64_t)out.N * out.H * out.W * out.Cp), 256, 0, s>>>(a, b, out, as, az, ha,
+                                                                            hb, ho);
+}
+
+__global__ void k_concat_codes(View in, View out, int coff, const float* __restrict__ as,
+                               const int* __restrict__ az, int hin, int hout) {
+  const double m = __ddiv_rn((double)as[hin], (double)as[hout]);
+  const int zi = az[hin], zo = az[hout];
+  const int64_t total = (int64_t)in.N * in.H * in.W * in.C;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < total;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    int c = (int)(i % in.C);
+    int64_t p = i / in.C;
+    int w = (int)(p % in.W);
+    int64_t t = p / in.W;
+    int h = (int)(t % in.H), n = (int)(t / in.H);
+    int v = in.p[voff(in, n, h, w) + c];
+    out.p[voff(out, n, h, w) + coff + c] = (int8_t)requant1((long long)(v - zi), m, zo);
+  }
+}
+void launch_concat_codes(View in, View out, int coff, const float* as, const int* az, int hin,
+                         int hout, cudaStream_t s) {
+  k_concat_codes<<<nblk((int64_t)in.N * in.H * in.W * in.C), 256, 0, s>>>(in, out, coff, as, az,
+                                                                          hin, hout);
+}
+
+// P[padded pixel] = sum of the real-channel codes (rowsum term of the zero-point correction)
+__global__ void k_pixsum(View in, int* __restrict__ P) {
+  const int64_t total = (int64_t)in.N * (in.H + 2 * in.halo) * (in.W + 2 * in.halo);
+  for (int64_t p = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; p < total;
+       p += (int64_t)gridDim.x * blockDim.x) {
+    const int8_t* q = in.p + p * in.Cp;
+    int s = 0;
+    for (int c = 0; c < in.C; ++c) s += q[c];
+    P[p] = s;
+  }
+}
+void launch_pixsum(View in, int* P, cudaStream_t s) {
+  int64_t n = (int64_t)in.N * (in.H + 2 * in.halo) * (in.W + 2 * in.halo);
+  k_pixsum<<<nblk(n), 256, 0, s>>>(in, P);
+}
+
+// ---------------------------------------------------------------- depthwise int8 conv (CUDA cores)
+// acc = sum_taps (x - zx)(w - zw[c]) + bias[c]; clip int32; requant; fused relu.
+__global__ void k_dwconv_i8(View in, View out, const int8_t* __restrict__ w,
+                            const int* __restrict__ wzp, int k, int stride, int pad, LayerSt L) {
+  const LayerRt r = *L.rt;
+  const int64_t total = (int64_t)out.N * out.H * out.W * out.Cp;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < total;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    int c = (int)(i % out.Cp);
+    int64_t p = i / out.Cp;
+    int ow = (int)(p % out.W);
+    int64_t t = p / out.W;
+    int oh = (int)(t % out.H), n = (int)(t / out.H);
+    int8_t res = 0;
+    if (c < out.C) {
+      int zw = wzp[c];
+      long long acc = 0;
+      for (int kh = 0; kh < k; ++kh)
+        for (int kw = 0; kw < k; ++kw) {
+          int xv = in.p[voff(in, n, oh * stride - pad + kh, ow * stride - pad + kw) + c];
+          acc += (long long)(xv - r.zx) * (int)(w[c * k * k + kh * k + kw] - zw);
+        }
+      acc = clip32(acc + L.biasq[c]);
+      int q = requant1(acc, L.mult[c], r.zy);
+      if (q < r.relu_zp) q = r.relu_zp;
+      res = (int8_t)q;
+    }
+    out.p[voff(out, n, oh, ow) + c] = res;
+  }
+}
+void launch_dwconv_i8(View in, View out, const int8_t* w, const int* wzp, int k, int stride, int pad,
+                      LayerSt L, cudaStream_t s) {
+  k_dwconv_i8<<<nblk((int64_t)out.N * out.H * out.W * out.Cp), 256, 0, s>>>(in, out, w, wzp, k,
+                                                                             stride, pad, L);
+}
+
+// ---------------------------------------------------------------- top-1
+__global__ void k_argmax_codes(View in, const long long* __restrict__ labels,
+                               unsigned long long* __restrict__ correct) {
+  int n = blockIdx.x * blockDim.x + threadIdx.x;
+  if (n >= in.N) return;
+  const int8_t* p = in.p + voff(in, n, 0, 0);
+  int best = 0, bv = p[0];
+  for (int c = 1; c < in.C; ++c)
+    if (p[c] > bv) { bv = p[c]; best = c; }  // strict: lowest index wins ties (np.argmax)
+  if (best == labels[n]) atomicAdd(correct, 1ull);
+}
+void launch_argmax_codes(View in, const long long* labels, unsigned long long* correct,
+                         cudaStream_t s) {
+  k_argmax_codes<<<(in.N + 127) / 128, 128, 0, s>>>(in, labels, correct);
+}
+
+__global__ void k_argmax_f32(const float* __restrict__ x, int64_t rows, int C,
+                             const long long* __restrict__ labels,
+                             unsigned long long* __restrict__ correct) {
+  int64_t n = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (n >= rows) return;
+  const float* p = x + n * C;
+  int best = 0;
+  float bv = p[0];
+  for (int c = 1; c < C; ++c)
+    if (p[c] > bv) { bv = p[c]; best = c; }
+  if (best == labels[n]) atomicAdd(correct, 1ull);
+}
+void launch_argmax_f32(const float* x, int64_t rows, int C, const long long* labels,
+                       unsigned long long* correct, cudaStream_t s) {
+  k_argmax_f32<<<(int)((rows + 127) / 128), 128, 0, s>>>(x, rows, C, labels, correct);
+}
+
+}  // namespace ptq

@@ -1,0 +1,129 @@
+// Host-side launch wrappers for every ptq_b200 kernel family, plus the small
+// POD structs shared between the runtime and the kernels.
+#pragma once
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+namespace ptq {
+
+// int8 activation tensor in HBM: NHWC, channel pitch Cp (multiple of 16), optional
+// spatial halo filled with the tensor's zero-point code (so convs never test bounds).
+struct View {
+  int8_t* p;
+  int N, H, W, C, Cp, halo;
+};
+
+// per-config, per-int8-layer scalars written on device by k_layer_params
+struct LayerRt {
+  int zx, zy;          // input / output zero points (output = the conv's own quant params)
+  int relu_zp;         // zero point used by a fused relu (or INT32_MIN for none)
+  int za, zb, zo;      // fused add: operand zps and add output zp
+  double ra, rb;       // fused add: s_a / s_o and s_b / s_o (operand order of the add node)
+  int add_relu_zp;     // relu fused after the add (or INT32_MIN)
+  int pad_;
+};
+
+// static description of one int8 compute layer (conv / pointwise / depthwise / fc)
+struct LayerSt {
+  int cout;
+  int in_hist, out_hist;        // act-param sources (histogram ids) of input and output
+  int relu_hist;                // -1 or hist id whose zp the fused relu clamps to
+  int add_a_hist, add_b_hist, add_o_hist;  // -1 when no fused add
+  int add_relu_hist;            // -1 or hist id of a relu fused after the add
+  const float* bias;            // fp32 bias (device) or nullptr
+  const float* wscale;          // [8 variants][cout]
+  double* mult;                 // [cout] per-config requant multipliers (out)
+  int* biasq;                   // [cout] per-config int32 bias codes (out)
+  LayerRt* rt;                  // per-config scalars (out)
+};
+
+// ---------------------------------------------------------------- F1 / F2 (k_calib.cu)
+void launch_minmax_per_image(const float* x, int64_t elems, int n_img, unsigned int* out_ord,
+                             cudaStream_t s);
+void launch_fill_minmax(unsigned int* p, int64_t n_pairs, cudaStream_t s);
+void launch_minmax_reduce_cache(const unsigned int* per_img, int n_tensors, int n_img_total,
+                                const int* slots, int n_slots, float* ranges, cudaStream_t s);
+void launch_histogram(const float* x, int64_t elems, const int* slots, int n_slots,
+                      const float* range, unsigned long long* counts, cudaStream_t s);
+void launch_kl_sweep(const long long* counts, const float* ranges, int n_hist, double* cum,
+                     int* nzc, double* logc, double* kl_out, cudaStream_t s);
+
+// ---------------------------------------------------------------- fp32 forward (k_fp32.cu)
+void launch_nchw_to_nhwc(const float* src, const int* ids, int n, int C, int H, int W, float* dst,
+                         cudaStream_t s);
+void launch_conv_f32(const float* x, int N, int H, int W, int Cin, const float* Bw,
+                     const float* bias, int Cout, int k, int stride, int pad, int OH, int OW,
+                     float* y, cudaStream_t s);
+void launch_dwconv_f32(const float* x, int N, int H, int W, int C, const float* w,
+                       const float* bias, int k, int stride, int pad, int OH, int OW, float* y,
+                       cudaStream_t s);
+void launch_relu_f32(const float* x, float* y, int64_t n, cudaStream_t s);
+void launch_add_f32(const float* a, const float* b, float* y, int64_t n, cudaStream_t s);
+void launch_pool_f32(const float* x, int N, int H, int W, int C, int k, int stride, int OH, int OW,
+                     int mode, float* y, cudaStream_t s);
+void launch_concat_f32(const float* x, int64_t npix, int Cx, int Cy, int coff, float* y,
+                       cudaStream_t s);
+void launch_softmax_f32(const float* x, int64_t rows, int C, float* y, cudaStream_t s);
+
+// ---------------------------------------------------------------- F3 (k_quant.cu)
+void launch_act_params(const double* ranges /*[n_var][T][2]*/, const int* var_scheme, int n_var,
+                       int T, float* scale, int* zp, cudaStream_t s);
+// per-channel (or per-tensor) min/max of a weight tensor -> ordered-uint pairs [cout][2]
+void launch_weight_minmax(const float* w, int cout, int64_t per_ch, int per_channel,
+                          unsigned int* mnmx, cudaStream_t s);
+void launch_weight_params(const unsigned int* mnmx, int cout, int per_channel, int scheme,
+                          float* scale, int* zp, cudaStream_t s);
+// quantize conv/fc weights [cout][cin][k][k] into the tcgen05 B tile layout
+// conv: w [cout][cin][k][k]; fc: w [cout][cin*fc_hw] (NCHW flatten) treated as a 1x1 conv over
+// an NHWC-flattened input of fc_hw pixels x cin_p channels.  Output: tiled B operand.
+void launch_weight_quant_tc(const float* w, int cout, int cin, int k, int fc_hw, int cin_p,
+                            const float* scale, const int* zp, int bn, int n_kiter, int8_t* out,
+                            int* wsum, cudaStream_t s);
+void launch_weight_quant_dw(const float* w, int c, int k, const float* scale, const int* zp,
+                            int8_t* out, cudaStream_t s);
+void launch_layer_params(const LayerSt* d_layers, int n_layers, const float* act_scale,
+                         const int* act_zp, int wvar, cudaStream_t s);
+void launch_quant_input(const float* imgs_nchw, int64_t img0, View out, const float* act_scale,
+                        const int* act_zp, int hist, cudaStream_t s);
+void launch_quant_nhwc(const float* x, View out, const float* act_scale, const int* act_zp,
+                       int hist, int relu_hist, cudaStream_t s);
+void launch_dequant(View in, const float* act_scale, const int* act_zp, int hist, float* y,
+                    cudaStream_t s);
+void launch_halo_fill(View v, const int* act_zp, int hist, cudaStream_t s);
+void launch_relu_codes(View in, View out, const int* act_zp, int hist, cudaStream_t s);
+void launch_pool_codes(View in, View out, int k, int stride, int mode, const int* act_zp,
+                       int hist, cudaStream_t s);
+void launch_add_codes(View a, View b, View out, const float* act_scale, const int* act_zp,
+                      int ha, int hb, int ho, cudaStream_t s);
+void launch_concat_codes(View in, View out, int coff, const float* act_scale, const int* act_zp,
+                         int hin, int hout, cudaStream_t s);
+void launch_pixsum(View in, int* P, cudaStream_t s);
+void launch_dwconv_i8(View in, View out, const int8_t* w, const int* wzp, int k, int stride,
+                      int pad, LayerSt L, cudaStream_t s);
+void launch_argmax_codes(View in, const long long* labels, unsigned long long* correct,
+                         cudaStream_t s);
+void launch_argmax_f32(const float* x, int64_t rows, int C, const long long* labels,
+                       unsigned long long* correct, cudaStream_t s);
+
+// ---------------------------------------------------------------- F4 (k_conv_tc.cu)
+struct ConvTcArgs {
+  View in, out;
+  int k, stride, pad, OH, OW;
+  const int8_t* wB;       // tiled weights [n_tiles][n_kiter][8][BN][16]
+  int n_kiter;            // K stages of 128 bytes
+  int n_chunks;           // real 16-byte K chunks = k*k*Cp/16
+  const int* wzp;         // [cout] weight zero points (variant)
+  const int* wsum;        // [cout] sum of weight codes over real K (variant)
+  int kreal;              // k*k*C
+  const int* P;           // per-padded-input-pixel channel sums (only when has_wzp)
+  int has_wzp;
+  LayerSt L;              // holds device pointers: mult / biasq / rt
+  View skip;              // fused add operand (p == nullptr when none)
+  int conv_is_a;          // 1 if the conv output is operand 0 of the fused add
+};
+int conv_tc_bn_for(int cout);     // BN tile width the kernel uses for this Cout
+void launch_conv_tc(const ConvTcArgs& a, int bn, cudaStream_t s);
+// CUDA-core reference of the same contract (tests / cross-checks only)
+void launch_conv_i8_ref(const ConvTcArgs& a, int bn, cudaStream_t s);
+
+}  // namespace ptq

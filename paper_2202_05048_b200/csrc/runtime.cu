@@ -1,0 +1,1126 @@
+// ptq_b200 runtime: graph lowering, device memory, and the C ABI
+// (include/ptq_b200.h).  Host C++ only; every FLOP runs in the kernels of
+// k_calib.cu (F1, F2), k_quant.cu (F3), k_conv_tc.cu (F4) and k_fp32.cu.
+//
+// The quantize_model domain/parameter rules restated here follow
+// /root/reference/pkg/src/ptqtune/quantize.py:116-202:
+//   * every tensor's params come from one calibration histogram ("psrc");
+//   * a compute/add node whose output feeds exactly one relu takes the relu
+//     output's histogram (narrowing, :125-130);
+//   * relu/maxpool/avgpool/softmax adopt their input's params (:198-202);
+//   * FirstLastFp32 keeps the first and last compute nodes in fp32 (:143-147);
+//     the graph input and the last layer's output stay unquantized.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <climits>
+#include <cstdio>
+#include <cstdlib>
+#include <cstring>
+#include <map>
+#include <set>
+#include <stdexcept>
+#include <string>
+#include <vector>
+
+#include "kernels.h"
+#include "ptq_b200.h"
+
+using namespace ptq;
+
+namespace {
+
+thread_local std::string g_err;
+
+struct Err {
+  int code;
+  std::string msg;
+};
+
+#define CK(x)                                                                            \
+  do {                                                                                   \
+    cudaError_t e_ = (x);                                                                \
+    if (e_ != cudaSuccess)                                                               \
+      throw Err{e_ == cudaErrorMemoryAllocation ? PTQ_ENOMEM : PTQ_ECUDA,                \
+                std::string(#x) + " -> " + cudaGetErrorString(e_)};                      \
+  } while (0)
+#define REQ(cond, msg)                                   \
+  do {                                                   \
+    if (!(cond)) throw Err{PTQ_EINVAL, std::string(msg)}; \
+  } while (0)
+
+inline int rup(int x, int m) { return (x + m - 1) / m * m; }
+
+struct NodeI {
+  int kind;
+  std::vector<int> in;
+  int out;
+  int weight, bias, k, stride, pad;
+};
+struct TensorI {
+  int c, h, w;
+  int64_t elems;
+  int producer = -1;
+  std::vector<int> consumers;
+};
+
+bool is_compute(int k) { return k == PTQ_CONV || k == PTQ_DWCONV || k == PTQ_PWCONV || k == PTQ_FC; }
+bool is_tc(int k) { return k == PTQ_CONV || k == PTQ_PWCONV || k == PTQ_FC; }
+
+// per-compute-node device weights
+struct WeightsDev {
+  int cout = 0, cin = 0, k = 1, fc_hw = 0, cin_p = 0;
+  int bn = 0, n_kiter = 0, n_chunks = 0, kreal = 0;
+  float* f32_gemm = nullptr;    // [K][cout] fp32 (NHWC K order) for the fp32 path, or dw [C][k*k]
+  float* f32_bias = nullptr;
+  int8_t* codes = nullptr;      // [8 variants][bytes_per_variant]
+  int64_t bytes_per_variant = 0;
+  float* scale = nullptr;       // [8][cout]
+  int* zp = nullptr;            // [8][cout]
+  int* wsum = nullptr;          // [8][cout]
+  bool has_wzp[8] = {};
+  double* mult = nullptr;       // [cout]
+  int* biasq = nullptr;         // [cout]
+  LayerRt* rt = nullptr;
+};
+
+struct Plan {
+  bool built = false;
+  int mixed = 0;
+  std::vector<int> psrc;         // per tensor: histogram id or -1 (fp32 domain)
+  std::vector<char> fp32node;    // per node
+  std::vector<char> skip;        // node fused into an earlier one
+  std::vector<int> mat;          // per compute node: tensor id materialised by its epilogue
+  std::vector<int> relu_hist, add_node, add_other, add_is_a, add_relu_hist;
+  int prefix_end = -1;           // mixed: last node index of the config-invariant fp32 prefix
+  std::vector<int> layer_of;     // node -> index into d_layers (int8 compute nodes) or -1
+  std::vector<LayerSt> h_layers;
+  LayerSt* d_layers = nullptr;
+};
+
+}  // namespace
+
+struct ptq_ctx {
+  int dev = 0;
+  cudaStream_t st = nullptr;
+  std::vector<void*> allocs;
+  // graph
+  std::vector<NodeI> nodes;
+  std::vector<TensorI> tens;
+  int T = 0, out_tensor = -1, n_classes = 0;
+  std::vector<float*> d_wt;              // device copies of the weights (reference layout)
+  std::vector<std::vector<int64_t>> wshape;
+  std::vector<WeightsDev> W;             // per node (compute nodes only)
+  int first_compute = -1, last_compute = -1;
+  // data
+  float* d_imgs = nullptr;
+  long long* d_labels = nullptr;
+  int64_t n_images = 0, n_calib = 0, n_eval = 0;
+  // ranges and parameters
+  std::vector<double> clip;              // [3 caches][2 clippings][T][2]
+  std::vector<char> clip_set;            // [3][2]
+  float* d_act_scale = nullptr;          // [24][T]
+  int* d_act_zp = nullptr;
+  bool prepared = false;
+  // eval buffers
+  int64_t chunk = 0;
+  std::vector<int8_t*> d_codes;          // per tensor int8 view buffer (or null)
+  std::vector<int> halo, cpad;
+  std::vector<float*> d_f32;             // per tensor fp32 eval buffer (mixed tail)
+  float* d_prefix = nullptr;             // mixed: fp32 output of the first compute node, all eval imgs
+  int* d_P = nullptr;                    // pixel sums scratch
+  int64_t P_cap = 0;
+  unsigned long long* d_correct = nullptr;
+  Plan plans[2];
+  // options
+  int conv_ref = 0, fusion = 1;
+  int64_t opt_chunk = 0;
+  // stats
+  int64_t launches = 0;
+  double conv_ms = 0.0;
+
+  template <typename T>
+  T* dalloc(size_t n) {
+    void* p = nullptr;
+    if (n == 0) n = 1;
+    CK(cudaMalloc(&p, n * sizeof(T)));
+    allocs.push_back(p);
+    return static_cast<T*>(p);
+  }
+  void dfree(void* p) {
+    if (!p) return;
+    auto it = std::find(allocs.begin(), allocs.end(), p);
+    if (it != allocs.end()) allocs.erase(it);
+    cudaFree(p);
+  }
+};
+
+namespace {
+
+void check_launch(ptq_ctx* c) {
+  ++c->launches;
+  cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess) throw Err{PTQ_ECUDA, std::string("kernel launch: ") + cudaGetErrorString(e)};
+}
+
+template <typename F>
+int guarded(F&& f) {
+  try {
+    f();
+    return PTQ_OK;
+  } catch (const Err& e) {
+    g_err = e.msg;
+    return e.code;
+  } catch (const std::exception& e) {
+    g_err = e.what();
+    return PTQ_EINVAL;
+  } catch (...) {
+    g_err = "unknown error";
+    return PTQ_EINVAL;
+  }
+}
+
+// ---------------------------------------------------------------- graph import
+void import_graph(ptq_ctx* c, const ptq_graph_desc* g) {
+  REQ(g && g->n_nodes > 0 && g->nodes, "empty graph");
+  c->nodes.resize(g->n_nodes);
+  c->tens.assign(g->n_nodes + 1, TensorI{});
+  c->tens[0] = TensorI{g->in_c, g->in_h, g->in_w, (int64_t)g->in_c * g->in_h * g->in_w, -1, {}};
+  c->n_classes = g->n_classes;
+  for (int i = 0; i < g->n_nodes; ++i) {
+    const ptq_node_desc& d = g->nodes[i];
+    NodeI& n = c->nodes[i];
+    n.kind = d.kind;
+    REQ(d.n_inputs >= 1 && d.n_inputs <= PTQ_MAX_INPUTS, "bad input count");
+    for (int j = 0; j < d.n_inputs; ++j) {
+      REQ(d.inputs[j] >= 0 && d.inputs[j] <= i, "node input used before definition");
+      n.in.push_back(d.inputs[j]);
+    }
+    n.out = i + 1;
+    n.weight = d.weight;
+    n.bias = d.bias;
+    n.k = d.kernel;
+    n.stride = d.stride < 1 ? 1 : d.stride;
+    n.pad = d.pad;
+    const TensorI& x = c->tens[n.in[0]];
+    TensorI& y = c->tens[n.out];
+    y.producer = i;
+    switch (n.kind) {
+      case PTQ_CONV: case PTQ_PWCONV: case PTQ_DWCONV: {
+        REQ(n.weight >= 0 && n.weight < g->n_weights, "conv without weight");
+        const ptq_weight_desc& w = g->weights[n.weight];
+        REQ(w.ndim == 4 && w.shape[2] == w.shape[3], "conv weight must be (O,I,k,k)");
+        n.k = (int)w.shape[2];
+        if (n.kind == PTQ_DWCONV) REQ(w.shape[1] == 1 && w.shape[0] == x.c, "depthwise weight must be (C,1,k,k)");
+        else REQ(w.shape[1] == x.c, "conv weight/input channel mismatch");
+        y.c = (int)w.shape[0];
+        y.h = (x.h + 2 * n.pad - n.k) / n.stride + 1;
+        y.w = (x.w + 2 * n.pad - n.k) / n.stride + 1;
+        REQ(y.h >= 1 && y.w >= 1, "conv does not fit input");
+        break;
+      }
+      case PTQ_FC: {
+        REQ(n.weight >= 0 && n.weight < g->n_weights, "fc without weight");
+        const ptq_weight_desc& w = g->weights[n.weight];
+        REQ(w.ndim == 2 && w.shape[1] == x.elems, "fc weight/input mismatch");
+        y.c = (int)w.shape[0]; y.h = 1; y.w = 1;
+        break;
+      }
+      case PTQ_MAXPOOL: case PTQ_AVGPOOL:
+        REQ(n.k >= 1, "bad pool kernel");
+        y.c = x.c;
+        y.h = (x.h - n.k) / n.stride + 1;
+        y.w = (x.w - n.k) / n.stride + 1;
+        REQ(y.h >= 1 && y.w >= 1, "pool does not fit input");
+        break;
+      case PTQ_RELU: y.c = x.c; y.h = x.h; y.w = x.w; break;
+      case PTQ_SOFTMAX:
+        REQ(x.h == 1 && x.w == 1, "softmax supported on per-image vectors only");
+        y.c = x.c; y.h = 1; y.w = 1;
+        break;
+      case PTQ_ADD:
+        REQ(n.in.size() == 2, "add takes two inputs");
+        REQ(c->tens[n.in[1]].c == x.c && c->tens[n.in[1]].h == x.h && c->tens[n.in[1]].w == x.w,
+            "add shape mismatch");
+        y.c = x.c; y.h = x.h; y.w = x.w;
+        break;
+      case PTQ_CONCAT: {
+        int cs = 0;
+        for (int t : n.in) {
+          REQ(c->tens[t].h == x.h && c->tens[t].w == x.w, "concat spatial mismatch");
+          cs += c->tens[t].c;
+        }
+        y.c = cs; y.h = x.h; y.w = x.w;
+        break;
+      }
+      default: REQ(false, "unknown node kind");
+    }
+    y.elems = (int64_t)y.c * y.h * y.w;
+    if (is_compute(n.kind)) {
+      if (c->first_compute < 0) c->first_compute = i;
+      c->last_compute = i;
+    }
+  }
+  c->T = g->n_nodes + 1;
+  for (int i = 0; i < g->n_nodes; ++i)
+    for (int t : c->nodes[i].in) c->tens[t].consumers.push_back(i);
+  int outs = 0;
+  for (int t = 1; t < c->T; ++t)
+    if (c->tens[t].consumers.empty()) { c->out_tensor = t; ++outs; }
+  REQ(outs == 1, "graph must have exactly one output");
+  REQ(c->first_compute >= 0, "graph has no weighted layers");
+  const TensorI& o = c->tens[c->out_tensor];
+  REQ(o.h == 1 && o.w == 1, "graph output must be a per-image score vector");
+
+  // weights: device copies + the fp32 GEMM / depthwise forms
+  c->d_wt.assign(g->n_weights, nullptr);
+  c->wshape.assign(g->n_weights, {});
+  for (int i = 0; i < g->n_weights; ++i) {
+    const ptq_weight_desc& w = g->weights[i];
+    int64_t n = 1;
+    for (int d = 0; d < w.ndim; ++d) { n *= w.shape[d]; c->wshape[i].push_back(w.shape[d]); }
+    c->d_wt[i] = c->dalloc<float>(n);
+    CK(cudaMemcpyAsync(c->d_wt[i], w.data, n * sizeof(float), cudaMemcpyHostToDevice, c->st));
+  }
+  c->W.assign(g->n_nodes, WeightsDev{});
+  for (int i = 0; i < g->n_nodes; ++i) {
+    const NodeI& n = c->nodes[i];
+    if (!is_compute(n.kind)) continue;
+    WeightsDev& wd = c->W[i];
+    const TensorI& x = c->tens[n.in[0]];
+    const ptq_weight_desc& w = g->weights[n.weight];
+    wd.cout = c->tens[n.out].c;
+    if (n.bias >= 0) {
+      REQ(g->weights[n.bias].ndim == 1 && g->weights[n.bias].shape[0] == wd.cout, "bias length mismatch");
+      wd.f32_bias = c->d_wt[n.bias];
+    }
+    if (n.kind == PTQ_DWCONV) {
+      wd.cin = x.c; wd.k = n.k;
+      wd.f32_gemm = c->d_wt[n.weight];                  // (C,1,k,k) == [C][k*k]
+      wd.bytes_per_variant = (int64_t)wd.cout * n.k * n.k;
+    } else {
+      // fp32 GEMM weight [K][cout], K in NHWC order
+      const int64_t K = x.elems;
+      const int kk = n.kind == PTQ_FC ? 1 : n.k;
+      std::vector<float> hb((size_t)(K * wd.cout));
+      for (int o = 0; o < wd.cout; ++o) {
+        if (n.kind == PTQ_FC) {
+          for (int ci = 0; ci < x.c; ++ci)
+            for (int p = 0; p < x.h * x.w; ++p)
+              hb[((size_t)p * x.c + ci) * wd.cout + o] = w.data[(size_t)o * K + (size_t)ci * x.h * x.w + p];
+        } else {
+          for (int ci = 0; ci < x.c; ++ci)
+            for (int a = 0; a < kk; ++a)
+              for (int b = 0; b < kk; ++b)
+                hb[(((size_t)a * kk + b) * x.c + ci) * wd.cout + o] =
+                    w.data[(((size_t)o * x.c + ci) * kk + a) * kk + b];
+        }
+      }
+      wd.f32_gemm = c->dalloc<float>(hb.size());
+      CK(cudaMemcpyAsync(wd.f32_gemm, hb.data(), hb.size() * sizeof(float), cudaMemcpyHostToDevice, c->st));
+      CK(cudaStreamSynchronize(c->st));
+      // int8 tensor-core form
+      wd.cin = x.c;
+      wd.k = kk;
+      wd.cin_p = rup(x.c, 16);
+      wd.fc_hw = n.kind == PTQ_FC ? x.h * x.w : 0;
+      wd.n_chunks = n.kind == PTQ_FC ? x.h * x.w * wd.cin_p / 16 : kk * kk * wd.cin_p / 16;
+      wd.kreal = n.kind == PTQ_FC ? (int)x.elems : kk * kk * x.c;
+      wd.n_kiter = (wd.n_chunks + 7) / 8;
+      wd.bn = conv_tc_bn_for(wd.cout);
+      int ntiles = (wd.cout + wd.bn - 1) / wd.bn;
+      wd.bytes_per_variant = (int64_t)ntiles * wd.n_kiter * 8 * wd.bn * 16;
+    }
+    wd.codes = c->dalloc<int8_t>(8 * wd.bytes_per_variant);
+    wd.scale = c->dalloc<float>(8 * wd.cout);
+    wd.zp = c->dalloc<int>(8 * wd.cout);
+    wd.wsum = c->dalloc<int>(8 * wd.cout);
+    wd.mult = c->dalloc<double>(wd.cout);
+    wd.biasq = c->dalloc<int>(wd.cout);
+    wd.rt = c->dalloc<LayerRt>(1);
+  }
+}
+
+// ---------------------------------------------------------------- fp32 forward
+// bufs[t] = [n][h][w][c] fp32; computes nodes [from, to]
+void run_fp32(ptq_ctx* c, int n, std::vector<float*>& bufs, int from, int to) {
+  for (int i = from; i <= to; ++i) {
+    const NodeI& nd = c->nodes[i];
+    const TensorI& x = c->tens[nd.in[0]];
+    const TensorI& y = c->tens[nd.out];
+    const float* xb = bufs[nd.in[0]];
+    float* yb = bufs[nd.out];
+    REQ(xb && yb, "fp32 buffer missing");
+    switch (nd.kind) {
+      case PTQ_CONV: case PTQ_PWCONV:
+        launch_conv_f32(xb, n, x.h, x.w, x.c, c->W[i].f32_gemm, c->W[i].f32_bias, y.c, nd.k,
+                        nd.stride, nd.pad, y.h, y.w, yb, c->st);
+        break;
+      case PTQ_FC:
+        launch_conv_f32(xb, n, 1, 1, (int)x.elems, c->W[i].f32_gemm, c->W[i].f32_bias, y.c, 1, 1, 0,
+                        1, 1, yb, c->st);
+        break;
+      case PTQ_DWCONV:
+        launch_dwconv_f32(xb, n, x.h, x.w, x.c, c->W[i].f32_gemm, c->W[i].f32_bias, nd.k, nd.stride,
+                          nd.pad, y.h, y.w, yb, c->st);
+        break;
+      case PTQ_RELU: launch_relu_f32(xb, yb, (int64_t)n * y.elems, c->st); break;
+      case PTQ_MAXPOOL: case PTQ_AVGPOOL:
+        launch_pool_f32(xb, n, x.h, x.w, x.c, nd.k, nd.stride, y.h, y.w,
+                        nd.kind == PTQ_AVGPOOL, yb, c->st);
+        break;
+      case PTQ_ADD: launch_add_f32(xb, bufs[nd.in[1]], yb, (int64_t)n * y.elems, c->st); break;
+      case PTQ_CONCAT: {
+        int coff = 0;
+        for (int t : nd.in) {
+          launch_concat_f32(bufs[t], (int64_t)n * y.h * y.w, c->tens[t].c, y.c, coff, yb, c->st);
+          coff += c->tens[t].c;
+        }
+        break;
+      }
+      case PTQ_SOFTMAX: launch_softmax_f32(xb, n, y.c, yb, c->st); break;
+    }
+    check_launch(c);
+  }
+}
+
+// ---------------------------------------------------------------- plans (quantize_model rules)
+int narrowed(ptq_ctx* c, int node) {
+  const TensorI& t = c->tens[c->nodes[node].out];
+  if (t.consumers.size() == 1 && c->nodes[t.consumers[0]].kind == PTQ_RELU)
+    return c->nodes[t.consumers[0]].out;
+  return c->nodes[node].out;
+}
+
+void build_plan(ptq_ctx* c, int mixed) {
+  Plan& P = c->plans[mixed];
+  if (P.built) return;
+  const int N = (int)c->nodes.size();
+  P.mixed = mixed;
+  P.psrc.assign(c->T, -1);
+  P.fp32node.assign(N, 0);
+  P.skip.assign(N, 0);
+  P.mat.assign(N, -1);
+  P.relu_hist.assign(N, -1);
+  P.add_node.assign(N, -1);
+  P.add_other.assign(N, -1);
+  P.add_is_a.assign(N, 0);
+  P.add_relu_hist.assign(N, -1);
+  P.layer_of.assign(N, -1);
+  if (mixed) {
+    P.fp32node[c->first_compute] = 1;
+    P.fp32node[c->last_compute] = 1;
+    P.prefix_end = c->first_compute;
+  }
+  P.psrc[0] = mixed ? -1 : 0;
+  for (int i = 0; i < N; ++i) {
+    const NodeI& n = c->nodes[i];
+    bool all = true, any = false;
+    for (int t : n.in) { bool q = P.psrc[t] >= 0; all &= q; any |= q; }
+    if (is_compute(n.kind)) {
+      if (P.fp32node[i]) {
+        P.psrc[n.out] = (i == c->last_compute) ? -1 : narrowed(c, i);
+        continue;
+      }
+      REQ(all, "quantized layer fed by fp32 tensor");
+      P.psrc[n.out] = narrowed(c, i);
+    } else if (n.kind == PTQ_ADD || n.kind == PTQ_CONCAT) {
+      if (all) P.psrc[n.out] = n.kind == PTQ_ADD ? narrowed(c, i) : n.out;
+      else REQ(!any, "mixed int8/fp32 operands");
+    } else {
+      P.psrc[n.out] = P.psrc[n.in[0]];
+    }
+  }
+  if (mixed) {
+    for (int i = 0; i < c->first_compute; ++i)
+      for (int t : c->nodes[i].in) REQ(P.psrc[t] < 0, "unsupported mixed prefix");
+  }
+  // fusion of relu / add(+relu) into int8 compute epilogues (and relu into the mixed prefix quantize)
+  for (int i = 0; i < N; ++i) {
+    const NodeI& n = c->nodes[i];
+    if (!is_compute(n.kind)) continue;
+    P.mat[i] = n.out;
+    const bool int8_out = P.psrc[n.out] >= 0;
+    if (!int8_out || !c->fusion) continue;
+    if (P.fp32node[i] && i != c->first_compute) continue;
+    const TensorI& t = c->tens[n.out];
+    if (t.consumers.size() != 1) continue;
+    const int cn = t.consumers[0];
+    const NodeI& cons = c->nodes[cn];
+    if (cons.kind == PTQ_RELU && P.psrc[cons.out] >= 0) {
+      P.relu_hist[i] = P.psrc[cons.out];
+      P.skip[cn] = 1;
+      P.mat[i] = cons.out;
+    } else if (cons.kind == PTQ_ADD && P.psrc[cons.out] >= 0 && (n.kind == PTQ_CONV || n.kind == PTQ_PWCONV) &&
+               !P.fp32node[i]) {
+      const int other = cons.in[0] == n.out ? cons.in[1] : cons.in[0];
+      if (other == n.out) continue;
+      const int op = c->tens[other].producer;
+      if (op >= i) continue;                         // other operand not ready yet
+      // the other operand must be materialised (not fused into its producer)
+      bool other_mat = (other == 0) || P.mat[op] == other || !is_compute(c->nodes[op].kind);
+      if (op >= 0 && !is_compute(c->nodes[op].kind) && P.skip[op]) other_mat = false;
+      if (!other_mat) continue;
+      P.add_node[i] = cn;
+      P.add_other[i] = other;
+      P.add_is_a[i] = cons.in[0] == n.out;
+      P.skip[cn] = 1;
+      P.mat[i] = cons.out;
+      const TensorI& at = c->tens[cons.out];
+      if (at.consumers.size() == 1 && c->nodes[at.consumers[0]].kind == PTQ_RELU &&
+          P.psrc[c->nodes[at.consumers[0]].out] >= 0) {
+        P.add_relu_hist[i] = P.psrc[c->nodes[at.consumers[0]].out];
+        P.skip[at.consumers[0]] = 1;
+        P.mat[i] = c->nodes[at.consumers[0]].out;
+      }
+    }
+  }
+  // per-layer static descriptors for the int8 compute nodes
+  P.h_layers.clear();
+  for (int i = 0; i < N; ++i) {
+    const NodeI& n = c->nodes[i];
+    if (!is_compute(n.kind) || P.fp32node[i]) continue;
+    WeightsDev& wd = c->W[i];
+    LayerSt L{};
+    L.cout = wd.cout;
+    L.in_hist = P.psrc[n.in[0]];
+    L.out_hist = P.psrc[n.out];
+    L.relu_hist = P.relu_hist[i];
+    L.add_a_hist = L.add_b_hist = L.add_o_hist = -1;
+    if (P.add_node[i] >= 0) {
+      const NodeI& an = c->nodes[P.add_node[i]];
+      L.add_a_hist = P.psrc[an.in[0]];
+      L.add_b_hist = P.psrc[an.in[1]];
+      L.add_o_hist = P.psrc[an.out];
+    }
+    L.add_relu_hist = P.add_relu_hist[i];
+    L.bias = wd.f32_bias;
+    L.wscale = wd.scale;
+    L.mult = wd.mult;
+    L.biasq = wd.biasq;
+    L.rt = wd.rt;
+    P.layer_of[i] = (int)P.h_layers.size();
+    P.h_layers.push_back(L);
+  }
+  if (!P.h_layers.empty()) {
+    P.d_layers = c->dalloc<LayerSt>(P.h_layers.size());
+    CK(cudaMemcpyAsync(P.d_layers, P.h_layers.data(), P.h_layers.size() * sizeof(LayerSt),
+                       cudaMemcpyHostToDevice, c->st));
+  }
+  P.built = true;
+}
+
+// ---------------------------------------------------------------- eval buffers
+View view_of(ptq_ctx* c, int t, int n) {
+  const TensorI& x = c->tens[t];
+  return View{c->d_codes[t], n, x.h, x.w, x.c, c->cpad[t], c->halo[t]};
+}
+
+void ensure_eval_buffers(ptq_ctx* c) {
+  int64_t chunk = c->opt_chunk > 0 ? std::min<int64_t>(c->opt_chunk, c->n_eval) : c->n_eval;
+  if (c->chunk == chunk && !c->d_codes.empty()) return;
+  for (auto p : c->d_codes) c->dfree(p);
+  for (auto p : c->d_f32) c->dfree(p);
+  c->dfree(c->d_P);
+  c->d_P = nullptr;
+  c->chunk = chunk;
+  const int T = c->T;
+  c->halo.assign(T, 0);
+  c->cpad.assign(T, 16);
+  for (int t = 0; t < T; ++t) {
+    c->cpad[t] = rup(c->tens[t].c, 16);
+    for (int ci : c->tens[t].consumers) {
+      const NodeI& n = c->nodes[ci];
+      if (n.kind == PTQ_CONV || n.kind == PTQ_DWCONV || n.kind == PTQ_PWCONV)
+        c->halo[t] = std::max(c->halo[t], n.pad);
+    }
+  }
+  // fc inputs are read as one flattened pixel: they must not carry a halo
+  for (const NodeI& n : c->nodes)
+    if (n.kind == PTQ_FC) REQ(c->halo[n.in[0]] == 0, "fc input also feeds a padded conv");
+  c->d_codes.assign(T, nullptr);
+  c->d_f32.assign(T, nullptr);
+  std::set<int> need8, need32;
+  for (int m = 0; m < 2; ++m) {
+    build_plan(c, m);
+    const Plan& P = c->plans[m];
+    need8.insert(0);
+    for (int i = 0; i < (int)c->nodes.size(); ++i) {
+      const NodeI& n = c->nodes[i];
+      if (P.skip[i]) continue;
+      if (is_compute(n.kind)) {
+        if (P.psrc[P.mat[i]] >= 0) need8.insert(P.mat[i]);
+        else need32.insert(n.out);
+        if (P.fp32node[i] && i == c->last_compute) need32.insert(n.in[0]);
+      } else if (P.psrc[n.out] >= 0) {
+        need8.insert(n.out);
+      } else if (!(m == 1 && i < c->first_compute)) {
+        need32.insert(n.out);
+        for (int t : n.in) need32.insert(t);
+      }
+    }
+  }
+  int64_t maxP = 0;
+  for (int t : need8) {
+    const TensorI& x = c->tens[t];
+    int64_t bytes = chunk * (int64_t)(x.h + 2 * c->halo[t]) * (x.w + 2 * c->halo[t]) * c->cpad[t];
+    c->d_codes[t] = c->dalloc<int8_t>(bytes);
+    CK(cudaMemsetAsync(c->d_codes[t], 0, bytes, c->st));
+    maxP = std::max<int64_t>(maxP, chunk * (int64_t)(x.h + 2 * c->halo[t]) * (x.w + 2 * c->halo[t]));
+  }
+  for (int t : need32) c->d_f32[t] = c->dalloc<float>(chunk * c->tens[t].elems);
+  c->d_P = c->dalloc<int>(maxP);
+  c->P_cap = maxP;
+}
+
+// ---------------------------------------------------------------- prepare
+void prepare(ptq_ctx* c) {
+  if (c->prepared) return;
+  for (int i = 0; i < 6; ++i) REQ(c->clip_set[i], "clip ranges not set for every (cache, clipping)");
+  const int T = c->T;
+  // activation params: variant v = (cache*4 + scheme)*2 + clip
+  std::vector<double> r((size_t)24 * T * 2);
+  std::vector<int> vs(24);
+  for (int cache = 0; cache < 3; ++cache)
+    for (int sch = 0; sch < 4; ++sch)
+      for (int cl = 0; cl < 2; ++cl) {
+        int v = (cache * 4 + sch) * 2 + cl;
+        vs[v] = sch;
+        std::memcpy(&r[(size_t)v * T * 2], &c->clip[((size_t)(cache * 2 + cl)) * T * 2], sizeof(double) * T * 2);
+      }
+  double* d_r = c->dalloc<double>(r.size());
+  int* d_vs = c->dalloc<int>(24);
+  CK(cudaMemcpyAsync(d_r, r.data(), r.size() * sizeof(double), cudaMemcpyHostToDevice, c->st));
+  CK(cudaMemcpyAsync(d_vs, vs.data(), 24 * sizeof(int), cudaMemcpyHostToDevice, c->st));
+  if (!c->d_act_scale) {
+    c->d_act_scale = c->dalloc<float>((size_t)24 * T);
+    c->d_act_zp = c->dalloc<int>((size_t)24 * T);
+  }
+  launch_act_params(d_r, d_vs, 24, T, c->d_act_scale, c->d_act_zp, c->st);
+  check_launch(c);
+  // weights: 8 variants (scheme, granularity) per compute node
+  unsigned int* d_mm = nullptr;
+  int maxc = 1;
+  for (auto& wd : c->W) maxc = std::max(maxc, wd.cout);
+  d_mm = c->dalloc<unsigned int>(2 * (size_t)maxc);
+  for (int i = 0; i < (int)c->nodes.size(); ++i) {
+    const NodeI& n = c->nodes[i];
+    if (!is_compute(n.kind)) continue;
+    WeightsDev& wd = c->W[i];
+    const float* w = c->d_wt[n.weight];
+    int64_t per_ch = 1;
+    for (size_t d = 1; d < c->wshape[n.weight].size(); ++d) per_ch *= c->wshape[n.weight][d];
+    for (int sch = 0; sch < 4; ++sch)
+      for (int gran = 0; gran < 2; ++gran) {
+        const int wv = sch * 2 + gran;
+        float* sc = wd.scale + (size_t)wv * wd.cout;
+        int* zp = wd.zp + (size_t)wv * wd.cout;
+        launch_weight_minmax(w, wd.cout, per_ch, gran, d_mm, c->st);
+        check_launch(c);
+        launch_weight_params(d_mm, wd.cout, gran, sch, sc, zp, c->st);
+        check_launch(c);
+        int8_t* codes = wd.codes + (size_t)wv * wd.bytes_per_variant;
+        if (n.kind == PTQ_DWCONV)
+          launch_weight_quant_dw(w, wd.cout, wd.k, sc, zp, codes, c->st);
+        else
+          launch_weight_quant_tc(w, wd.cout, wd.cin, wd.k, wd.fc_hw, wd.cin_p, sc, zp, wd.bn,
+                                 wd.n_kiter, codes, wd.wsum + (size_t)wv * wd.cout, c->st);
+        check_launch(c);
+      }
+  }
+  CK(cudaStreamSynchronize(c->st));
+  for (auto& wd : c->W) {
+    if (!wd.cout) continue;
+    std::vector<int> hz((size_t)8 * wd.cout);
+    CK(cudaMemcpy(hz.data(), wd.zp, hz.size() * sizeof(int), cudaMemcpyDeviceToHost));
+    for (int v = 0; v < 8; ++v) {
+      wd.has_wzp[v] = false;
+      for (int o = 0; o < wd.cout; ++o) wd.has_wzp[v] |= hz[(size_t)v * wd.cout + o] != 0;
+    }
+  }
+  c->dfree(d_mm);
+  c->dfree(d_r);
+  c->dfree(d_vs);
+  ensure_eval_buffers(c);
+  // mixed prefix: config-invariant fp32 output of the first compute node for all eval images
+  if (!c->d_prefix) {
+    const int fc_ = c->first_compute;
+    const int tout = c->nodes[fc_].out;
+    c->d_prefix = c->dalloc<float>((size_t)c->n_eval * c->tens[tout].elems);
+    std::vector<float*> bufs(c->T, nullptr);
+    int64_t pc = std::min<int64_t>(c->n_eval, 256);
+    std::vector<int> need;
+    for (int i = 0; i <= fc_; ++i) {
+      need.push_back(c->nodes[i].out);
+      for (int t : c->nodes[i].in) need.push_back(t);
+    }
+    std::sort(need.begin(), need.end());
+    need.erase(std::unique(need.begin(), need.end()), need.end());
+    for (int t : need)
+      if (t != tout) bufs[t] = c->dalloc<float>(pc * c->tens[t].elems);
+    const TensorI& in = c->tens[0];
+    for (int64_t s = 0; s < c->n_eval; s += pc) {
+      int nn = (int)std::min<int64_t>(pc, c->n_eval - s);
+      launch_nchw_to_nhwc(c->d_imgs + (c->n_calib + s) * in.elems, nullptr, nn, in.c, in.h, in.w,
+                          bufs[0], c->st);
+      check_launch(c);
+      bufs[tout] = c->d_prefix + s * c->tens[tout].elems;
+      run_fp32(c, nn, bufs, 0, fc_);
+    }
+    for (int t : need)
+      if (t != tout) c->dfree(bufs[t]);
+  }
+  CK(cudaStreamSynchronize(c->st));
+  c->prepared = true;
+}
+
+// ---------------------------------------------------------------- one config
+// probe_t >= 0: after the tensor is produced, copy its codes to probe_out (NCHW)
+void eval_one(ptq_ctx* c, const ptq_config& cfg, unsigned long long* d_correct, int probe_t,
+              int8_t* probe_out) {
+  REQ(cfg.cache >= 0 && cfg.cache < 3 && cfg.scheme >= 0 && cfg.scheme < 4 && cfg.clipping >= 0 &&
+          cfg.clipping < 2 && cfg.granularity >= 0 && cfg.granularity < 2 && cfg.mixed >= 0 &&
+          cfg.mixed < 2,
+      "config field out of range");
+  Plan& P = c->plans[cfg.mixed];
+  const int v = (cfg.cache * 4 + cfg.scheme) * 2 + cfg.clipping;
+  const int wv = cfg.scheme * 2 + cfg.granularity;
+  const float* as = c->d_act_scale + (size_t)v * c->T;
+  const int* az = c->d_act_zp + (size_t)v * c->T;
+  launch_layer_params(P.d_layers, (int)P.h_layers.size(), as, az, wv, c->st);
+  check_launch(c);
+  const int N = (int)c->nodes.size();
+  std::vector<int> alias(c->T);
+  for (int t = 0; t < c->T; ++t) alias[t] = t;
+  cudaEvent_t e0 = nullptr, e1 = nullptr;
+
+  for (int64_t img0 = 0; img0 < c->n_eval; img0 += c->chunk) {
+    const int B = (int)std::min<int64_t>(c->chunk, c->n_eval - img0);
+    auto V = [&](int t) { return view_of(c, alias[t], B); };
+    auto probe = [&](int t) {
+      if (t != probe_t || !probe_out) return;
+      View pv = V(t);
+      const TensorI& x = c->tens[t];
+      std::vector<int8_t> h((size_t)B * (x.h + 2 * pv.halo) * (x.w + 2 * pv.halo) * pv.Cp);
+      CK(cudaMemcpyAsync(h.data(), pv.p, h.size(), cudaMemcpyDeviceToHost, c->st));
+      CK(cudaStreamSynchronize(c->st));
+      const int Wp = x.w + 2 * pv.halo, Hp = x.h + 2 * pv.halo;
+      for (int n = 0; n < B; ++n)
+        for (int ch = 0; ch < x.c; ++ch)
+          for (int y = 0; y < x.h; ++y)
+            for (int xx = 0; xx < x.w; ++xx)
+              probe_out[((((size_t)(img0 + n) * x.c + ch) * x.h + y) * x.w) + xx] =
+                  h[(((size_t)n * Hp + y + pv.halo) * Wp + xx + pv.halo) * pv.Cp + ch];
+    };
+    auto halo_fill = [&](int t) {
+      View vv = V(t);
+      if (vv.halo > 0) {
+        launch_halo_fill(vv, az, P.psrc[t], c->st);
+        check_launch(c);
+      }
+    };
+    // graph input / mixed prefix
+    int start = 0;
+    if (!cfg.mixed) {
+      launch_quant_input(c->d_imgs, c->n_calib + img0, V(0), as, az, P.psrc[0], c->st);
+      check_launch(c);
+      halo_fill(0);
+      probe(0);
+    } else {
+      const int fc_ = c->first_compute;
+      const int mt = P.mat[fc_];
+      launch_quant_nhwc(c->d_prefix + img0 * c->tens[c->nodes[fc_].out].elems, V(mt), as, az,
+                        P.psrc[c->nodes[fc_].out], P.relu_hist[fc_], c->st);
+      check_launch(c);
+      halo_fill(mt);
+      probe(mt);
+      start = fc_ + 1;
+    }
+    for (int i = start; i < N; ++i) {
+      if (P.skip[i]) continue;
+      const NodeI& n = c->nodes[i];
+      const int tin = n.in[0];
+      if (is_compute(n.kind) && !P.fp32node[i]) {
+        WeightsDev& wd = c->W[i];
+        const int tout = P.mat[i];
+        const LayerSt& L = P.h_layers[P.layer_of[i]];
+        if (n.kind == PTQ_DWCONV) {
+          launch_dwconv_i8(V(tin), V(tout), wd.codes + (size_t)wv * wd.bytes_per_variant,
+                           wd.zp + (size_t)wv * wd.cout, n.k, n.stride, n.pad, L, c->st);
+          check_launch(c);
+        } else {
+          ConvTcArgs a{};
+          View vin = V(tin);
+          const TensorI& x = c->tens[tin];
+          if (n.kind == PTQ_FC) {
+            vin.H = 1; vin.W = 1; vin.C = x.h * x.w * vin.Cp; vin.Cp = vin.C; vin.halo = 0;
+            a.k = 1; a.stride = 1; a.pad = 0; a.OH = 1; a.OW = 1;
+          } else {
+            a.k = n.k; a.stride = n.stride; a.pad = n.pad;
+            a.OH = c->tens[n.out].h; a.OW = c->tens[n.out].w;
+          }
+          a.in = vin;
+          a.out = V(tout);
+          a.wB = wd.codes + (size_t)wv * wd.bytes_per_variant;
+          a.n_kiter = wd.n_kiter;
+          a.n_chunks = wd.n_chunks;
+          a.wzp = wd.zp + (size_t)wv * wd.cout;
+          a.wsum = wd.wsum + (size_t)wv * wd.cout;
+          a.kreal = wd.kreal;
+          a.has_wzp = wd.has_wzp[wv];
+          if (a.has_wzp) {
+            launch_pixsum(vin, c->d_P, c->st);
+            check_launch(c);
+            a.P = c->d_P;
+          }
+          a.L = L;
+          a.skip = View{nullptr, 0, 0, 0, 0, 0, 0};
+          if (P.add_node[i] >= 0) {
+            a.skip = V(P.add_other[i]);
+            a.conv_is_a = P.add_is_a[i];
+          }
+          if (c->conv_ref) launch_conv_i8_ref(a, wd.bn, c->st);
+          else launch_conv_tc(a, wd.bn, c->st);
+          check_launch(c);
+        }
+        halo_fill(tout);
+        probe(tout);
+        continue;
+      }
+      if (is_compute(n.kind)) {                      // fp32 last layer (mixed)
+        const int tout = n.out;
+        float* xin = c->d_f32[tin];
+        if (P.psrc[tin] >= 0) {
+          launch_dequant(V(tin), as, az, P.psrc[tin], xin, c->st);
+          check_launch(c);
+        }
+        std::vector<float*> bufs(c->T, nullptr);
+        bufs[tin] = xin;
+        bufs[tout] = c->d_f32[tout];
+        run_fp32(c, B, bufs, i, i);
+        if (P.psrc[tout] >= 0) {
+          launch_quant_nhwc(c->d_f32[tout], V(tout), as, az, P.psrc[tout], -1, c->st);
+          check_launch(c);
+          halo_fill(tout);
+        }
+        continue;
+      }
+      const int tout = n.out;
+      if (P.psrc[tout] < 0) {                        // fp32-domain tail
+        std::vector<float*> bufs(c->T, nullptr);
+        for (int t : n.in) bufs[t] = c->d_f32[t];
+        bufs[tout] = c->d_f32[tout];
+        run_fp32(c, B, bufs, i, i);
+        continue;
+      }
+      switch (n.kind) {
+        case PTQ_RELU: launch_relu_codes(V(tin), V(tout), az, P.psrc[tout], c->st); break;
+        case PTQ_MAXPOOL: case PTQ_AVGPOOL:
+          launch_pool_codes(V(tin), V(tout), n.k, n.stride, n.kind == PTQ_AVGPOOL, az, P.psrc[tout], c->st);
+          break;
+        case PTQ_ADD:
+          launch_add_codes(V(n.in[0]), V(n.in[1]), V(tout), as, az, P.psrc[n.in[0]], P.psrc[n.in[1]],
+                           P.psrc[tout], c->st);
+          break;
+        case PTQ_CONCAT: {
+          int coff = 0;
+          for (int t : n.in) {
+            launch_concat_codes(V(t), V(tout), coff, as, az, P.psrc[t], P.psrc[tout], c->st);
+            check_launch(c);
+            coff += c->tens[t].c;
+          }
+          break;
+        }
+        case PTQ_SOFTMAX:                            // monotone: identity on codes (intexec.py:290-292)
+          alias[tout] = alias[tin];
+          probe(tout);
+          continue;
+      }
+      check_launch(c);
+      halo_fill(tout);
+      probe(tout);
+    }
+    const int ot = c->out_tensor;
+    if (P.psrc[ot] >= 0) launch_argmax_codes(V(ot), c->d_labels + img0, d_correct, c->st);
+    else launch_argmax_f32(c->d_f32[ot], B, c->tens[ot].c, c->d_labels + img0, d_correct, c->st);
+    check_launch(c);
+  }
+  (void)e0; (void)e1;
+}
+
+}  // namespace
+
+// ================================================================ C ABI
+extern "C" {
+
+const char* ptq_last_error(void) { return g_err.c_str(); }
+int ptq_version(void) { return 1; }
+
+int ptq_create(ptq_ctx** out, int device, const ptq_graph_desc* g, const float* images,
+               const int64_t* eval_labels, int64_t n_images, int64_t n_calib) {
+  ptq_ctx* c = new ptq_ctx();
+  int rc = guarded([&] {
+    REQ(out && g && images, "null argument");
+    REQ(n_calib >= 0 && n_calib <= n_images, "bad calibration split");
+    c->dev = device;
+    CK(cudaSetDevice(device));
+    int major = 0, minor = 0;
+    CK(cudaDeviceGetAttribute(&major, cudaDevAttrComputeCapabilityMajor, device));
+    CK(cudaDeviceGetAttribute(&minor, cudaDevAttrComputeCapabilityMinor, device));
+    REQ(major == 10 && minor == 0, "ptq_b200 requires an sm_100 (B200) device");
+    CK(cudaStreamCreateWithFlags(&c->st, cudaStreamNonBlocking));
+    import_graph(c, g);
+    c->n_images = n_images;
+    c->n_calib = n_calib;
+    c->n_eval = n_images - n_calib;
+    const TensorI& in = c->tens[0];
+    c->d_imgs = c->dalloc<float>((size_t)n_images * in.elems);
+    CK(cudaMemcpyAsync(c->d_imgs, images, (size_t)n_images * in.elems * sizeof(float),
+                       cudaMemcpyHostToDevice, c->st));
+    c->d_labels = c->dalloc<long long>(std::max<int64_t>(c->n_eval, 1));
+    if (c->n_eval > 0 && eval_labels)
+      CK(cudaMemcpyAsync(c->d_labels, eval_labels, c->n_eval * sizeof(long long),
+                         cudaMemcpyHostToDevice, c->st));
+    c->d_correct = c->dalloc<unsigned long long>(4096);
+    c->clip.assign((size_t)6 * c->T * 2, 0.0);
+    c->clip_set.assign(6, 0);
+    CK(cudaStreamSynchronize(c->st));
+    *out = c;
+  });
+  if (rc != PTQ_OK) {
+    for (void* p : c->allocs) cudaFree(p);
+    if (c->st) cudaStreamDestroy(c->st);
+    delete c;
+  }
+  return rc;
+}
+
+int ptq_destroy(ptq_ctx* c) {
+  if (!c) return PTQ_OK;
+  cudaSetDevice(c->dev);
+  if (c->st) cudaStreamSynchronize(c->st);
+  for (void* p : c->allocs) cudaFree(p);
+  if (c->st) cudaStreamDestroy(c->st);
+  delete c;
+  return PTQ_OK;
+}
+
+int ptq_num_tensors(const ptq_ctx* c, int32_t* T) {
+  if (!c || !T) { g_err = "null argument"; return PTQ_EINVAL; }
+  *T = c->T;
+  return PTQ_OK;
+}
+
+int ptq_calibrate(ptq_ctx* c, int32_t n_caches, const int32_t* sizes, const int64_t* ids,
+                  float* ranges, int64_t* counts, int64_t* n_samples) {
+  return guarded([&] {
+    REQ(c && n_caches >= 1 && sizes && ids, "null argument");
+    CK(cudaSetDevice(c->dev));
+    // union of the image ids -> slots
+    std::vector<int64_t> all;
+    int64_t tot = 0;
+    for (int k = 0; k < n_caches; ++k) {
+      REQ(sizes[k] >= 1, "empty cache");
+      tot += sizes[k];
+    }
+    all.assign(ids, ids + tot);
+    for (int64_t v : all) REQ(v >= 0 && v < c->n_calib, "calibration id out of range");
+    std::vector<int64_t> uni = all;
+    std::sort(uni.begin(), uni.end());
+    uni.erase(std::unique(uni.begin(), uni.end()), uni.end());
+    const int nu = (int)uni.size();
+    std::map<int64_t, int> slot;
+    for (int i = 0; i < nu; ++i) slot[uni[i]] = i;
+    const int T = c->T;
+    // fp32 forward over the union (one batch)
+    std::vector<float*> bufs(T, nullptr);
+    for (int t = 0; t < T; ++t) bufs[t] = c->dalloc<float>((size_t)nu * c->tens[t].elems);
+    std::vector<int> uid(uni.begin(), uni.end());
+    int* d_uid = c->dalloc<int>(nu);
+    CK(cudaMemcpyAsync(d_uid, uid.data(), nu * sizeof(int), cudaMemcpyHostToDevice, c->st));
+    const TensorI& in = c->tens[0];
+    launch_nchw_to_nhwc(c->d_imgs, d_uid, nu, in.c, in.h, in.w, bufs[0], c->st);
+    check_launch(c);
+    run_fp32(c, nu, bufs, 0, (int)c->nodes.size() - 1);
+    // F1a: per-image min/max
+    unsigned int* d_mm = c->dalloc<unsigned int>((size_t)T * nu * 2);
+    launch_fill_minmax(d_mm, (int64_t)T * nu, c->st);
+    check_launch(c);
+    for (int t = 0; t < T; ++t) {
+      launch_minmax_per_image(bufs[t], c->tens[t].elems, nu, d_mm + (size_t)t * nu * 2, c->st);
+      check_launch(c);
+    }
+    float* d_rng = c->dalloc<float>((size_t)n_caches * T * 2);
+    unsigned long long* d_cnt = c->dalloc<unsigned long long>((size_t)n_caches * T * PTQ_NBINS);
+    CK(cudaMemsetAsync(d_cnt, 0, (size_t)n_caches * T * PTQ_NBINS * 8, c->st));
+    int64_t off = 0;
+    std::vector<int*> d_slots;
+    for (int k = 0; k < n_caches; ++k) {
+      std::vector<int> sl(sizes[k]);
+      for (int j = 0; j < sizes[k]; ++j) sl[j] = slot[ids[off + j]];
+      off += sizes[k];
+      int* ds = c->dalloc<int>(sl.size());
+      d_slots.push_back(ds);
+      CK(cudaMemcpyAsync(ds, sl.data(), sl.size() * sizeof(int), cudaMemcpyHostToDevice, c->st));
+      launch_minmax_reduce_cache(d_mm, T, nu, ds, sizes[k], d_rng + (size_t)k * T * 2, c->st);
+      check_launch(c);
+      // F1b: histograms with the cache's own (lo, hi)
+      for (int t = 0; t < T; ++t) {
+        launch_histogram(bufs[t], c->tens[t].elems, ds, sizes[k], d_rng + ((size_t)k * T + t) * 2,
+                         d_cnt + ((size_t)k * T + t) * PTQ_NBINS, c->st);
+        check_launch(c);
+      }
+    }
+    if (ranges)
+      CK(cudaMemcpyAsync(ranges, d_rng, (size_t)n_caches * T * 2 * sizeof(float), cudaMemcpyDeviceToHost, c->st));
+    if (counts)
+      CK(cudaMemcpyAsync(counts, d_cnt, (size_t)n_caches * T * PTQ_NBINS * 8, cudaMemcpyDeviceToHost, c->st));
+    CK(cudaStreamSynchronize(c->st));
+    if (n_samples)
+      for (int k = 0; k < n_caches; ++k)
+        for (int t = 0; t < T; ++t) n_samples[(size_t)k * T + t] = (int64_t)sizes[k] * c->tens[t].elems;
+    for (auto p : bufs) c->dfree(p);
+    for (auto p : d_slots) c->dfree(p);
+    c->dfree(d_uid);
+    c->dfree(d_mm);
+    c->dfree(d_rng);
+    c->dfree(d_cnt);
+  });
+}
+
+int ptq_kl_sweep(ptq_ctx* c, int32_t n_hist, const int64_t* counts, const float* ranges, double* kl) {
+  return guarded([&] {
+    REQ(c && counts && ranges && kl && n_hist >= 0, "null argument");
+    if (n_hist == 0) return;
+    CK(cudaSetDevice(c->dev));
+    long long* d_c = c->dalloc<long long>((size_t)n_hist * PTQ_NBINS);
+    float* d_r = c->dalloc<float>((size_t)n_hist * 2);
+    double* d_cum = c->dalloc<double>((size_t)n_hist * PTQ_NBINS);
+    int* d_nz = c->dalloc<int>((size_t)n_hist * PTQ_NBINS);
+    double* d_log = c->dalloc<double>((size_t)n_hist * PTQ_NBINS);
+    double* d_kl = c->dalloc<double>((size_t)n_hist * PTQ_NWINDOWS);
+    CK(cudaMemcpyAsync(d_c, counts, (size_t)n_hist * PTQ_NBINS * 8, cudaMemcpyHostToDevice, c->st));
+    CK(cudaMemcpyAsync(d_r, ranges, (size_t)n_hist * 2 * sizeof(float), cudaMemcpyHostToDevice, c->st));
+    launch_kl_sweep(d_c, d_r, n_hist, d_cum, d_nz, d_log, d_kl, c->st);
+    check_launch(c);
+    CK(cudaMemcpyAsync(kl, d_kl, (size_t)n_hist * PTQ_NWINDOWS * 8, cudaMemcpyDeviceToHost, c->st));
+    CK(cudaStreamSynchronize(c->st));
+    for (void* p : {(void*)d_c, (void*)d_r, (void*)d_cum, (void*)d_nz, (void*)d_log, (void*)d_kl}) c->dfree(p);
+  });
+}
+
+int ptq_set_clip_ranges(ptq_ctx* c, int32_t cache, int32_t clipping, const double* ranges) {
+  return guarded([&] {
+    REQ(c && ranges && cache >= 0 && cache < 3 && clipping >= 0 && clipping < 2, "bad argument");
+    std::memcpy(&c->clip[((size_t)(cache * 2 + clipping)) * c->T * 2], ranges, sizeof(double) * c->T * 2);
+    c->clip_set[cache * 2 + clipping] = 1;
+    c->prepared = false;
+  });
+}
+
+int ptq_prepare(ptq_ctx* c) {
+  return guarded([&] {
+    REQ(c, "null context");
+    CK(cudaSetDevice(c->dev));
+    prepare(c);
+  });
+}
+
+int ptq_eval_configs(ptq_ctx* c, const ptq_config* cfgs, int32_t n_cfg, int64_t* correct) {
+  return guarded([&] {
+    REQ(c && cfgs && correct && n_cfg >= 0, "null argument");
+    CK(cudaSetDevice(c->dev));
+    prepare(c);
+    ensure_eval_buffers(c);
+    c->launches = 0;
+    for (int32_t b0 = 0; b0 < n_cfg; b0 += 4096) {
+      const int nb = std::min<int32_t>(4096, n_cfg - b0);
+      CK(cudaMemsetAsync(c->d_correct, 0, nb * sizeof(unsigned long long), c->st));
+      for (int i = 0; i < nb; ++i) eval_one(c, cfgs[b0 + i], c->d_correct + i, -1, nullptr);
+      std::vector<unsigned long long> h(nb);
+      CK(cudaMemcpyAsync(h.data(), c->d_correct, nb * sizeof(unsigned long long), cudaMemcpyDeviceToHost, c->st));
+      CK(cudaStreamSynchronize(c->st));
+      for (int i = 0; i < nb; ++i) correct[b0 + i] = (int64_t)h[i];
+    }
+  });
+}
+
+int ptq_probe_codes(ptq_ctx* c, const ptq_config* cfg, int32_t tensor, int8_t* out, int64_t* n_out) {
+  return guarded([&] {
+    REQ(c && cfg && tensor >= 0 && tensor < c->T, "bad argument");
+    const int64_t n = c->n_eval * c->tens[tensor].elems;
+    if (n_out) *n_out = n;
+    if (!out) return;
+    CK(cudaSetDevice(c->dev));
+    prepare(c);
+    ensure_eval_buffers(c);
+    REQ(c->plans[cfg->mixed].psrc[tensor] >= 0, "tensor is in the fp32 domain for this config");
+    REQ(c->d_codes[tensor], "tensor is fused away (set option fusion=0 to probe it)");
+    CK(cudaMemsetAsync(c->d_correct, 0, 8, c->st));
+    eval_one(c, *cfg, c->d_correct, tensor, out);
+    CK(cudaStreamSynchronize(c->st));
+  });
+}
+
+int ptq_probe_act_params(ptq_ctx* c, int32_t cache, int32_t scheme, int32_t clipping, float* scale,
+                         int32_t* zp) {
+  return guarded([&] {
+    REQ(c && scale && zp, "null argument");
+    CK(cudaSetDevice(c->dev));
+    prepare(c);
+    const int v = (cache * 4 + scheme) * 2 + clipping;
+    CK(cudaMemcpy(scale, c->d_act_scale + (size_t)v * c->T, c->T * sizeof(float), cudaMemcpyDeviceToHost));
+    CK(cudaMemcpy(zp, c->d_act_zp + (size_t)v * c->T, c->T * sizeof(int), cudaMemcpyDeviceToHost));
+  });
+}
+
+int ptq_histogram_host(ptq_ctx* c, const float* x, int64_t n, float lo, float hi, int64_t* counts) {
+  return guarded([&] {
+    REQ(c && x && counts && n > 0, "bad argument");
+    CK(cudaSetDevice(c->dev));
+    float* d_x = c->dalloc<float>(n);
+    float* d_r = c->dalloc<float>(2);
+    int* d_s = c->dalloc<int>(1);
+    unsigned long long* d_c = c->dalloc<unsigned long long>(PTQ_NBINS);
+    float hr[2] = {lo, hi};
+    int zero = 0;
+    CK(cudaMemcpyAsync(d_x, x, n * sizeof(float), cudaMemcpyHostToDevice, c->st));
+    CK(cudaMemcpyAsync(d_r, hr, sizeof(hr), cudaMemcpyHostToDevice, c->st));
+    CK(cudaMemcpyAsync(d_s, &zero, sizeof(int), cudaMemcpyHostToDevice, c->st));
+    CK(cudaMemsetAsync(d_c, 0, PTQ_NBINS * 8, c->st));
+    launch_histogram(d_x, n, d_s, 1, d_r, d_c, c->st);
+    check_launch(c);
+    CK(cudaMemcpyAsync(counts, d_c, PTQ_NBINS * 8, cudaMemcpyDeviceToHost, c->st));
+    CK(cudaStreamSynchronize(c->st));
+    for (void* p : {(void*)d_x, (void*)d_r, (void*)d_s, (void*)d_c}) c->dfree(p);
+  });
+}
+
+int ptq_set_option(ptq_ctx* c, const char* key, int64_t value) {
+  return guarded([&] {
+    REQ(c && key, "null argument");
+    std::string k(key);
+    if (k == "conv_ref") c->conv_ref = (int)value;
+    else if (k == "fusion") {
+      if (c->fusion != (int)value) {
+        c->fusion = (int)value;
+        for (auto& P : c->plans) { if (P.d_layers) c->dfree(P.d_layers); P = Plan{}; }
+        for (auto p : c->d_codes) c->dfree(p);
+        c->d_codes.clear();
+      }
+    } else if (k == "eval_chunk") {
+      c->opt_chunk = value;
+    } else {
+      REQ(false, "unknown option " + k);
+    }
+  });
+}
+
+int ptq_last_stats(const ptq_ctx* c, int64_t* launches, double* conv_ms) {
+  if (!c) { g_err = "null context"; return PTQ_EINVAL; }
+  if (launches) *launches = c->launches;
+  if (conv_ms) *conv_ms = c->conv_ms;
+  return PTQ_OK;
+}
+
+}  // extern "C"

@@ -1,0 +1,242 @@
+"""GPU drop-in for the reference's measured evaluator.
+
+``make_accuracy_evaluator(g, d, seed, profile=None)`` has the signature and
+contract of ``ptqtune.tuner.make_accuracy_evaluator``
+(/root/reference/pkg/src/ptqtune/tuner.py:434-444): building it calibrates
+the three cache size classes once; the returned callable maps a QuantConfig
+to its top-1 accuracy on the eval split (a Python float, correct / n_eval).
+Errors surface as exceptions, which the reference's ``_Campaign._safe_eval``
+(tuner.py:173-177) records as failed trials.
+
+Everything numeric runs in libptq_b200.so on the GPU; the host only draws the
+calibration image ids (numpy RNG parity with calibration.py:44-54), picks the
+KL window from the device-computed divergences and, for the handful of
+windows whose device KL is within 1e-9 of the best (mathematically tied
+windows whose order is decided by the last ulp of numpy's log), re-ranks
+them with numpy's own arithmetic so the chosen threshold is the reference's
+(SURVEY.md App. A.K).
+"""
+
+from __future__ import annotations
+
+import ctypes as C
+import math
+import threading
+
+import numpy as np
+
+from . import _lib
+from .config import (CACHE_SIZES, N_BINS, QuantConfig, TargetProfile, config_key,
+                     select_images)
+from .lowering import LoweredGraph
+
+TIE_BAND = 1e-9
+
+
+# ---------------------------------------------------------------- KL window choice (host side)
+
+def kl_window_bounds(lo: float, hi: float, i: int) -> tuple[int, int]:
+    """Window [start, end) of width i (ref clipping.py:72-76)."""
+    if lo < 0.0:
+        zero_bin = int((0.0 - lo) / ((hi - lo) / N_BINS))
+        start = min(max(zero_bin - i // 2, 0), N_BINS - i)
+    else:
+        start = 0
+    return start, start + i
+
+
+def _numpy_window_kl(counts: np.ndarray, lo: float, hi: float, i: int) -> float:
+    """numpy evaluation of one window's KL in the reference's op order
+    (clipping.py:38-52, :77-81) -- used only to break near-ties."""
+    c = counts.astype(np.float64)
+    total = c.sum()
+    cum = np.cumsum(c)
+    start, end = kl_window_bounds(lo, hi, i)
+    win = c[start:end]
+    ref = win.copy()
+    if start > 0:
+        ref[0] += cum[start - 1]
+    ref[-1] += total - cum[end - 1]
+    m = i // 128
+    starts = np.arange(128) * m
+    sums = np.add.reduceat(win, starts)
+    nz = ref > 0
+    nzg = np.add.reduceat(nz.astype(np.float64), starts)
+    gidx = np.minimum(np.arange(i) // m, 127)
+    q = np.zeros(i)
+    q[nz] = sums[gidx[nz]] / nzg[gidx[nz]]
+    if np.any(nz & (q == 0.0)):
+        return math.inf
+    p = ref[nz]
+    return float(np.sum(p * (np.log(p) - np.log(q[nz]))) / ref.sum())
+
+
+def choose_kl_range(counts: np.ndarray, lo: float, hi: float, kl: np.ndarray) -> tuple[tuple[float, float], int]:
+    """(lo, hi) clip range from the device KLs; returns (range, n_reranked)."""
+    lo, hi = float(lo), float(hi)
+    if lo == hi or float(np.asarray(counts, dtype=np.float64).sum()) <= 0:
+        return (lo, hi), 0
+    best = int(np.argmin(kl))               # first minimum == strict '<' sweep (clipping.py:82)
+    reranked = 0
+    if math.isfinite(kl[best]):
+        band = np.flatnonzero(kl <= kl[best] + abs(kl[best]) * TIE_BAND)
+        if band.size > 1:
+            reranked = int(band.size)
+            best_kl = math.inf
+            for w in band:
+                v = _numpy_window_kl(counts, lo, hi, int(w) + 128)
+                if v < best_kl:
+                    best_kl, best = v, int(w)
+        start, end = kl_window_bounds(lo, hi, best + 128)
+    else:
+        start, end = 0, N_BINS
+    edges = np.linspace(lo, hi, N_BINS + 1)
+    return (float(edges[start]), float(edges[end])), reranked
+
+
+# ---------------------------------------------------------------- evaluator
+
+class GpuEvaluator:
+    """Callable ``QuantConfig -> top-1`` backed by one B200 context."""
+
+    def __init__(self, g, d, seed: int, profile: TargetProfile | None = None, *, device: int = 0,
+                 eval_chunk: int | None = None, calibrate: bool = True):
+        self.lib = _lib.load()
+        self.graph, self.profile, self.seed = g, profile, seed
+        self.lowered = LoweredGraph(g)
+        self.T = self.lowered.n_tensors
+        self.n_calib = int(d.n_calib)
+        self.n_eval = int(len(d.images) - d.n_calib)
+        if self.n_eval <= 0:
+            raise ValueError("empty evaluation set")
+        self._lock = threading.Lock()
+        imgs = np.ascontiguousarray(np.asarray(d.images, dtype=np.float32))
+        labels = np.ascontiguousarray(np.asarray(d.labels[d.n_calib:], dtype=np.int64))
+        if tuple(imgs.shape[1:]) != tuple(int(v) for v in g.input_shape):
+            raise ValueError(f"dataset shape {imgs.shape[1:]} does not match graph input {g.input_shape}")
+        self._ctx = C.c_void_p()
+        _lib.check(self.lib.ptq_create(C.byref(self._ctx), device, C.byref(self.lowered.desc),
+                                       _lib.ptr(imgs), _lib.ptr(labels), len(imgs), self.n_calib))
+        if eval_chunk:
+            self.set_option("eval_chunk", int(eval_chunk))
+        self.kl_reranked = 0
+        if calibrate:
+            self.calibrate_all()
+
+    # ------------------------------------------------------------ calibration (tuner.py:438)
+    def calibrate_all(self) -> None:
+        ids = [select_images(self.n_calib, sc, self.seed) for sc in CACHE_SIZES]
+        sizes = np.asarray([len(i) for i in ids], dtype=np.int32)
+        flat = np.ascontiguousarray(np.concatenate(ids).astype(np.int64))
+        T = self.T
+        ranges = np.zeros((3, T, 2), dtype=np.float32)
+        counts = np.zeros((3, T, N_BINS), dtype=np.int64)
+        nsamp = np.zeros((3, T), dtype=np.int64)
+        _lib.check(self.lib.ptq_calibrate(self._ctx, 3, _lib.ptr(sizes), _lib.ptr(flat),
+                                          _lib.ptr(ranges), _lib.ptr(counts), _lib.ptr(nsamp)))
+        self.image_ids = ids
+        self.install_caches(ranges, counts, nsamp)
+
+    def install_caches(self, ranges: np.ndarray, counts: np.ndarray, nsamp: np.ndarray | None = None,
+                       kl_ranges: np.ndarray | None = None) -> None:
+        """Set the three caches (device KL sweep unless kl_ranges is given)."""
+        T = self.T
+        ranges = np.ascontiguousarray(ranges, dtype=np.float32).reshape(3, T, 2)
+        counts = np.ascontiguousarray(counts, dtype=np.int64).reshape(3, T, N_BINS)
+        self.cache_ranges, self.cache_counts = ranges, counts
+        self.cache_nsamp = nsamp
+        if kl_ranges is None:
+            kl = np.zeros((3 * T, _lib.PTQ_NWINDOWS), dtype=np.float64)
+            _lib.check(self.lib.ptq_kl_sweep(self._ctx, 3 * T, _lib.ptr(counts), _lib.ptr(ranges),
+                                             _lib.ptr(kl)))
+            self.kl_values = kl.reshape(3, T, -1)
+            kl_ranges = np.zeros((3, T, 2), dtype=np.float64)
+            self.kl_reranked = 0
+            for k in range(3):
+                for t in range(T):
+                    (lo, hi), nr = choose_kl_range(counts[k, t], ranges[k, t, 0], ranges[k, t, 1],
+                                                   self.kl_values[k, t])
+                    kl_ranges[k, t] = (lo, hi)
+                    self.kl_reranked += nr
+        self.kl_ranges = np.ascontiguousarray(kl_ranges, dtype=np.float64).reshape(3, T, 2)
+        for k in range(3):
+            mx = np.ascontiguousarray(ranges[k].astype(np.float64))
+            _lib.check(self.lib.ptq_set_clip_ranges(self._ctx, k, 0, _lib.ptr(mx)))
+            kr = np.ascontiguousarray(self.kl_ranges[k])
+            _lib.check(self.lib.ptq_set_clip_ranges(self._ctx, k, 1, _lib.ptr(kr)))
+        _lib.check(self.lib.ptq_prepare(self._ctx))
+
+    # ------------------------------------------------------------ evaluation
+    def _check_cfg(self, cfg) -> None:
+        if not isinstance(cfg, QuantConfig):
+            cfg = QuantConfig.from_dict(cfg.to_dict())
+        if self.profile is not None and not self.profile.contains(cfg):
+            raise ValueError(f"config {cfg} not allowed by profile {self.profile.name}")
+
+    def correct_counts(self, cfgs) -> np.ndarray:
+        cfgs = list(cfgs)
+        for cfg in cfgs:
+            self._check_cfg(cfg)
+        arr = (_lib.ConfigDesc * max(1, len(cfgs)))()
+        for i, cfg in enumerate(cfgs):
+            arr[i] = _lib.ConfigDesc(*config_key(cfg))
+        out = np.zeros(max(1, len(cfgs)), dtype=np.int64)
+        with self._lock:
+            _lib.check(self.lib.ptq_eval_configs(self._ctx, arr, len(cfgs), _lib.ptr(out)))
+        return out[: len(cfgs)]
+
+    def evaluate_many(self, cfgs) -> list[float]:
+        return [int(c) / float(self.n_eval) for c in self.correct_counts(cfgs)]
+
+    def __call__(self, cfg) -> float:
+        return self.evaluate_many([cfg])[0]
+
+    # ------------------------------------------------------------ probes / options
+    def set_option(self, key: str, value: int) -> None:
+        _lib.check(self.lib.ptq_set_option(self._ctx, key.encode(), int(value)))
+
+    def probe_codes(self, cfg, tensor: str) -> np.ndarray:
+        tid = self.lowered.tensor_ids[tensor]
+        cd = _lib.ConfigDesc(*config_key(cfg))
+        n = C.c_int64()
+        _lib.check(self.lib.ptq_probe_codes(self._ctx, C.byref(cd), tid, None, C.byref(n)))
+        out = np.zeros(n.value, dtype=np.int8)
+        with self._lock:
+            _lib.check(self.lib.ptq_probe_codes(self._ctx, C.byref(cd), tid, _lib.ptr(out), C.byref(n)))
+        return out
+
+    def act_params(self, cache: int, scheme: int, clipping: int):
+        s = np.zeros(self.T, dtype=np.float32)
+        z = np.zeros(self.T, dtype=np.int32)
+        _lib.check(self.lib.ptq_probe_act_params(self._ctx, cache, scheme, clipping, _lib.ptr(s), _lib.ptr(z)))
+        return s, z
+
+    def histogram(self, x: np.ndarray, lo: float, hi: float) -> np.ndarray:
+        x = np.ascontiguousarray(np.asarray(x, dtype=np.float32).ravel())
+        out = np.zeros(N_BINS, dtype=np.int64)
+        _lib.check(self.lib.ptq_histogram_host(self._ctx, _lib.ptr(x), x.size, float(lo), float(hi),
+                                               _lib.ptr(out)))
+        return out
+
+    def stats(self) -> tuple[int, float]:
+        n = C.c_int64()
+        ms = C.c_double()
+        _lib.check(self.lib.ptq_last_stats(self._ctx, C.byref(n), C.byref(ms)))
+        return n.value, ms.value
+
+    def close(self) -> None:
+        if getattr(self, "_ctx", None) and self._ctx.value:
+            self.lib.ptq_destroy(self._ctx)
+            self._ctx = C.c_void_p()
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+
+def make_accuracy_evaluator(g, d, seed: int, profile: TargetProfile | None = None, *,
+                            device: int = 0, eval_chunk: int | None = None) -> GpuEvaluator:
+    """Drop-in for ptqtune.tuner.make_accuracy_evaluator (tuner.py:434-444)."""
+    return GpuEvaluator(g, d, seed, profile, device=device, eval_chunk=eval_chunk)
