@@ -100,6 +100,15 @@ int ptq_num_tensors(const ptq_ctx* ctx, int32_t* T);
 int ptq_calibrate(ptq_ctx* ctx, int32_t n_caches, const int32_t* cache_sizes, const int64_t* ids,
                   float* ranges, int64_t* counts, int64_t* n_samples);
 
+/* The same in two phases, for calibration images sharded across ranks: phase 1
+ * runs the fp32 forward over this rank's ids and returns the local per-cache
+ * ranges (+inf/-inf for a cache with no local images); the host MIN/MAX-reduces
+ * them across ranks; phase 2 bins the retained activations with the global
+ * ranges (the host SUM-reduces the counts).  sizes may contain zeros. */
+int ptq_calib_forward(ptq_ctx* ctx, int32_t n_caches, const int32_t* cache_sizes,
+                      const int64_t* ids, float* local_ranges);
+int ptq_calib_histogram(ptq_ctx* ctx, const float* ranges, int64_t* counts);
+
 /* KL sweep (clipping.py:55-86): kl[h][w] for window width 128+w of histogram h;
  * +inf for infeasible windows and for histograms the reference does not sweep
  * (min == max or empty).  counts [n_hist][2048], ranges [n_hist][2] as above. */
@@ -133,10 +142,17 @@ int ptq_histogram_host(ptq_ctx* ctx, const float* x, int64_t n, float lo, float 
                        int64_t* counts);
 /* Runtime options: "conv_ref" (1 = CUDA-core reference conv instead of tcgen05,
  * tests only), "fusion" (0 = materialise every tensor so each can be probed),
- * "eval_chunk" (images per eval pass; default = whole eval set). */
+ * "eval_chunk" (images per eval pass; default = whole eval set), "time_conv" (1 =
+ * record CUDA events around every int8 conv launch for ptq_last_stats),
+ * "reset_stats" (zero the cumulative kernel-launch counter). */
 int ptq_set_option(ptq_ctx* ctx, const char* key, int64_t value);
-/* Launch-count / timing statistics of the last ptq_eval_configs call. */
-int ptq_last_stats(const ptq_ctx* ctx, int64_t* kernel_launches, double* conv_ms_event);
+/* Statistics of the last ptq_eval_configs call: kernel launches, summed CUDA-event
+ * time of the int8 conv launches (option "time_conv"), their algorithmic int8
+ * ops (2*M*N*K with unpadded dims) and the number of timed conv launches. */
+int ptq_last_stats(const ptq_ctx* ctx, int64_t* kernel_launches, double* conv_ms_event,
+                   double* conv_ops, int64_t* conv_launches);
+/* The CUDA stream (cudaStream_t) every kernel of this context runs on. */
+int ptq_stream(const ptq_ctx* ctx, void** stream);
 
 #ifdef __cplusplus
 }

@@ -25,7 +25,8 @@ KINDS = {"conv2d": 0, "depthwise_conv2d": 1, "pointwise_conv2d": 2, "fully_conne
 EXPORTS = ("ptq_last_error", "ptq_version", "ptq_create", "ptq_destroy", "ptq_num_tensors",
            "ptq_calibrate", "ptq_kl_sweep", "ptq_set_clip_ranges", "ptq_prepare",
            "ptq_eval_configs", "ptq_probe_codes", "ptq_probe_act_params", "ptq_histogram_host",
-           "ptq_set_option", "ptq_last_stats")
+           "ptq_set_option", "ptq_last_stats", "ptq_calib_forward", "ptq_calib_histogram",
+           "ptq_stream")
 
 
 class NodeDesc(C.Structure):
@@ -85,7 +86,11 @@ def load() -> C.CDLL:
         "ptq_probe_act_params": [P, i32, i32, i32, P, P],
         "ptq_histogram_host": [P, P, i64, C.c_float, C.c_float, P],
         "ptq_set_option": [P, C.c_char_p, i64],
-        "ptq_last_stats": [P, C.POINTER(i64), C.POINTER(C.c_double)],
+        "ptq_last_stats": [P, C.POINTER(i64), C.POINTER(C.c_double), C.POINTER(C.c_double),
+                           C.POINTER(i64)],
+        "ptq_calib_forward": [P, i32, P, P, P],
+        "ptq_calib_histogram": [P, P, P],
+        "ptq_stream": [P, C.POINTER(P)],
     }
     for name, args in sig.items():
         f = getattr(lib, name)

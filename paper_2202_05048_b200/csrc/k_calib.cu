@@ -76,6 +76,11 @@ __global__ void k_minmax_reduce_cache(const unsigned int* __restrict__ per_img, 
                                       float* __restrict__ ranges /*[T][2]*/) {
   int t = blockIdx.x * blockDim.x + threadIdx.x;
   if (t >= n_tensors) return;
+  if (n_slots == 0) {  // identity element for the cross-rank MIN/MAX allreduce
+    ranges[2 * t] = INFINITY;
+    ranges[2 * t + 1] = -INFINITY;
+    return;
+  }
   unsigned int lo = 0xffffffffu, hi = 0u;
   for (int j = 0; j < n_slots; ++j) {
     const unsigned int* q = per_img + ((int64_t)t * n_img_total + slots[j]) * 2;

@@ -132,12 +132,18 @@ struct ptq_ctx {
   int64_t P_cap = 0;
   unsigned long long* d_correct = nullptr;
   Plan plans[2];
+  // calibration state kept between ptq_calib_forward and ptq_calib_histogram
+  std::vector<float*> cal_bufs;
+  std::vector<int*> cal_slots;
+  std::vector<int> cal_sizes;
   // options
-  int conv_ref = 0, fusion = 1;
+  int conv_ref = 0, fusion = 1, time_conv = 0;
   int64_t opt_chunk = 0;
   // stats
   int64_t launches = 0;
-  double conv_ms = 0.0;
+  double conv_ms = 0.0, conv_ops = 0.0;
+  std::vector<cudaEvent_t> ev_pool;
+  size_t ev_used = 0;
 
   template <typename T>
   T* dalloc(size_t n) {
@@ -643,10 +649,10 @@ void prepare(ptq_ctx* c) {
   c->dfree(d_vs);
   ensure_eval_buffers(c);
   // mixed prefix: config-invariant fp32 output of the first compute node for all eval images
-  if (!c->d_prefix) {
+  {
     const int fc_ = c->first_compute;
     const int tout = c->nodes[fc_].out;
-    c->d_prefix = c->dalloc<float>((size_t)c->n_eval * c->tens[tout].elems);
+    if (!c->d_prefix) c->d_prefix = c->dalloc<float>((size_t)c->n_eval * c->tens[tout].elems);
     std::vector<float*> bufs(c->T, nullptr);
     int64_t pc = std::min<int64_t>(c->n_eval, 256);
     std::vector<int> need;
@@ -779,9 +785,22 @@ void eval_one(ptq_ctx* c, const ptq_config& cfg, unsigned long long* d_correct, 
             a.skip = V(P.add_other[i]);
             a.conv_is_a = P.add_is_a[i];
           }
+          cudaEvent_t ea = nullptr, eb = nullptr;
+          if (c->time_conv) {
+            while (c->ev_pool.size() < c->ev_used + 2) {
+              cudaEvent_t e;
+              CK(cudaEventCreate(&e));
+              c->ev_pool.push_back(e);
+            }
+            ea = c->ev_pool[c->ev_used++];
+            eb = c->ev_pool[c->ev_used++];
+            CK(cudaEventRecord(ea, c->st));
+          }
           if (c->conv_ref) launch_conv_i8_ref(a, wd.bn, c->st);
           else launch_conv_tc(a, wd.bn, c->st);
           check_launch(c);
+          if (c->time_conv) CK(cudaEventRecord(eb, c->st));
+          c->conv_ops += 2.0 * (double)B * a.OH * a.OW * (double)wd.cout * (double)wd.kreal;
         }
         halo_fill(tout);
         probe(tout);
@@ -900,6 +919,7 @@ int ptq_destroy(ptq_ctx* c) {
   cudaSetDevice(c->dev);
   if (c->st) cudaStreamSynchronize(c->st);
   for (void* p : c->allocs) cudaFree(p);
+  for (auto e : c->ev_pool) cudaEventDestroy(e);
   if (c->st) cudaStreamDestroy(c->st);
   delete c;
   return PTQ_OK;
@@ -911,81 +931,120 @@ int ptq_num_tensors(const ptq_ctx* c, int32_t* T) {
   return PTQ_OK;
 }
 
-int ptq_calibrate(ptq_ctx* c, int32_t n_caches, const int32_t* sizes, const int64_t* ids,
-                  float* ranges, int64_t* counts, int64_t* n_samples) {
+int ptq_calib_forward(ptq_ctx* c, int32_t n_caches, const int32_t* sizes, const int64_t* ids,
+                      float* local_ranges) {
   return guarded([&] {
-    REQ(c && n_caches >= 1 && sizes && ids, "null argument");
+    REQ(c && n_caches >= 1 && sizes, "null argument");
     CK(cudaSetDevice(c->dev));
-    // union of the image ids -> slots
-    std::vector<int64_t> all;
+    for (auto p : c->cal_bufs) c->dfree(p);
+    for (auto p : c->cal_slots) c->dfree(p);
+    c->cal_bufs.clear();
+    c->cal_slots.clear();
+    c->cal_sizes.assign(sizes, sizes + n_caches);
     int64_t tot = 0;
     for (int k = 0; k < n_caches; ++k) {
-      REQ(sizes[k] >= 1, "empty cache");
+      REQ(sizes[k] >= 0, "negative cache size");
       tot += sizes[k];
     }
-    all.assign(ids, ids + tot);
-    for (int64_t v : all) REQ(v >= 0 && v < c->n_calib, "calibration id out of range");
-    std::vector<int64_t> uni = all;
+    REQ(tot == 0 || ids, "null ids");
+    std::vector<int64_t> uni(ids, ids + tot);
+    for (int64_t v : uni) REQ(v >= 0 && v < c->n_calib, "calibration id out of range");
     std::sort(uni.begin(), uni.end());
     uni.erase(std::unique(uni.begin(), uni.end()), uni.end());
     const int nu = (int)uni.size();
     std::map<int64_t, int> slot;
     for (int i = 0; i < nu; ++i) slot[uni[i]] = i;
     const int T = c->T;
-    // fp32 forward over the union (one batch)
-    std::vector<float*> bufs(T, nullptr);
-    for (int t = 0; t < T; ++t) bufs[t] = c->dalloc<float>((size_t)nu * c->tens[t].elems);
-    std::vector<int> uid(uni.begin(), uni.end());
-    int* d_uid = c->dalloc<int>(nu);
-    CK(cudaMemcpyAsync(d_uid, uid.data(), nu * sizeof(int), cudaMemcpyHostToDevice, c->st));
-    const TensorI& in = c->tens[0];
-    launch_nchw_to_nhwc(c->d_imgs, d_uid, nu, in.c, in.h, in.w, bufs[0], c->st);
-    check_launch(c);
-    run_fp32(c, nu, bufs, 0, (int)c->nodes.size() - 1);
-    // F1a: per-image min/max
-    unsigned int* d_mm = c->dalloc<unsigned int>((size_t)T * nu * 2);
-    launch_fill_minmax(d_mm, (int64_t)T * nu, c->st);
-    check_launch(c);
-    for (int t = 0; t < T; ++t) {
-      launch_minmax_per_image(bufs[t], c->tens[t].elems, nu, d_mm + (size_t)t * nu * 2, c->st);
-      check_launch(c);
-    }
     float* d_rng = c->dalloc<float>((size_t)n_caches * T * 2);
-    unsigned long long* d_cnt = c->dalloc<unsigned long long>((size_t)n_caches * T * PTQ_NBINS);
-    CK(cudaMemsetAsync(d_cnt, 0, (size_t)n_caches * T * PTQ_NBINS * 8, c->st));
+    unsigned int* d_mm = c->dalloc<unsigned int>((size_t)T * std::max(nu, 1) * 2);
+    if (nu > 0) {
+      // fp32 forward over the union of the caches' images (one batch)
+      c->cal_bufs.assign(T, nullptr);
+      for (int t = 0; t < T; ++t) c->cal_bufs[t] = c->dalloc<float>((size_t)nu * c->tens[t].elems);
+      std::vector<int> uid(uni.begin(), uni.end());
+      int* d_uid = c->dalloc<int>(nu);
+      CK(cudaMemcpyAsync(d_uid, uid.data(), nu * sizeof(int), cudaMemcpyHostToDevice, c->st));
+      const TensorI& in = c->tens[0];
+      launch_nchw_to_nhwc(c->d_imgs, d_uid, nu, in.c, in.h, in.w, c->cal_bufs[0], c->st);
+      check_launch(c);
+      run_fp32(c, nu, c->cal_bufs, 0, (int)c->nodes.size() - 1);
+      // F1a: exact per-image min/max of every tensor
+      launch_fill_minmax(d_mm, (int64_t)T * nu, c->st);
+      check_launch(c);
+      for (int t = 0; t < T; ++t) {
+        launch_minmax_per_image(c->cal_bufs[t], c->tens[t].elems, nu, d_mm + (size_t)t * nu * 2, c->st);
+        check_launch(c);
+      }
+      CK(cudaStreamSynchronize(c->st));
+      c->dfree(d_uid);
+    }
     int64_t off = 0;
-    std::vector<int*> d_slots;
     for (int k = 0; k < n_caches; ++k) {
       std::vector<int> sl(sizes[k]);
       for (int j = 0; j < sizes[k]; ++j) sl[j] = slot[ids[off + j]];
       off += sizes[k];
-      int* ds = c->dalloc<int>(sl.size());
-      d_slots.push_back(ds);
-      CK(cudaMemcpyAsync(ds, sl.data(), sl.size() * sizeof(int), cudaMemcpyHostToDevice, c->st));
-      launch_minmax_reduce_cache(d_mm, T, nu, ds, sizes[k], d_rng + (size_t)k * T * 2, c->st);
+      int* ds = c->dalloc<int>(std::max<size_t>(sl.size(), 1));
+      c->cal_slots.push_back(ds);
+      if (!sl.empty())
+        CK(cudaMemcpyAsync(ds, sl.data(), sl.size() * sizeof(int), cudaMemcpyHostToDevice, c->st));
+      launch_minmax_reduce_cache(d_mm, T, std::max(nu, 1), ds, sizes[k], d_rng + (size_t)k * T * 2, c->st);
       check_launch(c);
-      // F1b: histograms with the cache's own (lo, hi)
+    }
+    if (local_ranges)
+      CK(cudaMemcpyAsync(local_ranges, d_rng, (size_t)n_caches * T * 2 * sizeof(float),
+                         cudaMemcpyDeviceToHost, c->st));
+    CK(cudaStreamSynchronize(c->st));
+    c->dfree(d_mm);
+    c->dfree(d_rng);
+  });
+}
+
+int ptq_calib_histogram(ptq_ctx* c, const float* ranges, int64_t* counts) {
+  return guarded([&] {
+    REQ(c && ranges && counts, "null argument");
+    REQ(c->cal_sizes.size() == c->cal_slots.size(), "ptq_calib_forward must run first");
+    CK(cudaSetDevice(c->dev));
+    const int T = c->T, nk = (int)c->cal_sizes.size();
+    float* d_rng = c->dalloc<float>((size_t)nk * T * 2);
+    unsigned long long* d_cnt = c->dalloc<unsigned long long>((size_t)nk * T * PTQ_NBINS);
+    CK(cudaMemcpyAsync(d_rng, ranges, (size_t)nk * T * 2 * sizeof(float), cudaMemcpyHostToDevice, c->st));
+    CK(cudaMemsetAsync(d_cnt, 0, (size_t)nk * T * PTQ_NBINS * 8, c->st));
+    for (int k = 0; k < nk; ++k) {
+      if (c->cal_sizes[k] == 0) continue;
+      // F1b: histograms with the cache's global (lo, hi)
       for (int t = 0; t < T; ++t) {
-        launch_histogram(bufs[t], c->tens[t].elems, ds, sizes[k], d_rng + ((size_t)k * T + t) * 2,
-                         d_cnt + ((size_t)k * T + t) * PTQ_NBINS, c->st);
+        launch_histogram(c->cal_bufs[t], c->tens[t].elems, c->cal_slots[k], c->cal_sizes[k],
+                         d_rng + ((size_t)k * T + t) * 2, d_cnt + ((size_t)k * T + t) * PTQ_NBINS, c->st);
         check_launch(c);
       }
     }
-    if (ranges)
-      CK(cudaMemcpyAsync(ranges, d_rng, (size_t)n_caches * T * 2 * sizeof(float), cudaMemcpyDeviceToHost, c->st));
-    if (counts)
-      CK(cudaMemcpyAsync(counts, d_cnt, (size_t)n_caches * T * PTQ_NBINS * 8, cudaMemcpyDeviceToHost, c->st));
+    CK(cudaMemcpyAsync(counts, d_cnt, (size_t)nk * T * PTQ_NBINS * 8, cudaMemcpyDeviceToHost, c->st));
     CK(cudaStreamSynchronize(c->st));
-    if (n_samples)
-      for (int k = 0; k < n_caches; ++k)
-        for (int t = 0; t < T; ++t) n_samples[(size_t)k * T + t] = (int64_t)sizes[k] * c->tens[t].elems;
-    for (auto p : bufs) c->dfree(p);
-    for (auto p : d_slots) c->dfree(p);
-    c->dfree(d_uid);
-    c->dfree(d_mm);
+    for (auto p : c->cal_bufs) c->dfree(p);
+    for (auto p : c->cal_slots) c->dfree(p);
+    c->cal_bufs.clear();
+    c->cal_slots.clear();
+    c->cal_sizes.clear();
     c->dfree(d_rng);
     c->dfree(d_cnt);
   });
+}
+
+int ptq_calibrate(ptq_ctx* c, int32_t n_caches, const int32_t* sizes, const int64_t* ids,
+                  float* ranges, int64_t* counts, int64_t* n_samples) {
+  if (!c || n_caches < 1 || !sizes) { g_err = "null argument"; return PTQ_EINVAL; }
+  std::vector<float> r((size_t)n_caches * c->T * 2);
+  std::vector<int64_t> cnt((size_t)n_caches * c->T * PTQ_NBINS);
+  int rc = ptq_calib_forward(c, n_caches, sizes, ids, r.data());
+  if (rc != PTQ_OK) return rc;
+  rc = ptq_calib_histogram(c, r.data(), cnt.data());
+  if (rc != PTQ_OK) return rc;
+  if (ranges) std::memcpy(ranges, r.data(), r.size() * sizeof(float));
+  if (counts) std::memcpy(counts, cnt.data(), cnt.size() * sizeof(int64_t));
+  if (n_samples)
+    for (int k = 0; k < n_caches; ++k)
+      for (int t = 0; t < c->T; ++t) n_samples[(size_t)k * c->T + t] = (int64_t)sizes[k] * c->tens[t].elems;
+  return PTQ_OK;
 }
 
 int ptq_kl_sweep(ptq_ctx* c, int32_t n_hist, const int64_t* counts, const float* ranges, double* kl) {
@@ -1032,7 +1091,9 @@ int ptq_eval_configs(ptq_ctx* c, const ptq_config* cfgs, int32_t n_cfg, int64_t*
     CK(cudaSetDevice(c->dev));
     prepare(c);
     ensure_eval_buffers(c);
-    c->launches = 0;
+    c->conv_ops = 0.0;
+    c->conv_ms = 0.0;
+    c->ev_used = 0;
     for (int32_t b0 = 0; b0 < n_cfg; b0 += 4096) {
       const int nb = std::min<int32_t>(4096, n_cfg - b0);
       CK(cudaMemsetAsync(c->d_correct, 0, nb * sizeof(unsigned long long), c->st));
@@ -1041,6 +1102,11 @@ int ptq_eval_configs(ptq_ctx* c, const ptq_config* cfgs, int32_t n_cfg, int64_t*
       CK(cudaMemcpyAsync(h.data(), c->d_correct, nb * sizeof(unsigned long long), cudaMemcpyDeviceToHost, c->st));
       CK(cudaStreamSynchronize(c->st));
       for (int i = 0; i < nb; ++i) correct[b0 + i] = (int64_t)h[i];
+    }
+    for (size_t e = 0; e + 1 < c->ev_used; e += 2) {
+      float ms = 0.f;
+      CK(cudaEventElapsedTime(&ms, c->ev_pool[e], c->ev_pool[e + 1]));
+      c->conv_ms += ms;
     }
   });
 }
@@ -1101,6 +1167,8 @@ int ptq_set_option(ptq_ctx* c, const char* key, int64_t value) {
     REQ(c && key, "null argument");
     std::string k(key);
     if (k == "conv_ref") c->conv_ref = (int)value;
+    else if (k == "time_conv") c->time_conv = (int)value;
+    else if (k == "reset_stats") c->launches = 0;
     else if (k == "fusion") {
       if (c->fusion != (int)value) {
         c->fusion = (int)value;
@@ -1116,10 +1184,19 @@ int ptq_set_option(ptq_ctx* c, const char* key, int64_t value) {
   });
 }
 
-int ptq_last_stats(const ptq_ctx* c, int64_t* launches, double* conv_ms) {
+int ptq_last_stats(const ptq_ctx* c, int64_t* launches, double* conv_ms, double* conv_ops,
+                   int64_t* conv_launches) {
   if (!c) { g_err = "null context"; return PTQ_EINVAL; }
   if (launches) *launches = c->launches;
   if (conv_ms) *conv_ms = c->conv_ms;
+  if (conv_ops) *conv_ops = c->conv_ops;
+  if (conv_launches) *conv_launches = (int64_t)(c->ev_used / 2);
+  return PTQ_OK;
+}
+
+int ptq_stream(const ptq_ctx* c, void** stream) {
+  if (!c || !stream) { g_err = "null argument"; return PTQ_EINVAL; }
+  *stream = (void*)c->st;
   return PTQ_OK;
 }
 

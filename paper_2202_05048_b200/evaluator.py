@@ -125,17 +125,36 @@ class GpuEvaluator:
 
     # ------------------------------------------------------------ calibration (tuner.py:438)
     def calibrate_all(self) -> None:
-        ids = [select_images(self.n_calib, sc, self.seed) for sc in CACHE_SIZES]
-        sizes = np.asarray([len(i) for i in ids], dtype=np.int32)
-        flat = np.ascontiguousarray(np.concatenate(ids).astype(np.int64))
-        T = self.T
-        ranges = np.zeros((3, T, 2), dtype=np.float32)
-        counts = np.zeros((3, T, N_BINS), dtype=np.int64)
-        nsamp = np.zeros((3, T), dtype=np.int64)
-        _lib.check(self.lib.ptq_calibrate(self._ctx, 3, _lib.ptr(sizes), _lib.ptr(flat),
-                                          _lib.ptr(ranges), _lib.ptr(counts), _lib.ptr(nsamp)))
-        self.image_ids = ids
+        """Build the S1/S2/S3 caches; under torch.distributed the images of each
+        cache are sharded across ranks (dist.sharded_calibration)."""
+        from . import dist
+        ranges, counts, n_img = dist.sharded_calibration(self, self.n_calib, self.seed, self.T)
+        elems = self.tensor_elems()
+        nsamp = n_img[:, None] * elems[None, :]
+        self.image_ids = [select_images(self.n_calib, sc, self.seed) for sc in CACHE_SIZES]
         self.install_caches(ranges, counts, nsamp)
+
+    # backend protocol of dist.sharded_calibration
+    def forward_minmax(self, sizes: np.ndarray, ids: np.ndarray) -> np.ndarray:
+        sizes = np.ascontiguousarray(sizes, dtype=np.int32)
+        ids = np.ascontiguousarray(ids, dtype=np.int64)
+        out = np.zeros((len(sizes), self.T, 2), dtype=np.float32)
+        _lib.check(self.lib.ptq_calib_forward(self._ctx, len(sizes), _lib.ptr(sizes),
+                                              _lib.ptr(ids) if ids.size else None, _lib.ptr(out)))
+        return out
+
+    def histogram(self, ranges: np.ndarray, lo=None, hi=None) -> np.ndarray:
+        if lo is not None:                       # single host array (parity probe)
+            return self.histogram_array(ranges, lo, hi)
+        ranges = np.ascontiguousarray(ranges, dtype=np.float32)
+        out = np.zeros((ranges.shape[0], self.T, N_BINS), dtype=np.int64)
+        _lib.check(self.lib.ptq_calib_histogram(self._ctx, _lib.ptr(ranges), _lib.ptr(out)))
+        return out
+
+    def tensor_elems(self) -> np.ndarray:
+        from .ir import tensor_shapes
+        shapes = tensor_shapes(self.graph)
+        return np.asarray([int(np.prod(shapes[t])) for t in self.lowered.tensor_names], dtype=np.int64)
 
     def install_caches(self, ranges: np.ndarray, counts: np.ndarray, nsamp: np.ndarray | None = None,
                        kl_ranges: np.ndarray | None = None) -> None:
@@ -211,18 +230,31 @@ class GpuEvaluator:
         _lib.check(self.lib.ptq_probe_act_params(self._ctx, cache, scheme, clipping, _lib.ptr(s), _lib.ptr(z)))
         return s, z
 
-    def histogram(self, x: np.ndarray, lo: float, hi: float) -> np.ndarray:
+    def evaluate_grid(self, cfgs) -> np.ndarray:
+        """Correct counts of every config, configs dealt round-robin over ranks."""
+        from . import dist
+        cfgs = list(cfgs)
+        rank, n = dist.world()
+        mine = self.correct_counts(dist.shard(cfgs, rank, n))
+        return dist.gather_counts(mine, len(cfgs))
+
+    def histogram_array(self, x: np.ndarray, lo: float, hi: float) -> np.ndarray:
         x = np.ascontiguousarray(np.asarray(x, dtype=np.float32).ravel())
         out = np.zeros(N_BINS, dtype=np.int64)
         _lib.check(self.lib.ptq_histogram_host(self._ctx, _lib.ptr(x), x.size, float(lo), float(hi),
                                                _lib.ptr(out)))
         return out
 
-    def stats(self) -> tuple[int, float]:
-        n = C.c_int64()
-        ms = C.c_double()
-        _lib.check(self.lib.ptq_last_stats(self._ctx, C.byref(n), C.byref(ms)))
-        return n.value, ms.value
+    def stats(self) -> dict:
+        n, ms, ops, nc = C.c_int64(), C.c_double(), C.c_double(), C.c_int64()
+        _lib.check(self.lib.ptq_last_stats(self._ctx, C.byref(n), C.byref(ms), C.byref(ops), C.byref(nc)))
+        return {"launches": n.value, "conv_ms": ms.value, "conv_ops": ops.value,
+                "conv_launches": nc.value}
+
+    def stream_handle(self) -> int:
+        s = C.c_void_p()
+        _lib.check(self.lib.ptq_stream(self._ctx, C.byref(s)))
+        return s.value or 0
 
     def close(self) -> None:
         if getattr(self, "_ctx", None) and self._ctx.value:
