@@ -102,6 +102,20 @@ __device__ __forceinline__ int np_bin(double x, double lo, double hi, double den
   return idx;
 }
 
+// Fast path: an approximate position fe = (x - lo) * fl(2048 / (hi - lo)) is within a
+// few ulps of numpy's f-index, and numpy's edges are within a few ulps of the exact
+// bin edges.  When fe's fractional part keeps a margin `eps` (in bin units) from both
+// neighbouring edges, numpy's truncation and both fixups provably leave floor(fe)
+// unchanged, so only near-edge values pay for the exact division + edge checks.
+__device__ __forceinline__ int np_bin_fast(double x, double lo, double hi, double denom,
+                                           double rc, double eps) {
+  const double fe = __dmul_rn(__dsub_rn(x, lo), rc);
+  const int k = (int)fe;
+  const double frac = __dsub_rn(fe, (double)k);
+  if (k < PTQ_NBINS && frac > eps && frac < 1.0 - eps) return k;
+  return np_bin(x, lo, hi, denom);
+}
+
 // x: [n_img_total][elems]; slots: image slots of this cache; range: lo, hi (fp32 values).
 // counts: [2048] int64 (accumulated).
 __global__ void __launch_bounds__(512) k_histogram(const float* __restrict__ x, int64_t elems,
@@ -114,25 +128,42 @@ __global__ void __launch_bounds__(512) k_histogram(const float* __restrict__ x, 
   const double lo = (double)range[0], hi = (double)range[1];
   const double denom = __dsub_rn(hi, lo);
   const bool degenerate = !(lo < hi);
-  const int64_t total = elems * n_slots;
+  const double rc = degenerate ? 0.0 : __ddiv_rn((double)PTQ_NBINS, denom);
+  const double mag = fmax(fabs(lo), fabs(hi));
+  const double eps = degenerate ? 1.0 : 16.0 * 2.220446049250313e-16 * mag * rc + 1e-9;
   const int lane = threadIdx.x & 31;
-  for (int64_t base = blockIdx.x * (int64_t)blockDim.x; base < total;
-       base += (int64_t)gridDim.x * blockDim.x) {
-    int64_t i = base + threadIdx.x;
-    bool valid = i < total;
-    int bin = 0;
-    if (valid && !degenerate) {
-      int j = (int)(i / elems);
-      int64_t off = i - (int64_t)j * elems;
-      float v = __ldg(x + (int64_t)slots[j] * elems + off);
-      bin = np_bin((double)v, lo, hi, denom);
+  if (degenerate) {                       // lo == hi: every value lands in bin 0 (:86-87)
+    if (blockIdx.x == 0 && threadIdx.x == 0) atomicAdd(counts, (unsigned long long)(elems * n_slots));
+    return;
+  }
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  for (int j = 0; j < n_slots; ++j) {
+    const float* img = x + (int64_t)slots[j] * elems;
+    const int64_t nv = ((((uintptr_t)img) & 15) == 0) ? (elems >> 2) : 0;
+    const float4* img4 = reinterpret_cast<const float4*>(img);
+    for (int64_t base = blockIdx.x * (int64_t)blockDim.x; base < nv; base += stride) {
+      const int64_t i = base + threadIdx.x;
+      const bool valid = i < nv;
+      int b[4] = {0, 0, 0, 0};
+      if (valid) {
+        const float4 v = __ldg(img4 + i);
+        b[0] = np_bin_fast((double)v.x, lo, hi, denom, rc, eps);
+        b[1] = np_bin_fast((double)v.y, lo, hi, denom, rc, eps);
+        b[2] = np_bin_fast((double)v.z, lo, hi, denom, rc, eps);
+        b[3] = np_bin_fast((double)v.w, lo, hi, denom, rc, eps);
+      }
+      // warp-aggregated increments: post-ReLU tensors pile up in bin 0
+      const unsigned int act = __ballot_sync(0xffffffffu, valid);
+      if (valid) {
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+          const unsigned int peers = __match_any_sync(act, b[q]);
+          if (lane == __ffs(peers) - 1) atomicAdd(&sh[b[q]], __popc(peers));
+        }
+      }
     }
-    // warp-aggregated increments: post-ReLU tensors pile up in bin 0
-    unsigned int act = __ballot_sync(0xffffffffu, valid);
-    if (valid) {
-      unsigned int peers = __match_any_sync(act, bin);
-      if (lane == __ffs(peers) - 1) atomicAdd(&sh[bin], __popc(peers));
-    }
+    for (int64_t i = nv * 4 + blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < elems; i += stride)
+      atomicAdd(&sh[np_bin_fast((double)__ldg(img + i), lo, hi, denom, rc, eps)], 1u);
   }
   __syncthreads();
   for (int i = threadIdx.x; i < PTQ_NBINS; i += blockDim.x)

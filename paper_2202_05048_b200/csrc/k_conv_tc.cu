@@ -7,22 +7,23 @@
 // add on codes.  The contraction runs as D[s32] = A[s8] x B[s8] with
 //   sum (x-zx)(w-zw) = sum x*w - zw*sum x - zx*sum w + K*zx*zw
 // where the halo of the NHWC input holds the zero-point code (so padded taps
-// contribute exactly 0), sum w is per output channel (precomputed) and sum x is
-// per output pixel (from per-pixel channel sums P, only when some zw != 0).
+// contribute exactly 0), -zx*sum w + K*zx*zw + bias is a per-channel constant
+// (EpiParam.cc, computed per config by k_layer_params) and sum x is a
+// per-output-pixel term from per-pixel channel sums P (only when some zw != 0).
 //
-// Kernel anatomy (one 128 x BN output tile per CTA, 192 threads):
-//   warps 0-3  A producers: one output pixel (GEMM row) per thread; gather the
-//              row's 16-byte K chunks with cp.async into the UMMA K-major
-//              no-swizzle canonical layout; completion signalled with
-//              cp.async.mbarrier.arrive.noinc on the stage's full barrier.
-//   warp 4     B producer: one cp.async.bulk (TMA bulk engine) per stage from
-//              the pre-tiled weight image, complete_tx on the same barrier.
-//   warp 5     TMEM allocator + single-thread tcgen05.mma.kind::i8 issuer
-//              (M=128, N=BN, K=32 per instruction, 4 per 128-byte stage);
-//              tcgen05.commit frees a stage / signals the accumulator.
-//   warps 0-3  epilogue: tcgen05.ld 32x32b (thread = TMEM lane = output row),
-//              zero-point correction, bias, int32 clip, fp64 requant, relu /
-//              fused add, 16-byte stores of int8 codes.
+// Persistent, warp-specialised kernel (one CTA per SM, 448 threads):
+//   warps 0-3   A producers: one GEMM row (output pixel) per thread; gather the
+//               row's 16-byte K chunks with cp.async into the UMMA K-major
+//               no-swizzle canonical layout (8-row x 16-byte core matrices);
+//               cp.async.mbarrier.arrive.noinc signals the stage's full barrier.
+//   warp 4      B producer: one cp.async.bulk per stage from the pre-tiled
+//               weight image (TMA bulk engine, complete_tx on the same barrier).
+//   warp 5      TMEM allocator + single-thread tcgen05.mma.kind::i8 issuer
+//               (M=128, N=BN, K=32 per instruction, 4 per 128-byte stage).
+//               Two TMEM accumulators so tile t+1's MMAs overlap tile t's epilogue.
+//   warps 6-13  epilogue: tcgen05.ld 32x32b (TMEM lane = output row), int32
+//               zero-point correction, fp64 requant (explicit _rn intrinsics,
+//               reference op order), relu / fused add, 16-byte code stores.
 #include <climits>
 
 #include "common.cuh"
@@ -32,8 +33,9 @@ namespace ptq {
 
 constexpr int TC_BM = 128;
 constexpr int TC_STAGES = 4;
-constexpr int TC_THREADS = 192;
-constexpr int TC_A_STAGE = TC_BM * 128;  // 16 KB: 8 chunks x 128 rows x 16 B
+constexpr int TC_A_STAGE = TC_BM * 128;            // 16 KB: 8 chunks x 128 rows x 16 B
+constexpr int TC_EPI_WARPS = 8;
+constexpr int TC_THREADS = (6 + TC_EPI_WARPS) * 32;
 
 __device__ __forceinline__ uint64_t umma_desc(uint32_t saddr, uint32_t lbo, uint32_t sbo) {
   uint64_t d = 0;
@@ -84,22 +86,56 @@ __device__ __forceinline__ int64_t vpix(const View& v, int n, int h, int w) {
   return ((int64_t)n * Hp + h + v.halo) * Wp + w + v.halo;
 }
 
-// shared epilogue math for one output element (used by the tensor-core kernel
-// and by the CUDA-core reference kernel).  `dot` = sum x*w over the padded K.
-__device__ __forceinline__ int epi_code(long long dot, int c, long long rowsum, const ConvTcArgs& a,
-                                        const LayerRt& rt, int skip_code) {
+// ---------------------------------------------------------------- exact epilogue pieces
+// int32 -> fp64 without the (slow) conversion pipe: 2^52 + 2^31 + x is exact, then subtract
+__device__ __forceinline__ double i2d(int x) {
+  return __dsub_rn(__hiloint2double(0x43300000, x ^ (int)0x80000000), 4503601774854144.0);
+}
+// floor(r) for |r| < 2^51 on the FP64 pipe: round-down add of 1.5*2^52 leaves floor(r)
+// in the low word (two's complement)
+__device__ __forceinline__ int floor_i(double r) {
+  return __double2loint(__dadd_rd(r, 6755399441055744.0));
+}
+__device__ __forceinline__ int clampi(int x, int lo, int hi) { return x < lo ? lo : (x > hi ? hi : x); }
+
+// clip(RHU(acc*m) + zp, lo, 127) with acc pre-clamped to the saturation margins
+__device__ __forceinline__ int requant_fast(int acc, const EpiParam& e, int zp, int lo) {
+  acc = clampi(acc, e.alo, e.ahi);
+  const double r = __dadd_rn(__dmul_rn(i2d(acc), e.m), 0.5);   // fl(fl(acc*m) + 0.5)
+  return clampi(floor_i(r) + zp, lo, PTQ_QMAX);
+}
+// residual add on codes (intexec.py:245-276): clip(RHU(xs*ra + ys*rb) + zo)
+__device__ __forceinline__ int add_fast(int xa, int xb, const LayerRt& rt, int lo) {
+  const double s = __dadd_rn(__dmul_rn(i2d(xa - rt.za), rt.ra), __dmul_rn(i2d(xb - rt.zb), rt.rb));
+  return clampi(floor_i(__dadd_rn(s, 0.5)) + rt.zo, lo, PTQ_QMAX);
+}
+
+// 16 output channels of one row, fast path (no int32 saturation possible)
+template <bool SKIP, bool CONV_A>
+__device__ __forceinline__ void epi_chunk16(const uint32_t (&v)[16], const EpiParam* __restrict__ ep,
+                                            int cb, int rowsum, const LayerRt& rt, int lo_conv,
+                                            int lo_add, const int8_t* sk, int8_t* codes) {
+#pragma unroll
+  for (int g = 0; g < 2; ++g) {
+    EpiParam e[8];
+#pragma unroll
+    for (int j = 0; j < 8; ++j) e[j] = ep[cb + g * 8 + j];       // batched broadcast loads
+#pragma unroll
+    for (int j = 0; j < 8; ++j) {
+      const int jj = g * 8 + j;
+      int q = requant_fast((int)v[jj] - e[j].zw * rowsum + e[j].cc, e[j], rt.zy, lo_conv);
+      if (SKIP) q = CONV_A ? add_fast(q, sk[jj], rt, lo_add) : add_fast(sk[jj], q, rt, lo_add);
+      codes[jj] = (int8_t)q;
+    }
+  }
+}
+// general (slow) path: 64-bit accumulator with the reference's int32 saturation
+__device__ __forceinline__ int epi_slow(long long dot, int c, long long rowsum, const ConvTcArgs& a,
+                                        const LayerRt& rt) {
   long long zw = a.wzp[c];
   long long acc = dot - zw * rowsum - (long long)rt.zx * a.wsum[c] + (long long)a.kreal * rt.zx * zw;
   acc = clip32(acc + a.L.biasq[c]);
-  int q = requant1(acc, a.L.mult[c], rt.zy);
-  if (q < rt.relu_zp) q = rt.relu_zp;
-  if (a.skip.p) {
-    int xa = a.conv_is_a ? q : skip_code, xb = a.conv_is_a ? skip_code : q;
-    double s = __dadd_rn(__dmul_rn((double)(xa - rt.za), rt.ra), __dmul_rn((double)(xb - rt.zb), rt.rb));
-    q = clip8(rhu(s) + (double)rt.zo);
-    if (q < rt.add_relu_zp) q = rt.add_relu_zp;
-  }
-  return q;
+  return requant1(acc, a.L.mult[c], rt.zy);
 }
 
 __device__ __forceinline__ long long pixel_rowsum(const ConvTcArgs& a, int n, int ih0, int iw0) {
@@ -111,28 +147,50 @@ __device__ __forceinline__ long long pixel_rowsum(const ConvTcArgs& a, int n, in
   return s;
 }
 
+struct RowGeo {
+  bool ok;
+  int n, oh, ow, ih0, iw0;
+};
+__device__ __forceinline__ RowGeo row_geo(const ConvTcArgs& a, int64_t m, int64_t M) {
+  RowGeo g{};
+  g.ok = m < M;
+  if (g.ok) {
+    g.ow = (int)(m % a.OW);
+    int64_t t = m / a.OW;
+    g.oh = (int)(t % a.OH);
+    g.n = (int)(t / a.OH);
+  }
+  g.ih0 = g.oh * a.stride - a.pad + a.in.halo;
+  g.iw0 = g.ow * a.stride - a.pad + a.in.halo;
+  return g;
+}
+
 template <int BN>
-__global__ void __launch_bounds__(TC_THREADS, 1) k_conv_tc(const ConvTcArgs a) {
+__global__ void __launch_bounds__(TC_THREADS, 1) k_conv_tc(const __grid_constant__ ConvTcArgs a) {
   extern __shared__ __align__(1024) uint8_t smem[];
   uint8_t* sA = smem;
   uint8_t* sB = smem + TC_STAGES * TC_A_STAGE;
   uint64_t* full = reinterpret_cast<uint64_t*>(sB + TC_STAGES * BN * 128);
   uint64_t* empty = full + TC_STAGES;
-  uint64_t* accb = empty + TC_STAGES;
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(accb + 1);
-  constexpr uint32_t TMEM_COLS = BN < 32 ? 32 : BN;
+  uint64_t* tfull = empty + TC_STAGES;
+  uint64_t* tempty = tfull + 2;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
+  constexpr uint32_t TMEM_COLS = (2 * BN) < 32 ? 32 : 2 * BN;
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int64_t M = (int64_t)a.in.N * a.OH * a.OW;
-  const int64_t m0 = (int64_t)blockIdx.x * TC_BM;
-  const int nt = blockIdx.y;
+  const int n_nt = (a.L.cout + BN - 1) / BN;
+  const int64_t n_tiles = ((M + TC_BM - 1) / TC_BM) * n_nt;
 
   if (threadIdx.x == 0) {
     for (int s = 0; s < TC_STAGES; ++s) {
       mbar_init(&full[s], 128 + 1);
       mbar_init(&empty[s], 1);
     }
-    mbar_init(accb, 1);
+    for (int b = 0; b < 2; ++b) {
+      mbar_init(&tfull[b], 1);
+      mbar_init(&tempty[b], TC_EPI_WARPS * 32);
+    }
     fence_mbar_init();
   }
   if (warp == 5) {
@@ -146,103 +204,134 @@ __global__ void __launch_bounds__(TC_THREADS, 1) k_conv_tc(const ConvTcArgs a) {
   tc_fence_after();
   const uint32_t tmem = *tmem_slot;
 
-  // per-row geometry (warps 0-3: row r = threadIdx.x)
-  const int r = threadIdx.x;
-  const int64_t m = m0 + r;
-  const bool row_ok = (warp < 4) && (m < M);
-  int n_img = 0, oh = 0, ow = 0;
-  if (row_ok) {
-    ow = (int)(m % a.OW);
-    int64_t t = m / a.OW;
-    oh = (int)(t % a.OH);
-    n_img = (int)(t / a.OH);
-  }
-  const int Wp = a.in.W + 2 * a.in.halo, Hp = a.in.H + 2 * a.in.halo;
-  const int ih0 = oh * a.stride - a.pad + a.in.halo, iw0 = ow * a.stride - a.pad + a.in.halo;
-
   if (warp < 4) {
-    // ------------------------------------------------ A producer (implicit im2col gather)
+    // ------------------------------------------------ A producers (implicit im2col gather)
+    const int r = threadIdx.x;
     const int Cp = a.in.Cp, cpc = Cp >> 4;
-    const int8_t* base = a.in.p + (((int64_t)n_img * Hp + ih0) * Wp + iw0) * Cp;
-    int kh = 0, kw = 0, ch = 0, kk = 0;
-    for (int it = 0; it < a.n_kiter; ++it) {
-      const int s = it % TC_STAGES;
-      const uint32_t ph = (uint32_t)(it / TC_STAGES) & 1u;
-      mbar_wait(&empty[s], ph ^ 1u);
-      uint8_t* dst = sA + s * TC_A_STAGE + r * 16;
+    const int Wp = a.in.W + 2 * a.in.halo, Hp = a.in.H + 2 * a.in.halo;
+    uint32_t it = 0;
+    for (int64_t tile = blockIdx.x; tile < n_tiles; tile += gridDim.x) {
+      const int64_t mt = tile / n_nt;
+      const RowGeo g = row_geo(a, mt * TC_BM + r, M);
+      const int8_t* base = a.in.p + (((int64_t)g.n * Hp + g.ih0) * Wp + g.iw0) * Cp;
+      int kh = 0, kw = 0, ch = 0, kk = 0;
+      for (int ki = 0; ki < a.n_kiter; ++ki, ++it) {
+        const int s = it % TC_STAGES;
+        const uint32_t ph = (it / TC_STAGES) & 1u;
+        mbar_wait(&empty[s], ph ^ 1u);
+        uint8_t* dst = sA + s * TC_A_STAGE + r * 16;
 #pragma unroll
-      for (int j = 0; j < 8; ++j) {
-        const bool v = row_ok && kk < a.n_chunks;
-        const int8_t* src = v ? base + ((int64_t)kh * Wp + kw) * Cp + ch * 16 : a.in.p;
-        cp_async16(dst + j * (TC_BM * 16), src, v ? 16u : 0u);
-        ++kk;
-        if (++ch == cpc) {
-          ch = 0;
-          if (++kw == a.k) { kw = 0; ++kh; }
+        for (int j = 0; j < 8; ++j) {
+          const bool v = g.ok && kk < a.n_chunks;
+          const int8_t* src = v ? base + ((int64_t)kh * Wp + kw) * Cp + ch * 16 : a.in.p;
+          cp_async16(dst + j * (TC_BM * 16), src, v ? 16u : 0u);
+          ++kk;
+          if (++ch == cpc) {
+            ch = 0;
+            if (++kw == a.k) { kw = 0; ++kh; }
+          }
         }
+        cp_async_mbar_arrive_noinc(&full[s]);
       }
-      cp_async_mbar_arrive_noinc(&full[s]);
     }
   } else if (warp == 4) {
     // ------------------------------------------------ B producer (bulk copies of pre-tiled weights)
     if (lane == 0) {
-      const int8_t* gB = a.wB + (int64_t)nt * a.n_kiter * BN * 128;
-      for (int it = 0; it < a.n_kiter; ++it) {
-        const int s = it % TC_STAGES;
-        const uint32_t ph = (uint32_t)(it / TC_STAGES) & 1u;
-        mbar_wait(&empty[s], ph ^ 1u);
-        mbar_arrive_expect_tx(&full[s], BN * 128);
-        bulk_g2s(sB + s * BN * 128, gB + (int64_t)it * BN * 128, BN * 128, &full[s]);
+      uint32_t it = 0;
+      for (int64_t tile = blockIdx.x; tile < n_tiles; tile += gridDim.x) {
+        const int nt = (int)(tile % n_nt);
+        const int8_t* gB = a.wB + (int64_t)nt * a.n_kiter * BN * 128;
+        for (int ki = 0; ki < a.n_kiter; ++ki, ++it) {
+          const int s = it % TC_STAGES;
+          const uint32_t ph = (it / TC_STAGES) & 1u;
+          mbar_wait(&empty[s], ph ^ 1u);
+          mbar_arrive_expect_tx(&full[s], BN * 128);
+          bulk_g2s(sB + s * BN * 128, gB + (int64_t)ki * BN * 128, BN * 128, &full[s]);
+        }
       }
     }
-  } else {
+  } else if (warp == 5) {
     // ------------------------------------------------ MMA issuer
     if (lane == 0) {
       const uint32_t idesc = idesc_i8<BN>();
-      for (int it = 0; it < a.n_kiter; ++it) {
-        const int s = it % TC_STAGES;
-        const uint32_t ph = (uint32_t)(it / TC_STAGES) & 1u;
-        mbar_wait(&full[s], ph);
+      uint32_t it = 0, lt = 0;
+      for (int64_t tile = blockIdx.x; tile < n_tiles; tile += gridDim.x, ++lt) {
+        const uint32_t buf = lt & 1u, uph = (lt >> 1) & 1u;
+        mbar_wait(&tempty[buf], uph ^ 1u);           // epilogue drained this accumulator
         tc_fence_after();
-        fence_proxy_async();
-        const uint32_t a0 = smem_u32(sA + s * TC_A_STAGE), b0 = smem_u32(sB + s * BN * 128);
+        const uint32_t d = tmem + buf * BN;
+        for (int ki = 0; ki < a.n_kiter; ++ki, ++it) {
+          const int s = it % TC_STAGES;
+          const uint32_t ph = (it / TC_STAGES) & 1u;
+          mbar_wait(&full[s], ph);
+          tc_fence_after();
+          fence_proxy_async();
+          const uint32_t a0 = smem_u32(sA + s * TC_A_STAGE), b0 = smem_u32(sB + s * BN * 128);
 #pragma unroll
-        for (int ks = 0; ks < 4; ++ks) {
-          const uint64_t ad = umma_desc(a0 + ks * 2 * (TC_BM * 16), TC_BM * 16, 128);
-          const uint64_t bd = umma_desc(b0 + ks * 2 * (BN * 16), BN * 16, 128);
-          mma_i8(tmem, ad, bd, idesc, (it | ks) != 0);
+          for (int ks = 0; ks < 4; ++ks) {
+            const uint64_t ad = umma_desc(a0 + ks * 2 * (TC_BM * 16), TC_BM * 16, 128);
+            const uint64_t bd = umma_desc(b0 + ks * 2 * (BN * 16), BN * 16, 128);
+            mma_i8(d, ad, bd, idesc, (ki | ks) != 0);
+          }
+          mma_commit(&empty[s]);                     // frees the smem stage when the MMAs land
         }
-        mma_commit(&empty[s]);
+        mma_commit(&tfull[buf]);                     // accumulator ready for the epilogue
       }
-      mma_commit(accb);
     }
     __syncwarp();
-  }
-
-  if (warp < 4) {
-    // ------------------------------------------------ epilogue
-    mbar_wait(accb, 0);
-    tc_fence_after();
+  } else {
+    // ------------------------------------------------ epilogue warps
+    const int q = warp & 3;                          // TMEM lane quarter this warp may access
+    const int half = (warp - 6) >> 2;
+    constexpr int CPH = BN / 2 < 16 ? 16 : BN / 2;   // columns per epilogue half
+    const int c_lo = half * CPH, c_hi = (half + 1) * CPH < BN ? (half + 1) * CPH : BN;
+    const int row = q * 32 + lane;
     const LayerRt rt = *a.L.rt;
-    const long long rowsum = row_ok ? pixel_rowsum(a, n_img, ih0, iw0) : 0;
+    const int lo_conv = rt.relu_zp > PTQ_QMIN ? rt.relu_zp : PTQ_QMIN;
+    const int lo_add = rt.add_relu_zp > PTQ_QMIN ? rt.add_relu_zp : PTQ_QMIN;
     const int Cout = a.L.cout;
-    int8_t* orow = row_ok ? a.out.p + vpix(a.out, n_img, oh, ow) * a.out.Cp : nullptr;
-    const int8_t* srow = (row_ok && a.skip.p) ? a.skip.p + vpix(a.skip, n_img, oh, ow) * a.skip.Cp : nullptr;
+    const EpiParam* __restrict__ ep = a.L.ep;
+    uint32_t lt = 0;
+    for (int64_t tile = blockIdx.x; tile < n_tiles; tile += gridDim.x, ++lt) {
+      const uint32_t buf = lt & 1u, uph = (lt >> 1) & 1u;
+      const int64_t mt = tile / n_nt;
+      const int nt = (int)(tile % n_nt);
+      const RowGeo g = row_geo(a, mt * TC_BM + row, M);
+      const long long rowsum = (g.ok && c_lo < c_hi) ? pixel_rowsum(a, g.n, g.ih0, g.iw0) : 0;
+      int8_t* orow = g.ok ? a.out.p + vpix(a.out, g.n, g.oh, g.ow) * a.out.Cp : nullptr;
+      const int8_t* srow = (g.ok && a.skip.p) ? a.skip.p + vpix(a.skip, g.n, g.oh, g.ow) * a.skip.Cp : nullptr;
+      mbar_wait(&tfull[buf], uph);
+      tc_fence_after();
 #pragma unroll 1
-    for (int c0 = 0; c0 < BN; c0 += 16) {
-      uint32_t v[16];
-      tmem_ld16(tmem + ((uint32_t)(warp * 32) << 16) + (uint32_t)c0, v);
-      const int cb = nt * BN + c0;
-      if (!row_ok || cb >= a.out.Cp) continue;
-      alignas(16) int8_t codes[16];
-      alignas(16) int8_t sk[16];
-      if (srow) *reinterpret_cast<int4*>(sk) = *reinterpret_cast<const int4*>(srow + cb);
+      for (int c0 = c_lo; c0 < c_hi; c0 += 16) {
+        uint32_t v[16];
+        tmem_ld16(tmem + ((uint32_t)(q * 32) << 16) + buf * BN + (uint32_t)c0, v);
+        const int cb = nt * BN + c0;
+        if (!g.ok || cb >= a.out.Cp) continue;
+        alignas(16) int8_t codes[16];
+        alignas(16) int8_t sk[16];
+        if (srow) *reinterpret_cast<int4*>(sk) = *reinterpret_cast<const int4*>(srow + cb);
+        if (!rt.slow && cb + 16 <= Cout) {
+          if (!srow) epi_chunk16<false, false>(v, ep, cb, (int)rowsum, rt, lo_conv, lo_add, sk, codes);
+          else if (a.conv_is_a) epi_chunk16<true, true>(v, ep, cb, (int)rowsum, rt, lo_conv, lo_add, sk, codes);
+          else epi_chunk16<true, false>(v, ep, cb, (int)rowsum, rt, lo_conv, lo_add, sk, codes);
+        } else {
 #pragma unroll
-      for (int j = 0; j < 16; ++j) {
-        const int c = cb + j;
-        codes[j] = c < Cout ? (int8_t)epi_code((long long)(int)v[j], c, rowsum, a, rt, srow ? sk[j] : 0) : (int8_t)0;
+          for (int j = 0; j < 16; ++j) {
+            const int c = cb + j;
+            int code = 0;
+            if (c < Cout) {
+              code = epi_slow((long long)(int)v[j], c, rowsum, a, rt);
+              if (code < lo_conv) code = lo_conv;
+              if (srow) code = a.conv_is_a ? add_fast(code, sk[j], rt, lo_add) : add_fast(sk[j], code, rt, lo_add);
+            }
+            codes[j] = (int8_t)code;
+          }
+        }
+        *reinterpret_cast<int4*>(orow + cb) = *reinterpret_cast<int4*>(codes);
       }
-      *reinterpret_cast<int4*>(orow + cb) = *reinterpret_cast<int4*>(codes);
+      tc_fence_before();
+      mbar_arrive(&tempty[buf]);                     // accumulator buffer may be reused
     }
   }
 
@@ -266,26 +355,31 @@ __global__ void k_conv_i8_ref(const ConvTcArgs a) {
        i += (int64_t)gridDim.x * blockDim.x) {
     const int c = (int)(i % a.out.Cp);
     const int64_t m = i / a.out.Cp;
-    const int ow = (int)(m % a.OW);
-    const int64_t t = m / a.OW;
-    const int oh = (int)(t % a.OH), n = (int)(t / a.OH);
-    int8_t* orow = a.out.p + vpix(a.out, n, oh, ow) * a.out.Cp;
+    const RowGeo g = row_geo(a, m, M);
+    int8_t* orow = a.out.p + vpix(a.out, g.n, g.oh, g.ow) * a.out.Cp;
     if (c >= Cout) { orow[c] = 0; continue; }
     const int Wp = a.in.W + 2 * a.in.halo, Hp = a.in.H + 2 * a.in.halo;
-    const int ih0 = oh * a.stride - a.pad + a.in.halo, iw0 = ow * a.stride - a.pad + a.in.halo;
     const int cpc = a.in.Cp >> 4;
     const int ntile = c / BN, row = c % BN;
     long long dot = 0;
     for (int kk = 0; kk < a.n_chunks; ++kk) {
       const int tap = kk / cpc, ch = kk % cpc;
       const int kh = tap / a.k, kw = tap % a.k;
-      const int8_t* xs = a.in.p + (((int64_t)n * Hp + ih0 + kh) * Wp + iw0 + kw) * a.in.Cp + ch * 16;
+      const int8_t* xs = a.in.p + (((int64_t)g.n * Hp + g.ih0 + kh) * Wp + g.iw0 + kw) * a.in.Cp + ch * 16;
       const int8_t* ws = a.wB + (((int64_t)ntile * a.n_kiter + kk / 8) * 8 + kk % 8) * BN * 16 + row * 16;
       for (int b = 0; b < 16; ++b) dot += (long long)xs[b] * ws[b];
     }
-    const long long rowsum = pixel_rowsum(a, n, ih0, iw0);
-    const int sk = a.skip.p ? a.skip.p[vpix(a.skip, n, oh, ow) * a.skip.Cp + c] : 0;
-    orow[c] = (int8_t)epi_code(dot, c, rowsum, a, rt, sk);
+    const long long rowsum = pixel_rowsum(a, g.n, g.ih0, g.iw0);
+    int q = epi_slow(dot, c, rowsum, a, rt);
+    if (q < rt.relu_zp) q = rt.relu_zp;
+    if (a.skip.p) {
+      const int sk = a.skip.p[vpix(a.skip, g.n, g.oh, g.ow) * a.skip.Cp + c];
+      const int xa = a.conv_is_a ? q : sk, xb = a.conv_is_a ? sk : q;
+      const double s = __dadd_rn(__dmul_rn((double)(xa - rt.za), rt.ra), __dmul_rn((double)(xb - rt.zb), rt.rb));
+      q = clip8(rhu(s) + (double)rt.zo);
+      if (q < rt.add_relu_zp) q = rt.add_relu_zp;
+    }
+    orow[c] = (int8_t)q;
   }
 }
 
@@ -297,18 +391,26 @@ int conv_tc_bn_for(int cout) {
   return 256;
 }
 
+static int g_num_sms = 0;
+
 template <int BN>
 static void launch_bn(const ConvTcArgs& a, cudaStream_t s) {
   const size_t smem = (size_t)TC_STAGES * TC_A_STAGE + (size_t)TC_STAGES * BN * 128 +
-                      (2 * TC_STAGES + 1) * 8 + 16;
+                      (2 * TC_STAGES + 4) * 8 + 16;
   static bool configured = false;
   if (!configured) {
     cudaFuncSetAttribute(k_conv_tc<BN>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     configured = true;
   }
+  if (!g_num_sms) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&g_num_sms, cudaDevAttrMultiProcessorCount, dev);
+  }
   const int64_t M = (int64_t)a.in.N * a.OH * a.OW;
-  dim3 g((unsigned)((M + TC_BM - 1) / TC_BM), (unsigned)((a.L.cout + BN - 1) / BN));
-  k_conv_tc<BN><<<g, TC_THREADS, smem, s>>>(a);
+  const int64_t tiles = ((M + TC_BM - 1) / TC_BM) * ((a.L.cout + BN - 1) / BN);
+  const int grid = (int)(tiles < g_num_sms ? tiles : g_num_sms);   // persistent: one CTA per SM
+  k_conv_tc<BN><<<grid, TC_THREADS, smem, s>>>(a);
 }
 
 void launch_conv_tc(const ConvTcArgs& a, int bn, cudaStream_t s) {

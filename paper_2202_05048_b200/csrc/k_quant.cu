@@ -189,13 +189,36 @@ __global__ void k_layer_params(const LayerSt* __restrict__ layers, const float* 
   const LayerSt L = layers[blockIdx.x];
   const double sx = (double)as[L.in_hist], sy = (double)as[L.out_hist];
   const float* ws = L.wscale + (int64_t)wvar * L.cout;
+  const long long zx = az[L.in_hist];
+  __shared__ int slow;
+  if (threadIdx.x == 0) slow = 0;
+  __syncthreads();
   for (int o = threadIdx.x; o < L.cout; o += blockDim.x) {
     double sw = (double)ws[o];
-    double sxw = __dmul_rn(sx, sw);
-    L.mult[o] = __ddiv_rn(sxw, sy);
-    if (L.bias) L.biasq[o] = (int)clip32((long long)rha(__ddiv_rn((double)L.bias[o], sxw)));
-    else L.biasq[o] = 0;
+    double sxw = __dmul_rn(sx, sw);                     // s_in * s_w (quantize.py:178-179)
+    double m = __ddiv_rn(sxw, sy);                      // (sx * sw) / sy (intexec.py:201)
+    int bq = L.bias ? (int)clip32((long long)rha(__ddiv_rn((double)L.bias[o], sxw))) : 0;
+    L.mult[o] = m;
+    L.biasq[o] = bq;
+    if (L.ep) {
+      const long long zw = L.wzp8[(int64_t)wvar * L.cout + o];
+      const long long sw8 = L.wsum8[(int64_t)wvar * L.cout + o];
+      const long long cc = (long long)bq - zx * sw8 + (long long)L.kreal * zx * zw;
+      const bool big = cc >= (1LL << 30) || cc <= -(1LL << 30);
+      if (big) atomicOr(&slow, 1);
+      EpiParam e;
+      e.m = m;
+      e.cc = big ? 0 : (int)cc;
+      e.zw = (int)zw;
+      // saturation margins (not exactness-critical): any acc beyond them has |acc*m| > 300
+      const double hi = ceil(300.0 / m) + 1.0, lo = floor(-300.0 / m) - 1.0;
+      e.ahi = hi > 2147483647.0 ? 2147483647 : (int)hi;
+      e.alo = lo < -2147483648.0 ? (int)0x80000000 : (int)lo;
+      e.pad0 = e.pad1 = 0;
+      L.ep[o] = e;
+    }
   }
+  __syncthreads();
   if (threadIdx.x == 0) {
     LayerRt r;
     r.zx = az[L.in_hist];
@@ -208,12 +231,14 @@ __global__ void k_layer_params(const LayerSt* __restrict__ layers, const float* 
       r.zo = az[L.add_o_hist];
       r.ra = __ddiv_rn((double)as[L.add_a_hist], so);
       r.rb = __ddiv_rn((double)as[L.add_b_hist], so);
+      // the fast add path floors via a 2^52 magic add: needs |xs*ra + ys*rb| < 2^50
+      if (!(r.ra + r.rb < 1e12)) slow = 1;
     } else {
       r.za = r.zb = r.zo = 0;
       r.ra = r.rb = 0.0;
     }
     r.add_relu_zp = L.add_relu_hist >= 0 ? az[L.add_relu_hist] : INT_MIN;
-    r.pad_ = 0;
+    r.slow = slow;
     *L.rt = r;
   }
 }
@@ -312,7 +337,12 @@ __global__ void k_halo_fill(View v, const int* __restrict__ az, int hist) {
     int h = (int)((p / Wp) % Hp);
     if (h >= v.halo && h < v.halo + v.H && w >= v.halo && w < v.halo + v.W) continue;
     int8_t* d = v.p + p * v.Cp;
-    for (int c = 0; c < v.Cp; ++c) d[c] = z;
+    for (int c0 = 0; c0 < v.Cp; c0 += 16) {
+      alignas(16) int8_t b[16];
+#pragma unroll
+      for (int j = 0; j < 16; ++j) b[j] = (c0 + j < v.C) ? z : (int8_t)0;  // pad channels stay 0
+      *reinterpret_cast<int4*>(d + c0) = *reinterpret_cast<const int4*>(b);
+    }
   }
 }
 void launch_halo_fill(View v, const int* az, int hist, cudaStream_t s) {
@@ -437,9 +467,16 @@ __global__ void k_pixsum(View in, int* __restrict__ P) {
   const int64_t total = (int64_t)in.N * (in.H + 2 * in.halo) * (in.W + 2 * in.halo);
   for (int64_t p = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; p < total;
        p += (int64_t)gridDim.x * blockDim.x) {
-    const int8_t* q = in.p + p * in.Cp;
+    // pad channels always hold code 0, so the whole Cp-byte pixel can be summed
+    const int4* q = reinterpret_cast<const int4*>(in.p + p * in.Cp);
     int s = 0;
-    for (int c = 0; c < in.C; ++c) s += q[c];
+    for (int j = 0; j < (in.Cp >> 4); ++j) {
+      int4 v = __ldg(q + j);
+      s = __dp4a(v.x, 0x01010101, s);
+      s = __dp4a(v.y, 0x01010101, s);
+      s = __dp4a(v.z, 0x01010101, s);
+      s = __dp4a(v.w, 0x01010101, s);
+    }
     P[p] = s;
   }
 }

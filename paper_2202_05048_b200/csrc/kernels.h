@@ -20,7 +20,17 @@ struct LayerRt {
   int za, zb, zo;      // fused add: operand zps and add output zp
   double ra, rb;       // fused add: s_a / s_o and s_b / s_o (operand order of the add node)
   int add_relu_zp;     // relu fused after the add (or INT32_MIN)
-  int pad_;
+  int slow;            // 1: some |cc| >= 2^30, the epilogue must clip acc to int32 in 64-bit
+};
+
+// per-config, per-output-channel epilogue constants of the tensor-core conv:
+//   acc = dot - zw*rowsum + cc  (cc = bias - zx*sum(w) + K*zx*zw), out = requant(acc, m)
+struct alignas(16) EpiParam {
+  double m;
+  int cc;              // valid when the layer's rt.slow == 0 (|cc| < 2^30, no int32 clip possible)
+  int zw;
+  int alo, ahi;        // acc clamp: outside [alo, ahi] |acc*m| > 300, so the code saturates anyway
+  int pad0, pad1;
 };
 
 // static description of one int8 compute layer (conv / pointwise / depthwise / fc)
@@ -35,6 +45,10 @@ struct LayerSt {
   double* mult;                 // [cout] per-config requant multipliers (out)
   int* biasq;                   // [cout] per-config int32 bias codes (out)
   LayerRt* rt;                  // per-config scalars (out)
+  const int* wzp8;              // [8][cout] weight zero points (tensor-core layers)
+  const int* wsum8;             // [8][cout] sum of weight codes
+  int kreal;                    // real K = k*k*Cin
+  EpiParam* ep;                 // [cout] per-config epilogue constants (out), or nullptr
 };
 
 // ---------------------------------------------------------------- F1 / F2 (k_calib.cu)

@@ -82,6 +82,7 @@ struct WeightsDev {
   double* mult = nullptr;       // [cout]
   int* biasq = nullptr;         // [cout]
   LayerRt* rt = nullptr;
+  EpiParam* ep = nullptr;       // [cout] tensor-core epilogue constants
 };
 
 struct Plan {
@@ -344,6 +345,7 @@ void import_graph(ptq_ctx* c, const ptq_graph_desc* g) {
     wd.mult = c->dalloc<double>(wd.cout);
     wd.biasq = c->dalloc<int>(wd.cout);
     wd.rt = c->dalloc<LayerRt>(1);
+    wd.ep = c->dalloc<EpiParam>(wd.cout);
   }
 }
 
@@ -442,10 +444,22 @@ void build_plan(ptq_ctx* c, int mixed) {
       for (int t : c->nodes[i].in) REQ(P.psrc[t] < 0, "unsupported mixed prefix");
   }
   // fusion of relu / add(+relu) into int8 compute epilogues (and relu into the mixed prefix quantize)
+  std::vector<char> materialized(c->T, 0);
+  materialized[0] = 1;
   for (int i = 0; i < N; ++i) {
     const NodeI& n = c->nodes[i];
-    if (!is_compute(n.kind)) continue;
+    if (P.skip[i]) continue;
+    if (!is_compute(n.kind)) {
+      materialized[n.out] = 1;
+      continue;
+    }
     P.mat[i] = n.out;
+    struct MarkMat {
+      std::vector<char>& m;
+      Plan& P;
+      int i;
+      ~MarkMat() { m[P.mat[i]] = 1; }
+    } mark{materialized, P, i};
     const bool int8_out = P.psrc[n.out] >= 0;
     if (!int8_out || !c->fusion) continue;
     if (P.fp32node[i] && i != c->first_compute) continue;
@@ -461,12 +475,8 @@ void build_plan(ptq_ctx* c, int mixed) {
                !P.fp32node[i]) {
       const int other = cons.in[0] == n.out ? cons.in[1] : cons.in[0];
       if (other == n.out) continue;
-      const int op = c->tens[other].producer;
-      if (op >= i) continue;                         // other operand not ready yet
-      // the other operand must be materialised (not fused into its producer)
-      bool other_mat = (other == 0) || P.mat[op] == other || !is_compute(c->nodes[op].kind);
-      if (op >= 0 && !is_compute(c->nodes[op].kind) && P.skip[op]) other_mat = false;
-      if (!other_mat) continue;
+      // the other operand must already be materialised when this conv runs
+      if (!materialized[other]) continue;
       P.add_node[i] = cn;
       P.add_other[i] = other;
       P.add_is_a[i] = cons.in[0] == n.out;
@@ -505,6 +515,10 @@ void build_plan(ptq_ctx* c, int mixed) {
     L.mult = wd.mult;
     L.biasq = wd.biasq;
     L.rt = wd.rt;
+    L.wzp8 = wd.zp;
+    L.wsum8 = wd.wsum;
+    L.kreal = wd.kreal;
+    L.ep = n.kind == PTQ_DWCONV ? nullptr : wd.ep;
     P.layer_of[i] = (int)P.h_layers.size();
     P.h_layers.push_back(L);
   }
