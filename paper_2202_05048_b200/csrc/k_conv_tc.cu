@@ -98,36 +98,52 @@ __device__ __forceinline__ int floor_i(double r) {
 }
 __device__ __forceinline__ int clampi(int x, int lo, int hi) { return x < lo ? lo : (x > hi ? hi : x); }
 
-// clip(RHU(acc*m) + zp, lo, 127) with acc pre-clamped to the saturation margins
-__device__ __forceinline__ int requant_fast(int acc, const EpiParam& e, int zp, int lo) {
-  acc = clampi(acc, e.alo, e.ahi);
-  const double r = __dadd_rn(__dmul_rn(i2d(acc), e.m), 0.5);   // fl(fl(acc*m) + 0.5)
-  return clampi(floor_i(r) + zp, lo, PTQ_QMAX);
+__device__ __forceinline__ int imin(int a, int b) { return a < b ? a : b; }
+__device__ __forceinline__ int imax(int a, int b) { return a > b ? a : b; }
+
+// clip(RHU(acc*m) + zp, lo, 127): acc clamped to the layer's saturation margin, then
+// fl(fl(acc*m) + 0.5) exactly as the reference, floor and +zp in one round-down add
+__device__ __forceinline__ int requant_fast(int acc, double m, const LayerRt& rt, int lo) {
+  acc = imin(imax(acc, -rt.aclamp), rt.aclamp);
+  const double r = __dadd_rn(__dmul_rn(i2d(acc), m), 0.5);
+  return imin(imax(__double2loint(__dadd_rd(r, rt.mg_zy)), lo), PTQ_QMAX);
 }
-// residual add on codes (intexec.py:245-276): clip(RHU(xs*ra + ys*rb) + zo)
-__device__ __forceinline__ int add_fast(int xa, int xb, const LayerRt& rt, int lo) {
-  const double s = __dadd_rn(__dmul_rn(i2d(xa - rt.za), rt.ra), __dmul_rn(i2d(xb - rt.zb), rt.rb));
-  return clampi(floor_i(__dadd_rn(s, 0.5)) + rt.zo, lo, PTQ_QMAX);
+// residual add on codes (intexec.py:245-276): clip(RHU(xs*ra + ys*rb) + zo); the two
+// products come from 256-entry tables of fl((code - z) * r) (same fp64 op, precomputed)
+__device__ __forceinline__ int add_fast(int ca, int cb, const double* ta, const double* tb,
+                                        const LayerRt& rt, int lo) {
+  const double s = __dadd_rn(__dadd_rn(ta[ca + 128], tb[cb + 128]), 0.5);
+  return imin(imax(__double2loint(__dadd_rd(s, rt.mg_zo)), lo), PTQ_QMAX);
 }
 
 // 16 output channels of one row, fast path (no int32 saturation possible)
-template <bool SKIP, bool CONV_A>
+template <bool WZP, bool SKIP, bool CONV_A>
 __device__ __forceinline__ void epi_chunk16(const uint32_t (&v)[16], const EpiParam* __restrict__ ep,
                                             int cb, int rowsum, const LayerRt& rt, int lo_conv,
-                                            int lo_add, const int8_t* sk, int8_t* codes) {
+                                            int lo_add, const int4 skv, const double* ta,
+                                            const double* tb, int4& out) {
+  uint32_t packed[4] = {0u, 0u, 0u, 0u};
+  const uint32_t skw[4] = {(uint32_t)skv.x, (uint32_t)skv.y, (uint32_t)skv.z, (uint32_t)skv.w};
 #pragma unroll
-  for (int g = 0; g < 2; ++g) {
-    EpiParam e[8];
+  for (int g = 0; g < 4; ++g) {
+    int4 raw[4];
 #pragma unroll
-    for (int j = 0; j < 8; ++j) e[j] = ep[cb + g * 8 + j];       // batched broadcast loads
+    for (int j = 0; j < 4; ++j) raw[j] = __ldg(reinterpret_cast<const int4*>(ep + cb + g * 4) + j);
 #pragma unroll
-    for (int j = 0; j < 8; ++j) {
-      const int jj = g * 8 + j;
-      int q = requant_fast((int)v[jj] - e[j].zw * rowsum + e[j].cc, e[j], rt.zy, lo_conv);
-      if (SKIP) q = CONV_A ? add_fast(q, sk[jj], rt, lo_add) : add_fast(sk[jj], q, rt, lo_add);
-      codes[jj] = (int8_t)q;
+    for (int j = 0; j < 4; ++j) {
+      const int jj = g * 4 + j;
+      const double m = __hiloint2double(raw[j].y, raw[j].x);
+      int acc = (int)v[jj] + raw[j].z;
+      if (WZP) acc -= raw[j].w * rowsum;
+      int q = requant_fast(acc, m, rt, lo_conv);
+      if (SKIP) {
+        const int s = (int)(int8_t)(skw[jj >> 2] >> (8 * (jj & 3)));
+        q = CONV_A ? add_fast(q, s, ta, tb, rt, lo_add) : add_fast(s, q, ta, tb, rt, lo_add);
+      }
+      packed[jj >> 2] |= ((uint32_t)q & 0xffu) << (8 * (jj & 3));
     }
   }
+  out = make_int4((int)packed[0], (int)packed[1], (int)packed[2], (int)packed[3]);
 }
 // general (slow) path: 64-bit accumulator with the reference's int32 saturation
 __device__ __forceinline__ int epi_slow(long long dot, int c, long long rowsum, const ConvTcArgs& a,
@@ -175,6 +191,7 @@ __global__ void __launch_bounds__(TC_THREADS, 1) k_conv_tc(const __grid_constant
   uint64_t* tfull = empty + TC_STAGES;
   uint64_t* tempty = tfull + 2;
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
+  double* add_tab = reinterpret_cast<double*>(tempty + 4);     // [2][256]
   constexpr uint32_t TMEM_COLS = (2 * BN) < 32 ? 32 : 2 * BN;
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -291,6 +308,17 @@ __global__ void __launch_bounds__(TC_THREADS, 1) k_conv_tc(const __grid_constant
     const int lo_add = rt.add_relu_zp > PTQ_QMIN ? rt.add_relu_zp : PTQ_QMIN;
     const int Cout = a.L.cout;
     const EpiParam* __restrict__ ep = a.L.ep;
+    // 256-entry tables of the add's two fp64 products fl((code - z) * r) (intexec.py:269-270)
+    double* ta = add_tab;
+    double* tb = add_tab + 256;
+    if (a.skip.p) {
+      for (int i = threadIdx.x - 6 * 32; i < 256; i += TC_EPI_WARPS * 32) {
+        ta[i] = __dmul_rn(i2d(i - 128 - rt.za), rt.ra);
+        tb[i] = __dmul_rn(i2d(i - 128 - rt.zb), rt.rb);
+      }
+      asm volatile("bar.sync 1, %0;" ::"n"(TC_EPI_WARPS * 32) : "memory");
+    }
+    const bool wzp = a.has_wzp != 0;
     uint32_t lt = 0;
     for (int64_t tile = blockIdx.x; tile < n_tiles; tile += gridDim.x, ++lt) {
       const uint32_t buf = lt & 1u, uph = (lt >> 1) & 1u;
@@ -308,27 +336,43 @@ __global__ void __launch_bounds__(TC_THREADS, 1) k_conv_tc(const __grid_constant
         tmem_ld16(tmem + ((uint32_t)(q * 32) << 16) + buf * BN + (uint32_t)c0, v);
         const int cb = nt * BN + c0;
         if (!g.ok || cb >= a.out.Cp) continue;
-        alignas(16) int8_t codes[16];
-        alignas(16) int8_t sk[16];
-        if (srow) *reinterpret_cast<int4*>(sk) = *reinterpret_cast<const int4*>(srow + cb);
+        const int4 skv = srow ? *reinterpret_cast<const int4*>(srow + cb) : make_int4(0, 0, 0, 0);
+        int4 res;
         if (!rt.slow && cb + 16 <= Cout) {
-          if (!srow) epi_chunk16<false, false>(v, ep, cb, (int)rowsum, rt, lo_conv, lo_add, sk, codes);
-          else if (a.conv_is_a) epi_chunk16<true, true>(v, ep, cb, (int)rowsum, rt, lo_conv, lo_add, sk, codes);
-          else epi_chunk16<true, false>(v, ep, cb, (int)rowsum, rt, lo_conv, lo_add, sk, codes);
+          const int rs = (int)rowsum;
+          if (!srow) {
+            if (wzp) epi_chunk16<true, false, false>(v, ep, cb, rs, rt, lo_conv, lo_add, skv, ta, tb, res);
+            else epi_chunk16<false, false, false>(v, ep, cb, rs, rt, lo_conv, lo_add, skv, ta, tb, res);
+          } else if (a.conv_is_a) {
+            if (wzp) epi_chunk16<true, true, true>(v, ep, cb, rs, rt, lo_conv, lo_add, skv, ta, tb, res);
+            else epi_chunk16<false, true, true>(v, ep, cb, rs, rt, lo_conv, lo_add, skv, ta, tb, res);
+          } else {
+            if (wzp) epi_chunk16<true, true, false>(v, ep, cb, rs, rt, lo_conv, lo_add, skv, ta, tb, res);
+            else epi_chunk16<false, true, false>(v, ep, cb, rs, rt, lo_conv, lo_add, skv, ta, tb, res);
+          }
         } else {
-#pragma unroll
+          // exact 64-bit path (int32 saturation possible) and partial channel chunks
+          const int8_t* sk = reinterpret_cast<const int8_t*>(&skv);
+          alignas(16) int8_t codes[16];
+#pragma unroll 1
           for (int j = 0; j < 16; ++j) {
             const int c = cb + j;
             int code = 0;
             if (c < Cout) {
               code = epi_slow((long long)(int)v[j], c, rowsum, a, rt);
               if (code < lo_conv) code = lo_conv;
-              if (srow) code = a.conv_is_a ? add_fast(code, sk[j], rt, lo_add) : add_fast(sk[j], code, rt, lo_add);
+              if (srow) {
+                const int xa = a.conv_is_a ? code : sk[j], xb = a.conv_is_a ? sk[j] : code;
+                const double s2 = __dadd_rn(__dmul_rn(i2d(xa - rt.za), rt.ra), __dmul_rn(i2d(xb - rt.zb), rt.rb));
+                code = clip8(rhu(s2) + (double)rt.zo);
+                if (code < lo_add) code = lo_add;
+              }
             }
             codes[j] = (int8_t)code;
           }
+          res = *reinterpret_cast<const int4*>(codes);
         }
-        *reinterpret_cast<int4*>(orow + cb) = *reinterpret_cast<int4*>(codes);
+        *reinterpret_cast<int4*>(orow + cb) = res;
       }
       tc_fence_before();
       mbar_arrive(&tempty[buf]);                     // accumulator buffer may be reused
@@ -396,7 +440,7 @@ static int g_num_sms = 0;
 template <int BN>
 static void launch_bn(const ConvTcArgs& a, cudaStream_t s) {
   const size_t smem = (size_t)TC_STAGES * TC_A_STAGE + (size_t)TC_STAGES * BN * 128 +
-                      (2 * TC_STAGES + 4) * 8 + 16;
+                      (2 * TC_STAGES + 4) * 8 + 16 + 512 * 8;
   static bool configured = false;
   if (!configured) {
     cudaFuncSetAttribute(k_conv_tc<BN>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);

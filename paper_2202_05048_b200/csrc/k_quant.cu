@@ -191,7 +191,12 @@ __global__ void k_layer_params(const LayerSt* __restrict__ layers, const float* 
   const float* ws = L.wscale + (int64_t)wvar * L.cout;
   const long long zx = az[L.in_hist];
   __shared__ int slow;
-  if (threadIdx.x == 0) slow = 0;
+  __shared__ unsigned long long m_max_bits, m_min_bits;   // m > 0: bit order == value order
+  if (threadIdx.x == 0) {
+    slow = 0;
+    m_max_bits = 0ull;
+    m_min_bits = ~0ull;
+  }
   __syncthreads();
   for (int o = threadIdx.x; o < L.cout; o += blockDim.x) {
     double sw = (double)ws[o];
@@ -210,17 +215,26 @@ __global__ void k_layer_params(const LayerSt* __restrict__ layers, const float* 
       e.m = m;
       e.cc = big ? 0 : (int)cc;
       e.zw = (int)zw;
-      // saturation margins (not exactness-critical): any acc beyond them has |acc*m| > 300
-      const double hi = ceil(300.0 / m) + 1.0, lo = floor(-300.0 / m) - 1.0;
-      e.ahi = hi > 2147483647.0 ? 2147483647 : (int)hi;
-      e.alo = lo < -2147483648.0 ? (int)0x80000000 : (int)lo;
-      e.pad0 = e.pad1 = 0;
       L.ep[o] = e;
+      if (!(m > 0.0) || !isfinite(m)) atomicOr(&slow, 1);
+      atomicMax(&m_max_bits, (unsigned long long)__double_as_longlong(m));
+      atomicMin(&m_min_bits, (unsigned long long)__double_as_longlong(m));
     }
   }
   __syncthreads();
   if (threadIdx.x == 0) {
     LayerRt r;
+    // fast-path acc clamp: |A*m| <= 2^30 for every channel, and A*m > 300 for every channel
+    // (so clamped accumulators still saturate exactly as the unclamped ones would)
+    r.aclamp = 0;
+    if (L.ep && !slow) {
+      const double mmax = __longlong_as_double((long long)m_max_bits);
+      const double mmin = __longlong_as_double((long long)m_min_bits);
+      const double A = floor(1073741824.0 / mmax);
+      const double need = ceil(300.0 / mmin) + 2.0;
+      if (A >= need) r.aclamp = A > 2147483647.0 ? 2147483647 : (int)A;
+      else slow = 1;
+    }
     r.zx = az[L.in_hist];
     r.zy = az[L.out_hist];
     r.relu_zp = L.relu_hist >= 0 ? az[L.relu_hist] : INT_MIN;
@@ -239,6 +253,8 @@ __global__ void k_layer_params(const LayerSt* __restrict__ layers, const float* 
     }
     r.add_relu_zp = L.add_relu_hist >= 0 ? az[L.add_relu_hist] : INT_MIN;
     r.slow = slow;
+    r.mg_zy = 6755399441055744.0 + (double)r.zy;
+    r.mg_zo = 6755399441055744.0 + (double)r.zo;
     *L.rt = r;
   }
 }

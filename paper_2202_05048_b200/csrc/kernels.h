@@ -20,7 +20,10 @@ struct LayerRt {
   int za, zb, zo;      // fused add: operand zps and add output zp
   double ra, rb;       // fused add: s_a / s_o and s_b / s_o (operand order of the add node)
   int add_relu_zp;     // relu fused after the add (or INT32_MIN)
-  int slow;            // 1: some |cc| >= 2^30, the epilogue must clip acc to int32 in 64-bit
+  int slow;            // 1: the fast epilogue's range preconditions fail -> exact 64-bit path
+  int aclamp;          // fast path clamps acc to [-aclamp, aclamp]: beyond it every channel
+                       // saturates (|acc*m| > 300) and |acc*m| stays < 2^30 for the floor trick
+  double mg_zy, mg_zo; // 1.5*2^52 + zp: floor(r) + zp via one round-down add
 };
 
 // per-config, per-output-channel epilogue constants of the tensor-core conv:
@@ -29,8 +32,6 @@ struct alignas(16) EpiParam {
   double m;
   int cc;              // valid when the layer's rt.slow == 0 (|cc| < 2^30, no int32 clip possible)
   int zw;
-  int alo, ahi;        // acc clamp: outside [alo, ahi] |acc*m| > 300, so the code saturates anyway
-  int pad0, pad1;
 };
 
 // static description of one int8 compute layer (conv / pointwise / depthwise / fc)
