@@ -108,20 +108,17 @@ __device__ __forceinline__ int requant_fast(int acc, double m, const LayerRt& rt
   const double r = __dadd_rn(__dmul_rn(i2d(acc), m), 0.5);
   return imin(imax(__double2loint(__dadd_rd(r, rt.mg_zy)), lo), PTQ_QMAX);
 }
-// residual add on codes (intexec.py:245-276): clip(RHU(xs*ra + ys*rb) + zo); the two
-// products come from 256-entry tables of fl((code - z) * r) (same fp64 op, precomputed)
-__device__ __forceinline__ int add_fast(int ca, int cb, const double* ta, const double* tb,
-                                        const LayerRt& rt, int lo) {
-  const double s = __dadd_rn(__dadd_rn(ta[ca + 128], tb[cb + 128]), 0.5);
-  return imin(imax(__double2loint(__dadd_rd(s, rt.mg_zo)), lo), PTQ_QMAX);
+// residual add on codes (intexec.py:245-276): clip(RHU(xs*ra + ys*rb) + zo)
+__device__ __forceinline__ int add_fast(int ca, int cb, const LayerRt& rt, int lo) {
+  const double s = __dadd_rn(__dmul_rn(i2d(ca - rt.za), rt.ra), __dmul_rn(i2d(cb - rt.zb), rt.rb));
+  return imin(imax(__double2loint(__dadd_rd(__dadd_rn(s, 0.5), rt.mg_zo)), lo), PTQ_QMAX);
 }
 
 // 16 output channels of one row, fast path (no int32 saturation possible)
 template <bool WZP, bool SKIP, bool CONV_A>
 __device__ __forceinline__ void epi_chunk16(const uint32_t (&v)[16], const EpiParam* __restrict__ ep,
                                             int cb, int rowsum, const LayerRt& rt, int lo_conv,
-                                            int lo_add, const int4 skv, const double* ta,
-                                            const double* tb, int4& out) {
+                                            int lo_add, const int4 skv, int4& out) {
   uint32_t packed[4] = {0u, 0u, 0u, 0u};
   const uint32_t skw[4] = {(uint32_t)skv.x, (uint32_t)skv.y, (uint32_t)skv.z, (uint32_t)skv.w};
 #pragma unroll
@@ -138,7 +135,7 @@ __device__ __forceinline__ void epi_chunk16(const uint32_t (&v)[16], const EpiPa
       int q = requant_fast(acc, m, rt, lo_conv);
       if (SKIP) {
         const int s = (int)(int8_t)(skw[jj >> 2] >> (8 * (jj & 3)));
-        q = CONV_A ? add_fast(q, s, ta, tb, rt, lo_add) : add_fast(s, q, ta, tb, rt, lo_add);
+        q = CONV_A ? add_fast(q, s, rt, lo_add) : add_fast(s, q, rt, lo_add);
       }
       packed[jj >> 2] |= ((uint32_t)q & 0xffu) << (8 * (jj & 3));
     }
@@ -152,6 +149,31 @@ __device__ __forceinline__ int epi_slow(long long dot, int c, long long rowsum, 
   long long acc = dot - zw * rowsum - (long long)rt.zx * a.wsum[c] + (long long)a.kreal * rt.zx * zw;
   acc = clip32(acc + a.L.biasq[c]);
   return requant1(acc, a.L.mult[c], rt.zy);
+}
+
+// exact 64-bit path for a whole 16-channel chunk (int32 saturation possible, or a partial
+// chunk); kept out of line so it costs the hot loop no registers
+__device__ __noinline__ int4 epi_slow_chunk(const uint32_t* v, int cb, long long rowsum,
+                                            const ConvTcArgs& a, const LayerRt& rt, int lo_conv,
+                                            int lo_add, int4 skv) {
+  const int8_t* sk = reinterpret_cast<const int8_t*>(&skv);
+  uint32_t packed[4] = {0u, 0u, 0u, 0u};
+  for (int j = 0; j < 16; ++j) {
+    const int c = cb + j;
+    int code = 0;
+    if (c < a.L.cout) {
+      code = epi_slow((long long)(int)v[j], c, rowsum, a, rt);
+      if (code < lo_conv) code = lo_conv;
+      if (a.skip.p) {
+        const int xa = a.conv_is_a ? code : sk[j], xb = a.conv_is_a ? sk[j] : code;
+        const double s2 = __dadd_rn(__dmul_rn(i2d(xa - rt.za), rt.ra), __dmul_rn(i2d(xb - rt.zb), rt.rb));
+        code = clip8(rhu(s2) + (double)rt.zo);
+        if (code < lo_add) code = lo_add;
+      }
+    }
+    packed[j >> 2] |= ((uint32_t)code & 0xffu) << (8 * (j & 3));
+  }
+  return make_int4((int)packed[0], (int)packed[1], (int)packed[2], (int)packed[3]);
 }
 
 __device__ __forceinline__ long long pixel_rowsum(const ConvTcArgs& a, int n, int ih0, int iw0) {
@@ -191,7 +213,6 @@ __global__ void __launch_bounds__(TC_THREADS, 1) k_conv_tc(const __grid_constant
   uint64_t* tfull = empty + TC_STAGES;
   uint64_t* tempty = tfull + 2;
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
-  double* add_tab = reinterpret_cast<double*>(tempty + 4);     // [2][256]
   constexpr uint32_t TMEM_COLS = (2 * BN) < 32 ? 32 : 2 * BN;
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -308,16 +329,6 @@ __global__ void __launch_bounds__(TC_THREADS, 1) k_conv_tc(const __grid_constant
     const int lo_add = rt.add_relu_zp > PTQ_QMIN ? rt.add_relu_zp : PTQ_QMIN;
     const int Cout = a.L.cout;
     const EpiParam* __restrict__ ep = a.L.ep;
-    // 256-entry tables of the add's two fp64 products fl((code - z) * r) (intexec.py:269-270)
-    double* ta = add_tab;
-    double* tb = add_tab + 256;
-    if (a.skip.p) {
-      for (int i = threadIdx.x - 6 * 32; i < 256; i += TC_EPI_WARPS * 32) {
-        ta[i] = __dmul_rn(i2d(i - 128 - rt.za), rt.ra);
-        tb[i] = __dmul_rn(i2d(i - 128 - rt.zb), rt.rb);
-      }
-      asm volatile("bar.sync 1, %0;" ::"n"(TC_EPI_WARPS * 32) : "memory");
-    }
     const bool wzp = a.has_wzp != 0;
     uint32_t lt = 0;
     for (int64_t tile = blockIdx.x; tile < n_tiles; tile += gridDim.x, ++lt) {
@@ -341,36 +352,17 @@ __global__ void __launch_bounds__(TC_THREADS, 1) k_conv_tc(const __grid_constant
         if (!rt.slow && cb + 16 <= Cout) {
           const int rs = (int)rowsum;
           if (!srow) {
-            if (wzp) epi_chunk16<true, false, false>(v, ep, cb, rs, rt, lo_conv, lo_add, skv, ta, tb, res);
-            else epi_chunk16<false, false, false>(v, ep, cb, rs, rt, lo_conv, lo_add, skv, ta, tb, res);
+            if (wzp) epi_chunk16<true, false, false>(v, ep, cb, rs, rt, lo_conv, lo_add, skv, res);
+            else epi_chunk16<false, false, false>(v, ep, cb, rs, rt, lo_conv, lo_add, skv, res);
           } else if (a.conv_is_a) {
-            if (wzp) epi_chunk16<true, true, true>(v, ep, cb, rs, rt, lo_conv, lo_add, skv, ta, tb, res);
-            else epi_chunk16<false, true, true>(v, ep, cb, rs, rt, lo_conv, lo_add, skv, ta, tb, res);
+            if (wzp) epi_chunk16<true, true, true>(v, ep, cb, rs, rt, lo_conv, lo_add, skv, res);
+            else epi_chunk16<false, true, true>(v, ep, cb, rs, rt, lo_conv, lo_add, skv, res);
           } else {
-            if (wzp) epi_chunk16<true, true, false>(v, ep, cb, rs, rt, lo_conv, lo_add, skv, ta, tb, res);
-            else epi_chunk16<false, true, false>(v, ep, cb, rs, rt, lo_conv, lo_add, skv, ta, tb, res);
+            if (wzp) epi_chunk16<true, true, false>(v, ep, cb, rs, rt, lo_conv, lo_add, skv, res);
+            else epi_chunk16<false, true, false>(v, ep, cb, rs, rt, lo_conv, lo_add, skv, res);
           }
         } else {
-          // exact 64-bit path (int32 saturation possible) and partial channel chunks
-          const int8_t* sk = reinterpret_cast<const int8_t*>(&skv);
-          alignas(16) int8_t codes[16];
-#pragma unroll 1
-          for (int j = 0; j < 16; ++j) {
-            const int c = cb + j;
-            int code = 0;
-            if (c < Cout) {
-              code = epi_slow((long long)(int)v[j], c, rowsum, a, rt);
-              if (code < lo_conv) code = lo_conv;
-              if (srow) {
-                const int xa = a.conv_is_a ? code : sk[j], xb = a.conv_is_a ? sk[j] : code;
-                const double s2 = __dadd_rn(__dmul_rn(i2d(xa - rt.za), rt.ra), __dmul_rn(i2d(xb - rt.zb), rt.rb));
-                code = clip8(rhu(s2) + (double)rt.zo);
-                if (code < lo_add) code = lo_add;
-              }
-            }
-            codes[j] = (int8_t)code;
-          }
-          res = *reinterpret_cast<const int4*>(codes);
+          res = epi_slow_chunk(v, cb, rowsum, a, rt, lo_conv, lo_add, skv);
         }
         *reinterpret_cast<int4*>(orow + cb) = res;
       }
@@ -440,7 +432,7 @@ static int g_num_sms = 0;
 template <int BN>
 static void launch_bn(const ConvTcArgs& a, cudaStream_t s) {
   const size_t smem = (size_t)TC_STAGES * TC_A_STAGE + (size_t)TC_STAGES * BN * 128 +
-                      (2 * TC_STAGES + 4) * 8 + 16 + 512 * 8;
+                      (2 * TC_STAGES + 4) * 8 + 16;
   static bool configured = false;
   if (!configured) {
     cudaFuncSetAttribute(k_conv_tc<BN>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
