@@ -190,9 +190,17 @@ def run_b200(args):
         if world > 1:
             dist.barrier()
 
+    phases = {}
+
     def step():
+        t0 = time.perf_counter()
         ev.calibrate_all()                  # fp32 forward, min/max, histograms, KL, prepare
-        return ev.evaluate_grid(space)      # 96 configs (sharded over ranks)
+        t1 = time.perf_counter()
+        out = ev.evaluate_grid(space)       # 96 configs (sharded over ranks)
+        t2 = time.perf_counter()
+        phases["calibrate_prepare_s"] = round(t1 - t0, 4)
+        phases["eval_configs_s"] = round(t2 - t1, 4)
+        return out
 
     for _ in range(args.warmup):
         step()
@@ -276,7 +284,7 @@ def run_b200(args):
                 "roofline": roofline, "cpu_baseline": cb,
                 "e2e": {"value": len(space) / e2e_s, "unit": UNIT, "h2d_bytes_per_step": int(h2d),
                         "d2h_bytes_per_step": int(d2h)},
-                "gpu_launches": int(launches), "clocks": clk.summary(),
+                "gpu_launches": int(launches), "clocks": clk.summary(), "phases_wall": phases,
                 "best_config": space[best].to_dict(), "best_top1": int(counts[best]) / args.n_eval}
         print(json.dumps(line), flush=True)
     if world > 1:

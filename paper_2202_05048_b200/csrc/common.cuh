@@ -50,6 +50,21 @@ __device__ __forceinline__ int quant1(float x, double s64, double zp64) {
   return clip8(rha(__dadd_rn(__ddiv_rn((double)x, s64), zp64)));
 }
 
+// Same result as quant1 with a multiply by r = fl(1/s) instead of the division: the
+// fast value is within a few ulps of the reference's fl(fl(x/s) + zp), so whenever it is
+// farther than that from a half-integer both round (RHA) identically; otherwise (rare)
+// fall back to the exact division.
+__device__ __forceinline__ int quant1_fast(float x, double r, double s64, double zp64) {
+  const double t = __dadd_rn(__dmul_rn((double)x, r), zp64);
+  const double a = fabs(t);
+  const double fr = __dsub_rn(a, floor(a));
+  if (fabs(fr - 0.5) > 1e-14 * (a + 1.0)) {
+    const double q = floor(__dadd_rn(a, 0.5));
+    return clip8(t < 0.0 ? -q : q);
+  }
+  return quant1(x, s64, zp64);
+}
+
 // requantize an int32-clipped accumulator: clip(RHU(acc * m) + zp)   (ref intexec.py:72-85)
 __device__ __forceinline__ int requant1(long long acc, double m, int zp) {
   return clip8(rhu(__dmul_rn((double)acc, m)) + (double)zp);
@@ -147,7 +162,7 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
   asm volatile(
       "{\n\t.reg .pred P1;\n\t"
       "WAIT_%=:\n\t"
-      "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1;\n\t"
+      "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1, 10000000;\n\t"
       "@!P1 bra WAIT_%=;\n\t}" ::"r"(a),
       "r"(parity)
       : "memory");

@@ -137,16 +137,19 @@ __global__ void __launch_bounds__(512) k_histogram(const float* __restrict__ x, 
     return;
   }
   const int64_t stride = (int64_t)gridDim.x * blockDim.x;
-  for (int j = 0; j < n_slots; ++j) {
-    const float* img = x + (int64_t)slots[j] * elems;
-    const int64_t nv = ((((uintptr_t)img) & 15) == 0) ? (elems >> 2) : 0;
-    const float4* img4 = reinterpret_cast<const float4*>(img);
-    for (int64_t base = blockIdx.x * (int64_t)blockDim.x; base < nv; base += stride) {
-      const int64_t i = base + threadIdx.x;
-      const bool valid = i < nv;
+  // every per-image slice is 16-byte aligned (elems % 4 == 0) except for tiny tensors:
+  // flatten (image, float4) work items so small tensors still spread over all blocks
+  const bool vec = (elems & 3) == 0 && ((((uintptr_t)x) & 15) == 0);
+  const int64_t nv = vec ? (elems >> 2) : 0;
+  const int64_t total_v = nv * n_slots;
+  {
+    for (int64_t base = blockIdx.x * (int64_t)blockDim.x; base < total_v; base += stride) {
+      const int64_t w = base + threadIdx.x;
+      const bool valid = w < total_v;
       int b[4] = {0, 0, 0, 0};
       if (valid) {
-        const float4 v = __ldg(img4 + i);
+        const int j = (int)(w / nv);
+        const float4 v = __ldg(reinterpret_cast<const float4*>(x + (int64_t)slots[j] * elems) + (w - (int64_t)j * nv));
         b[0] = np_bin_fast((double)v.x, lo, hi, denom, rc, eps);
         b[1] = np_bin_fast((double)v.y, lo, hi, denom, rc, eps);
         b[2] = np_bin_fast((double)v.z, lo, hi, denom, rc, eps);
@@ -162,8 +165,14 @@ __global__ void __launch_bounds__(512) k_histogram(const float* __restrict__ x, 
         }
       }
     }
-    for (int64_t i = nv * 4 + blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < elems; i += stride)
-      atomicAdd(&sh[np_bin_fast((double)__ldg(img + i), lo, hi, denom, rc, eps)], 1u);
+  }
+  if (!vec) {                             // scalar path (element count not a multiple of 4)
+    const int64_t total = elems * n_slots;
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < total; i += stride) {
+      const int j = (int)(i / elems);
+      const float v = __ldg(x + (int64_t)slots[j] * elems + (i - (int64_t)j * elems));
+      atomicAdd(&sh[np_bin_fast((double)v, lo, hi, denom, rc, eps)], 1u);
+    }
   }
   __syncthreads();
   for (int i = threadIdx.x; i < PTQ_NBINS; i += blockDim.x)

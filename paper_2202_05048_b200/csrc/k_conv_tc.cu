@@ -153,9 +153,11 @@ __device__ __forceinline__ int epi_slow(long long dot, int c, long long rowsum, 
 
 // exact 64-bit path for a whole 16-channel chunk (int32 saturation possible, or a partial
 // chunk); kept out of line so it costs the hot loop no registers
-__device__ __noinline__ int4 epi_slow_chunk(const uint32_t* v, int cb, long long rowsum,
+__device__ __noinline__ int4 epi_slow_chunk(uint32_t taddr, int cb, long long rowsum,
                                             const ConvTcArgs& a, const LayerRt& rt, int lo_conv,
                                             int lo_add, int4 skv) {
+  uint32_t v[16];
+  tmem_ld16(taddr, v);                      // warp-uniform branch: re-read the accumulators
   const int8_t* sk = reinterpret_cast<const int8_t*>(&skv);
   uint32_t packed[4] = {0u, 0u, 0u, 0u};
   for (int j = 0; j < 16; ++j) {
@@ -346,7 +348,7 @@ __global__ void __launch_bounds__(TC_THREADS, 1) k_conv_tc(const __grid_constant
         uint32_t v[16];
         tmem_ld16(tmem + ((uint32_t)(q * 32) << 16) + buf * BN + (uint32_t)c0, v);
         const int cb = nt * BN + c0;
-        if (!g.ok || cb >= a.out.Cp) continue;
+        if (cb >= a.out.Cp) continue;            // warp-uniform: the slow path re-reads TMEM
         const int4 skv = srow ? *reinterpret_cast<const int4*>(srow + cb) : make_int4(0, 0, 0, 0);
         int4 res;
         if (!rt.slow && cb + 16 <= Cout) {
@@ -362,9 +364,10 @@ __global__ void __launch_bounds__(TC_THREADS, 1) k_conv_tc(const __grid_constant
             else epi_chunk16<false, true, false>(v, ep, cb, rs, rt, lo_conv, lo_add, skv, res);
           }
         } else {
-          res = epi_slow_chunk(v, cb, rowsum, a, rt, lo_conv, lo_add, skv);
+          res = epi_slow_chunk(tmem + ((uint32_t)(q * 32) << 16) + buf * BN + (uint32_t)c0, cb, rowsum,
+                               a, rt, lo_conv, lo_add, skv);
         }
-        *reinterpret_cast<int4*>(orow + cb) = res;
+        if (g.ok) *reinterpret_cast<int4*>(orow + cb) = res;
       }
       tc_fence_before();
       mbar_arrive(&tempty[buf]);                     // accumulator buffer may be reused

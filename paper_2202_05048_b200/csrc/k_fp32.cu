@@ -199,6 +199,27 @@ __global__ void k_softmax_f32(const float* __restrict__ x, int64_t rows, int C, 
   for (int c = lane; c < C; c += 32) y[r * C + c] = expf(p[c] - mx) / s;
 }
 
+// fp32 GEMM weight [K][cout] (K in NHWC order) from the reference layout: conv OIHW
+// (K = (kh*k + kw)*cin + c) or fc (O, C*H*W) flattened NCHW (K = p*cin + c, p = h*W + w)
+__global__ void k_gemm_weight(const float* __restrict__ w, int cout, int cin, int k, int hw,
+                              float* __restrict__ out, int64_t total) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < total;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    const int o = (int)(i % cout);
+    const int64_t kidx = i / cout;
+    const int ci = (int)(kidx % cin);
+    const int64_t t = kidx / cin;
+    int64_t src;
+    if (hw > 0) {
+      src = ((int64_t)o * cin + ci) * hw + t;
+    } else {
+      const int a = (int)(t / k), b = (int)(t % k);
+      src = (((int64_t)o * cin + ci) * k + a) * k + b;
+    }
+    out[i] = __ldg(w + src);
+  }
+}
+
 // ---------------------------------------------------------------- launch wrappers
 static inline int gblk(int64_t n) {
   int64_t b = (n + 255) / 256;
@@ -220,6 +241,10 @@ void launch_dwconv_f32(const float* x, int N, int H, int W, int C, const float* 
                        cudaStream_t s) {
   k_dwconv_f32<<<gblk((int64_t)N * OH * OW * C), 256, 0, s>>>(x, N, H, W, C, w, bias, k, stride,
                                                              pad, OH, OW, y);
+}
+void launch_gemm_weight(const float* w, int cout, int cin, int k, int hw, float* out, cudaStream_t s) {
+  const int64_t total = (int64_t)cout * cin * (hw > 0 ? hw : k * k);
+  k_gemm_weight<<<gblk(total), 256, 0, s>>>(w, cout, cin, k, hw, out, total);
 }
 void launch_relu_f32(const float* x, float* y, int64_t n, cudaStream_t s) {
   k_relu_f32<<<gblk(n), 256, 0, s>>>(x, y, n);

@@ -268,6 +268,7 @@ void launch_layer_params(const LayerSt* d_layers, int n_layers, const float* act
 __global__ void k_quant_input(const float* __restrict__ imgs, int64_t img0, View out,
                               const float* __restrict__ as, const int* __restrict__ az, int hist) {
   const double s = (double)as[hist], z = (double)az[hist];
+  const double rs = __ddiv_rn(1.0, s);
   const int64_t npix = (int64_t)out.N * out.H * out.W;
   const int64_t plane = (int64_t)out.H * out.W;
   for (int64_t p = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; p < npix;
@@ -282,7 +283,7 @@ __global__ void k_quant_input(const float* __restrict__ imgs, int64_t img0, View
 #pragma unroll
       for (int j = 0; j < 16; ++j) {
         int c = c0 + j;
-        v[j] = c < out.C ? (int8_t)quant1(__ldg(src + (int64_t)c * plane), s, z) : (int8_t)0;
+        v[j] = c < out.C ? (int8_t)quant1_fast(__ldg(src + (int64_t)c * plane), rs, s, z) : (int8_t)0;
       }
       *reinterpret_cast<int4*>(dst + c0) = *reinterpret_cast<int4*>(v);
     }
@@ -297,6 +298,7 @@ void launch_quant_input(const float* imgs, int64_t img0, View out, const float* 
 __global__ void k_quant_nhwc(const float* __restrict__ x, View out, const float* __restrict__ as,
                              const int* __restrict__ az, int hist, int relu_hist) {
   const double s = (double)as[hist], z = (double)az[hist];
+  const double rs = __ddiv_rn(1.0, s);
   const int rz = relu_hist >= 0 ? az[relu_hist] : INT_MIN;
   const int64_t total = (int64_t)out.N * out.H * out.W * out.Cp;
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < total;
@@ -309,7 +311,7 @@ __global__ void k_quant_nhwc(const float* __restrict__ x, View out, const float*
     int n = (int)(t / out.H);
     int8_t code = 0;
     if (c < out.C) {
-      int q = quant1(__ldg(x + p * out.C + c), s, z);
+      int q = quant1_fast(__ldg(x + p * out.C + c), rs, s, z);
       code = (int8_t)(q > rz ? q : rz);
     }
     out.p[voff(out, n, h, w) + c] = code;
@@ -387,43 +389,59 @@ void launch_relu_codes(View in, View out, const int* az, int hist, cudaStream_t 
 }
 
 // mode 0: max; mode 1: avg = requant(sum - zp*area, 1.0/area, zp)
+// one thread per (output pixel, 16-channel chunk): 16-byte loads, SIMD byte max
 __global__ void k_pool_codes(View in, View out, int k, int stride, int mode,
                              const int* __restrict__ az, int hist) {
   const int z = az[hist];
   const int area = k * k;
   const double m = __ddiv_rn(1.0, (double)area);
-  const int64_t total = (int64_t)out.N * out.H * out.W * out.Cp;
+  const int nch = out.Cp >> 4;
+  const int64_t total = (int64_t)out.N * out.H * out.W * nch;
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < total;
        i += (int64_t)gridDim.x * blockDim.x) {
-    int c = (int)(i % out.Cp);
-    int64_t p = i / out.Cp;
-    int ow = (int)(p % out.W);
-    int64_t t = p / out.W;
-    int oh = (int)(t % out.H), n = (int)(t / out.H);
-    int8_t r = 0;
-    if (c < out.C) {
-      if (mode == 0) {
-        int mx = -128;
-        for (int kh = 0; kh < k; ++kh)
-          for (int kw = 0; kw < k; ++kw) {
-            int v = in.p[voff(in, n, oh * stride + kh, ow * stride + kw) + c];
-            mx = v > mx ? v : mx;
-          }
-        r = (int8_t)mx;
-      } else {
-        long long sum = 0;
-        for (int kh = 0; kh < k; ++kh)
-          for (int kw = 0; kw < k; ++kw) sum += in.p[voff(in, n, oh * stride + kh, ow * stride + kw) + c];
-        r = (int8_t)requant1(sum - (long long)z * area, m, z);
+    const int c0 = (int)(i % nch) * 16;
+    const int64_t p = i / nch;
+    const int ow = (int)(p % out.W);
+    const int64_t t = p / out.W;
+    const int oh = (int)(t % out.H), n = (int)(t / out.H);
+    int4 r;
+    if (mode == 0) {
+      uint32_t mx[4] = {0x80808080u, 0x80808080u, 0x80808080u, 0x80808080u};
+      for (int kh = 0; kh < k; ++kh)
+        for (int kw = 0; kw < k; ++kw) {
+          const int4 v = *reinterpret_cast<const int4*>(in.p + voff(in, n, oh * stride + kh, ow * stride + kw) + c0);
+          mx[0] = __vmaxs4(mx[0], (uint32_t)v.x);
+          mx[1] = __vmaxs4(mx[1], (uint32_t)v.y);
+          mx[2] = __vmaxs4(mx[2], (uint32_t)v.z);
+          mx[3] = __vmaxs4(mx[3], (uint32_t)v.w);
+        }
+      r = make_int4((int)mx[0], (int)mx[1], (int)mx[2], (int)mx[3]);
+    } else {
+      int sum[16];
+#pragma unroll
+      for (int j = 0; j < 16; ++j) sum[j] = 0;
+      for (int kh = 0; kh < k; ++kh)
+        for (int kw = 0; kw < k; ++kw) {
+          const int4 v = *reinterpret_cast<const int4*>(in.p + voff(in, n, oh * stride + kh, ow * stride + kw) + c0);
+          const uint32_t w4[4] = {(uint32_t)v.x, (uint32_t)v.y, (uint32_t)v.z, (uint32_t)v.w};
+#pragma unroll
+          for (int j = 0; j < 16; ++j) sum[j] += (int)(int8_t)(w4[j >> 2] >> (8 * (j & 3)));
+        }
+      uint32_t pk[4] = {0u, 0u, 0u, 0u};
+#pragma unroll
+      for (int j = 0; j < 16; ++j) {
+        const int q = (c0 + j < out.C) ? requant1((long long)sum[j] - (long long)z * area, m, z) : 0;
+        pk[j >> 2] |= ((uint32_t)q & 0xffu) << (8 * (j & 3));
       }
+      r = make_int4((int)pk[0], (int)pk[1], (int)pk[2], (int)pk[3]);
     }
-    out.p[voff(out, n, oh, ow) + c] = r;
+    *reinterpret_cast<int4*>(out.p + voff(out, n, oh, ow) + c0) = r;
   }
 }
 void launch_pool_codes(View in, View out, int k, int stride, int mode, const int* az, int hist,
                        cudaStream_t s) {
-  k_pool_codes<<<nblk((int64_t)out.N * out.H * out.W * out.Cp), 256, 0, s>>>(in, out, k, stride,
-                                                                             mode, az, hist);
+  k_pool_codes<<<nblk((int64_t)out.N * out.H * out.W * (out.Cp >> 4)), 256, 0, s>>>(
+      in, out, k, stride, mode, az, hist);
 }
 
 __device__ __forceinline__ int add_codes1(int xa, int xb, int za, int zb, double ra, double rb, int zo) {

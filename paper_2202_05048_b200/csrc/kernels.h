@@ -72,6 +72,7 @@ void launch_conv_f32(const float* x, int N, int H, int W, int Cin, const float* 
 void launch_dwconv_f32(const float* x, int N, int H, int W, int C, const float* w,
                        const float* bias, int k, int stride, int pad, int OH, int OW, float* y,
                        cudaStream_t s);
+void launch_gemm_weight(const float* w, int cout, int cin, int k, int hw, float* out, cudaStream_t s);
 void launch_relu_f32(const float* x, float* y, int64_t n, cudaStream_t s);
 void launch_add_f32(const float* a, const float* b, float* y, int64_t n, cudaStream_t s);
 void launch_pool_f32(const float* x, int N, int H, int W, int C, int k, int stride, int OH, int OW,

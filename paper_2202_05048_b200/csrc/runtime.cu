@@ -13,6 +13,7 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <chrono>
 #include <climits>
 #include <cstdio>
 #include <cstdlib>
@@ -31,6 +32,25 @@ using namespace ptq;
 namespace {
 
 thread_local std::string g_err;
+
+// PTQ_TRACE=1: device-synchronised wall time of every runtime phase on stderr
+struct Trace {
+  const char* name;
+  std::chrono::steady_clock::time_point t0;
+  bool on;
+  explicit Trace(const char* n) : name(n), on(std::getenv("PTQ_TRACE") != nullptr) {
+    if (on) {
+      cudaDeviceSynchronize();
+      t0 = std::chrono::steady_clock::now();
+    }
+  }
+  ~Trace() {
+    if (!on) return;
+    cudaDeviceSynchronize();
+    double ms = std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count();
+    std::fprintf(stderr, "[ptq-trace] %-28s %9.3f ms\n", name, ms);
+  }
+};
 
 struct Err {
   int code;
@@ -147,10 +167,14 @@ struct ptq_ctx {
   size_t ev_used = 0;
 
   template <typename T>
+  // stream-ordered allocations from the device's default memory pool, which keeps freed
+  // blocks (release threshold = max) so the 30 GB calibration activations and the eval
+  // buffers are recycled across steps and across evaluator instances instead of being
+  // mapped and unmapped each time
   T* dalloc(size_t n) {
     void* p = nullptr;
     if (n == 0) n = 1;
-    CK(cudaMalloc(&p, n * sizeof(T)));
+    CK(cudaMallocAsync(&p, n * sizeof(T), st));
     allocs.push_back(p);
     return static_cast<T*>(p);
   }
@@ -158,7 +182,7 @@ struct ptq_ctx {
     if (!p) return;
     auto it = std::find(allocs.begin(), allocs.end(), p);
     if (it != allocs.end()) allocs.erase(it);
-    cudaFree(p);
+    cudaFreeAsync(p, st);
   }
 };
 
@@ -189,6 +213,7 @@ int guarded(F&& f) {
 
 // ---------------------------------------------------------------- graph import
 void import_graph(ptq_ctx* c, const ptq_graph_desc* g) {
+  Trace tr("import_graph");
   REQ(g && g->n_nodes > 0 && g->nodes, "empty graph");
   c->nodes.resize(g->n_nodes);
   c->tens.assign(g->n_nodes + 1, TensorI{});
@@ -306,26 +331,13 @@ void import_graph(ptq_ctx* c, const ptq_graph_desc* g) {
       wd.f32_gemm = c->d_wt[n.weight];                  // (C,1,k,k) == [C][k*k]
       wd.bytes_per_variant = (int64_t)wd.cout * n.k * n.k;
     } else {
-      // fp32 GEMM weight [K][cout], K in NHWC order
-      const int64_t K = x.elems;
+      // fp32 GEMM weight [K][cout], K in NHWC order (built on the device)
       const int kk = n.kind == PTQ_FC ? 1 : n.k;
-      std::vector<float> hb((size_t)(K * wd.cout));
-      for (int o = 0; o < wd.cout; ++o) {
-        if (n.kind == PTQ_FC) {
-          for (int ci = 0; ci < x.c; ++ci)
-            for (int p = 0; p < x.h * x.w; ++p)
-              hb[((size_t)p * x.c + ci) * wd.cout + o] = w.data[(size_t)o * K + (size_t)ci * x.h * x.w + p];
-        } else {
-          for (int ci = 0; ci < x.c; ++ci)
-            for (int a = 0; a < kk; ++a)
-              for (int b = 0; b < kk; ++b)
-                hb[(((size_t)a * kk + b) * x.c + ci) * wd.cout + o] =
-                    w.data[(((size_t)o * x.c + ci) * kk + a) * kk + b];
-        }
-      }
-      wd.f32_gemm = c->dalloc<float>(hb.size());
-      CK(cudaMemcpyAsync(wd.f32_gemm, hb.data(), hb.size() * sizeof(float), cudaMemcpyHostToDevice, c->st));
-      CK(cudaStreamSynchronize(c->st));
+      const int64_t K = n.kind == PTQ_FC ? x.elems : (int64_t)kk * kk * x.c;
+      wd.f32_gemm = c->dalloc<float>((size_t)(K * wd.cout));
+      launch_gemm_weight(c->d_wt[n.weight], wd.cout, x.c, kk, n.kind == PTQ_FC ? x.h * x.w : 0,
+                         wd.f32_gemm, c->st);
+      check_launch(c);
       // int8 tensor-core form
       wd.cin = x.c;
       wd.k = kk;
@@ -537,6 +549,7 @@ View view_of(ptq_ctx* c, int t, int n) {
 }
 
 void ensure_eval_buffers(ptq_ctx* c) {
+  Trace tr("ensure_eval_buffers");
   int64_t chunk = c->opt_chunk > 0 ? std::min<int64_t>(c->opt_chunk, c->n_eval) : c->n_eval;
   if (c->chunk == chunk && !c->d_codes.empty()) return;
   for (auto p : c->d_codes) c->dfree(p);
@@ -596,6 +609,7 @@ void ensure_eval_buffers(ptq_ctx* c) {
 // ---------------------------------------------------------------- prepare
 void prepare(ptq_ctx* c) {
   if (c->prepared) return;
+  Trace tr("prepare");
   for (int i = 0; i < 6; ++i) REQ(c->clip_set[i], "clip ranges not set for every (cache, clipping)");
   const int T = c->T;
   // activation params: variant v = (cache*4 + scheme)*2 + clip
@@ -619,6 +633,7 @@ void prepare(ptq_ctx* c) {
   launch_act_params(d_r, d_vs, 24, T, c->d_act_scale, c->d_act_zp, c->st);
   check_launch(c);
   // weights: 8 variants (scheme, granularity) per compute node
+  Trace trw("prepare.weights");
   unsigned int* d_mm = nullptr;
   int maxc = 1;
   for (auto& wd : c->W) maxc = std::max(maxc, wd.cout);
@@ -664,6 +679,7 @@ void prepare(ptq_ctx* c) {
   ensure_eval_buffers(c);
   // mixed prefix: config-invariant fp32 output of the first compute node for all eval images
   {
+    Trace trp("prepare.mixed_prefix");
     const int fc_ = c->first_compute;
     const int tout = c->nodes[fc_].out;
     if (!c->d_prefix) c->d_prefix = c->dalloc<float>((size_t)c->n_eval * c->tens[tout].elems);
@@ -902,6 +918,12 @@ int ptq_create(ptq_ctx** out, int device, const ptq_graph_desc* g, const float* 
     CK(cudaDeviceGetAttribute(&minor, cudaDevAttrComputeCapabilityMinor, device));
     REQ(major == 10 && minor == 0, "ptq_b200 requires an sm_100 (B200) device");
     CK(cudaStreamCreateWithFlags(&c->st, cudaStreamNonBlocking));
+    {
+      cudaMemPool_t pool;
+      CK(cudaDeviceGetDefaultMemPool(&pool, device));
+      uint64_t thr = UINT64_MAX;
+      CK(cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr));
+    }
     import_graph(c, g);
     c->n_images = n_images;
     c->n_calib = n_calib;
@@ -921,7 +943,8 @@ int ptq_create(ptq_ctx** out, int device, const ptq_graph_desc* g, const float* 
     *out = c;
   });
   if (rc != PTQ_OK) {
-    for (void* p : c->allocs) cudaFree(p);
+    for (void* p : c->allocs) cudaFreeAsync(p, c->st);
+    if (c->st) cudaStreamSynchronize(c->st);
     if (c->st) cudaStreamDestroy(c->st);
     delete c;
   }
@@ -932,7 +955,8 @@ int ptq_destroy(ptq_ctx* c) {
   if (!c) return PTQ_OK;
   cudaSetDevice(c->dev);
   if (c->st) cudaStreamSynchronize(c->st);
-  for (void* p : c->allocs) cudaFree(p);
+  for (void* p : c->allocs) cudaFreeAsync(p, c->st);
+  if (c->st) cudaStreamSynchronize(c->st);
   for (auto e : c->ev_pool) cudaEventDestroy(e);
   if (c->st) cudaStreamDestroy(c->st);
   delete c;
@@ -948,6 +972,7 @@ int ptq_num_tensors(const ptq_ctx* c, int32_t* T) {
 int ptq_calib_forward(ptq_ctx* c, int32_t n_caches, const int32_t* sizes, const int64_t* ids,
                       float* local_ranges) {
   return guarded([&] {
+    Trace tr("calib_forward");
     REQ(c && n_caches >= 1 && sizes, "null argument");
     CK(cudaSetDevice(c->dev));
     for (auto p : c->cal_bufs) c->dfree(p);
@@ -1015,6 +1040,7 @@ int ptq_calib_forward(ptq_ctx* c, int32_t n_caches, const int32_t* sizes, const 
 
 int ptq_calib_histogram(ptq_ctx* c, const float* ranges, int64_t* counts) {
   return guarded([&] {
+    Trace tr("calib_histogram");
     REQ(c && ranges && counts, "null argument");
     REQ(c->cal_sizes.size() == c->cal_slots.size(), "ptq_calib_forward must run first");
     CK(cudaSetDevice(c->dev));
@@ -1063,6 +1089,7 @@ int ptq_calibrate(ptq_ctx* c, int32_t n_caches, const int32_t* sizes, const int6
 
 int ptq_kl_sweep(ptq_ctx* c, int32_t n_hist, const int64_t* counts, const float* ranges, double* kl) {
   return guarded([&] {
+    Trace tr("kl_sweep");
     REQ(c && counts && ranges && kl && n_hist >= 0, "null argument");
     if (n_hist == 0) return;
     CK(cudaSetDevice(c->dev));
@@ -1101,6 +1128,7 @@ int ptq_prepare(ptq_ctx* c) {
 
 int ptq_eval_configs(ptq_ctx* c, const ptq_config* cfgs, int32_t n_cfg, int64_t* correct) {
   return guarded([&] {
+    Trace tr("eval_configs");
     REQ(c && cfgs && correct && n_cfg >= 0, "null argument");
     CK(cudaSetDevice(c->dev));
     prepare(c);

@@ -21,7 +21,10 @@ from __future__ import annotations
 
 import ctypes as C
 import math
+import os
+import sys
 import threading
+import time
 
 import numpy as np
 
@@ -31,6 +34,21 @@ from .config import (CACHE_SIZES, N_BINS, QuantConfig, TargetProfile, config_key
 from .lowering import LoweredGraph
 
 TIE_BAND = 1e-9
+
+
+class _trace:
+    """PTQ_TRACE=1: wall time of host-side evaluator phases on stderr."""
+
+    def __init__(self, name):
+        self.name = name
+
+    def __enter__(self):
+        self.t0 = time.perf_counter()
+
+    def __exit__(self, *a):
+        if os.environ.get("PTQ_TRACE"):
+            print(f"[ptq-trace] py:{self.name:25s} {1e3 * (time.perf_counter() - self.t0):9.3f} ms",
+                  file=sys.stderr, flush=True)
 
 
 # ---------------------------------------------------------------- KL window choice (host side)
@@ -128,7 +146,8 @@ class GpuEvaluator:
         """Build the S1/S2/S3 caches; under torch.distributed the images of each
         cache are sharded across ranks (dist.sharded_calibration)."""
         from . import dist
-        ranges, counts, n_img = dist.sharded_calibration(self, self.n_calib, self.seed, self.T)
+        with _trace("sharded_calibration"):
+            ranges, counts, n_img = dist.sharded_calibration(self, self.n_calib, self.seed, self.T)
         elems = self.tensor_elems()
         nsamp = n_img[:, None] * elems[None, :]
         self.image_ids = [select_images(self.n_calib, sc, self.seed) for sc in CACHE_SIZES]
@@ -171,19 +190,21 @@ class GpuEvaluator:
             self.kl_values = kl.reshape(3, T, -1)
             kl_ranges = np.zeros((3, T, 2), dtype=np.float64)
             self.kl_reranked = 0
-            for k in range(3):
-                for t in range(T):
-                    (lo, hi), nr = choose_kl_range(counts[k, t], ranges[k, t, 0], ranges[k, t, 1],
-                                                   self.kl_values[k, t])
-                    kl_ranges[k, t] = (lo, hi)
-                    self.kl_reranked += nr
+            with _trace("choose_kl_ranges"):
+                for k in range(3):
+                    for t in range(T):
+                        (lo, hi), nr = choose_kl_range(counts[k, t], ranges[k, t, 0], ranges[k, t, 1],
+                                                       self.kl_values[k, t])
+                        kl_ranges[k, t] = (lo, hi)
+                        self.kl_reranked += nr
         self.kl_ranges = np.ascontiguousarray(kl_ranges, dtype=np.float64).reshape(3, T, 2)
         for k in range(3):
             mx = np.ascontiguousarray(ranges[k].astype(np.float64))
             _lib.check(self.lib.ptq_set_clip_ranges(self._ctx, k, 0, _lib.ptr(mx)))
             kr = np.ascontiguousarray(self.kl_ranges[k])
             _lib.check(self.lib.ptq_set_clip_ranges(self._ctx, k, 1, _lib.ptr(kr)))
-        _lib.check(self.lib.ptq_prepare(self._ctx))
+        with _trace("prepare"):
+            _lib.check(self.lib.ptq_prepare(self._ctx))
 
     # ------------------------------------------------------------ evaluation
     def _check_cfg(self, cfg) -> None:
