@@ -204,11 +204,11 @@ def run_b200(args):
 
     for _ in range(args.warmup):
         step()
-    ev.set_option("time_conv", 1)
+    ev.set_option("time_conv", 4)           # CUDA events around the conv launches of 4 configs/step
     times, counts = [], None
     launches = 0
     conv_ms = conv_ops = 0.0
-    conv_n = 0
+    conv_n = conv_total = 0
     with ClockSampler(local) as clk:
         for _ in range(args.steps):
             barrier()
@@ -222,6 +222,7 @@ def run_b200(args):
             barrier()
             st = ev.stats()
             launches, conv_ms, conv_ops, conv_n = st["launches"], st["conv_ms"], st["conv_ops"], st["conv_launches"]
+            conv_total = st["conv_launches_total"]
             times.append(e0.elapsed_time(e1))
     ev.set_option("time_conv", 0)
     t_ms = float(np.median(times))
@@ -240,8 +241,11 @@ def run_b200(args):
     roofline = {"bound": "tensor", "achieved": achieved, "peak": peak, "unit": "TOP/s",
                 "frac": achieved / peak if peak else None, "traffic": None,
                 "kernel": "k_conv_tc (tcgen05.mma.kind::i8)",
-                "launches_per_step": conv_n, "kernel_ms_per_step": conv_ms,
-                "share_of_step": conv_ms / t_ms if t_ms else None,
+                "timed_launches": conv_n, "timed_ms": conv_ms,
+                "avg_launch_ms": conv_ms / conv_n if conv_n else None,
+                "launches_per_step": conv_total,
+                "kernel_ms_per_step": conv_ms * conv_total / conv_n if conv_n else None,
+                "share_of_step": (conv_ms * conv_total / conv_n) / t_ms if conv_n and t_ms else None,
                 "peak_basis": ("int8 dense = 2 x measured bf16 burst (MEASURED_PEAKS.json bf16_tflops)"
                                if bf16 else "int8 dense = 2 x fallback bf16 1.59 PF")}
 

@@ -142,15 +142,17 @@ int ptq_histogram_host(ptq_ctx* ctx, const float* x, int64_t n, float lo, float 
                        int64_t* counts);
 /* Runtime options: "conv_ref" (1 = CUDA-core reference conv instead of tcgen05,
  * tests only), "fusion" (0 = materialise every tensor so each can be probed),
- * "eval_chunk" (images per eval pass; default = whole eval set), "time_conv" (1 =
- * record CUDA events around every int8 conv launch for ptq_last_stats),
+ * "eval_chunk" (images per eval pass; default = whole eval set), "time_conv" (N =
+ * record CUDA events around the int8 conv launches of the first N configs of each
+ * ptq_eval_configs call, for ptq_last_stats),
  * "reset_stats" (zero the cumulative kernel-launch counter). */
 int ptq_set_option(ptq_ctx* ctx, const char* key, int64_t value);
-/* Statistics of the last ptq_eval_configs call: kernel launches, summed CUDA-event
- * time of the int8 conv launches (option "time_conv"), their algorithmic int8
- * ops (2*M*N*K with unpadded dims) and the number of timed conv launches. */
+/* Statistics: cumulative kernel launches (option "reset_stats" zeroes it) and, for the
+ * last ptq_eval_configs call, the summed CUDA-event time of the int8 conv launches of
+ * the first "time_conv" configs, their algorithmic int8 ops (2*M*N*K, unpadded dims),
+ * the number of timed conv launches and the total number of conv launches. */
 int ptq_last_stats(const ptq_ctx* ctx, int64_t* kernel_launches, double* conv_ms_event,
-                   double* conv_ops, int64_t* conv_launches);
+                   double* conv_ops, int64_t* conv_launches, int64_t* conv_launches_total);
 /* The CUDA stream (cudaStream_t) every kernel of this context runs on. */
 int ptq_stream(const ptq_ctx* ctx, void** stream);
 

@@ -87,7 +87,7 @@ def load() -> C.CDLL:
         "ptq_histogram_host": [P, P, i64, C.c_float, C.c_float, P],
         "ptq_set_option": [P, C.c_char_p, i64],
         "ptq_last_stats": [P, C.POINTER(i64), C.POINTER(C.c_double), C.POINTER(C.c_double),
-                           C.POINTER(i64)],
+                           C.POINTER(i64), C.POINTER(i64)],
         "ptq_calib_forward": [P, i32, P, P, P],
         "ptq_calib_histogram": [P, P, P],
         "ptq_stream": [P, C.POINTER(P)],

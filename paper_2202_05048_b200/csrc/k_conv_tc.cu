@@ -191,14 +191,15 @@ struct RowGeo {
   bool ok;
   int n, oh, ow, ih0, iw0;
 };
-__device__ __forceinline__ RowGeo row_geo(const ConvTcArgs& a, int64_t m, int64_t M) {
+__device__ __forceinline__ RowGeo row_geo(const ConvTcArgs& a, int m, int M) {
   RowGeo g{};
   g.ok = m < M;
-  if (g.ok) {
-    g.ow = (int)(m % a.OW);
-    int64_t t = m / a.OW;
-    g.oh = (int)(t % a.OH);
-    g.n = (int)(t / a.OH);
+  if (g.ok) {                                  // M < 2^31: multiply-high divisions
+    const uint32_t t = a.div_ow.div((uint32_t)m);
+    g.ow = m - (int)t * a.OW;
+    const uint32_t nn = a.div_oh.div(t);
+    g.oh = (int)t - (int)nn * a.OH;
+    g.n = (int)nn;
   }
   g.ih0 = g.oh * a.stride - a.pad + a.in.halo;
   g.iw0 = g.ow * a.stride - a.pad + a.in.halo;
@@ -218,9 +219,9 @@ __global__ void __launch_bounds__(TC_THREADS, 1) k_conv_tc(const __grid_constant
   constexpr uint32_t TMEM_COLS = (2 * BN) < 32 ? 32 : 2 * BN;
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int64_t M = (int64_t)a.in.N * a.OH * a.OW;
+  const int M = a.in.N * a.OH * a.OW;
   const int n_nt = (a.L.cout + BN - 1) / BN;
-  const int64_t n_tiles = ((M + TC_BM - 1) / TC_BM) * n_nt;
+  const int n_tiles = ((M + TC_BM - 1) / TC_BM) * n_nt;
 
   if (threadIdx.x == 0) {
     for (int s = 0; s < TC_STAGES; ++s) {
@@ -250,8 +251,8 @@ __global__ void __launch_bounds__(TC_THREADS, 1) k_conv_tc(const __grid_constant
     const int Cp = a.in.Cp, cpc = Cp >> 4;
     const int Wp = a.in.W + 2 * a.in.halo, Hp = a.in.H + 2 * a.in.halo;
     uint32_t it = 0;
-    for (int64_t tile = blockIdx.x; tile < n_tiles; tile += gridDim.x) {
-      const int64_t mt = tile / n_nt;
+    for (int tile = blockIdx.x; tile < n_tiles; tile += gridDim.x) {
+      const int mt = (int)a.div_nt.div((uint32_t)tile);
       const RowGeo g = row_geo(a, mt * TC_BM + r, M);
       const int8_t* base = a.in.p + (((int64_t)g.n * Hp + g.ih0) * Wp + g.iw0) * Cp;
       int kh = 0, kw = 0, ch = 0, kk = 0;
@@ -278,8 +279,8 @@ __global__ void __launch_bounds__(TC_THREADS, 1) k_conv_tc(const __grid_constant
     // ------------------------------------------------ B producer (bulk copies of pre-tiled weights)
     if (lane == 0) {
       uint32_t it = 0;
-      for (int64_t tile = blockIdx.x; tile < n_tiles; tile += gridDim.x) {
-        const int nt = (int)(tile % n_nt);
+      for (int tile = blockIdx.x; tile < n_tiles; tile += gridDim.x) {
+        const int nt = tile - (int)a.div_nt.div((uint32_t)tile) * n_nt;
         const int8_t* gB = a.wB + (int64_t)nt * a.n_kiter * BN * 128;
         for (int ki = 0; ki < a.n_kiter; ++ki, ++it) {
           const int s = it % TC_STAGES;
@@ -295,7 +296,7 @@ __global__ void __launch_bounds__(TC_THREADS, 1) k_conv_tc(const __grid_constant
     if (lane == 0) {
       const uint32_t idesc = idesc_i8<BN>();
       uint32_t it = 0, lt = 0;
-      for (int64_t tile = blockIdx.x; tile < n_tiles; tile += gridDim.x, ++lt) {
+      for (int tile = blockIdx.x; tile < n_tiles; tile += gridDim.x, ++lt) {
         const uint32_t buf = lt & 1u, uph = (lt >> 1) & 1u;
         mbar_wait(&tempty[buf], uph ^ 1u);           // epilogue drained this accumulator
         tc_fence_after();
@@ -333,10 +334,10 @@ __global__ void __launch_bounds__(TC_THREADS, 1) k_conv_tc(const __grid_constant
     const EpiParam* __restrict__ ep = a.L.ep;
     const bool wzp = a.has_wzp != 0;
     uint32_t lt = 0;
-    for (int64_t tile = blockIdx.x; tile < n_tiles; tile += gridDim.x, ++lt) {
+    for (int tile = blockIdx.x; tile < n_tiles; tile += gridDim.x, ++lt) {
       const uint32_t buf = lt & 1u, uph = (lt >> 1) & 1u;
-      const int64_t mt = tile / n_nt;
-      const int nt = (int)(tile % n_nt);
+      const int mt = (int)a.div_nt.div((uint32_t)tile);
+      const int nt = tile - mt * n_nt;
       const RowGeo g = row_geo(a, mt * TC_BM + row, M);
       const long long rowsum = (g.ok && c_lo < c_hi) ? pixel_rowsum(a, g.n, g.ih0, g.iw0) : 0;
       int8_t* orow = g.ok ? a.out.p + vpix(a.out, g.n, g.oh, g.ow) * a.out.Cp : nullptr;
@@ -386,14 +387,14 @@ __global__ void __launch_bounds__(TC_THREADS, 1) k_conv_tc(const __grid_constant
 // Same contract, direct sum over the tiled weight image (tests / cross-checks only).
 template <int BN>
 __global__ void k_conv_i8_ref(const ConvTcArgs a) {
-  const int64_t M = (int64_t)a.in.N * a.OH * a.OW;
+  const int M = a.in.N * a.OH * a.OW;
   const int Cout = a.L.cout;
-  const int64_t total = M * a.out.Cp;
+  const int64_t total = (int64_t)M * a.out.Cp;
   const LayerRt rt = *a.L.rt;
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < total;
        i += (int64_t)gridDim.x * blockDim.x) {
     const int c = (int)(i % a.out.Cp);
-    const int64_t m = i / a.out.Cp;
+    const int m = (int)(i / a.out.Cp);
     const RowGeo g = row_geo(a, m, M);
     int8_t* orow = a.out.p + vpix(a.out, g.n, g.oh, g.ow) * a.out.Cp;
     if (c >= Cout) { orow[c] = 0; continue; }
@@ -452,7 +453,16 @@ static void launch_bn(const ConvTcArgs& a, cudaStream_t s) {
   k_conv_tc<BN><<<grid, TC_THREADS, smem, s>>>(a);
 }
 
-void launch_conv_tc(const ConvTcArgs& a, int bn, cudaStream_t s) {
+static ConvTcArgs with_divs(const ConvTcArgs& a0, int bn) {
+  ConvTcArgs a = a0;
+  a.div_ow = FastDiv::make((uint32_t)a.OW);
+  a.div_oh = FastDiv::make((uint32_t)a.OH);
+  a.div_nt = FastDiv::make((uint32_t)((a.L.cout + bn - 1) / bn));
+  return a;
+}
+
+void launch_conv_tc(const ConvTcArgs& a0, int bn, cudaStream_t s) {
+  const ConvTcArgs a = with_divs(a0, bn);
   switch (bn) {
     case 16: launch_bn<16>(a, s); break;
     case 32: launch_bn<32>(a, s); break;
@@ -462,7 +472,8 @@ void launch_conv_tc(const ConvTcArgs& a, int bn, cudaStream_t s) {
   }
 }
 
-void launch_conv_i8_ref(const ConvTcArgs& a, int bn, cudaStream_t s) {
+void launch_conv_i8_ref(const ConvTcArgs& a0, int bn, cudaStream_t s) {
+  const ConvTcArgs a = with_divs(a0, bn);
   const int64_t total = (int64_t)a.in.N * a.OH * a.OW * a.out.Cp;
   int64_t b = (total + 255) / 256;
   int blocks = (int)(b > 148 * 64 ? 148 * 64 : (b < 1 ? 1 : b));

@@ -264,63 +264,67 @@ void launch_layer_params(const LayerSt* d_layers, int n_layers, const float* act
 }
 
 // ---------------------------------------------------------------- quantize / dequantize
-// images NCHW fp32 -> int8 view (one thread per pixel, Cp bytes written, pads = 0)
+// images NCHW fp32 -> int8 view: grid.y = image row (n, h), threads over w; Cp bytes per
+// pixel written as 16-byte stores, pad channels 0
 __global__ void k_quant_input(const float* __restrict__ imgs, int64_t img0, View out,
                               const float* __restrict__ as, const int* __restrict__ az, int hist) {
   const double s = (double)as[hist], z = (double)az[hist];
   const double rs = __ddiv_rn(1.0, s);
-  const int64_t npix = (int64_t)out.N * out.H * out.W;
+  const int n = blockIdx.x / out.H, h = blockIdx.x - (blockIdx.x / out.H) * out.H;
   const int64_t plane = (int64_t)out.H * out.W;
-  for (int64_t p = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; p < npix;
-       p += (int64_t)gridDim.x * blockDim.x) {
-    int n = (int)(p / plane);
-    int64_t hw = p - (int64_t)n * plane;
-    int h = (int)(hw / out.W), w = (int)(hw - (int64_t)h * out.W);
+  const float* src0 = imgs + (img0 + n) * out.C * plane + (int64_t)h * out.W;
+  for (int w = blockIdx.y * blockDim.x + threadIdx.x; w < out.W; w += gridDim.y * blockDim.x) {
     int8_t* dst = out.p + voff(out, n, h, w);
-    const float* src = imgs + ((img0 + n) * out.C) * plane + hw;
     for (int c0 = 0; c0 < out.Cp; c0 += 16) {
-      alignas(16) int8_t v[16];
+      uint32_t pk[4] = {0u, 0u, 0u, 0u};
 #pragma unroll
       for (int j = 0; j < 16; ++j) {
-        int c = c0 + j;
-        v[j] = c < out.C ? (int8_t)quant1_fast(__ldg(src + (int64_t)c * plane), rs, s, z) : (int8_t)0;
+        const int c = c0 + j;
+        if (c < out.C) {
+          const int q = quant1_fast(__ldg(src0 + (int64_t)c * plane + w), rs, s, z);
+          pk[j >> 2] |= ((uint32_t)q & 0xffu) << (8 * (j & 3));
+        }
       }
-      *reinterpret_cast<int4*>(dst + c0) = *reinterpret_cast<int4*>(v);
+      *reinterpret_cast<int4*>(dst + c0) = make_int4((int)pk[0], (int)pk[1], (int)pk[2], (int)pk[3]);
     }
   }
 }
 void launch_quant_input(const float* imgs, int64_t img0, View out, const float* as, const int* az,
                         int hist, cudaStream_t s) {
-  k_quant_input<<<nblk((int64_t)out.N * out.H * out.W), 256, 0, s>>>(imgs, img0, out, as, az, hist);
+  dim3 g(out.N * out.H, (out.W + 127) / 128);
+  k_quant_input<<<g, 128, 0, s>>>(imgs, img0, out, as, az, hist);
 }
 
-// fp32 NHWC (pitch C) -> int8 view, optional fused relu clamp
+// fp32 NHWC (pitch C) -> int8 view, optional fused relu clamp; grid.y = (n, h) row, threads
+// over (w, 16-channel chunk)
 __global__ void k_quant_nhwc(const float* __restrict__ x, View out, const float* __restrict__ as,
                              const int* __restrict__ az, int hist, int relu_hist) {
   const double s = (double)as[hist], z = (double)az[hist];
   const double rs = __ddiv_rn(1.0, s);
   const int rz = relu_hist >= 0 ? az[relu_hist] : INT_MIN;
-  const int64_t total = (int64_t)out.N * out.H * out.W * out.Cp;
-  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < total;
-       i += (int64_t)gridDim.x * blockDim.x) {
-    int c = (int)(i % out.Cp);
-    int64_t p = i / out.Cp;
-    int w = (int)(p % out.W);
-    int64_t t = p / out.W;
-    int h = (int)(t % out.H);
-    int n = (int)(t / out.H);
-    int8_t code = 0;
-    if (c < out.C) {
-      int q = quant1_fast(__ldg(x + p * out.C + c), rs, s, z);
-      code = (int8_t)(q > rz ? q : rz);
+  const int n = blockIdx.x / out.H, h = blockIdx.x - (blockIdx.x / out.H) * out.H;
+  const int nch = out.Cp >> 4;
+  const float* row = x + ((int64_t)n * out.H + h) * out.W * out.C;
+  for (int i = blockIdx.y * blockDim.x + threadIdx.x; i < out.W * nch; i += gridDim.y * blockDim.x) {
+    const int w = i / nch, c0 = (i - w * nch) * 16;
+    const float* src = row + (int64_t)w * out.C + c0;
+    uint32_t pk[4] = {0u, 0u, 0u, 0u};
+#pragma unroll
+    for (int j = 0; j < 16; ++j) {
+      if (c0 + j < out.C) {
+        int q = quant1_fast(__ldg(src + j), rs, s, z);
+        q = q > rz ? q : rz;
+        pk[j >> 2] |= ((uint32_t)q & 0xffu) << (8 * (j & 3));
+      }
     }
-    out.p[voff(out, n, h, w) + c] = code;
+    *reinterpret_cast<int4*>(out.p + voff(out, n, h, w) + c0) = make_int4((int)pk[0], (int)pk[1], (int)pk[2], (int)pk[3]);
   }
 }
 void launch_quant_nhwc(const float* x, View out, const float* as, const int* az, int hist,
                        int relu_hist, cudaStream_t s) {
-  k_quant_nhwc<<<nblk((int64_t)out.N * out.H * out.W * out.Cp), 256, 0, s>>>(x, out, as, az, hist,
-                                                                            relu_hist);
+  const int per_row = out.W * (out.Cp >> 4);
+  dim3 g(out.N * out.H, (per_row + 127) / 128);
+  k_quant_nhwc<<<g, 128, 0, s>>>(x, out, as, az, hist, relu_hist);
 }
 
 __global__ void k_dequant(View in, const float* __restrict__ as, const int* __restrict__ az,
@@ -494,6 +498,42 @@ void launch_concat_codes(View in, View out, int coff, const float* as, const int
                          int hout, cudaStream_t s) {
   k_concat_codes<<<nblk((int64_t)in.N * in.H * in.W * in.C), 256, 0, s>>>(in, out, coff, as, az,
                                                                           hin, hout);
+}
+
+// packed im2col of a few-channel input (the RGB stem): one thread per (output pixel, 16 B)
+__global__ void k_im2col(View in, int k, int stride, int pad, int OH, int OW, int8_t* __restrict__ out,
+                         int out_cp, int64_t total) {
+  const int K = k * k * in.C;
+  const int nch = out_cp >> 4;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < total;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    const int j = (int)(i % nch);
+    const int64_t m = i / nch;
+    const int ow = (int)(m % OW);
+    const int64_t t = m / OW;
+    const int oh = (int)(t % OH), n = (int)(t / OH);
+    int kb = j * 16;
+    int tap = kb / in.C, c = kb - tap * in.C;
+    int kh = tap / k, kw = tap - kh * k;
+    uint32_t pk[4] = {0u, 0u, 0u, 0u};
+#pragma unroll
+    for (int b = 0; b < 16; ++b) {
+      if (kb + b < K) {
+        const int v = in.p[voff(in, n, oh * stride - pad + kh, ow * stride - pad + kw) + c];
+        pk[b >> 2] |= ((uint32_t)v & 0xffu) << (8 * (b & 3));
+        if (++c == in.C) {
+          c = 0;
+          if (++kw == k) { kw = 0; ++kh; }
+        }
+      }
+    }
+    *reinterpret_cast<int4*>(out + m * out_cp + j * 16) = make_int4((int)pk[0], (int)pk[1], (int)pk[2], (int)pk[3]);
+  }
+}
+void launch_im2col(View in, int k, int stride, int pad, int OH, int OW, int8_t* out, int out_cp,
+                   cudaStream_t s) {
+  const int64_t total = (int64_t)in.N * OH * OW * (out_cp >> 4);
+  k_im2col<<<nblk(total), 256, 0, s>>>(in, k, stride, pad, OH, OW, out, out_cp, total);
 }
 
 // P[padded pixel] = sum of the real-channel codes (rowsum term of the zero-point correction)

@@ -122,6 +122,32 @@ void launch_argmax_f32(const float* x, int64_t rows, int C, const long long* lab
                        unsigned long long* correct, cudaStream_t s);
 
 // ---------------------------------------------------------------- F4 (k_conv_tc.cu)
+// n / d and n % d for 0 <= n < 2^31 with a multiply-high (CUTLASS-style round-up magic)
+struct FastDiv {
+  uint32_t d, mul, shr;
+  static FastDiv make(uint32_t d) {
+    FastDiv f{d, 0u, 0u};
+    if (d > 1) {
+      uint32_t l = 0;
+      while ((1u << l) < d) ++l;                 // ceil(log2 d)
+      const uint32_t p = 31 + l;
+      f.mul = (uint32_t)(((1ull << p) + d - 1) / d);
+      f.shr = p - 32;
+    }
+    return f;
+  }
+#ifdef __CUDACC__
+  __device__ __forceinline__ uint32_t div(uint32_t n) const {
+    return d == 1 ? n : (__umulhi(n, mul) >> shr);
+  }
+#endif
+};
+
+// packed im2col for convs with few input channels (the RGB stem): row m of `out` holds
+// the k*k*C codes of output pixel m in (kh, kw, c) order, zero padded to out_cp bytes
+void launch_im2col(View in, int k, int stride, int pad, int OH, int OW, int8_t* out, int out_cp,
+                   cudaStream_t s);
+
 struct ConvTcArgs {
   View in, out;
   int k, stride, pad, OH, OW;
@@ -136,6 +162,7 @@ struct ConvTcArgs {
   LayerSt L;              // holds device pointers: mult / biasq / rt
   View skip;              // fused add operand (p == nullptr when none)
   int conv_is_a;          // 1 if the conv output is operand 0 of the fused add
+  FastDiv div_ow, div_oh, div_nt;   // m -> (n, oh, ow) and tile -> (m-tile, n-tile)
 };
 int conv_tc_bn_for(int cout);     // BN tile width the kernel uses for this Cout
 void launch_conv_tc(const ConvTcArgs& a, int bn, cudaStream_t s);

@@ -91,6 +91,9 @@ bool is_tc(int k) { return k == PTQ_CONV || k == PTQ_PWCONV || k == PTQ_FC; }
 struct WeightsDev {
   int cout = 0, cin = 0, k = 1, fc_hw = 0, cin_p = 0;
   int bn = 0, n_kiter = 0, n_chunks = 0, kreal = 0;
+  bool im2col = false;          // few-channel conv: packed im2col + 1x1 tensor-core GEMM
+  int im_cp = 0;                // im2col row pitch (k*k*Cin rounded up to 16)
+  int q_cin_p = 0, q_k = 1, q_fc_hw = 0;   // weight-quantizer view of the K layout
   float* f32_gemm = nullptr;    // [K][cout] fp32 (NHWC K order) for the fp32 path, or dw [C][k*k]
   float* f32_bias = nullptr;
   int8_t* codes = nullptr;      // [8 variants][bytes_per_variant]
@@ -150,6 +153,7 @@ struct ptq_ctx {
   std::vector<float*> d_f32;             // per tensor fp32 eval buffer (mixed tail)
   float* d_prefix = nullptr;             // mixed: fp32 output of the first compute node, all eval imgs
   int* d_P = nullptr;                    // pixel sums scratch
+  int8_t* d_im2col = nullptr;            // packed im2col scratch (few-channel convs)
   int64_t P_cap = 0;
   unsigned long long* d_correct = nullptr;
   Plan plans[2];
@@ -163,6 +167,8 @@ struct ptq_ctx {
   // stats
   int64_t launches = 0;
   double conv_ms = 0.0, conv_ops = 0.0;
+  int cur_cfg = 0;
+  int64_t conv_launches_total = 0;
   std::vector<cudaEvent_t> ev_pool;
   size_t ev_used = 0;
 
@@ -345,6 +351,20 @@ void import_graph(ptq_ctx* c, const ptq_graph_desc* g) {
       wd.fc_hw = n.kind == PTQ_FC ? x.h * x.w : 0;
       wd.n_chunks = n.kind == PTQ_FC ? x.h * x.w * wd.cin_p / 16 : kk * kk * wd.cin_p / 16;
       wd.kreal = n.kind == PTQ_FC ? (int)x.elems : kk * kk * x.c;
+      wd.q_cin_p = wd.cin_p;
+      wd.q_k = kk;
+      wd.q_fc_hw = wd.fc_hw;
+      if (n.kind != PTQ_FC && kk > 1 && x.c < 16) {
+        // per-tap channel padding would inflate K (RGB stem: 49 x 16 vs 147 bytes): gather a
+        // packed (kh, kw, c) im2col row per output pixel instead and run a 1x1 GEMM over it;
+        // the weight quantizer sees it as an fc over k*k "pixels" of Cin unpadded channels
+        wd.im2col = true;
+        wd.im_cp = rup(kk * kk * x.c, 16);
+        wd.n_chunks = wd.im_cp / 16;
+        wd.q_cin_p = x.c;
+        wd.q_k = 1;
+        wd.q_fc_hw = kk * kk;
+      }
       wd.n_kiter = (wd.n_chunks + 7) / 8;
       wd.bn = conv_tc_bn_for(wd.cout);
       int ntiles = (wd.cout + wd.bn - 1) / wd.bn;
@@ -602,6 +622,16 @@ void ensure_eval_buffers(ptq_ctx* c) {
     maxP = std::max<int64_t>(maxP, chunk * (int64_t)(x.h + 2 * c->halo[t]) * (x.w + 2 * c->halo[t]));
   }
   for (int t : need32) c->d_f32[t] = c->dalloc<float>(chunk * c->tens[t].elems);
+  int64_t im_bytes = 0;
+  for (int i = 0; i < (int)c->nodes.size(); ++i)
+    if (c->W[i].im2col)
+      im_bytes = std::max<int64_t>(im_bytes, chunk * (int64_t)c->tens[c->nodes[i].out].h *
+                                                 c->tens[c->nodes[i].out].w * c->W[i].im_cp);
+  c->dfree(c->d_im2col);
+  c->d_im2col = im_bytes ? c->dalloc<int8_t>(im_bytes) : nullptr;
+  for (int i = 0; i < (int)c->nodes.size(); ++i)
+    if (c->W[i].im2col)
+      maxP = std::max<int64_t>(maxP, chunk * (int64_t)c->tens[c->nodes[i].out].h * c->tens[c->nodes[i].out].w);
   c->d_P = c->dalloc<int>(maxP);
   c->P_cap = maxP;
 }
@@ -658,7 +688,7 @@ void prepare(ptq_ctx* c) {
         if (n.kind == PTQ_DWCONV)
           launch_weight_quant_dw(w, wd.cout, wd.k, sc, zp, codes, c->st);
         else
-          launch_weight_quant_tc(w, wd.cout, wd.cin, wd.k, wd.fc_hw, wd.cin_p, sc, zp, wd.bn,
+          launch_weight_quant_tc(w, wd.cout, wd.cin, wd.q_k, wd.q_fc_hw, wd.q_cin_p, sc, zp, wd.bn,
                                  wd.n_kiter, codes, wd.wsum + (size_t)wv * wd.cout, c->st);
         check_launch(c);
       }
@@ -791,6 +821,12 @@ void eval_one(ptq_ctx* c, const ptq_config& cfg, unsigned long long* d_correct, 
           if (n.kind == PTQ_FC) {
             vin.H = 1; vin.W = 1; vin.C = x.h * x.w * vin.Cp; vin.Cp = vin.C; vin.halo = 0;
             a.k = 1; a.stride = 1; a.pad = 0; a.OH = 1; a.OW = 1;
+          } else if (wd.im2col) {
+            const TensorI& y = c->tens[n.out];
+            launch_im2col(vin, n.k, n.stride, n.pad, y.h, y.w, c->d_im2col, wd.im_cp, c->st);
+            check_launch(c);
+            vin = View{c->d_im2col, B, y.h, y.w, wd.kreal, wd.im_cp, 0};
+            a.k = 1; a.stride = 1; a.pad = 0; a.OH = y.h; a.OW = y.w;
           } else {
             a.k = n.k; a.stride = n.stride; a.pad = n.pad;
             a.OH = c->tens[n.out].h; a.OW = c->tens[n.out].w;
@@ -816,7 +852,9 @@ void eval_one(ptq_ctx* c, const ptq_config& cfg, unsigned long long* d_correct, 
             a.conv_is_a = P.add_is_a[i];
           }
           cudaEvent_t ea = nullptr, eb = nullptr;
-          if (c->time_conv) {
+          const bool timed = c->cur_cfg < c->time_conv;   // instrument only the leading configs
+          ++c->conv_launches_total;
+          if (timed) {
             while (c->ev_pool.size() < c->ev_used + 2) {
               cudaEvent_t e;
               CK(cudaEventCreate(&e));
@@ -829,8 +867,10 @@ void eval_one(ptq_ctx* c, const ptq_config& cfg, unsigned long long* d_correct, 
           if (c->conv_ref) launch_conv_i8_ref(a, wd.bn, c->st);
           else launch_conv_tc(a, wd.bn, c->st);
           check_launch(c);
-          if (c->time_conv) CK(cudaEventRecord(eb, c->st));
-          c->conv_ops += 2.0 * (double)B * a.OH * a.OW * (double)wd.cout * (double)wd.kreal;
+          if (timed) {
+            CK(cudaEventRecord(eb, c->st));
+            c->conv_ops += 2.0 * (double)B * a.OH * a.OW * (double)wd.cout * (double)wd.kreal;
+          }
         }
         halo_fill(tout);
         probe(tout);
@@ -1136,10 +1176,15 @@ int ptq_eval_configs(ptq_ctx* c, const ptq_config* cfgs, int32_t n_cfg, int64_t*
     c->conv_ops = 0.0;
     c->conv_ms = 0.0;
     c->ev_used = 0;
+    c->conv_launches_total = 0;
     for (int32_t b0 = 0; b0 < n_cfg; b0 += 4096) {
       const int nb = std::min<int32_t>(4096, n_cfg - b0);
       CK(cudaMemsetAsync(c->d_correct, 0, nb * sizeof(unsigned long long), c->st));
-      for (int i = 0; i < nb; ++i) eval_one(c, cfgs[b0 + i], c->d_correct + i, -1, nullptr);
+      for (int i = 0; i < nb; ++i) {
+        c->cur_cfg = b0 + i;
+        eval_one(c, cfgs[b0 + i], c->d_correct + i, -1, nullptr);
+      }
+      c->cur_cfg = 0;
       std::vector<unsigned long long> h(nb);
       CK(cudaMemcpyAsync(h.data(), c->d_correct, nb * sizeof(unsigned long long), cudaMemcpyDeviceToHost, c->st));
       CK(cudaStreamSynchronize(c->st));
@@ -1227,12 +1272,13 @@ int ptq_set_option(ptq_ctx* c, const char* key, int64_t value) {
 }
 
 int ptq_last_stats(const ptq_ctx* c, int64_t* launches, double* conv_ms, double* conv_ops,
-                   int64_t* conv_launches) {
+                   int64_t* conv_launches, int64_t* conv_launches_total) {
   if (!c) { g_err = "null context"; return PTQ_EINVAL; }
   if (launches) *launches = c->launches;
   if (conv_ms) *conv_ms = c->conv_ms;
   if (conv_ops) *conv_ops = c->conv_ops;
   if (conv_launches) *conv_launches = (int64_t)(c->ev_used / 2);
+  if (conv_launches_total) *conv_launches_total = c->conv_launches_total;
   return PTQ_OK;
 }
 

@@ -267,10 +267,11 @@ class GpuEvaluator:
         return out
 
     def stats(self) -> dict:
-        n, ms, ops, nc = C.c_int64(), C.c_double(), C.c_double(), C.c_int64()
-        _lib.check(self.lib.ptq_last_stats(self._ctx, C.byref(n), C.byref(ms), C.byref(ops), C.byref(nc)))
+        n, ms, ops, nc, nt = C.c_int64(), C.c_double(), C.c_double(), C.c_int64(), C.c_int64()
+        _lib.check(self.lib.ptq_last_stats(self._ctx, C.byref(n), C.byref(ms), C.byref(ops), C.byref(nc),
+                                           C.byref(nt)))
         return {"launches": n.value, "conv_ms": ms.value, "conv_ops": ops.value,
-                "conv_launches": nc.value}
+                "conv_launches": nc.value, "conv_launches_total": nt.value}
 
     def stream_handle(self) -> int:
         s = C.c_void_p()

@@ -1,0 +1,77 @@
+"""GPU parity on the ImageNet-shaped models (ResNet-50 / ResNet-18 / MobileNet-v2 /
+SqueezeNet IR) at a reduced 64x64 input so the numpy oracle finishes in seconds.
+
+These exercise what the 32x32 toys do not: bottleneck blocks with fused
+residual adds and downsample convs, BN=256 tiles and multi-stage K loops
+(K up to 4608), stride-2 3x3 convs, the packed-im2col RGB stem, 17 depthwise
+layers (MobileNet-v2) and fire-module concats (SqueezeNet).
+
+Staged parity P3: the GPU calibrates; the oracle is handed the GPU's caches
+and must reproduce every int8 tensor bit-exactly for Mixed=Off configs.
+"""
+import numpy as np
+import pytest
+
+from oracle import ptq_oracle as O
+from paper_2202_05048_b200 import GENERIC, build_model, enumerate_space, make_dataset
+
+pytestmark = pytest.mark.gpu
+SHAPE = (3, 64, 64)
+
+
+@pytest.fixture(scope="module")
+def ds64():
+    return make_dataset(n_calib=300, n_eval=12, seed=0, shape=SHAPE)
+
+
+def gpu_and_oracle(name, ds64):
+    from paper_2202_05048_b200.evaluator import GpuEvaluator
+    g = build_model(name, seed=0, shape=SHAPE)
+    ev = GpuEvaluator(g, ds64, 0, GENERIC)
+    caches = {}
+    for k, sc in enumerate(("S1", "S2", "S3")):
+        caches[sc] = {t: O.Hist(t, float(ev.cache_ranges[k, i, 0]), float(ev.cache_ranges[k, i, 1]),
+                                ev.cache_counts[k, i], int(ev.cache_nsamp[k, i]))
+                      for i, t in enumerate(ev.lowered.tensor_names)}
+        for i, t in enumerate(ev.lowered.tensor_names):      # device KL == oracle KL sweep
+            h = caches[sc][t]
+            assert O.clipped_range(h, "KL") == tuple(ev.kl_ranges[k, i]), (name, sc, t)
+    return g, ev, caches
+
+
+@pytest.mark.parametrize("name", ["resnet50", "mobilenet_v2", "squeezenet", "resnet18"])
+def test_codes_bit_exact(name, ds64):
+    g, ev, caches = gpu_and_oracle(name, ds64)
+    space = enumerate_space(GENERIC)
+    ev.set_option("fusion", 0)
+    try:
+        for ci in (2, 20, 54):                    # Asym/Channel, Sym/KL/Tensor, S2 Uint8/Channel
+            cfg = space[ci]
+            assert cfg.mixed == "Off"
+            qm = O.quantize_model(g, caches[cfg.cache], cfg)
+            seen = {"input": O.quantize_array(ds64.eval_images, qm.act["input"]).astype(np.int64)}
+            O.run_quantized(qm, ds64.eval_images, sink=lambda t, v: seen.__setitem__(t, v))
+            for t, v in seen.items():
+                if t not in qm.act:
+                    continue
+                got = ev.probe_codes(cfg, t).reshape(v.shape)
+                assert np.array_equal(got, v.astype(np.int8)), (name, ci, t)
+    finally:
+        ev.set_option("fusion", 1)
+    ev.close()
+
+
+@pytest.mark.parametrize("name", ["resnet50", "mobilenet_v2", "squeezenet"])
+def test_top1_matches_oracle(name, ds64):
+    g, ev, caches = gpu_and_oracle(name, ds64)
+    space = enumerate_space(GENERIC)
+    picks = [0, 2, 7, 13, 22, 31, 40, 47, 58, 66, 77, 95]
+    got = ev.correct_counts([space[i] for i in picks])
+    oev = O.make_accuracy_evaluator(g, ds64, 0, caches=caches)
+    for i, c in zip(picks, got):
+        want = round(oev(space[i]) * len(ds64.eval_labels))
+        if space[i].mixed == "Off":
+            assert int(c) == want, (name, space[i])
+        else:                                     # fp32 first/last layer: ulp-level drift allowed
+            assert abs(int(c) - want) <= 1, (name, space[i])
+    ev.close()
