@@ -153,6 +153,9 @@ int ptq_set_option(ptq_ctx* ctx, const char* key, int64_t value);
  * the number of timed conv launches and the total number of conv launches. */
 int ptq_last_stats(const ptq_ctx* ctx, int64_t* kernel_launches, double* conv_ms_event,
                    double* conv_ops, int64_t* conv_launches, int64_t* conv_launches_total);
+/* Per-launch CUDA-event times (ms) of the timed conv launches of the last
+ * ptq_eval_configs call, in launch order; *n = number available. */
+int ptq_conv_timings(const ptq_ctx* ctx, float* ms, int64_t cap, int64_t* n);
 /* The CUDA stream (cudaStream_t) every kernel of this context runs on. */
 int ptq_stream(const ptq_ctx* ctx, void** stream);
 

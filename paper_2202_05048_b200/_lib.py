@@ -26,7 +26,7 @@ EXPORTS = ("ptq_last_error", "ptq_version", "ptq_create", "ptq_destroy", "ptq_nu
            "ptq_calibrate", "ptq_kl_sweep", "ptq_set_clip_ranges", "ptq_prepare",
            "ptq_eval_configs", "ptq_probe_codes", "ptq_probe_act_params", "ptq_histogram_host",
            "ptq_set_option", "ptq_last_stats", "ptq_calib_forward", "ptq_calib_histogram",
-           "ptq_stream")
+           "ptq_stream", "ptq_conv_timings")
 
 
 class NodeDesc(C.Structure):
@@ -91,6 +91,7 @@ def load() -> C.CDLL:
         "ptq_calib_forward": [P, i32, P, P, P],
         "ptq_calib_histogram": [P, P, P],
         "ptq_stream": [P, C.POINTER(P)],
+        "ptq_conv_timings": [P, P, i64, C.POINTER(i64)],
     }
     for name, args in sig.items():
         f = getattr(lib, name)

@@ -32,9 +32,13 @@
 namespace ptq {
 
 constexpr int TC_BM = 128;
-constexpr int TC_STAGES = 4;
+// smem pipeline depth: small-N tiles need more stages in flight to cover load latency
+template <int BN>
+struct TcStages {
+  static constexpr int v = (200 * 1024) / (16384 + BN * 128) > 10 ? 10 : (200 * 1024) / (16384 + BN * 128);
+};
 constexpr int TC_A_STAGE = TC_BM * 128;            // 16 KB: 8 chunks x 128 rows x 16 B
-constexpr int TC_EPI_WARPS = 8;
+constexpr int TC_EPI_WARPS = 16;                   // 4 per SM sub-partition
 constexpr int TC_THREADS = (6 + TC_EPI_WARPS) * 32;
 
 __device__ __forceinline__ uint64_t umma_desc(uint32_t saddr, uint32_t lbo, uint32_t sbo) {
@@ -103,8 +107,9 @@ __device__ __forceinline__ int imax(int a, int b) { return a > b ? a : b; }
 
 // clip(RHU(acc*m) + zp, lo, 127): acc clamped to the layer's saturation margin, then
 // fl(fl(acc*m) + 0.5) exactly as the reference, floor and +zp in one round-down add
+template <bool CLAMP>
 __device__ __forceinline__ int requant_fast(int acc, double m, const LayerRt& rt, int lo) {
-  acc = imin(imax(acc, -rt.aclamp), rt.aclamp);
+  if (CLAMP) acc = imin(imax(acc, -rt.aclamp), rt.aclamp);   // else |acc*m| < 2^30 already
   const double r = __dadd_rn(__dmul_rn(i2d(acc), m), 0.5);
   return imin(imax(__double2loint(__dadd_rd(r, rt.mg_zy)), lo), PTQ_QMAX);
 }
@@ -115,7 +120,7 @@ __device__ __forceinline__ int add_fast(int ca, int cb, const LayerRt& rt, int l
 }
 
 // 16 output channels of one row, fast path (no int32 saturation possible)
-template <bool WZP, bool SKIP, bool CONV_A>
+template <bool WZP, bool SKIP, bool CONV_A, bool CLAMP>
 __device__ __forceinline__ void epi_chunk16(const uint32_t (&v)[16], const EpiParam* __restrict__ ep,
                                             int cb, int rowsum, const LayerRt& rt, int lo_conv,
                                             int lo_add, const int4 skv, int4& out) {
@@ -125,14 +130,14 @@ __device__ __forceinline__ void epi_chunk16(const uint32_t (&v)[16], const EpiPa
   for (int g = 0; g < 4; ++g) {
     int4 raw[4];
 #pragma unroll
-    for (int j = 0; j < 4; ++j) raw[j] = __ldg(reinterpret_cast<const int4*>(ep + cb + g * 4) + j);
+    for (int j = 0; j < 4; ++j) raw[j] = reinterpret_cast<const int4*>(ep + cb + g * 4)[j];
 #pragma unroll
     for (int j = 0; j < 4; ++j) {
       const int jj = g * 4 + j;
       const double m = __hiloint2double(raw[j].y, raw[j].x);
       int acc = (int)v[jj] + raw[j].z;
       if (WZP) acc -= raw[j].w * rowsum;
-      int q = requant_fast(acc, m, rt, lo_conv);
+      int q = requant_fast<CLAMP>(acc, m, rt, lo_conv);
       if (SKIP) {
         const int s = (int)(int8_t)(skw[jj >> 2] >> (8 * (jj & 3)));
         q = CONV_A ? add_fast(q, s, rt, lo_add) : add_fast(s, q, rt, lo_add);
@@ -142,6 +147,24 @@ __device__ __forceinline__ void epi_chunk16(const uint32_t (&v)[16], const EpiPa
   }
   out = make_int4((int)packed[0], (int)packed[1], (int)packed[2], (int)packed[3]);
 }
+template <bool NOCLAMP>
+__device__ __forceinline__ void epi_dispatch(const uint32_t (&v)[16], const EpiParam* __restrict__ ep,
+                                             int cb, int rs, const LayerRt& rt, int lo_conv, int lo_add,
+                                             const int4 skv, int4& res, bool skip, int conv_is_a,
+                                             bool wzp) {
+  constexpr bool C = !NOCLAMP;
+  if (!skip) {
+    if (wzp) epi_chunk16<true, false, false, C>(v, ep, cb, rs, rt, lo_conv, lo_add, skv, res);
+    else epi_chunk16<false, false, false, C>(v, ep, cb, rs, rt, lo_conv, lo_add, skv, res);
+  } else if (conv_is_a) {
+    if (wzp) epi_chunk16<true, true, true, C>(v, ep, cb, rs, rt, lo_conv, lo_add, skv, res);
+    else epi_chunk16<false, true, true, C>(v, ep, cb, rs, rt, lo_conv, lo_add, skv, res);
+  } else {
+    if (wzp) epi_chunk16<true, true, false, C>(v, ep, cb, rs, rt, lo_conv, lo_add, skv, res);
+    else epi_chunk16<false, true, false, C>(v, ep, cb, rs, rt, lo_conv, lo_add, skv, res);
+  }
+}
+
 // general (slow) path: 64-bit accumulator with the reference's int32 saturation
 __device__ __forceinline__ int epi_slow(long long dot, int c, long long rowsum, const ConvTcArgs& a,
                                         const LayerRt& rt) {
@@ -208,6 +231,7 @@ __device__ __forceinline__ RowGeo row_geo(const ConvTcArgs& a, int m, int M) {
 
 template <int BN>
 __global__ void __launch_bounds__(TC_THREADS, 1) k_conv_tc(const __grid_constant__ ConvTcArgs a) {
+  constexpr int TC_STAGES = TcStages<BN>::v;
   extern __shared__ __align__(1024) uint8_t smem[];
   uint8_t* sA = smem;
   uint8_t* sB = smem + TC_STAGES * TC_A_STAGE;
@@ -216,6 +240,7 @@ __global__ void __launch_bounds__(TC_THREADS, 1) k_conv_tc(const __grid_constant
   uint64_t* tfull = empty + TC_STAGES;
   uint64_t* tempty = tfull + 2;
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
+  EpiParam* sparam = reinterpret_cast<EpiParam*>(tempty + 4);   // [Cout] per-channel epilogue constants
   constexpr uint32_t TMEM_COLS = (2 * BN) < 32 ? 32 : 2 * BN;
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -263,7 +288,7 @@ __global__ void __launch_bounds__(TC_THREADS, 1) k_conv_tc(const __grid_constant
         uint8_t* dst = sA + s * TC_A_STAGE + r * 16;
 #pragma unroll
         for (int j = 0; j < 8; ++j) {
-          const bool v = g.ok && kk < a.n_chunks;
+          const bool v = g.ok && kk < a.n_chunks && a.ablate != 2;
           const int8_t* src = v ? base + ((int64_t)kh * Wp + kw) * Cp + ch * 16 : a.in.p;
           cp_async16(dst + j * (TC_BM * 16), src, v ? 16u : 0u);
           ++kk;
@@ -323,15 +348,19 @@ __global__ void __launch_bounds__(TC_THREADS, 1) k_conv_tc(const __grid_constant
   } else {
     // ------------------------------------------------ epilogue warps
     const int q = warp & 3;                          // TMEM lane quarter this warp may access
-    const int half = (warp - 6) >> 2;
-    constexpr int CPH = BN / 2 < 16 ? 16 : BN / 2;   // columns per epilogue half
-    const int c_lo = half * CPH, c_hi = (half + 1) * CPH < BN ? (half + 1) * CPH : BN;
+    const int grp = (warp - 6) >> 2;                  // column group (4 groups per lane quarter)
+    constexpr int CPG = BN / 4 < 16 ? 16 : BN / 4;   // columns per group
+    const int c_lo = grp * CPG, c_hi = (grp + 1) * CPG < BN ? (grp + 1) * CPG : BN;
     const int row = q * 32 + lane;
     const LayerRt rt = *a.L.rt;
     const int lo_conv = rt.relu_zp > PTQ_QMIN ? rt.relu_zp : PTQ_QMIN;
     const int lo_add = rt.add_relu_zp > PTQ_QMIN ? rt.add_relu_zp : PTQ_QMIN;
     const int Cout = a.L.cout;
-    const EpiParam* __restrict__ ep = a.L.ep;
+    // stage the layer's per-channel epilogue constants in shared memory once (L1 misses on
+    // these broadcast loads were the top stall), then sync the 16 epilogue warps only
+    for (int i = threadIdx.x - 6 * 32; i < Cout; i += TC_EPI_WARPS * 32) sparam[i] = a.L.ep[i];
+    asm volatile("bar.sync 1, %0;" ::"n"(TC_EPI_WARPS * 32) : "memory");
+    const EpiParam* ep = sparam;
     const bool wzp = a.has_wzp != 0;
     uint32_t lt = 0;
     for (int tile = blockIdx.x; tile < n_tiles; tile += gridDim.x, ++lt) {
@@ -352,18 +381,12 @@ __global__ void __launch_bounds__(TC_THREADS, 1) k_conv_tc(const __grid_constant
         if (cb >= a.out.Cp) continue;            // warp-uniform: the slow path re-reads TMEM
         const int4 skv = srow ? *reinterpret_cast<const int4*>(srow + cb) : make_int4(0, 0, 0, 0);
         int4 res;
-        if (!rt.slow && cb + 16 <= Cout) {
+        if (a.ablate == 1) {
+          res = make_int4((int)v[0], (int)v[1], (int)v[2], (int)v[3]);
+        } else if (!rt.slow && cb + 16 <= Cout) {
           const int rs = (int)rowsum;
-          if (!srow) {
-            if (wzp) epi_chunk16<true, false, false>(v, ep, cb, rs, rt, lo_conv, lo_add, skv, res);
-            else epi_chunk16<false, false, false>(v, ep, cb, rs, rt, lo_conv, lo_add, skv, res);
-          } else if (a.conv_is_a) {
-            if (wzp) epi_chunk16<true, true, true>(v, ep, cb, rs, rt, lo_conv, lo_add, skv, res);
-            else epi_chunk16<false, true, true>(v, ep, cb, rs, rt, lo_conv, lo_add, skv, res);
-          } else {
-            if (wzp) epi_chunk16<true, true, false>(v, ep, cb, rs, rt, lo_conv, lo_add, skv, res);
-            else epi_chunk16<false, true, false>(v, ep, cb, rs, rt, lo_conv, lo_add, skv, res);
-          }
+          if (rt.noclamp) epi_dispatch<true>(v, ep, cb, rs, rt, lo_conv, lo_add, skv, res, srow != nullptr, a.conv_is_a, wzp);
+          else epi_dispatch<false>(v, ep, cb, rs, rt, lo_conv, lo_add, skv, res, srow != nullptr, a.conv_is_a, wzp);
         } else {
           res = epi_slow_chunk(tmem + ((uint32_t)(q * 32) << 16) + buf * BN + (uint32_t)c0, cb, rowsum,
                                a, rt, lo_conv, lo_add, skv);
@@ -435,11 +458,12 @@ static int g_num_sms = 0;
 
 template <int BN>
 static void launch_bn(const ConvTcArgs& a, cudaStream_t s) {
+  constexpr int TC_STAGES = TcStages<BN>::v;
   const size_t smem = (size_t)TC_STAGES * TC_A_STAGE + (size_t)TC_STAGES * BN * 128 +
-                      (2 * TC_STAGES + 4) * 8 + 16;
+                      (2 * TC_STAGES + 4) * 8 + 16 + (size_t)a.L.cout * sizeof(EpiParam);
   static bool configured = false;
   if (!configured) {
-    cudaFuncSetAttribute(k_conv_tc<BN>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    cudaFuncSetAttribute(k_conv_tc<BN>, cudaFuncAttributeMaxDynamicSharedMemorySize, 232448);
     configured = true;
   }
   if (!g_num_sms) {

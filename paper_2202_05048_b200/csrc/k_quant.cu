@@ -227,6 +227,7 @@ __global__ void k_layer_params(const LayerSt* __restrict__ layers, const float* 
     // fast-path acc clamp: |A*m| <= 2^30 for every channel, and A*m > 300 for every channel
     // (so clamped accumulators still saturate exactly as the unclamped ones would)
     r.aclamp = 0;
+    r.noclamp = 0;
     if (L.ep && !slow) {
       const double mmax = __longlong_as_double((long long)m_max_bits);
       const double mmin = __longlong_as_double((long long)m_min_bits);
@@ -234,6 +235,7 @@ __global__ void k_layer_params(const LayerSt* __restrict__ layers, const float* 
       const double need = ceil(300.0 / mmin) + 2.0;
       if (A >= need) r.aclamp = A > 2147483647.0 ? 2147483647 : (int)A;
       else slow = 1;
+      r.noclamp = mmax < 0.5;
     }
     r.zx = az[L.in_hist];
     r.zy = az[L.out_hist];
@@ -349,27 +351,41 @@ void launch_dequant(View in, const float* as, const int* az, int hist, float* y,
 }
 
 // fill the spatial halo with the zero-point code (all Cp bytes)
+// one thread per (halo pixel, 16-channel chunk); halo pixels of one image are enumerated as
+// the top/bottom halo rows (full padded width) followed by the left/right halo columns
 __global__ void k_halo_fill(View v, const int* __restrict__ az, int hist) {
   const int8_t z = (int8_t)az[hist];
   const int Hp = v.H + 2 * v.halo, Wp = v.W + 2 * v.halo;
-  const int64_t total = (int64_t)v.N * Hp * Wp;
-  for (int64_t p = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; p < total;
-       p += (int64_t)gridDim.x * blockDim.x) {
-    int w = (int)(p % Wp);
-    int h = (int)((p / Wp) % Hp);
-    if (h >= v.halo && h < v.halo + v.H && w >= v.halo && w < v.halo + v.W) continue;
-    int8_t* d = v.p + p * v.Cp;
-    for (int c0 = 0; c0 < v.Cp; c0 += 16) {
-      alignas(16) int8_t b[16];
-#pragma unroll
-      for (int j = 0; j < 16; ++j) b[j] = (c0 + j < v.C) ? z : (int8_t)0;  // pad channels stay 0
-      *reinterpret_cast<int4*>(d + c0) = *reinterpret_cast<const int4*>(b);
+  const int rows = 2 * v.halo * Wp, per_img = rows + 2 * v.halo * v.H;
+  const int nch = v.Cp >> 4;
+  const int64_t total = (int64_t)v.N * per_img * nch;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < total;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    const int c0 = (int)(i % nch) * 16;
+    const int64_t q = i / nch;
+    const int n = (int)(q / per_img), k = (int)(q - (int64_t)n * per_img);
+    int h, w;
+    if (k < rows) {                           // top halo rows then bottom halo rows
+      const int r = k / Wp;
+      h = r < v.halo ? r : v.H + r;           // r in [halo, 2*halo) -> bottom rows
+      w = k - r * Wp;
+    } else {                                  // left / right columns of the interior rows
+      const int k2 = k - rows, r = k2 / (2 * v.halo), cc = k2 - r * 2 * v.halo;
+      h = v.halo + r;
+      w = cc < v.halo ? cc : v.W + cc;
     }
+    int8_t* d = v.p + (((int64_t)n * Hp + h) * Wp + w) * v.Cp + c0;
+    uint32_t pk[4] = {0u, 0u, 0u, 0u};
+#pragma unroll
+    for (int j = 0; j < 16; ++j)                // pad channels stay 0
+      if (c0 + j < v.C) pk[j >> 2] |= ((uint32_t)(uint8_t)z) << (8 * (j & 3));
+    *reinterpret_cast<int4*>(d) = make_int4((int)pk[0], (int)pk[1], (int)pk[2], (int)pk[3]);
   }
 }
 void launch_halo_fill(View v, const int* az, int hist, cudaStream_t s) {
   if (v.halo <= 0) return;
-  int64_t n = (int64_t)v.N * (v.H + 2 * v.halo) * (v.W + 2 * v.halo);
+  const int Wp = v.W + 2 * v.halo;
+  const int64_t n = (int64_t)v.N * (2 * v.halo * Wp + 2 * v.halo * v.H) * (v.Cp >> 4);
   k_halo_fill<<<nblk(n), 256, 0, s>>>(v, az, hist);
 }
 
@@ -530,10 +546,54 @@ __global__ void k_im2col(View in, int k, int stride, int pad, int OH, int OW, in
     *reinterpret_cast<int4*>(out + m * out_cp + j * 16) = make_int4((int)pk[0], (int)pk[1], (int)pk[2], (int)pk[3]);
   }
 }
+// specialised (C, K): one thread per output pixel, one 4-byte load per tap (the C <= 4 codes
+// sit at the start of each 16-byte pixel), the whole packed row assembled in registers
+template <int C, int K>
+__global__ void k_im2col_ck(View in, int stride, int pad, int OH, int OW, int8_t* __restrict__ out,
+                            int64_t total) {
+  constexpr int KP = (K * K * C + 15) / 16 * 16;
+  const int Wp = in.W + 2 * in.halo, Hp = in.H + 2 * in.halo;
+  for (int64_t m = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; m < total;
+       m += (int64_t)gridDim.x * blockDim.x) {
+    const int ow = (int)(m % OW);
+    const int64_t t = m / OW;
+    const int oh = (int)(t % OH), n = (int)(t / OH);
+    const int8_t* base = in.p + (((int64_t)n * Hp + oh * stride - pad + in.halo) * Wp +
+                                 ow * stride - pad + in.halo) * in.Cp;
+    uint32_t w[KP / 4];
+#pragma unroll
+    for (int i = 0; i < KP / 4; ++i) w[i] = 0u;
+#pragma unroll
+    for (int kh = 0; kh < K; ++kh)
+#pragma unroll
+      for (int kw = 0; kw < K; ++kw) {
+        const uint32_t v = __ldg(reinterpret_cast<const uint32_t*>(base + ((int64_t)kh * Wp + kw) * in.Cp));
+#pragma unroll
+        for (int c = 0; c < C; ++c) {
+          const int pos = (kh * K + kw) * C + c;
+          w[pos >> 2] |= ((v >> (8 * c)) & 0xffu) << (8 * (pos & 3));
+        }
+      }
+    int4* dst = reinterpret_cast<int4*>(out + m * KP);
+#pragma unroll
+    for (int i = 0; i < KP / 16; ++i)
+      dst[i] = make_int4((int)w[4 * i], (int)w[4 * i + 1], (int)w[4 * i + 2], (int)w[4 * i + 3]);
+  }
+}
+
 void launch_im2col(View in, int k, int stride, int pad, int OH, int OW, int8_t* out, int out_cp,
                    cudaStream_t s) {
-  const int64_t total = (int64_t)in.N * OH * OW * (out_cp >> 4);
-  k_im2col<<<nblk(total), 256, 0, s>>>(in, k, stride, pad, OH, OW, out, out_cp, total);
+  const int64_t pixels = (int64_t)in.N * OH * OW;
+  if (in.C == 3 && k == 7) {
+    k_im2col_ck<3, 7><<<nblk(pixels, 128), 128, 0, s>>>(in, stride, pad, OH, OW, out, pixels);
+  } else if (in.C == 3 && k == 3) {
+    k_im2col_ck<3, 3><<<nblk(pixels, 128), 128, 0, s>>>(in, stride, pad, OH, OW, out, pixels);
+  } else if (in.C == 3 && k == 5) {
+    k_im2col_ck<3, 5><<<nblk(pixels, 128), 128, 0, s>>>(in, stride, pad, OH, OW, out, pixels);
+  } else {
+    const int64_t total = pixels * (out_cp >> 4);
+    k_im2col<<<nblk(total), 256, 0, s>>>(in, k, stride, pad, OH, OW, out, out_cp, total);
+  }
 }
 
 // P[padded pixel] = sum of the real-channel codes (rowsum term of the zero-point correction)

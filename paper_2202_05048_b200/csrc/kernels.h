@@ -24,6 +24,7 @@ struct LayerRt {
   int aclamp;          // fast path clamps acc to [-aclamp, aclamp]: beyond it every channel
                        // saturates (|acc*m| > 300) and |acc*m| stays < 2^30 for the floor trick
   double mg_zy, mg_zo; // 1.5*2^52 + zp: floor(r) + zp via one round-down add
+  int noclamp;         // max m < 0.5: |acc*m| < 2^30 for any int32 acc, no clamp needed
 };
 
 // per-config, per-output-channel epilogue constants of the tensor-core conv:
@@ -163,6 +164,7 @@ struct ConvTcArgs {
   View skip;              // fused add operand (p == nullptr when none)
   int conv_is_a;          // 1 if the conv output is operand 0 of the fused add
   FastDiv div_ow, div_oh, div_nt;   // m -> (n, oh, ow) and tile -> (m-tile, n-tile)
+  int ablate;             // profiling only: 1 = skip epilogue math, 2 = skip A gathers
 };
 int conv_tc_bn_for(int cout);     // BN tile width the kernel uses for this Cout
 void launch_conv_tc(const ConvTcArgs& a, int bn, cudaStream_t s);

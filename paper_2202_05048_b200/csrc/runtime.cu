@@ -162,7 +162,7 @@ struct ptq_ctx {
   std::vector<int*> cal_slots;
   std::vector<int> cal_sizes;
   // options
-  int conv_ref = 0, fusion = 1, time_conv = 0;
+  int conv_ref = 0, fusion = 1, time_conv = 0, ablate = 0;
   int64_t opt_chunk = 0;
   // stats
   int64_t launches = 0;
@@ -851,6 +851,7 @@ void eval_one(ptq_ctx* c, const ptq_config& cfg, unsigned long long* d_correct, 
             a.skip = V(P.add_other[i]);
             a.conv_is_a = P.add_is_a[i];
           }
+          a.ablate = c->ablate;
           cudaEvent_t ea = nullptr, eb = nullptr;
           const bool timed = c->cur_cfg < c->time_conv;   // instrument only the leading configs
           ++c->conv_launches_total;
@@ -1254,6 +1255,7 @@ int ptq_set_option(ptq_ctx* c, const char* key, int64_t value) {
     REQ(c && key, "null argument");
     std::string k(key);
     if (k == "conv_ref") c->conv_ref = (int)value;
+    else if (k == "ablate") c->ablate = (int)value;
     else if (k == "time_conv") c->time_conv = (int)value;
     else if (k == "reset_stats") c->launches = 0;
     else if (k == "fusion") {
@@ -1279,6 +1281,20 @@ int ptq_last_stats(const ptq_ctx* c, int64_t* launches, double* conv_ms, double*
   if (conv_ops) *conv_ops = c->conv_ops;
   if (conv_launches) *conv_launches = (int64_t)(c->ev_used / 2);
   if (conv_launches_total) *conv_launches_total = c->conv_launches_total;
+  return PTQ_OK;
+}
+
+int ptq_conv_timings(const ptq_ctx* c, float* ms, int64_t cap, int64_t* n) {
+  if (!c || !n) { g_err = "null argument"; return PTQ_EINVAL; }
+  *n = (int64_t)(c->ev_used / 2);
+  for (int64_t i = 0; ms && i < *n && i < cap; ++i) {
+    float v = 0.f;
+    if (cudaEventElapsedTime(&v, c->ev_pool[2 * i], c->ev_pool[2 * i + 1]) != cudaSuccess) {
+      g_err = "event timing unavailable";
+      return PTQ_ECUDA;
+    }
+    ms[i] = v;
+  }
   return PTQ_OK;
 }
 

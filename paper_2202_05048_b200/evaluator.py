@@ -273,6 +273,13 @@ class GpuEvaluator:
         return {"launches": n.value, "conv_ms": ms.value, "conv_ops": ops.value,
                 "conv_launches": nc.value, "conv_launches_total": nt.value}
 
+    def conv_timings(self) -> np.ndarray:
+        n = C.c_int64()
+        _lib.check(self.lib.ptq_conv_timings(self._ctx, None, 0, C.byref(n)))
+        out = np.zeros(n.value, dtype=np.float32)
+        _lib.check(self.lib.ptq_conv_timings(self._ctx, _lib.ptr(out), n.value, C.byref(n)))
+        return out
+
     def stream_handle(self) -> int:
         s = C.c_void_p()
         _lib.check(self.lib.ptq_stream(self._ctx, C.byref(s)))
