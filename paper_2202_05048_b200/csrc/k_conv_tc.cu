@@ -38,8 +38,8 @@ struct TcStages {
   static constexpr int v = (200 * 1024) / (16384 + BN * 128) > 10 ? 10 : (200 * 1024) / (16384 + BN * 128);
 };
 constexpr int TC_A_STAGE = TC_BM * 128;            // 16 KB: 8 chunks x 128 rows x 16 B
-constexpr int TC_EPI_WARPS = 16;                   // 4 per SM sub-partition
-constexpr int TC_THREADS = (6 + TC_EPI_WARPS) * 32;
+constexpr int TC_EPI_WARPS = 12;                   // 3 per SM sub-partition (register budget: no spills)
+constexpr int TC_THREADS = (4 + TC_EPI_WARPS) * 32;    // 16 warps: 4 per SM sub-partition
 
 __device__ __forceinline__ uint64_t umma_desc(uint32_t saddr, uint32_t lbo, uint32_t sbo) {
   uint64_t d = 0;
@@ -174,31 +174,42 @@ __device__ __forceinline__ int epi_slow(long long dot, int c, long long rowsum, 
   return requant1(acc, a.L.mult[c], rt.zy);
 }
 
-// exact 64-bit path for a whole 16-channel chunk (int32 saturation possible, or a partial
-// chunk); kept out of line so it costs the hot loop no registers
-__device__ __noinline__ int4 epi_slow_chunk(uint32_t taddr, int cb, long long rowsum,
-                                            const ConvTcArgs& a, const LayerRt& rt, int lo_conv,
-                                            int lo_add, int4 skv) {
-  uint32_t v[16];
-  tmem_ld16(taddr, v);                      // warp-uniform branch: re-read the accumulators
-  const int8_t* sk = reinterpret_cast<const int8_t*>(&skv);
-  uint32_t packed[4] = {0u, 0u, 0u, 0u};
+__device__ __forceinline__ uint32_t tmem_ld1(uint32_t taddr) {
+  uint32_t v;
+  asm volatile("tcgen05.ld.sync.aligned.32x32b.x1.b32 {%0}, [%1];" : "=r"(v) : "r"(taddr));
+  asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+  return v;
+}
+
+// exact 64-bit path for a 16-channel chunk (int32 saturation possible, or a partial chunk).
+// Rare (warp-uniform branch); written as a rolled loop that re-reads one TMEM column per
+// step so it holds no arrays and costs the fast path no registers.
+__device__ __forceinline__ int4 epi_slow_chunk(uint32_t taddr, int cb, long long rowsum,
+                                               const ConvTcArgs& a, const LayerRt& rt, int lo_conv,
+                                               int lo_add, int4 skv) {
+  const uint64_t sk_lo = ((uint64_t)(uint32_t)skv.y << 32) | (uint32_t)skv.x;
+  const uint64_t sk_hi = ((uint64_t)(uint32_t)skv.w << 32) | (uint32_t)skv.z;
+  uint64_t lo = 0, hi = 0;
+#pragma unroll 1
   for (int j = 0; j < 16; ++j) {
+    const uint32_t x = tmem_ld1(taddr + (uint32_t)j);
     const int c = cb + j;
     int code = 0;
     if (c < a.L.cout) {
-      code = epi_slow((long long)(int)v[j], c, rowsum, a, rt);
+      code = epi_slow((long long)(int)x, c, rowsum, a, rt);
       if (code < lo_conv) code = lo_conv;
       if (a.skip.p) {
-        const int xa = a.conv_is_a ? code : sk[j], xb = a.conv_is_a ? sk[j] : code;
+        const int skc = (int)(int8_t)(((j < 8) ? sk_lo : sk_hi) >> (8 * (j & 7)));
+        const int xa = a.conv_is_a ? code : skc, xb = a.conv_is_a ? skc : code;
         const double s2 = __dadd_rn(__dmul_rn(i2d(xa - rt.za), rt.ra), __dmul_rn(i2d(xb - rt.zb), rt.rb));
         code = clip8(rhu(s2) + (double)rt.zo);
         if (code < lo_add) code = lo_add;
       }
     }
-    packed[j >> 2] |= ((uint32_t)code & 0xffu) << (8 * (j & 3));
+    const uint64_t bits = (uint64_t)((uint32_t)code & 0xffu) << (8 * (j & 7));
+    if (j < 8) lo |= bits; else hi |= bits;
   }
-  return make_int4((int)packed[0], (int)packed[1], (int)packed[2], (int)packed[3]);
+  return make_int4((int)(uint32_t)lo, (int)(uint32_t)(lo >> 32), (int)(uint32_t)hi, (int)(uint32_t)(hi >> 32));
 }
 
 __device__ __forceinline__ long long pixel_rowsum(const ConvTcArgs& a, int n, int ih0, int iw0) {
@@ -250,7 +261,7 @@ __global__ void __launch_bounds__(TC_THREADS, 1) k_conv_tc(const __grid_constant
 
   if (threadIdx.x == 0) {
     for (int s = 0; s < TC_STAGES; ++s) {
-      mbar_init(&full[s], 128 + 1);
+      mbar_init(&full[s], 64 + 1);
       mbar_init(&empty[s], 1);
     }
     for (int b = 0; b < 2; ++b) {
@@ -259,7 +270,7 @@ __global__ void __launch_bounds__(TC_THREADS, 1) k_conv_tc(const __grid_constant
     }
     fence_mbar_init();
   }
-  if (warp == 5) {
+  if (warp == 3) {
     asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
                      smem_u32(tmem_slot)),
                  "r"(TMEM_COLS));
@@ -270,16 +281,19 @@ __global__ void __launch_bounds__(TC_THREADS, 1) k_conv_tc(const __grid_constant
   tc_fence_after();
   const uint32_t tmem = *tmem_slot;
 
-  if (warp < 4) {
+  if (warp < 2) {
     // ------------------------------------------------ A producers (implicit im2col gather)
+    // 64 threads, two GEMM rows (output pixels) each: r and r + 64
     const int r = threadIdx.x;
     const int Cp = a.in.Cp, cpc = Cp >> 4;
     const int Wp = a.in.W + 2 * a.in.halo, Hp = a.in.H + 2 * a.in.halo;
     uint32_t it = 0;
     for (int tile = blockIdx.x; tile < n_tiles; tile += gridDim.x) {
       const int mt = (int)a.div_nt.div((uint32_t)tile);
-      const RowGeo g = row_geo(a, mt * TC_BM + r, M);
-      const int8_t* base = a.in.p + (((int64_t)g.n * Hp + g.ih0) * Wp + g.iw0) * Cp;
+      const RowGeo g0 = row_geo(a, mt * TC_BM + r, M);
+      const RowGeo g1 = row_geo(a, mt * TC_BM + r + 64, M);
+      const int8_t* base0 = a.in.p + (((int64_t)g0.n * Hp + g0.ih0) * Wp + g0.iw0) * Cp;
+      const int8_t* base1 = a.in.p + (((int64_t)g1.n * Hp + g1.ih0) * Wp + g1.iw0) * Cp;
       int kh = 0, kw = 0, ch = 0, kk = 0;
       for (int ki = 0; ki < a.n_kiter; ++ki, ++it) {
         const int s = it % TC_STAGES;
@@ -288,9 +302,11 @@ __global__ void __launch_bounds__(TC_THREADS, 1) k_conv_tc(const __grid_constant
         uint8_t* dst = sA + s * TC_A_STAGE + r * 16;
 #pragma unroll
         for (int j = 0; j < 8; ++j) {
-          const bool v = g.ok && kk < a.n_chunks && a.ablate != 2;
-          const int8_t* src = v ? base + ((int64_t)kh * Wp + kw) * Cp + ch * 16 : a.in.p;
-          cp_async16(dst + j * (TC_BM * 16), src, v ? 16u : 0u);
+          const bool kin = kk < a.n_chunks && a.ablate != 2;
+          const int64_t off = ((int64_t)kh * Wp + kw) * Cp + ch * 16;
+          const bool v0 = g0.ok && kin, v1 = g1.ok && kin;
+          cp_async16(dst + j * (TC_BM * 16), v0 ? base0 + off : a.in.p, v0 ? 16u : 0u);
+          cp_async16(dst + j * (TC_BM * 16) + 64 * 16, v1 ? base1 + off : a.in.p, v1 ? 16u : 0u);
           ++kk;
           if (++ch == cpc) {
             ch = 0;
@@ -300,7 +316,7 @@ __global__ void __launch_bounds__(TC_THREADS, 1) k_conv_tc(const __grid_constant
         cp_async_mbar_arrive_noinc(&full[s]);
       }
     }
-  } else if (warp == 4) {
+  } else if (warp == 2) {
     // ------------------------------------------------ B producer (bulk copies of pre-tiled weights)
     if (lane == 0) {
       uint32_t it = 0;
@@ -316,7 +332,7 @@ __global__ void __launch_bounds__(TC_THREADS, 1) k_conv_tc(const __grid_constant
         }
       }
     }
-  } else if (warp == 5) {
+  } else if (warp == 3) {
     // ------------------------------------------------ MMA issuer
     if (lane == 0) {
       const uint32_t idesc = idesc_i8<BN>();
@@ -348,9 +364,9 @@ __global__ void __launch_bounds__(TC_THREADS, 1) k_conv_tc(const __grid_constant
   } else {
     // ------------------------------------------------ epilogue warps
     const int q = warp & 3;                          // TMEM lane quarter this warp may access
-    const int grp = (warp - 6) >> 2;                  // column group (4 groups per lane quarter)
-    constexpr int CPG = BN / 4 < 16 ? 16 : BN / 4;   // columns per group
-    const int c_lo = grp * CPG, c_hi = (grp + 1) * CPG < BN ? (grp + 1) * CPG : BN;
+    const int grp = (warp - 4) >> 2;                  // column group (3 groups per lane quarter)
+    constexpr int NCH = BN / 16;                      // 16-column chunks per tile
+    const int c_lo = (grp * NCH / 3) * 16, c_hi = ((grp + 1) * NCH / 3) * 16;
     const int row = q * 32 + lane;
     const LayerRt rt = *a.L.rt;
     const int lo_conv = rt.relu_zp > PTQ_QMIN ? rt.relu_zp : PTQ_QMIN;
@@ -358,7 +374,7 @@ __global__ void __launch_bounds__(TC_THREADS, 1) k_conv_tc(const __grid_constant
     const int Cout = a.L.cout;
     // stage the layer's per-channel epilogue constants in shared memory once (L1 misses on
     // these broadcast loads were the top stall), then sync the 16 epilogue warps only
-    for (int i = threadIdx.x - 6 * 32; i < Cout; i += TC_EPI_WARPS * 32) sparam[i] = a.L.ep[i];
+    for (int i = threadIdx.x - 4 * 32; i < Cout; i += TC_EPI_WARPS * 32) sparam[i] = a.L.ep[i];
     asm volatile("bar.sync 1, %0;" ::"n"(TC_EPI_WARPS * 32) : "memory");
     const EpiParam* ep = sparam;
     const bool wzp = a.has_wzp != 0;
@@ -400,7 +416,7 @@ __global__ void __launch_bounds__(TC_THREADS, 1) k_conv_tc(const __grid_constant
 
   tc_fence_before();
   __syncthreads();
-  if (warp == 5) {
+  if (warp == 3) {
     tc_fence_after();
     asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(TMEM_COLS));
   }
