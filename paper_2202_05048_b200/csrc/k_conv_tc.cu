@@ -105,63 +105,86 @@ __device__ __forceinline__ int clampi(int x, int lo, int hi) { return x < lo ? l
 __device__ __forceinline__ int imin(int a, int b) { return a < b ? a : b; }
 __device__ __forceinline__ int imax(int a, int b) { return a > b ? a : b; }
 
-// clip(RHU(acc*m) + zp, lo, 127): acc clamped to the layer's saturation margin, then
-// fl(fl(acc*m) + 0.5) exactly as the reference, floor and +zp in one round-down add
+// fp64 value of a 2^31-biased int32 (accb = acc + 2^31 mod 2^32): 2^52 + accb is exact
+__device__ __forceinline__ double b2d(uint32_t accb) {
+  return __dsub_rn(__hiloint2double(0x43300000, (int)accb), 4503601774854144.0);
+}
+// sign-extended byte b of w: PTX prmt with the sign-replicate selector bit (the
+// __byte_perm intrinsic only honours the low 3 selector bits)
+__device__ __forceinline__ int sbyte(uint32_t w, int b) {
+  int r;
+  asm("prmt.b32 %0, %1, 0, %2;" : "=r"(r) : "r"(w), "r"((uint32_t)(0x8880 | (b * 0x1110) | b)));
+  return r;
+}
+
+// per-layer epilogue constants held in registers by every epilogue thread
+struct EpiK {
+  uint32_t clo, chi;   // biased acc clamp bounds 2^31 -/+ aclamp
+  uint32_t ka, kb;     // 2^31 - za, 2^31 - zb: (x - z) + 2^31 in one add
+  int lo_conv, lo_add;
+};
+
+// clip(RHU(acc*m) + zp, lo, 127) on a biased accumulator: acc clamped to the layer's
+// saturation margin, then fl(fl(acc*m) + 0.5) exactly as the reference, floor and +zp in
+// one round-down add
 template <bool CLAMP>
-__device__ __forceinline__ int requant_fast(int acc, double m, const LayerRt& rt, int lo) {
-  if (CLAMP) acc = imin(imax(acc, -rt.aclamp), rt.aclamp);   // else |acc*m| < 2^30 already
-  const double r = __dadd_rn(__dmul_rn(i2d(acc), m), 0.5);
-  return imin(imax(__double2loint(__dadd_rd(r, rt.mg_zy)), lo), PTQ_QMAX);
+__device__ __forceinline__ int requant_fast(uint32_t accb, double m, const LayerRt& rt, const EpiK& k) {
+  if (CLAMP) accb = umin(umax(accb, k.clo), k.chi);      // else |acc*m| < 2^30 already
+  const double r = __dadd_rn(__dmul_rn(b2d(accb), m), 0.5);
+  return imin(imax(__double2loint(__dadd_rd(r, rt.mg_zy)), k.lo_conv), PTQ_QMAX);
 }
 // residual add on codes (intexec.py:245-276): clip(RHU(xs*ra + ys*rb) + zo)
-__device__ __forceinline__ int add_fast(int ca, int cb, const LayerRt& rt, int lo) {
-  const double s = __dadd_rn(__dmul_rn(i2d(ca - rt.za), rt.ra), __dmul_rn(i2d(cb - rt.zb), rt.rb));
-  return imin(imax(__double2loint(__dadd_rd(__dadd_rn(s, 0.5), rt.mg_zo)), lo), PTQ_QMAX);
+__device__ __forceinline__ int add_fast(int ca, int cb, const LayerRt& rt, const EpiK& k) {
+  const double s = __dadd_rn(__dmul_rn(b2d((uint32_t)ca + k.ka), rt.ra),
+                             __dmul_rn(b2d((uint32_t)cb + k.kb), rt.rb));
+  return imin(imax(__double2loint(__dadd_rd(__dadd_rn(s, 0.5), rt.mg_zo)), k.lo_add), PTQ_QMAX);
 }
 
 // 16 output channels of one row, fast path (no int32 saturation possible)
 template <bool WZP, bool SKIP, bool CONV_A, bool CLAMP>
 __device__ __forceinline__ void epi_chunk16(const uint32_t (&v)[16], const EpiParam* __restrict__ ep,
-                                            int cb, int rowsum, const LayerRt& rt, int lo_conv,
-                                            int lo_add, const int4 skv, int4& out) {
-  uint32_t packed[4] = {0u, 0u, 0u, 0u};
+                                            int cb, int rowsum, const LayerRt& rt, const EpiK& k,
+                                            const int4 skv, int4& out) {
+  uint32_t packed[4];
   const uint32_t skw[4] = {(uint32_t)skv.x, (uint32_t)skv.y, (uint32_t)skv.z, (uint32_t)skv.w};
 #pragma unroll
   for (int g = 0; g < 4; ++g) {
     int4 raw[4];
 #pragma unroll
     for (int j = 0; j < 4; ++j) raw[j] = reinterpret_cast<const int4*>(ep + cb + g * 4)[j];
+    int q[4];
 #pragma unroll
     for (int j = 0; j < 4; ++j) {
       const int jj = g * 4 + j;
       const double m = __hiloint2double(raw[j].y, raw[j].x);
-      int acc = (int)v[jj] + raw[j].z;
-      if (WZP) acc -= raw[j].w * rowsum;
-      int q = requant_fast<CLAMP>(acc, m, rt, lo_conv);
+      uint32_t accb = v[jj] + (uint32_t)raw[j].z;
+      if (WZP) accb -= (uint32_t)(raw[j].w * rowsum);
+      q[j] = requant_fast<CLAMP>(accb, m, rt, k);
       if (SKIP) {
-        const int s = (int)(int8_t)(skw[jj >> 2] >> (8 * (jj & 3)));
-        q = CONV_A ? add_fast(q, s, rt, lo_add) : add_fast(s, q, rt, lo_add);
+        const int s = sbyte(skw[g], j);
+        q[j] = CONV_A ? add_fast(q[j], s, rt, k) : add_fast(s, q[j], rt, k);
       }
-      packed[jj >> 2] |= ((uint32_t)q & 0xffu) << (8 * (jj & 3));
     }
+    packed[g] = __byte_perm(__byte_perm((uint32_t)q[0], (uint32_t)q[1], 0x0040),
+                            __byte_perm((uint32_t)q[2], (uint32_t)q[3], 0x0040), 0x5410);
   }
   out = make_int4((int)packed[0], (int)packed[1], (int)packed[2], (int)packed[3]);
 }
 template <bool NOCLAMP>
 __device__ __forceinline__ void epi_dispatch(const uint32_t (&v)[16], const EpiParam* __restrict__ ep,
-                                             int cb, int rs, const LayerRt& rt, int lo_conv, int lo_add,
+                                             int cb, int rs, const LayerRt& rt, const EpiK& k,
                                              const int4 skv, int4& res, bool skip, int conv_is_a,
                                              bool wzp) {
   constexpr bool C = !NOCLAMP;
   if (!skip) {
-    if (wzp) epi_chunk16<true, false, false, C>(v, ep, cb, rs, rt, lo_conv, lo_add, skv, res);
-    else epi_chunk16<false, false, false, C>(v, ep, cb, rs, rt, lo_conv, lo_add, skv, res);
+    if (wzp) epi_chunk16<true, false, false, C>(v, ep, cb, rs, rt, k, skv, res);
+    else epi_chunk16<false, false, false, C>(v, ep, cb, rs, rt, k, skv, res);
   } else if (conv_is_a) {
-    if (wzp) epi_chunk16<true, true, true, C>(v, ep, cb, rs, rt, lo_conv, lo_add, skv, res);
-    else epi_chunk16<false, true, true, C>(v, ep, cb, rs, rt, lo_conv, lo_add, skv, res);
+    if (wzp) epi_chunk16<true, true, true, C>(v, ep, cb, rs, rt, k, skv, res);
+    else epi_chunk16<false, true, true, C>(v, ep, cb, rs, rt, k, skv, res);
   } else {
-    if (wzp) epi_chunk16<true, true, false, C>(v, ep, cb, rs, rt, lo_conv, lo_add, skv, res);
-    else epi_chunk16<false, true, false, C>(v, ep, cb, rs, rt, lo_conv, lo_add, skv, res);
+    if (wzp) epi_chunk16<true, true, false, C>(v, ep, cb, rs, rt, k, skv, res);
+    else epi_chunk16<false, true, false, C>(v, ep, cb, rs, rt, k, skv, res);
   }
 }
 
@@ -366,14 +389,18 @@ __global__ void __launch_bounds__(TC_THREADS, 1) k_conv_tc(const __grid_constant
     const int q = warp & 3;                          // TMEM lane quarter this warp may access
     const int grp = (warp - 4) >> 2;                  // column group (3 groups per lane quarter)
     constexpr int NCH = BN / 16;                      // 16-column chunks per tile
-    const int c_lo = (grp * NCH / 3) * 16, c_hi = ((grp + 1) * NCH / 3) * 16;
     const int row = q * 32 + lane;
     const LayerRt rt = *a.L.rt;
-    const int lo_conv = rt.relu_zp > PTQ_QMIN ? rt.relu_zp : PTQ_QMIN;
-    const int lo_add = rt.add_relu_zp > PTQ_QMIN ? rt.add_relu_zp : PTQ_QMIN;
+    EpiK k;
+    k.lo_conv = rt.relu_zp > PTQ_QMIN ? rt.relu_zp : PTQ_QMIN;
+    k.lo_add = rt.add_relu_zp > PTQ_QMIN ? rt.add_relu_zp : PTQ_QMIN;
+    k.clo = 0x80000000u - (uint32_t)rt.aclamp;
+    k.chi = 0x80000000u + (uint32_t)rt.aclamp;
+    k.ka = 0x80000000u - (uint32_t)rt.za;
+    k.kb = 0x80000000u - (uint32_t)rt.zb;
     const int Cout = a.L.cout;
     // stage the layer's per-channel epilogue constants in shared memory once (L1 misses on
-    // these broadcast loads were the top stall), then sync the 16 epilogue warps only
+    // these broadcast loads were the top stall), then sync the 12 epilogue warps only
     for (int i = threadIdx.x - 4 * 32; i < Cout; i += TC_EPI_WARPS * 32) sparam[i] = a.L.ep[i];
     asm volatile("bar.sync 1, %0;" ::"n"(TC_EPI_WARPS * 32) : "memory");
     const EpiParam* ep = sparam;
@@ -383,29 +410,39 @@ __global__ void __launch_bounds__(TC_THREADS, 1) k_conv_tc(const __grid_constant
       const uint32_t buf = lt & 1u, uph = (lt >> 1) & 1u;
       const int mt = (int)a.div_nt.div((uint32_t)tile);
       const int nt = tile - mt * n_nt;
+      // chunks c = first, first+3, ...: the assignment rotates with the tile so the three
+      // column groups share BN/16 chunks evenly over consecutive tiles
+      const int first = (int)(((uint32_t)grp + 3u - lt % 3u) % 3u);
       const RowGeo g = row_geo(a, mt * TC_BM + row, M);
-      const long long rowsum = (g.ok && c_lo < c_hi) ? pixel_rowsum(a, g.n, g.ih0, g.iw0) : 0;
+      const long long rowsum = (g.ok && first < NCH) ? pixel_rowsum(a, g.n, g.ih0, g.iw0) : 0;
       int8_t* orow = g.ok ? a.out.p + vpix(a.out, g.n, g.oh, g.ow) * a.out.Cp : nullptr;
       const int8_t* srow = (g.ok && a.skip.p) ? a.skip.p + vpix(a.skip, g.n, g.oh, g.ow) * a.skip.Cp : nullptr;
+      // the residual operand does not depend on the accumulator: fetch it before the wait
+      // and one chunk ahead inside the loop (its load latency was the top stall)
+      const int cb0 = nt * BN + first * 16;
+      int4 sk_next = (srow && first < NCH && cb0 < a.out.Cp) ? __ldg(reinterpret_cast<const int4*>(srow + cb0))
+                                                            : make_int4(0, 0, 0, 0);
       mbar_wait(&tfull[buf], uph);
       tc_fence_after();
 #pragma unroll 1
-      for (int c0 = c_lo; c0 < c_hi; c0 += 16) {
+      for (int c = first; c < NCH; c += 3) {
         uint32_t v[16];
-        tmem_ld16(tmem + ((uint32_t)(q * 32) << 16) + buf * BN + (uint32_t)c0, v);
-        const int cb = nt * BN + c0;
+        tmem_ld16(tmem + ((uint32_t)(q * 32) << 16) + buf * BN + (uint32_t)(c * 16), v);
+        const int cb = nt * BN + c * 16;
         if (cb >= a.out.Cp) continue;            // warp-uniform: the slow path re-reads TMEM
-        const int4 skv = srow ? *reinterpret_cast<const int4*>(srow + cb) : make_int4(0, 0, 0, 0);
+        const int4 skv = sk_next;
+        if (srow && c + 3 < NCH && cb + 48 < a.out.Cp)
+          sk_next = __ldg(reinterpret_cast<const int4*>(srow + cb + 48));
         int4 res;
         if (a.ablate == 1) {
           res = make_int4((int)v[0], (int)v[1], (int)v[2], (int)v[3]);
         } else if (!rt.slow && cb + 16 <= Cout) {
           const int rs = (int)rowsum;
-          if (rt.noclamp) epi_dispatch<true>(v, ep, cb, rs, rt, lo_conv, lo_add, skv, res, srow != nullptr, a.conv_is_a, wzp);
-          else epi_dispatch<false>(v, ep, cb, rs, rt, lo_conv, lo_add, skv, res, srow != nullptr, a.conv_is_a, wzp);
+          if (rt.noclamp) epi_dispatch<true>(v, ep, cb, rs, rt, k, skv, res, srow != nullptr, a.conv_is_a, wzp);
+          else epi_dispatch<false>(v, ep, cb, rs, rt, k, skv, res, srow != nullptr, a.conv_is_a, wzp);
         } else {
-          res = epi_slow_chunk(tmem + ((uint32_t)(q * 32) << 16) + buf * BN + (uint32_t)c0, cb, rowsum,
-                               a, rt, lo_conv, lo_add, skv);
+          res = epi_slow_chunk(tmem + ((uint32_t)(q * 32) << 16) + buf * BN + (uint32_t)(c * 16), cb, rowsum,
+                               a, rt, k.lo_conv, k.lo_add, skv);
         }
         if (g.ok) *reinterpret_cast<int4*>(orow + cb) = res;
       }

@@ -213,7 +213,7 @@ __global__ void k_layer_params(const LayerSt* __restrict__ layers, const float* 
       if (big) atomicOr(&slow, 1);
       EpiParam e;
       e.m = m;
-      e.cc = big ? 0 : (int)cc;
+      e.cc = (int)((uint32_t)(big ? 0 : (int)cc) ^ 0x80000000u);   // biased by 2^31 (see i2d)
       e.zw = (int)zw;
       L.ep[o] = e;
       if (!(m > 0.0) || !isfinite(m)) atomicOr(&slow, 1);

@@ -31,7 +31,8 @@ struct LayerRt {
 //   acc = dot - zw*rowsum + cc  (cc = bias - zx*sum(w) + K*zx*zw), out = requant(acc, m)
 struct alignas(16) EpiParam {
   double m;
-  int cc;              // valid when the layer's rt.slow == 0 (|cc| < 2^30, no int32 clip possible)
+  int cc;              // cc + 2^31 (mod 2^32); valid when the layer's rt.slow == 0 (|cc| < 2^30,
+                       // no int32 clip possible).  The bias lets acc + 2^31 feed i2d directly.
   int zw;
 };
 

@@ -58,6 +58,25 @@ def test_codes_bit_exact(name, ds64):
                 assert np.array_equal(got, v.astype(np.int8)), (name, ci, t)
     finally:
         ev.set_option("fusion", 1)
+    # fused epilogues (relu / residual add folded into the conv): every tensor that is still
+    # materialised must carry the same codes
+    for ci in (2, 20):
+        cfg = space[ci]
+        qm = O.quantize_model(g, caches[cfg.cache], cfg)
+        seen = {}
+        O.run_quantized(qm, ds64.eval_images, sink=lambda t, v: seen.__setitem__(t, v))
+        fused_away = 0
+        for t, v in seen.items():
+            if t not in qm.act:
+                continue
+            try:
+                got = ev.probe_codes(cfg, t).reshape(v.shape)
+            except Exception as e:  # noqa: BLE001 - the library reports fused-away tensors
+                assert "fused away" in str(e)
+                fused_away += 1
+                continue
+            assert np.array_equal(got, v.astype(np.int8)), (name, ci, t, "fused")
+        assert fused_away > 0 or name == "squeezenet"
     ev.close()
 
 
