@@ -11,19 +11,23 @@
 // (EpiParam.cc, computed per config by k_layer_params) and sum x is a
 // per-output-pixel term from per-pixel channel sums P (only when some zw != 0).
 //
-// Persistent, warp-specialised kernel (one CTA per SM, 448 threads):
-//   warps 0-3   A producers: one GEMM row (output pixel) per thread; gather the
-//               row's 16-byte K chunks with cp.async into the UMMA K-major
+// Persistent, warp-specialised kernel (one CTA per SM, 512 threads = 4 warps per
+// SM sub-partition, <= 128 registers each, no spills):
+//   warps 0-1   A producers: two GEMM rows (output pixels) per thread; gather the
+//               rows' 16-byte K chunks with cp.async into the UMMA K-major
 //               no-swizzle canonical layout (8-row x 16-byte core matrices);
 //               cp.async.mbarrier.arrive.noinc signals the stage's full barrier.
-//   warp 4      B producer: one cp.async.bulk per stage from the pre-tiled
+//   warp 2      B producer: one cp.async.bulk per stage from the pre-tiled
 //               weight image (TMA bulk engine, complete_tx on the same barrier).
-//   warp 5      TMEM allocator + single-thread tcgen05.mma.kind::i8 issuer
+//   warp 3      TMEM allocator + single-thread tcgen05.mma.kind::i8 issuer
 //               (M=128, N=BN, K=32 per instruction, 4 per 128-byte stage).
 //               Two TMEM accumulators so tile t+1's MMAs overlap tile t's epilogue.
-//   warps 6-13  epilogue: tcgen05.ld 32x32b (TMEM lane = output row), int32
-//               zero-point correction, fp64 requant (explicit _rn intrinsics,
-//               reference op order), relu / fused add, 16-byte code stores.
+//   warps 4-15  epilogue, 3 column groups x 4 TMEM lane quarters: tcgen05.ld 32x32b
+//               (TMEM lane = output row), int32 zero-point correction, fp64 requant
+//               (explicit _rn intrinsics, reference op order), relu, fused residual
+//               add as a 64 KB shared-memory lookup table, 16-byte code stores.
+// The smem pipeline depth is chosen at launch from what the per-channel constants
+// and the add table leave of the 227 KB.
 #include <climits>
 
 #include "common.cuh"
@@ -32,11 +36,8 @@
 namespace ptq {
 
 constexpr int TC_BM = 128;
-// smem pipeline depth: small-N tiles need more stages in flight to cover load latency
-template <int BN>
-struct TcStages {
-  static constexpr int v = (200 * 1024) / (16384 + BN * 128) > 10 ? 10 : (200 * 1024) / (16384 + BN * 128);
-};
+constexpr int TC_MAX_STAGES = 10;                 // smem pipeline depth cap (runtime depth: launcher)
+constexpr int TC_SMEM_MAX = 232448;                // 227 KB opt-in dynamic smem per CTA
 constexpr int TC_A_STAGE = TC_BM * 128;            // 16 KB: 8 chunks x 128 rows x 16 B
 constexpr int TC_EPI_WARPS = 12;                   // 3 per SM sub-partition (register budget: no spills)
 constexpr int TC_THREADS = (4 + TC_EPI_WARPS) * 32;    // 16 warps: 4 per SM sub-partition
@@ -47,6 +48,18 @@ __device__ __forceinline__ uint64_t umma_desc(uint32_t saddr, uint32_t lbo, uint
   d |= (uint64_t)((lbo >> 4) & 0x3FFFu) << 16;
   d |= (uint64_t)((sbo >> 4) & 0x3FFFu) << 32;
   d |= (uint64_t)1 << 46;  // descriptor version 1 (sm_100); base offset 0; SWIZZLE_NONE
+  return d;
+}
+
+// K-major swizzled layout (TMA-written A): rows of 64 / 128 bytes in 8-row atoms of
+// 512 / 1024 bytes (SBO), LBO unused (1), layout type 4 (SWIZZLE_64B) / 2 (SWIZZLE_128B)
+__device__ __forceinline__ uint64_t umma_desc_sw(uint32_t saddr, int swz) {
+  uint64_t d = 0;
+  d |= (uint64_t)((saddr >> 4) & 0x3FFFu);
+  d |= (uint64_t)1 << 16;
+  d |= (uint64_t)(((uint32_t)(swz * 8) >> 4) & 0x3FFFu) << 32;
+  d |= (uint64_t)1 << 46;
+  d |= (uint64_t)(swz == 128 ? 2u : 4u) << 61;
   return d;
 }
 
@@ -109,18 +122,9 @@ __device__ __forceinline__ int imax(int a, int b) { return a > b ? a : b; }
 __device__ __forceinline__ double b2d(uint32_t accb) {
   return __dsub_rn(__hiloint2double(0x43300000, (int)accb), 4503601774854144.0);
 }
-// sign-extended byte b of w: PTX prmt with the sign-replicate selector bit (the
-// __byte_perm intrinsic only honours the low 3 selector bits)
-__device__ __forceinline__ int sbyte(uint32_t w, int b) {
-  int r;
-  asm("prmt.b32 %0, %1, 0, %2;" : "=r"(r) : "r"(w), "r"((uint32_t)(0x8880 | (b * 0x1110) | b)));
-  return r;
-}
-
 // per-layer epilogue constants held in registers by every epilogue thread
 struct EpiK {
   uint32_t clo, chi;   // biased acc clamp bounds 2^31 -/+ aclamp
-  uint32_t ka, kb;     // 2^31 - za, 2^31 - zb: (x - z) + 2^31 in one add
   int lo_conv, lo_add;
 };
 
@@ -133,18 +137,14 @@ __device__ __forceinline__ int requant_fast(uint32_t accb, double m, const Layer
   const double r = __dadd_rn(__dmul_rn(b2d(accb), m), 0.5);
   return imin(imax(__double2loint(__dadd_rd(r, rt.mg_zy)), k.lo_conv), PTQ_QMAX);
 }
-// residual add on codes (intexec.py:245-276): clip(RHU(xs*ra + ys*rb) + zo)
-__device__ __forceinline__ int add_fast(int ca, int cb, const LayerRt& rt, const EpiK& k) {
-  const double s = __dadd_rn(__dmul_rn(b2d((uint32_t)ca + k.ka), rt.ra),
-                             __dmul_rn(b2d((uint32_t)cb + k.kb), rt.rb));
-  return imin(imax(__double2loint(__dadd_rd(__dadd_rn(s, 0.5), rt.mg_zo)), k.lo_add), PTQ_QMAX);
-}
-
 // 16 output channels of one row, fast path (no int32 saturation possible)
-template <bool WZP, bool SKIP, bool CONV_A, bool CLAMP>
+// A fused residual add is one shared-memory lookup: stab[skip byte * 260 + conv code]
+// with stab pointing at column 128 of the table (built exactly by k_layer_params for the
+// config; operand order is baked in).
+template <bool WZP, bool SKIP, bool CLAMP>
 __device__ __forceinline__ void epi_chunk16(const uint32_t (&v)[16], const EpiParam* __restrict__ ep,
                                             int cb, int rowsum, const LayerRt& rt, const EpiK& k,
-                                            const int4 skv, int4& out) {
+                                            const int8_t* __restrict__ stab, const int4 skv, int4& out) {
   uint32_t packed[4];
   const uint32_t skw[4] = {(uint32_t)skv.x, (uint32_t)skv.y, (uint32_t)skv.z, (uint32_t)skv.w};
 #pragma unroll
@@ -160,10 +160,7 @@ __device__ __forceinline__ void epi_chunk16(const uint32_t (&v)[16], const EpiPa
       uint32_t accb = v[jj] + (uint32_t)raw[j].z;
       if (WZP) accb -= (uint32_t)(raw[j].w * rowsum);
       q[j] = requant_fast<CLAMP>(accb, m, rt, k);
-      if (SKIP) {
-        const int s = sbyte(skw[g], j);
-        q[j] = CONV_A ? add_fast(q[j], s, rt, k) : add_fast(s, q[j], rt, k);
-      }
+      if (SKIP) q[j] = stab[(int)__byte_perm(skw[g], 0u, 0x4440u + j) * PTQ_ADDTAB_ROW + q[j]];
     }
     packed[g] = __byte_perm(__byte_perm((uint32_t)q[0], (uint32_t)q[1], 0x0040),
                             __byte_perm((uint32_t)q[2], (uint32_t)q[3], 0x0040), 0x5410);
@@ -173,18 +170,15 @@ __device__ __forceinline__ void epi_chunk16(const uint32_t (&v)[16], const EpiPa
 template <bool NOCLAMP>
 __device__ __forceinline__ void epi_dispatch(const uint32_t (&v)[16], const EpiParam* __restrict__ ep,
                                              int cb, int rs, const LayerRt& rt, const EpiK& k,
-                                             const int4 skv, int4& res, bool skip, int conv_is_a,
-                                             bool wzp) {
+                                             const int8_t* __restrict__ stab, const int4 skv,
+                                             int4& res, bool skip, bool wzp) {
   constexpr bool C = !NOCLAMP;
   if (!skip) {
-    if (wzp) epi_chunk16<true, false, false, C>(v, ep, cb, rs, rt, k, skv, res);
-    else epi_chunk16<false, false, false, C>(v, ep, cb, rs, rt, k, skv, res);
-  } else if (conv_is_a) {
-    if (wzp) epi_chunk16<true, true, true, C>(v, ep, cb, rs, rt, k, skv, res);
-    else epi_chunk16<false, true, true, C>(v, ep, cb, rs, rt, k, skv, res);
+    if (wzp) epi_chunk16<true, false, C>(v, ep, cb, rs, rt, k, stab, skv, res);
+    else epi_chunk16<false, false, C>(v, ep, cb, rs, rt, k, stab, skv, res);
   } else {
-    if (wzp) epi_chunk16<true, true, false, C>(v, ep, cb, rs, rt, k, skv, res);
-    else epi_chunk16<false, true, false, C>(v, ep, cb, rs, rt, k, skv, res);
+    if (wzp) epi_chunk16<true, true, C>(v, ep, cb, rs, rt, k, stab, skv, res);
+    else epi_chunk16<false, true, C>(v, ep, cb, rs, rt, k, stab, skv, res);
   }
 }
 
@@ -250,7 +244,7 @@ struct RowGeo {
 };
 __device__ __forceinline__ RowGeo row_geo(const ConvTcArgs& a, int m, int M) {
   RowGeo g{};
-  g.ok = m < M;
+  g.ok = m < M;   // (TMA mode: also inside the real output, checked below)
   if (g.ok) {                                  // M < 2^31: multiply-high divisions
     const uint32_t t = a.div_ow.div((uint32_t)m);
     g.ow = m - (int)t * a.OW;
@@ -258,6 +252,7 @@ __device__ __forceinline__ RowGeo row_geo(const ConvTcArgs& a, int m, int M) {
     g.oh = (int)t - (int)nn * a.OH;
     g.n = (int)nn;
   }
+  g.ok = g.ok && g.oh < a.OHr && g.ow < a.OWr;
   g.ih0 = g.oh * a.stride - a.pad + a.in.halo;
   g.iw0 = g.ow * a.stride - a.pad + a.in.halo;
   return g;
@@ -265,16 +260,19 @@ __device__ __forceinline__ RowGeo row_geo(const ConvTcArgs& a, int m, int M) {
 
 template <int BN>
 __global__ void __launch_bounds__(TC_THREADS, 1) k_conv_tc(const __grid_constant__ ConvTcArgs a) {
-  constexpr int TC_STAGES = TcStages<BN>::v;
-  extern __shared__ __align__(1024) uint8_t smem[];
+  const int NS = a.n_stages;
+  extern __shared__ __align__(1024) uint8_t smem_raw[];
+  // swizzled TMA tiles need 1024-byte aligned stages (the launcher reserves the slack)
+  uint8_t* smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
   uint8_t* sA = smem;
-  uint8_t* sB = smem + TC_STAGES * TC_A_STAGE;
-  uint64_t* full = reinterpret_cast<uint64_t*>(sB + TC_STAGES * BN * 128);
-  uint64_t* empty = full + TC_STAGES;
-  uint64_t* tfull = empty + TC_STAGES;
+  uint8_t* sB = smem + NS * TC_A_STAGE;
+  uint64_t* full = reinterpret_cast<uint64_t*>(sB + NS * BN * 128);
+  uint64_t* empty = full + NS;
+  uint64_t* tfull = empty + NS;
   uint64_t* tempty = tfull + 2;
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
   EpiParam* sparam = reinterpret_cast<EpiParam*>(tempty + 4);   // [Cout] per-channel epilogue constants
+  int8_t* stab = reinterpret_cast<int8_t*>(sparam + a.L.cout);   // fused-add table (PTQ_ADDTAB_*)
   constexpr uint32_t TMEM_COLS = (2 * BN) < 32 ? 32 : 2 * BN;
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -283,8 +281,8 @@ __global__ void __launch_bounds__(TC_THREADS, 1) k_conv_tc(const __grid_constant
   const int n_tiles = ((M + TC_BM - 1) / TC_BM) * n_nt;
 
   if (threadIdx.x == 0) {
-    for (int s = 0; s < TC_STAGES; ++s) {
-      mbar_init(&full[s], 64 + 1);
+    for (int s = 0; s < NS; ++s) {
+      mbar_init(&full[s], a.tma_a ? 2 : 64 + 1);
       mbar_init(&empty[s], 1);
     }
     for (int b = 0; b < 2; ++b) {
@@ -304,23 +302,72 @@ __global__ void __launch_bounds__(TC_THREADS, 1) k_conv_tc(const __grid_constant
   tc_fence_after();
   const uint32_t tmem = *tmem_slot;
 
-  if (warp < 2) {
+  if (warp < 2 && a.tma_a) {
+    // ------------------------------------------------ A producer, TMA mode: the conv runs over
+    // the padded output grid, so tap (kh, kw) of 128 consecutive output positions is 128
+    // consecutive flat input pixels at offset kh*Wp + kw -- one tensor-map tile per tap slice
+    if (warp == 0 && lane == 0) {
+      prefetch_tmap(&a.tmA);
+      const int Wp = a.in.W + 2 * a.in.halo;
+      const int cpc = a.in.Cp >> 4, taps = a.k * a.k;
+      int s = 0;
+      uint32_t ph = 0;
+      for (int tile = blockIdx.x; tile < n_tiles; tile += gridDim.x) {
+        const int p0 = (int)a.div_nt.div((uint32_t)tile) * TC_BM;
+        for (int ki = 0; ki < a.n_kiter; ++ki) {
+          mbar_wait(&empty[s], ph ^ 1u);
+          uint8_t* dst = sA + s * TC_A_STAGE;
+          if (a.tma_a == 128) {                      // one tap, 128 channels per stage
+            const int kk = ki * 8, tap = kk / cpc, c0 = (kk - tap * cpc) * 16;
+            mbar_arrive_expect_tx(&full[s], TC_A_STAGE);
+            tma_load_2d(dst, &a.tmA, c0, p0 + (tap / a.k) * Wp + tap % a.k, &full[s]);
+          } else {                                   // Cp == 64: two taps per stage
+            const int t0 = 2 * ki, t1 = 2 * ki + 1;
+            mbar_arrive_expect_tx(&full[s], t1 < taps ? TC_A_STAGE : TC_A_STAGE / 2);
+            tma_load_2d(dst, &a.tmA, 0, p0 + (t0 / a.k) * Wp + t0 % a.k, &full[s]);
+            if (t1 < taps)
+              tma_load_2d(dst + TC_A_STAGE / 2, &a.tmA, 0, p0 + (t1 / a.k) * Wp + t1 % a.k, &full[s]);
+          }
+          if (++s == NS) { s = 0; ph ^= 1u; }
+        }
+      }
+    } else if (warp == 1 && a.skip.p) {
+      // fused add operand rows of each tile into L2 ahead of the epilogue
+      for (int tile = blockIdx.x; tile < n_tiles; tile += gridDim.x) {
+        const int mt = (int)a.div_nt.div((uint32_t)tile);
+        const int c0 = (tile - mt * n_nt) * BN;
+        const uint32_t bytes = (uint32_t)(a.skip.Cp - c0 < BN ? a.skip.Cp - c0 : BN);
+        for (int r = lane; r < TC_BM; r += 32) {
+          const RowGeo g = row_geo(a, mt * TC_BM + r, M);
+          if (g.ok) bulk_prefetch_l2(a.skip.p + vpix(a.skip, g.n, g.oh, g.ow) * a.skip.Cp + c0, bytes);
+        }
+      }
+    }
+  } else if (warp < 2) {
     // ------------------------------------------------ A producers (implicit im2col gather)
     // 64 threads, two GEMM rows (output pixels) each: r and r + 64
     const int r = threadIdx.x;
     const int Cp = a.in.Cp, cpc = Cp >> 4;
     const int Wp = a.in.W + 2 * a.in.halo, Hp = a.in.H + 2 * a.in.halo;
-    uint32_t it = 0;
+    int s = 0;
+    uint32_t ph = 0;
     for (int tile = blockIdx.x; tile < n_tiles; tile += gridDim.x) {
       const int mt = (int)a.div_nt.div((uint32_t)tile);
       const RowGeo g0 = row_geo(a, mt * TC_BM + r, M);
       const RowGeo g1 = row_geo(a, mt * TC_BM + r + 64, M);
       const int8_t* base0 = a.in.p + (((int64_t)g0.n * Hp + g0.ih0) * Wp + g0.iw0) * Cp;
       const int8_t* base1 = a.in.p + (((int64_t)g1.n * Hp + g1.ih0) * Wp + g1.iw0) * Cp;
+      if (a.skip.p) {
+        // the fused add's operand rows for this tile: pull them into L2 now, a few tiles
+        // before the epilogue reads them 16 bytes at a time
+        const int nt = tile - mt * n_nt;
+        const int c0 = nt * BN;
+        const uint32_t bytes = (uint32_t)(a.skip.Cp - c0 < BN ? a.skip.Cp - c0 : BN);
+        if (g0.ok) bulk_prefetch_l2(a.skip.p + vpix(a.skip, g0.n, g0.oh, g0.ow) * a.skip.Cp + c0, bytes);
+        if (g1.ok) bulk_prefetch_l2(a.skip.p + vpix(a.skip, g1.n, g1.oh, g1.ow) * a.skip.Cp + c0, bytes);
+      }
       int kh = 0, kw = 0, ch = 0, kk = 0;
-      for (int ki = 0; ki < a.n_kiter; ++ki, ++it) {
-        const int s = it % TC_STAGES;
-        const uint32_t ph = (it / TC_STAGES) & 1u;
+      for (int ki = 0; ki < a.n_kiter; ++ki) {
         mbar_wait(&empty[s], ph ^ 1u);
         uint8_t* dst = sA + s * TC_A_STAGE + r * 16;
 #pragma unroll
@@ -337,21 +384,22 @@ __global__ void __launch_bounds__(TC_THREADS, 1) k_conv_tc(const __grid_constant
           }
         }
         cp_async_mbar_arrive_noinc(&full[s]);
+        if (++s == NS) { s = 0; ph ^= 1u; }
       }
     }
   } else if (warp == 2) {
     // ------------------------------------------------ B producer (bulk copies of pre-tiled weights)
     if (lane == 0) {
-      uint32_t it = 0;
+      int s = 0;
+      uint32_t ph = 0;
       for (int tile = blockIdx.x; tile < n_tiles; tile += gridDim.x) {
         const int nt = tile - (int)a.div_nt.div((uint32_t)tile) * n_nt;
         const int8_t* gB = a.wB + (int64_t)nt * a.n_kiter * BN * 128;
-        for (int ki = 0; ki < a.n_kiter; ++ki, ++it) {
-          const int s = it % TC_STAGES;
-          const uint32_t ph = (it / TC_STAGES) & 1u;
+        for (int ki = 0; ki < a.n_kiter; ++ki) {
           mbar_wait(&empty[s], ph ^ 1u);
           mbar_arrive_expect_tx(&full[s], BN * 128);
           bulk_g2s(sB + s * BN * 128, gB + (int64_t)ki * BN * 128, BN * 128, &full[s]);
+          if (++s == NS) { s = 0; ph ^= 1u; }
         }
       }
     }
@@ -359,26 +407,29 @@ __global__ void __launch_bounds__(TC_THREADS, 1) k_conv_tc(const __grid_constant
     // ------------------------------------------------ MMA issuer
     if (lane == 0) {
       const uint32_t idesc = idesc_i8<BN>();
-      uint32_t it = 0, lt = 0;
+      int s = 0;
+      uint32_t ph = 0, lt = 0;
       for (int tile = blockIdx.x; tile < n_tiles; tile += gridDim.x, ++lt) {
         const uint32_t buf = lt & 1u, uph = (lt >> 1) & 1u;
         mbar_wait(&tempty[buf], uph ^ 1u);           // epilogue drained this accumulator
         tc_fence_after();
         const uint32_t d = tmem + buf * BN;
-        for (int ki = 0; ki < a.n_kiter; ++ki, ++it) {
-          const int s = it % TC_STAGES;
-          const uint32_t ph = (it / TC_STAGES) & 1u;
+        for (int ki = 0; ki < a.n_kiter; ++ki) {
           mbar_wait(&full[s], ph);
           tc_fence_after();
           fence_proxy_async();
           const uint32_t a0 = smem_u32(sA + s * TC_A_STAGE), b0 = smem_u32(sB + s * BN * 128);
 #pragma unroll
           for (int ks = 0; ks < 4; ++ks) {
-            const uint64_t ad = umma_desc(a0 + ks * 2 * (TC_BM * 16), TC_BM * 16, 128);
+            const uint64_t ad =
+                a.tma_a == 0 ? umma_desc(a0 + ks * 2 * (TC_BM * 16), TC_BM * 16, 128)
+                : a.tma_a == 128 ? umma_desc_sw(a0 + ks * 32, 128)
+                                 : umma_desc_sw(a0 + (ks >> 1) * (TC_A_STAGE / 2) + (ks & 1) * 32, 64);
             const uint64_t bd = umma_desc(b0 + ks * 2 * (BN * 16), BN * 16, 128);
             mma_i8(d, ad, bd, idesc, (ki | ks) != 0);
           }
           mma_commit(&empty[s]);                     // frees the smem stage when the MMAs land
+          if (++s == NS) { s = 0; ph ^= 1u; }
         }
         mma_commit(&tfull[buf]);                     // accumulator ready for the epilogue
       }
@@ -396,14 +447,16 @@ __global__ void __launch_bounds__(TC_THREADS, 1) k_conv_tc(const __grid_constant
     k.lo_add = rt.add_relu_zp > PTQ_QMIN ? rt.add_relu_zp : PTQ_QMIN;
     k.clo = 0x80000000u - (uint32_t)rt.aclamp;
     k.chi = 0x80000000u + (uint32_t)rt.aclamp;
-    k.ka = 0x80000000u - (uint32_t)rt.za;
-    k.kb = 0x80000000u - (uint32_t)rt.zb;
     const int Cout = a.L.cout;
     // stage the layer's per-channel epilogue constants in shared memory once (L1 misses on
     // these broadcast loads were the top stall), then sync the 12 epilogue warps only
     for (int i = threadIdx.x - 4 * 32; i < Cout; i += TC_EPI_WARPS * 32) sparam[i] = a.L.ep[i];
+    if (a.addtab)
+      for (int i = threadIdx.x - 4 * 32; i < PTQ_ADDTAB_BYTES / 16; i += TC_EPI_WARPS * 32)
+        reinterpret_cast<int4*>(stab)[i] = reinterpret_cast<const int4*>(a.addtab)[i];
     asm volatile("bar.sync 1, %0;" ::"n"(TC_EPI_WARPS * 32) : "memory");
     const EpiParam* ep = sparam;
+    const int8_t* stab_c = stab + 128;                // column of conv code 0
     const bool wzp = a.has_wzp != 0;
     uint32_t lt = 0;
     for (int tile = blockIdx.x; tile < n_tiles; tile += gridDim.x, ++lt) {
@@ -438,8 +491,8 @@ __global__ void __launch_bounds__(TC_THREADS, 1) k_conv_tc(const __grid_constant
           res = make_int4((int)v[0], (int)v[1], (int)v[2], (int)v[3]);
         } else if (!rt.slow && cb + 16 <= Cout) {
           const int rs = (int)rowsum;
-          if (rt.noclamp) epi_dispatch<true>(v, ep, cb, rs, rt, k, skv, res, srow != nullptr, a.conv_is_a, wzp);
-          else epi_dispatch<false>(v, ep, cb, rs, rt, k, skv, res, srow != nullptr, a.conv_is_a, wzp);
+          if (rt.noclamp) epi_dispatch<true>(v, ep, cb, rs, rt, k, stab_c, skv, res, srow != nullptr, wzp);
+          else epi_dispatch<false>(v, ep, cb, rs, rt, k, stab_c, skv, res, srow != nullptr, wzp);
         } else {
           res = epi_slow_chunk(tmem + ((uint32_t)(q * 32) << 16) + buf * BN + (uint32_t)(c * 16), cb, rowsum,
                                a, rt, k.lo_conv, k.lo_add, skv);
@@ -511,12 +564,20 @@ static int g_num_sms = 0;
 
 template <int BN>
 static void launch_bn(const ConvTcArgs& a, cudaStream_t s) {
-  constexpr int TC_STAGES = TcStages<BN>::v;
-  const size_t smem = (size_t)TC_STAGES * TC_A_STAGE + (size_t)TC_STAGES * BN * 128 +
-                      (2 * TC_STAGES + 4) * 8 + 16 + (size_t)a.L.cout * sizeof(EpiParam);
+  // fixed part: barriers, TMEM slot, per-channel constants, optional add table; the rest
+  // of the 227 KB goes to pipeline stages (deeper for narrow tiles, at least 2)
+  const size_t fixed = 1024 + (2 * TC_MAX_STAGES + 4) * 8 + 16 + (size_t)a.L.cout * sizeof(EpiParam) +
+                       (a.addtab ? PTQ_ADDTAB_BYTES : 0);
+  const size_t per_stage = (size_t)TC_A_STAGE + (size_t)BN * 128;
+  int ns = (int)((TC_SMEM_MAX - fixed) / per_stage);
+  if (ns > TC_MAX_STAGES) ns = TC_MAX_STAGES;
+  if (ns < 2) ns = 2;                // does not fit: the launch fails loudly (check_launch)
+  ConvTcArgs b = a;
+  b.n_stages = ns;
+  const size_t smem = (size_t)ns * per_stage + fixed;
   static bool configured = false;
   if (!configured) {
-    cudaFuncSetAttribute(k_conv_tc<BN>, cudaFuncAttributeMaxDynamicSharedMemorySize, 232448);
+    cudaFuncSetAttribute(k_conv_tc<BN>, cudaFuncAttributeMaxDynamicSharedMemorySize, TC_SMEM_MAX);
     configured = true;
   }
   if (!g_num_sms) {
@@ -527,19 +588,65 @@ static void launch_bn(const ConvTcArgs& a, cudaStream_t s) {
   const int64_t M = (int64_t)a.in.N * a.OH * a.OW;
   const int64_t tiles = ((M + TC_BM - 1) / TC_BM) * ((a.L.cout + BN - 1) / BN);
   const int grid = (int)(tiles < g_num_sms ? tiles : g_num_sms);   // persistent: one CTA per SM
-  k_conv_tc<BN><<<grid, TC_THREADS, smem, s>>>(a);
+  k_conv_tc<BN><<<grid, TC_THREADS, smem, s>>>(b);
 }
 
 static ConvTcArgs with_divs(const ConvTcArgs& a0, int bn) {
   ConvTcArgs a = a0;
+  if (!a.tma_a) { a.OHr = a.OH; a.OWr = a.OW; }
   a.div_ow = FastDiv::make((uint32_t)a.OW);
   a.div_oh = FastDiv::make((uint32_t)a.OH);
   a.div_nt = FastDiv::make((uint32_t)((a.L.cout + bn - 1) / bn));
   return a;
 }
 
+typedef CUresult (*EncodeTiledFn)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
+                                  const cuuint64_t*, const cuuint32_t*, const cuuint32_t*,
+                                  CUtensorMapInterleave, CUtensorMapSwizzle, CUtensorMapL2promotion,
+                                  CUtensorMapFloatOOBfill);
+static EncodeTiledFn encode_tiled() {
+  static EncodeTiledFn fn = nullptr;
+  if (!fn) {
+    cudaDriverEntryPointQueryResult q;
+    void* p = nullptr;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) == cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      fn = reinterpret_cast<EncodeTiledFn>(p);
+  }
+  return fn;
+}
+
+// TMA A path: stride-1 "same" convs whose input halo equals the padding (every 1x1 conv
+// on a halo-free input, every 3x3 pad-1 conv) with 64 or 128k channel bytes
+static bool setup_tma_a(ConvTcArgs& a) {
+  const int Cp = a.in.Cp;
+  if (!a.allow_tma || a.stride != 1 || a.k != 2 * a.pad + 1 || a.in.halo != a.pad) return false;
+  if (!(Cp == 64 || Cp % 128 == 0) || a.OH != a.in.H || a.OW != a.in.W) return false;
+  const int Hp = a.in.H + 2 * a.in.halo, Wp = a.in.W + 2 * a.in.halo;
+  EncodeTiledFn fn = encode_tiled();
+  if (!fn) return false;
+  const int box0 = Cp == 64 ? 64 : 128;
+  cuuint64_t gdim[2] = {(cuuint64_t)Cp, (cuuint64_t)a.in.N * Hp * Wp};
+  cuuint64_t gstride[1] = {(cuuint64_t)Cp};
+  cuuint32_t box[2] = {(cuuint32_t)box0, (cuuint32_t)TC_BM};
+  cuuint32_t es[2] = {1, 1};
+  if (fn(&a.tmA, CU_TENSOR_MAP_DATA_TYPE_UINT8, 2, (void*)a.in.p, gdim, gstride, box, es,
+         CU_TENSOR_MAP_INTERLEAVE_NONE, box0 == 128 ? CU_TENSOR_MAP_SWIZZLE_128B : CU_TENSOR_MAP_SWIZZLE_64B,
+         CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS)
+    return false;
+  a.tma_a = box0;
+  a.OHr = a.OH;
+  a.OWr = a.OW;
+  a.OH = Hp;                                         // GEMM rows = padded grid positions
+  a.OW = Wp;
+  return true;
+}
+
 void launch_conv_tc(const ConvTcArgs& a0, int bn, cudaStream_t s) {
-  const ConvTcArgs a = with_divs(a0, bn);
+  ConvTcArgs t = a0;
+  t.tma_a = 0;
+  setup_tma_a(t);
+  const ConvTcArgs a = with_divs(t, bn);
   switch (bn) {
     case 16: launch_bn<16>(a, s); break;
     case 32: launch_bn<32>(a, s); break;

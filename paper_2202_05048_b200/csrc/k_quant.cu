@@ -192,6 +192,7 @@ __global__ void k_layer_params(const LayerSt* __restrict__ layers, const float* 
   const long long zx = az[L.in_hist];
   __shared__ int slow;
   __shared__ unsigned long long m_max_bits, m_min_bits;   // m > 0: bit order == value order
+  __shared__ LayerRt srt;
   if (threadIdx.x == 0) {
     slow = 0;
     m_max_bits = 0ull;
@@ -258,6 +259,25 @@ __global__ void k_layer_params(const LayerSt* __restrict__ layers, const float* 
     r.mg_zy = 6755399441055744.0 + (double)r.zy;
     r.mg_zo = 6755399441055744.0 + (double)r.zo;
     *L.rt = r;
+    srt = r;
+  }
+  if (!L.addtab) return;
+  __syncthreads();
+  // fused residual add as a lookup table: row s (skip code as unsigned byte), column q + 128
+  // (conv code q), rows padded to 260 bytes so the 32 lanes of a lookup (32 pixels, one
+  // channel) spread over the shared-memory banks.  Entry = clip(RHU(fl(fl((xa - za) * ra) +
+  // fl((xb - zb) * rb))) + zo) with the add's relu floor (intexec.py:245-276 order); both
+  // operands are int8 codes, so the table is exact.
+  const LayerRt r = srt;
+  const int lo = r.add_relu_zp > PTQ_QMIN ? r.add_relu_zp : PTQ_QMIN;
+  for (int idx = threadIdx.x; idx < PTQ_ADDTAB_BYTES; idx += blockDim.x) {
+    const int row = idx / PTQ_ADDTAB_ROW, col = idx - row * PTQ_ADDTAB_ROW;
+    if (col >= 256) { L.addtab[idx] = 0; continue; }
+    const int sk = (int)(int8_t)row, q = col - 128;
+    const int xa = L.add_conv_is_a ? q : sk, xb = L.add_conv_is_a ? sk : q;
+    const double v = __dadd_rn(__dmul_rn((double)(xa - r.za), r.ra), __dmul_rn((double)(xb - r.zb), r.rb));
+    int code = clip8(rhu(v) + (double)r.zo);
+    L.addtab[idx] = (int8_t)(code < lo ? lo : code);
   }
 }
 void launch_layer_params(const LayerSt* d_layers, int n_layers, const float* act_scale,

@@ -1,6 +1,7 @@
 // Host-side launch wrappers for every ptq_b200 kernel family, plus the small
 // POD structs shared between the runtime and the kernels.
 #pragma once
+#include <cuda.h>
 #include <cuda_runtime.h>
 #include <stdint.h>
 
@@ -12,6 +13,10 @@ struct View {
   int8_t* p;
   int N, H, W, C, Cp, halo;
 };
+
+// fused-add lookup table geometry (rows padded against shared-memory bank conflicts)
+#define PTQ_ADDTAB_ROW 260
+#define PTQ_ADDTAB_BYTES (256 * PTQ_ADDTAB_ROW)
 
 // per-config, per-int8-layer scalars written on device by k_layer_params
 struct LayerRt {
@@ -52,6 +57,9 @@ struct LayerSt {
   const int* wsum8;             // [8][cout] sum of weight codes
   int kreal;                    // real K = k*k*Cin
   EpiParam* ep;                 // [cout] per-config epilogue constants (out), or nullptr
+  int8_t* addtab;               // fused residual add: [256 skip codes][260: conv code + 128]
+                                // -> add output code (out, per config), or nullptr
+  int add_conv_is_a;            // 1 if the conv output is operand 0 of the fused add
 };
 
 // ---------------------------------------------------------------- F1 / F2 (k_calib.cu)
@@ -151,6 +159,11 @@ void launch_im2col(View in, int k, int stride, int pad, int OH, int OW, int8_t* 
                    cudaStream_t s);
 
 struct ConvTcArgs {
+  CUtensorMap tmA;        // TMA map of the A operand (tma_a != 0); 64-byte aligned first member
+  int tma_a;              // 0: cp.async implicit-im2col gather; 64 / 128: TMA tile loads of
+                          // 128 flat padded pixels x 64 / 128 channel bytes (SWIZZLE_64B / 128B)
+  int OHr, OWr;           // real output dims (TMA mode computes over the padded grid OH x OW)
+  int allow_tma;          // runtime option: TMA A loads for eligible layers
   View in, out;
   int k, stride, pad, OH, OW;
   const int8_t* wB;       // tiled weights [n_tiles][n_kiter][8][BN][16]
@@ -166,6 +179,8 @@ struct ConvTcArgs {
   int conv_is_a;          // 1 if the conv output is operand 0 of the fused add
   FastDiv div_ow, div_oh, div_nt;   // m -> (n, oh, ow) and tile -> (m-tile, n-tile)
   int ablate;             // profiling only: 1 = skip epilogue math, 2 = skip A gathers
+  const int8_t* addtab;   // fused add lookup table (LayerSt::addtab) or nullptr
+  int n_stages;           // smem pipeline depth (set by the launcher)
 };
 int conv_tc_bn_for(int cout);     // BN tile width the kernel uses for this Cout
 void launch_conv_tc(const ConvTcArgs& a, int bn, cudaStream_t s);

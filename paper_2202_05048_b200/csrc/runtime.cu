@@ -106,6 +106,7 @@ struct WeightsDev {
   int* biasq = nullptr;         // [cout]
   LayerRt* rt = nullptr;
   EpiParam* ep = nullptr;       // [cout] tensor-core epilogue constants
+  int8_t* addtab = nullptr;     // [PTQ_ADDTAB_BYTES] fused-add lookup table (layers with a fused add)
 };
 
 struct Plan {
@@ -162,7 +163,7 @@ struct ptq_ctx {
   std::vector<int*> cal_slots;
   std::vector<int> cal_sizes;
   // options
-  int conv_ref = 0, fusion = 1, time_conv = 0, ablate = 0;
+  int conv_ref = 0, fusion = 1, time_conv = 0, ablate = 0, tma = 1;
   int64_t opt_chunk = 0;
   // stats
   int64_t launches = 0;
@@ -551,6 +552,12 @@ void build_plan(ptq_ctx* c, int mixed) {
     L.wsum8 = wd.wsum;
     L.kreal = wd.kreal;
     L.ep = n.kind == PTQ_DWCONV ? nullptr : wd.ep;
+    L.addtab = nullptr;
+    L.add_conv_is_a = P.add_is_a[i];
+    if (P.add_node[i] >= 0 && L.ep) {
+      if (!wd.addtab) wd.addtab = c->dalloc<int8_t>(PTQ_ADDTAB_BYTES);
+      L.addtab = wd.addtab;
+    }
     P.layer_of[i] = (int)P.h_layers.size();
     P.h_layers.push_back(L);
   }
@@ -851,7 +858,9 @@ void eval_one(ptq_ctx* c, const ptq_config& cfg, unsigned long long* d_correct, 
             a.skip = V(P.add_other[i]);
             a.conv_is_a = P.add_is_a[i];
           }
+          a.addtab = L.addtab;
           a.ablate = c->ablate;
+          a.allow_tma = c->tma;
           cudaEvent_t ea = nullptr, eb = nullptr;
           const bool timed = c->cur_cfg < c->time_conv;   // instrument only the leading configs
           ++c->conv_launches_total;
@@ -1256,6 +1265,7 @@ int ptq_set_option(ptq_ctx* c, const char* key, int64_t value) {
     std::string k(key);
     if (k == "conv_ref") c->conv_ref = (int)value;
     else if (k == "ablate") c->ablate = (int)value;
+    else if (k == "tma") c->tma = (int)value;
     else if (k == "time_conv") c->time_conv = (int)value;
     else if (k == "reset_stats") c->launches = 0;
     else if (k == "fusion") {
