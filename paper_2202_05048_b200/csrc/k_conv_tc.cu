@@ -321,12 +321,17 @@ __global__ void __launch_bounds__(TC_THREADS, 1) k_conv_tc(const __grid_constant
             const int kk = ki * 8, tap = kk / cpc, c0 = (kk - tap * cpc) * 16;
             mbar_arrive_expect_tx(&full[s], TC_A_STAGE);
             tma_load_2d(dst, &a.tmA, c0, p0 + (tap / a.k) * Wp + tap % a.k, &full[s]);
-          } else {                                   // Cp == 64: two taps per stage
+          } else if (a.tma_a == 64) {                // Cp == 64: two taps per stage
             const int t0 = 2 * ki, t1 = 2 * ki + 1;
             mbar_arrive_expect_tx(&full[s], t1 < taps ? TC_A_STAGE : TC_A_STAGE / 2);
             tma_load_2d(dst, &a.tmA, 0, p0 + (t0 / a.k) * Wp + t0 % a.k, &full[s]);
             if (t1 < taps)
               tma_load_2d(dst + TC_A_STAGE / 2, &a.tmA, 0, p0 + (t1 / a.k) * Wp + t1 % a.k, &full[s]);
+          } else {                                   // Cp == 16, k == 4 (s2d stem): 4 kw taps
+            const int t0 = 2 * ki, t1 = 2 * ki + 1;  // per box, two kh rows per stage
+            mbar_arrive_expect_tx(&full[s], t1 < a.k ? TC_A_STAGE : TC_A_STAGE / 2);
+            tma_load_3d(dst, &a.tmA, 0, p0 + t0 * Wp, 0, &full[s]);
+            if (t1 < a.k) tma_load_3d(dst + TC_A_STAGE / 2, &a.tmA, 0, p0 + t1 * Wp, 0, &full[s]);
           }
           if (++s == NS) { s = 0; ph ^= 1u; }
         }
@@ -422,7 +427,7 @@ __global__ void __launch_bounds__(TC_THREADS, 1) k_conv_tc(const __grid_constant
 #pragma unroll
           for (int ks = 0; ks < 4; ++ks) {
             const uint64_t ad =
-                a.tma_a == 0 ? umma_desc(a0 + ks * 2 * (TC_BM * 16), TC_BM * 16, 128)
+                (a.tma_a == 0 || a.tma_a == 65) ? umma_desc(a0 + ks * 2 * (TC_BM * 16), TC_BM * 16, 128)
                 : a.tma_a == 128 ? umma_desc_sw(a0 + ks * 32, 128)
                                  : umma_desc_sw(a0 + (ks >> 1) * (TC_A_STAGE / 2) + (ks & 1) * 32, 64);
             const uint64_t bd = umma_desc(b0 + ks * 2 * (BN * 16), BN * 16, 128);
@@ -467,7 +472,10 @@ __global__ void __launch_bounds__(TC_THREADS, 1) k_conv_tc(const __grid_constant
       // column groups share BN/16 chunks evenly over consecutive tiles
       const int first = (int)(((uint32_t)grp + 3u - lt % 3u) % 3u);
       const RowGeo g = row_geo(a, mt * TC_BM + row, M);
-      const long long rowsum = (g.ok && first < NCH) ? pixel_rowsum(a, g.n, g.ih0, g.iw0) : 0;
+      const long long rowsum =
+          (g.ok && first < NCH)
+              ? (a.Rpix ? (long long)a.Rpix[((int64_t)g.n * a.OHr + g.oh) * a.OWr + g.ow] : pixel_rowsum(a, g.n, g.ih0, g.iw0))
+              : 0;
       int8_t* orow = g.ok ? a.out.p + vpix(a.out, g.n, g.oh, g.ow) * a.out.Cp : nullptr;
       const int8_t* srow = (g.ok && a.skip.p) ? a.skip.p + vpix(a.skip, g.n, g.oh, g.ow) * a.skip.Cp : nullptr;
       // the residual operand does not depend on the accumulator: fetch it before the wait
@@ -538,7 +546,8 @@ __global__ void k_conv_i8_ref(const ConvTcArgs a) {
       const int8_t* ws = a.wB + (((int64_t)ntile * a.n_kiter + kk / 8) * 8 + kk % 8) * BN * 16 + row * 16;
       for (int b = 0; b < 16; ++b) dot += (long long)xs[b] * ws[b];
     }
-    const long long rowsum = pixel_rowsum(a, g.n, g.ih0, g.iw0);
+    const long long rowsum = a.Rpix ? (long long)a.Rpix[((int64_t)g.n * a.OHr + g.oh) * a.OWr + g.ow]
+                                    : pixel_rowsum(a, g.n, g.ih0, g.iw0);
     int q = epi_slow(dot, c, rowsum, a, rt);
     if (q < rt.relu_zp) q = rt.relu_zp;
     if (a.skip.p) {
@@ -620,11 +629,31 @@ static EncodeTiledFn encode_tiled() {
 // on a halo-free input, every 3x3 pad-1 conv) with 64 or 128k channel bytes
 static bool setup_tma_a(ConvTcArgs& a) {
   const int Cp = a.in.Cp;
-  if (!a.allow_tma || a.stride != 1 || a.k != 2 * a.pad + 1 || a.in.halo != a.pad) return false;
-  if (!(Cp == 64 || Cp % 128 == 0) || a.OH != a.in.H || a.OW != a.in.W) return false;
+  if (!a.allow_tma || a.stride != 1 || a.in.halo != a.pad) return false;
   const int Hp = a.in.H + 2 * a.in.halo, Wp = a.in.W + 2 * a.in.halo;
   EncodeTiledFn fn = encode_tiled();
   if (!fn) return false;
+  if (Cp == 16 && a.k == 4 && a.OH <= Hp - 3 && a.OW <= Wp - 3) {
+    // s2d stem: dims {16 B, pixels, 4 kw taps} with strides {16, 16} (the tap dimension
+    // overlaps the pixel one): a box {16, 128, 4} lands as [tap][row][16 B], the no-swizzle
+    // K-major layout of 4 K chunks, i.e. one kh row of taps for 128 GEMM rows
+    cuuint64_t gdim[3] = {16, (cuuint64_t)a.in.N * Hp * Wp, 4};
+    cuuint64_t gstride[2] = {16, 16};
+    cuuint32_t box[3] = {16, (cuuint32_t)TC_BM, 4};
+    cuuint32_t es[3] = {1, 1, 1};
+    if (fn(&a.tmA, CU_TENSOR_MAP_DATA_TYPE_UINT8, 3, (void*)a.in.p, gdim, gstride, box, es,
+           CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+           CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS)
+      return false;
+    a.tma_a = 65;
+    a.OHr = a.OH;
+    a.OWr = a.OW;
+    a.OH = Hp;
+    a.OW = Wp;
+    return true;
+  }
+  if (a.k != 2 * a.pad + 1) return false;
+  if (!(Cp == 64 || Cp % 128 == 0) || a.OH != a.in.H || a.OW != a.in.W) return false;
   const int box0 = Cp == 64 ? 64 : 128;
   cuuint64_t gdim[2] = {(cuuint64_t)Cp, (cuuint64_t)a.in.N * Hp * Wp};
   cuuint64_t gstride[1] = {(cuuint64_t)Cp};

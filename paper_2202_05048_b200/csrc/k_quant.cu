@@ -103,6 +103,16 @@ void launch_weight_params(const unsigned int* mnmx, int cout, int per_channel, i
 // value of the weight element feeding GEMM column o, K byte position kb (padded layout)
 __device__ __forceinline__ bool wsrc(int o, int64_t kb, int cin, int k, int fc_hw, int cin_p,
                                      int64_t* src_idx) {
+  if (fc_hw < 0) {                       // s2d stem: kb = (kh'*k' + kw')*16 + (2a+b)*cin + c
+    const int k2 = -fc_hw;
+    const int tap = (int)(kb >> 4), j = (int)(kb & 15);
+    if (tap >= k2 * k2 || j >= 4 * cin) return false;
+    const int sub = j / cin, c = j - sub * cin;
+    const int kh = 2 * (tap / k2) + (sub >> 1) - 1, kw = 2 * (tap % k2) + (sub & 1) - 1;
+    if (kh < 0 || kh >= k || kw < 0 || kw >= k) return false;
+    *src_idx = (((int64_t)o * cin + c) * k + kh) * k + kw;
+    return true;
+  }
   if (fc_hw > 0) {                       // fc: kb = pix*cin_p + c  ->  ref index c*fc_hw + pix
     int64_t pix = kb / cin_p;
     int c = (int)(kb - pix * cin_p);
@@ -164,7 +174,7 @@ void launch_weight_quant_tc(const float* w, int cout, int cin, int k, int fc_hw,
   int64_t total = (int64_t)nt * n_kiter * 8 * bn * 16;
   k_weight_quant_tc<<<nblk(total), 256, 0, s>>>(w, cout, cin, k, fc_hw, cin_p, scale, zp, bn,
                                                 n_kiter, out, total);
-  int64_t per_ch = fc_hw > 0 ? (int64_t)cin * fc_hw : (int64_t)cin * k * k;
+  int64_t per_ch = fc_hw > 0 ? (int64_t)cin * fc_hw : (int64_t)cin * k * k;   // s2d: fc_hw < 0
   k_weight_sum<<<cout, 128, 0, s>>>(w, per_ch, scale, zp, wsum);
 }
 
@@ -315,6 +325,76 @@ void launch_quant_input(const float* imgs, int64_t img0, View out, const float* 
                         int hist, cudaStream_t s) {
   dim3 g(out.N * out.H, (out.W + 127) / 128);
   k_quant_input<<<g, 128, 0, s>>>(imgs, img0, out, as, az, hist);
+}
+
+// graph input (NCHW fp32, C0 <= 4 channels, even H0/W0) -> space-to-depth int8 view for
+// the stride-2 stem: s2d pixel (R, Q) holds x[c][2R+a][2Q+b] at byte (2a+b)*C0 + c, so the
+// stride-2 kxk conv becomes a stride-1 k'xk' conv (k' = (k+1)/2) whose 16-byte pixels are
+// TMA-loadable.  Same per-element quantizer as k_quant_input.  grid.x = (n, R) row.
+__global__ void k_quant_input_s2d(const float* __restrict__ imgs, int64_t img0, int C0, View out,
+                                  const float* __restrict__ as, const int* __restrict__ az, int hist) {
+  const double s = (double)as[hist], z = (double)az[hist];
+  const double rs = __ddiv_rn(1.0, s);
+  const int n = blockIdx.x / out.H, R = blockIdx.x - (blockIdx.x / out.H) * out.H;
+  const int W0 = 2 * out.W;
+  const int64_t plane = (int64_t)(2 * out.H) * W0;
+  for (int Q = blockIdx.y * blockDim.x + threadIdx.x; Q < out.W; Q += gridDim.y * blockDim.x) {
+    uint32_t pk[4] = {0u, 0u, 0u, 0u};
+#pragma unroll
+    for (int a = 0; a < 2; ++a)
+      for (int c = 0; c < C0; ++c) {
+        const float2 v = __ldg(reinterpret_cast<const float2*>(imgs + (img0 + n) * C0 * plane + (int64_t)c * plane +
+                                                               (int64_t)(2 * R + a) * W0 + 2 * Q));
+        const int j0 = (2 * a) * C0 + c, j1 = (2 * a + 1) * C0 + c;
+        pk[j0 >> 2] |= ((uint32_t)quant1_fast(v.x, rs, s, z) & 0xffu) << (8 * (j0 & 3));
+        pk[j1 >> 2] |= ((uint32_t)quant1_fast(v.y, rs, s, z) & 0xffu) << (8 * (j1 & 3));
+      }
+    *reinterpret_cast<int4*>(out.p + voff(out, n, R, Q)) = make_int4((int)pk[0], (int)pk[1], (int)pk[2], (int)pk[3]);
+  }
+}
+void launch_quant_input_s2d(const float* imgs, int64_t img0, int C0, View out, const float* as,
+                            const int* az, int hist, cudaStream_t s) {
+  dim3 g(out.N * out.H, (out.W + 127) / 128);
+  k_quant_input_s2d<<<g, 128, 0, s>>>(imgs, img0, C0, out, as, az, hist);
+}
+
+// per-output-pixel sum of the input codes under the stem's real kxk window (halo taps hold
+// the zero point), read from the s2d view: tap (kh', kw') covers original rows 2kh'+a-1 and
+// columns 2kw'+b-1; sub-pixels outside [0, k) are masked out
+__global__ void k_stem_rowsum(View in, int k, int C0, int OH, int OW, int* __restrict__ R) {
+  const int k2 = (k + 1) / 2;
+  const int Hp = in.H + 2 * in.halo, Wp = in.W + 2 * in.halo;
+  const int64_t total = (int64_t)in.N * OH * OW;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < total;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    const int ow = (int)(i % OW);
+    const int64_t t = i / OW;
+    const int oh = (int)(t % OH), n = (int)(t / OH);
+    int sum = 0;
+    for (int th = 0; th < k2; ++th)
+      for (int tw = 0; tw < k2; ++tw) {
+        const int4 v = __ldg(reinterpret_cast<const int4*>(in.p + (((int64_t)n * Hp + oh + th) * Wp + ow + tw) * in.Cp));
+        uint32_t m[4] = {0u, 0u, 0u, 0u};
+        for (int a = 0; a < 2; ++a)
+          for (int b = 0; b < 2; ++b) {
+            const int kh = 2 * th + a - 1, kw = 2 * tw + b - 1;
+            if (kh < 0 || kh >= k || kw < 0 || kw >= k) continue;
+            for (int c = 0; c < C0; ++c) {
+              const int j = (2 * a + b) * C0 + c;
+              m[j >> 2] |= 1u << (8 * (j & 3));
+            }
+          }
+        sum = __dp4a(v.x, (int)m[0], sum);
+        sum = __dp4a(v.y, (int)m[1], sum);
+        sum = __dp4a(v.z, (int)m[2], sum);
+        sum = __dp4a(v.w, (int)m[3], sum);
+      }
+    R[i] = sum;
+  }
+}
+void launch_stem_rowsum(View in, int k, int C0, int OH, int OW, int* R, cudaStream_t s) {
+  const int64_t n = (int64_t)in.N * OH * OW;
+  k_stem_rowsum<<<nblk(n), 256, 0, s>>>(in, k, C0, OH, OW, R);
 }
 
 // fp32 NHWC (pitch C) -> int8 view, optional fused relu clamp; grid.y = (n, h) row, threads

@@ -101,7 +101,8 @@ void launch_weight_params(const unsigned int* mnmx, int cout, int per_channel, i
                           float* scale, int* zp, cudaStream_t s);
 // quantize conv/fc weights [cout][cin][k][k] into the tcgen05 B tile layout
 // conv: w [cout][cin][k][k]; fc: w [cout][cin*fc_hw] (NCHW flatten) treated as a 1x1 conv over
-// an NHWC-flattened input of fc_hw pixels x cin_p channels.  Output: tiled B operand.
+// an NHWC-flattened input of fc_hw pixels x cin_p channels; fc_hw = -k' selects the
+// space-to-depth stem layout (k'xk' taps of 16-byte s2d pixels).  Output: tiled B operand.
 void launch_weight_quant_tc(const float* w, int cout, int cin, int k, int fc_hw, int cin_p,
                             const float* scale, const int* zp, int bn, int n_kiter, int8_t* out,
                             int* wsum, cudaStream_t s);
@@ -111,6 +112,9 @@ void launch_layer_params(const LayerSt* d_layers, int n_layers, const float* act
                          const int* act_zp, int wvar, cudaStream_t s);
 void launch_quant_input(const float* imgs_nchw, int64_t img0, View out, const float* act_scale,
                         const int* act_zp, int hist, cudaStream_t s);
+void launch_quant_input_s2d(const float* imgs_nchw, int64_t img0, int C0, View out,
+                            const float* act_scale, const int* act_zp, int hist, cudaStream_t s);
+void launch_stem_rowsum(View in_s2d, int k, int C0, int OH, int OW, int* R, cudaStream_t s);
 void launch_quant_nhwc(const float* x, View out, const float* act_scale, const int* act_zp,
                        int hist, int relu_hist, cudaStream_t s);
 void launch_dequant(View in, const float* act_scale, const int* act_zp, int hist, float* y,
@@ -173,6 +177,7 @@ struct ConvTcArgs {
   const int* wsum;        // [cout] sum of weight codes over real K (variant)
   int kreal;              // k*k*C
   const int* P;           // per-padded-input-pixel channel sums (only when has_wzp)
+  const int* Rpix;        // per-output-pixel window sums (s2d stem with has_wzp) or nullptr
   int has_wzp;
   LayerSt L;              // holds device pointers: mult / biasq / rt
   View skip;              // fused add operand (p == nullptr when none)

@@ -137,6 +137,10 @@ struct ptq_ctx {
   std::vector<std::vector<int64_t>> wshape;
   std::vector<WeightsDev> W;             // per node (compute nodes only)
   int first_compute = -1, last_compute = -1;
+  // space-to-depth stem: the graph input feeds only a stride-2 kxk conv on <= 4 channels with
+  // odd padding (k-1)/2; its int8 codes are stored s2d (H/2 x W/2 pixels of 16 bytes) and
+  // the conv runs as a stride-1 k'xk' conv, k' = (k+1)/2, halo (pad+1)/2
+  int s2d_node = -1, s2d_k = 0, s2d_halo = 0;
   // data
   float* d_imgs = nullptr;
   long long* d_labels = nullptr;
@@ -355,7 +359,17 @@ void import_graph(ptq_ctx* c, const ptq_graph_desc* g) {
       wd.q_cin_p = wd.cin_p;
       wd.q_k = kk;
       wd.q_fc_hw = wd.fc_hw;
-      if (n.kind != PTQ_FC && kk > 1 && x.c < 16) {
+      const bool s2d = n.kind == PTQ_CONV && n.in[0] == 0 && c->tens[0].consumers.size() == 1 &&
+                       kk > 1 && x.c <= 4 && n.stride == 2 && n.pad == (kk - 1) / 2 && (n.pad & 1) &&
+                       x.h % 2 == 0 && x.w % 2 == 0;
+      if (s2d) {
+        c->s2d_node = i;
+        c->s2d_k = (kk + 1) / 2;
+        c->s2d_halo = (n.pad + 1) / 2;
+        wd.n_chunks = c->s2d_k * c->s2d_k;      // one 16-byte s2d pixel per tap
+        wd.q_k = kk;
+        wd.q_fc_hw = -c->s2d_k;
+      } else if (n.kind != PTQ_FC && kk > 1 && x.c < 16) {
         // per-tap channel padding would inflate K (RGB stem: 49 x 16 vs 147 bytes): gather a
         // packed (kh, kw, c) im2col row per output pixel instead and run a 1x1 GEMM over it;
         // the weight quantizer sees it as an fc over k*k "pixels" of Cin unpadded channels
@@ -572,6 +586,7 @@ void build_plan(ptq_ctx* c, int mixed) {
 // ---------------------------------------------------------------- eval buffers
 View view_of(ptq_ctx* c, int t, int n) {
   const TensorI& x = c->tens[t];
+  if (t == 0 && c->s2d_node >= 0) return View{c->d_codes[0], n, x.h / 2, x.w / 2, 4 * x.c, 16, c->s2d_halo};
   return View{c->d_codes[t], n, x.h, x.w, x.c, c->cpad[t], c->halo[t]};
 }
 
@@ -594,6 +609,10 @@ void ensure_eval_buffers(ptq_ctx* c) {
       if (n.kind == PTQ_CONV || n.kind == PTQ_DWCONV || n.kind == PTQ_PWCONV)
         c->halo[t] = std::max(c->halo[t], n.pad);
     }
+  }
+  if (c->s2d_node >= 0) {
+    c->halo[0] = c->s2d_halo;
+    c->cpad[0] = 16;
   }
   // fc inputs are read as one flattened pixel: they must not carry a halo
   for (const NodeI& n : c->nodes)
@@ -623,10 +642,15 @@ void ensure_eval_buffers(ptq_ctx* c) {
   int64_t maxP = 0;
   for (int t : need8) {
     const TensorI& x = c->tens[t];
-    int64_t bytes = chunk * (int64_t)(x.h + 2 * c->halo[t]) * (x.w + 2 * c->halo[t]) * c->cpad[t];
+    const int h = (t == 0 && c->s2d_node >= 0) ? x.h / 2 : x.h, w = (t == 0 && c->s2d_node >= 0) ? x.w / 2 : x.w;
+    int64_t bytes = chunk * (int64_t)(h + 2 * c->halo[t]) * (w + 2 * c->halo[t]) * c->cpad[t];
     c->d_codes[t] = c->dalloc<int8_t>(bytes);
     CK(cudaMemsetAsync(c->d_codes[t], 0, bytes, c->st));
-    maxP = std::max<int64_t>(maxP, chunk * (int64_t)(x.h + 2 * c->halo[t]) * (x.w + 2 * c->halo[t]));
+    maxP = std::max<int64_t>(maxP, chunk * (int64_t)(h + 2 * c->halo[t]) * (w + 2 * c->halo[t]));
+  }
+  if (c->s2d_node >= 0) {                        // per-output-pixel window sums of the stem
+    const TensorI& y = c->tens[c->nodes[c->s2d_node].out];
+    maxP = std::max<int64_t>(maxP, chunk * (int64_t)y.h * y.w);
   }
   for (int t : need32) c->d_f32[t] = c->dalloc<float>(chunk * c->tens[t].elems);
   int64_t im_bytes = 0;
@@ -774,6 +798,20 @@ void eval_one(ptq_ctx* c, const ptq_config& cfg, unsigned long long* d_correct, 
       if (t != probe_t || !probe_out) return;
       View pv = V(t);
       const TensorI& x = c->tens[t];
+      if (t == 0 && c->s2d_node >= 0) {
+        std::vector<int8_t> h2((size_t)B * (pv.H + 2 * pv.halo) * (pv.W + 2 * pv.halo) * pv.Cp);
+        CK(cudaMemcpyAsync(h2.data(), pv.p, h2.size(), cudaMemcpyDeviceToHost, c->st));
+        CK(cudaStreamSynchronize(c->st));
+        const int Wq = pv.W + 2 * pv.halo, Hq = pv.H + 2 * pv.halo;
+        for (int n = 0; n < B; ++n)
+          for (int ch = 0; ch < x.c; ++ch)
+            for (int y = 0; y < x.h; ++y)
+              for (int xx = 0; xx < x.w; ++xx)
+                probe_out[((((size_t)(img0 + n) * x.c + ch) * x.h + y) * x.w) + xx] =
+                    h2[(((size_t)n * Hq + y / 2 + pv.halo) * Wq + xx / 2 + pv.halo) * pv.Cp +
+                       ((y & 1) * 2 + (xx & 1)) * x.c + ch];
+        return;
+      }
       std::vector<int8_t> h((size_t)B * (x.h + 2 * pv.halo) * (x.w + 2 * pv.halo) * pv.Cp);
       CK(cudaMemcpyAsync(h.data(), pv.p, h.size(), cudaMemcpyDeviceToHost, c->st));
       CK(cudaStreamSynchronize(c->st));
@@ -795,7 +833,10 @@ void eval_one(ptq_ctx* c, const ptq_config& cfg, unsigned long long* d_correct, 
     // graph input / mixed prefix
     int start = 0;
     if (!cfg.mixed) {
-      launch_quant_input(c->d_imgs, c->n_calib + img0, V(0), as, az, P.psrc[0], c->st);
+      if (c->s2d_node >= 0)
+        launch_quant_input_s2d(c->d_imgs, c->n_calib + img0, c->tens[0].c, V(0), as, az, P.psrc[0], c->st);
+      else
+        launch_quant_input(c->d_imgs, c->n_calib + img0, V(0), as, az, P.psrc[0], c->st);
       check_launch(c);
       halo_fill(0);
       probe(0);
@@ -834,6 +875,9 @@ void eval_one(ptq_ctx* c, const ptq_config& cfg, unsigned long long* d_correct, 
             check_launch(c);
             vin = View{c->d_im2col, B, y.h, y.w, wd.kreal, wd.im_cp, 0};
             a.k = 1; a.stride = 1; a.pad = 0; a.OH = y.h; a.OW = y.w;
+          } else if (i == c->s2d_node) {            // stride-1 k'xk' conv over the s2d input
+            a.k = c->s2d_k; a.stride = 1; a.pad = c->s2d_halo;
+            a.OH = c->tens[n.out].h; a.OW = c->tens[n.out].w;
           } else {
             a.k = n.k; a.stride = n.stride; a.pad = n.pad;
             a.OH = c->tens[n.out].h; a.OW = c->tens[n.out].w;
@@ -847,7 +891,12 @@ void eval_one(ptq_ctx* c, const ptq_config& cfg, unsigned long long* d_correct, 
           a.wsum = wd.wsum + (size_t)wv * wd.cout;
           a.kreal = wd.kreal;
           a.has_wzp = wd.has_wzp[wv];
-          if (a.has_wzp) {
+          if (a.has_wzp && i == c->s2d_node) {
+            REQ((int64_t)B * a.OH * a.OW <= c->P_cap, "stem rowsum buffer too small");
+            launch_stem_rowsum(vin, n.k, c->tens[0].c, a.OH, a.OW, c->d_P, c->st);
+            check_launch(c);
+            a.Rpix = c->d_P;
+          } else if (a.has_wzp) {
             launch_pixsum(vin, c->d_P, c->st);
             check_launch(c);
             a.P = c->d_P;

@@ -18,6 +18,7 @@ ev = GpuEvaluator(g, ds, 0, GENERIC)
 ev.set_option("fusion", fusion)
 import os
 ev.set_option("ablate", int(os.environ.get("ABLATE", "0")))
+ev.set_option("tma", int(os.environ.get("TMA", "1")))
 caches = {}
 for k, sc in enumerate(("S1", "S2", "S3")):
     caches[sc] = {t: O.Hist(t, float(ev.cache_ranges[k, i, 0]), float(ev.cache_ranges[k, i, 1]),
