@@ -178,6 +178,104 @@ void launch_weight_quant_tc(const float* w, int cout, int cin, int k, int fc_hw,
   k_weight_sum<<<cout, 128, 0, s>>>(w, per_ch, scale, zp, wsum);
 }
 
+// ---------------------------------------------------------------- all 8 weight variants at once
+// variant wv = scheme * 2 + granularity (granularity 1 = per channel).  Per-channel min/max
+// once; the per-tensor pair is the min/max of those (exact); then params, codes and code
+// sums of every variant in one launch each (was 4 launches per variant per layer).
+__global__ void k_minmax_tensor(unsigned int* mnmx, int cout) {
+  unsigned int lo = 0xffffffffu, hi = 0u;
+  for (int o = threadIdx.x; o < cout; o += blockDim.x) {
+    lo = min(lo, mnmx[2 * o]);
+    hi = max(hi, mnmx[2 * o + 1]);
+  }
+  for (int d = 16; d; d >>= 1) {
+    lo = min(lo, __shfl_xor_sync(0xffffffffu, lo, d));
+    hi = max(hi, __shfl_xor_sync(0xffffffffu, hi, d));
+  }
+  __shared__ unsigned int sl[32], sh[32];
+  if ((threadIdx.x & 31) == 0) { sl[threadIdx.x >> 5] = lo; sh[threadIdx.x >> 5] = hi; }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    for (int q = 1; q < (int)(blockDim.x >> 5); ++q) { lo = min(lo, sl[q]); hi = max(hi, sh[q]); }
+    mnmx[2 * cout] = lo;
+    mnmx[2 * cout + 1] = hi;
+  }
+}
+__global__ void k_weight_params8(const unsigned int* __restrict__ mnmx, int cout, float* __restrict__ scale,
+                                 int* __restrict__ zp) {
+  const int o = blockIdx.x * blockDim.x + threadIdx.x, wv = blockIdx.y;
+  if (o >= cout) return;
+  const int sch = wv >> 1, per_channel = wv & 1;
+  const unsigned int* q = mnmx + 2 * (per_channel ? o : cout);
+  params_for_range(sch, (double)ord2f(q[0]), (double)ord2f(q[1]), scale + (int64_t)wv * cout + o,
+                   zp + (int64_t)wv * cout + o);
+}
+__global__ void k_weight_quant_tc8(const float* __restrict__ w, int cout, int cin, int k, int fc_hw,
+                                   int cin_p, const float* __restrict__ scale, const int* __restrict__ zp,
+                                   int bn, int n_kiter, int8_t* __restrict__ out, int64_t per_variant) {
+  const int wv = blockIdx.y;
+  const float* sc = scale + (int64_t)wv * cout;
+  const int* z = zp + (int64_t)wv * cout;
+  int8_t* o8 = out + (int64_t)wv * per_variant;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < per_variant;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    int b = (int)(i & 15);
+    int64_t r = i >> 4;
+    int row = (int)(r % bn); r /= bn;
+    int j = (int)(r & 7); r >>= 3;
+    int it = (int)(r % n_kiter);
+    int nt = (int)(r / n_kiter);
+    int o = nt * bn + row;
+    int64_t kb = ((int64_t)it * 8 + j) * 16 + b;
+    int8_t code = 0;
+    int64_t si;
+    if (o < cout && wsrc(o, kb, cin, k, fc_hw, cin_p, &si))
+      code = (int8_t)quant1(__ldg(w + si), (double)sc[o], (double)z[o]);
+    o8[i] = code;
+  }
+}
+__global__ void k_weight_sum8(const float* __restrict__ w, int64_t per_ch, int cout,
+                              const float* __restrict__ scale, const int* __restrict__ zp,
+                              int* __restrict__ wsum) {
+  const int o = blockIdx.x, wv = blockIdx.y;
+  const double s = (double)scale[(int64_t)wv * cout + o], z = (double)zp[(int64_t)wv * cout + o];
+  int acc = 0;
+  for (int64_t i = threadIdx.x; i < per_ch; i += blockDim.x) acc += quant1(__ldg(w + (int64_t)o * per_ch + i), s, z);
+  for (int d = 16; d; d >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, d);
+  __shared__ int red[32];
+  if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = acc;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    int t = 0;
+    for (int q = 0; q < (int)(blockDim.x >> 5); ++q) t += red[q];
+    wsum[(int64_t)wv * cout + o] = t;
+  }
+}
+__global__ void k_weight_quant_dw8(const float* __restrict__ w, int c, int kk, const float* __restrict__ scale,
+                                   const int* __restrict__ zp, int8_t* __restrict__ out) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x, wv = blockIdx.y;
+  if (i >= c * kk) return;
+  const int ch = i / kk;
+  out[(int64_t)wv * c * kk + i] =
+      (int8_t)quant1(__ldg(w + i), (double)scale[(int64_t)wv * c + ch], (double)zp[(int64_t)wv * c + ch]);
+}
+void launch_weight_prepare8(const float* w, int cout, int64_t per_ch, bool depthwise, int cin, int k,
+                            int fc_hw, int cin_p, int bn, int n_kiter, int64_t bytes_per_variant,
+                            unsigned int* mnmx /*[2*(cout+1)]*/, float* scale, int* zp, int8_t* codes,
+                            int* wsum, cudaStream_t s) {
+  k_init_minmax<<<(cout + 255) / 256, 256, 0, s>>>(mnmx, cout);
+  k_weight_minmax<<<cout, 256, 0, s>>>(w, cout, per_ch, 1, mnmx);
+  k_minmax_tensor<<<1, 1024, 0, s>>>(mnmx, cout);
+  k_weight_params8<<<dim3((cout + 127) / 128, 8), 128, 0, s>>>(mnmx, cout, scale, zp);
+  if (depthwise) {
+    k_weight_quant_dw8<<<dim3((unsigned)((cout * k * k + 255) / 256), 8), 256, 0, s>>>(w, cout, k * k, scale, zp, codes);
+  } else {
+    k_weight_quant_tc8<<<dim3(nblk(bytes_per_variant, 256, 148 * 4), 8), 256, 0, s>>>(
+        w, cout, cin, k, fc_hw, cin_p, scale, zp, bn, n_kiter, codes, bytes_per_variant);
+    k_weight_sum8<<<dim3(cout, 8), 128, 0, s>>>(w, per_ch, cout, scale, zp, wsum);
+  }
+}
+
 // depthwise: out [c][k*k] codes
 __global__ void k_weight_quant_dw(const float* __restrict__ w, int c, int kk,
                                   const float* __restrict__ scale, const int* __restrict__ zp,

@@ -106,6 +106,11 @@ void launch_weight_params(const unsigned int* mnmx, int cout, int per_channel, i
 void launch_weight_quant_tc(const float* w, int cout, int cin, int k, int fc_hw, int cin_p,
                             const float* scale, const int* zp, int bn, int n_kiter, int8_t* out,
                             int* wsum, cudaStream_t s);
+// all 8 (scheme, granularity) variants of one weight tensor: params, codes, code sums
+void launch_weight_prepare8(const float* w, int cout, int64_t per_ch, bool depthwise, int cin, int k,
+                            int fc_hw, int cin_p, int bn, int n_kiter, int64_t bytes_per_variant,
+                            unsigned int* mnmx, float* scale, int* zp, int8_t* codes, int* wsum,
+                            cudaStream_t s);
 void launch_weight_quant_dw(const float* w, int c, int k, const float* scale, const int* zp,
                             int8_t* out, cudaStream_t s);
 void launch_layer_params(const LayerSt* d_layers, int n_layers, const float* act_scale,

@@ -698,7 +698,7 @@ void prepare(ptq_ctx* c) {
   unsigned int* d_mm = nullptr;
   int maxc = 1;
   for (auto& wd : c->W) maxc = std::max(maxc, wd.cout);
-  d_mm = c->dalloc<unsigned int>(2 * (size_t)maxc);
+  d_mm = c->dalloc<unsigned int>(2 * (size_t)maxc + 2);
   for (int i = 0; i < (int)c->nodes.size(); ++i) {
     const NodeI& n = c->nodes[i];
     if (!is_compute(n.kind)) continue;
@@ -706,23 +706,10 @@ void prepare(ptq_ctx* c) {
     const float* w = c->d_wt[n.weight];
     int64_t per_ch = 1;
     for (size_t d = 1; d < c->wshape[n.weight].size(); ++d) per_ch *= c->wshape[n.weight][d];
-    for (int sch = 0; sch < 4; ++sch)
-      for (int gran = 0; gran < 2; ++gran) {
-        const int wv = sch * 2 + gran;
-        float* sc = wd.scale + (size_t)wv * wd.cout;
-        int* zp = wd.zp + (size_t)wv * wd.cout;
-        launch_weight_minmax(w, wd.cout, per_ch, gran, d_mm, c->st);
-        check_launch(c);
-        launch_weight_params(d_mm, wd.cout, gran, sch, sc, zp, c->st);
-        check_launch(c);
-        int8_t* codes = wd.codes + (size_t)wv * wd.bytes_per_variant;
-        if (n.kind == PTQ_DWCONV)
-          launch_weight_quant_dw(w, wd.cout, wd.k, sc, zp, codes, c->st);
-        else
-          launch_weight_quant_tc(w, wd.cout, wd.cin, wd.q_k, wd.q_fc_hw, wd.q_cin_p, sc, zp, wd.bn,
-                                 wd.n_kiter, codes, wd.wsum + (size_t)wv * wd.cout, c->st);
-        check_launch(c);
-      }
+    launch_weight_prepare8(w, wd.cout, per_ch, n.kind == PTQ_DWCONV, wd.cin, n.kind == PTQ_DWCONV ? wd.k : wd.q_k,
+                           wd.q_fc_hw, wd.q_cin_p, wd.bn, wd.n_kiter, wd.bytes_per_variant, d_mm, wd.scale,
+                           wd.zp, wd.codes, wd.wsum, c->st);
+    check_launch(c);
   }
   CK(cudaStreamSynchronize(c->st));
   for (auto& wd : c->W) {

@@ -92,12 +92,13 @@ def _numpy_window_kl(counts: np.ndarray, lo: float, hi: float, i: int) -> float:
 def choose_kl_range(counts: np.ndarray, lo: float, hi: float, kl: np.ndarray) -> tuple[tuple[float, float], int]:
     """(lo, hi) clip range from the device KLs; returns (range, n_reranked)."""
     lo, hi = float(lo), float(hi)
-    if lo == hi or float(np.asarray(counts, dtype=np.float64).sum()) <= 0:
+    if lo == hi or int(counts.sum()) <= 0:
         return (lo, hi), 0
-    best = int(np.argmin(kl))               # first minimum == strict '<' sweep (clipping.py:82)
+    best = int(kl.argmin())                 # first minimum == strict '<' sweep (clipping.py:82)
     reranked = 0
-    if math.isfinite(kl[best]):
-        band = np.flatnonzero(kl <= kl[best] + abs(kl[best]) * TIE_BAND)
+    kb = float(kl[best])
+    if math.isfinite(kb):
+        band = np.flatnonzero(kl <= kb + abs(kb) * TIE_BAND)
         if band.size > 1:
             reranked = int(band.size)
             best_kl = math.inf
@@ -108,8 +109,20 @@ def choose_kl_range(counts: np.ndarray, lo: float, hi: float, kl: np.ndarray) ->
         start, end = kl_window_bounds(lo, hi, best + 128)
     else:
         start, end = 0, N_BINS
-    edges = np.linspace(lo, hi, N_BINS + 1)
-    return (float(edges[start]), float(edges[end])), reranked
+    return (_linspace_edge(lo, hi, start), _linspace_edge(lo, hi, end)), reranked
+
+
+def _linspace_edge(lo: float, hi: float, k: int) -> float:
+    """np.linspace(lo, hi, N_BINS + 1)[k] without building the array (numpy
+    function_base.linspace: fl(k * fl(delta / div)) + lo, last = hi, and the
+    step == 0 branch (k / div) * delta + lo)."""
+    if k >= N_BINS:
+        return hi
+    delta = hi - lo
+    step = delta / N_BINS
+    if step == 0:
+        return (k / N_BINS) * delta + lo
+    return k * step + lo
 
 
 # ---------------------------------------------------------------- evaluator

@@ -1,0 +1,18 @@
+"""Phase timing of calibration + prepare on ResNet-50 (PTQ_TRACE=1 prints the runtime's
+device-synchronised phase times).  Usage: PTQ_TRACE=1 python tools/trace_calib.py"""
+import sys
+import time
+
+sys.path.insert(0, ".")
+from paper_2202_05048_b200 import GENERIC, build_model, enumerate_space, make_dataset  # noqa: E402
+from paper_2202_05048_b200.evaluator import GpuEvaluator  # noqa: E402
+
+g = build_model("resnet50", 0)
+d = make_dataset(n_calib=300, n_eval=1000, seed=0, shape=(3, 224, 224))
+ev = GpuEvaluator(g, d, 0, GENERIC)
+cfg = enumerate_space(GENERIC)[0]
+for it in range(3):
+    t0 = time.perf_counter()
+    ev.calibrate_all()
+    ev.correct_counts([cfg])
+    print(f"iter {it}: calibrate_all + 1 config {time.perf_counter() - t0:.3f} s", file=sys.stderr)
