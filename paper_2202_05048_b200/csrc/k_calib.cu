@@ -117,13 +117,15 @@ __device__ __forceinline__ int np_bin_fast(double x, double lo, double hi, doubl
 }
 
 // x: [n_img_total][elems]; slots: image slots of this cache; range: lo, hi (fp32 values).
-// counts: [2048] int64 (accumulated).
+// counts: [2048] int64 (accumulated).  Four shared sub-histograms (one per warp % 4) spread
+// the atomics; exact zeros (post-ReLU tensors pile up there) are counted in registers and
+// added to the zero bin once per warp.
 __global__ void __launch_bounds__(512) k_histogram(const float* __restrict__ x, int64_t elems,
                                                    const int* __restrict__ slots, int n_slots,
                                                    const float* __restrict__ range,
                                                    unsigned long long* __restrict__ counts) {
-  __shared__ unsigned int sh[PTQ_NBINS];
-  for (int i = threadIdx.x; i < PTQ_NBINS; i += blockDim.x) sh[i] = 0;
+  __shared__ unsigned int sh[4 * PTQ_NBINS];
+  for (int i = threadIdx.x; i < 4 * PTQ_NBINS; i += blockDim.x) sh[i] = 0;
   __syncthreads();
   const double lo = (double)range[0], hi = (double)range[1];
   const double denom = __dsub_rn(hi, lo);
@@ -131,52 +133,45 @@ __global__ void __launch_bounds__(512) k_histogram(const float* __restrict__ x, 
   const double rc = degenerate ? 0.0 : __ddiv_rn((double)PTQ_NBINS, denom);
   const double mag = fmax(fabs(lo), fabs(hi));
   const double eps = degenerate ? 1.0 : 16.0 * 2.220446049250313e-16 * mag * rc + 1e-9;
-  const int lane = threadIdx.x & 31;
   if (degenerate) {                       // lo == hi: every value lands in bin 0 (:86-87)
     if (blockIdx.x == 0 && threadIdx.x == 0) atomicAdd(counts, (unsigned long long)(elems * n_slots));
     return;
   }
+  const int z0 = (lo <= 0.0 && 0.0 <= hi) ? np_bin(0.0, lo, hi, denom) : -1;
+  unsigned int* my = sh + ((threadIdx.x >> 5) & 3) * PTQ_NBINS;
+  unsigned int zc = 0;
+  auto put = [&](float v) {
+    if (v == 0.0f && z0 >= 0) ++zc;
+    else atomicAdd(&my[np_bin_fast((double)v, lo, hi, denom, rc, eps)], 1u);
+  };
   const int64_t stride = (int64_t)gridDim.x * blockDim.x;
   // every per-image slice is 16-byte aligned (elems % 4 == 0) except for tiny tensors:
   // flatten (image, float4) work items so small tensors still spread over all blocks
   const bool vec = (elems & 3) == 0 && ((((uintptr_t)x) & 15) == 0);
-  const int64_t nv = vec ? (elems >> 2) : 0;
-  const int64_t total_v = nv * n_slots;
-  {
-    for (int64_t base = blockIdx.x * (int64_t)blockDim.x; base < total_v; base += stride) {
-      const int64_t w = base + threadIdx.x;
-      const bool valid = w < total_v;
-      int b[4] = {0, 0, 0, 0};
-      if (valid) {
-        const int j = (int)(w / nv);
-        const float4 v = __ldg(reinterpret_cast<const float4*>(x + (int64_t)slots[j] * elems) + (w - (int64_t)j * nv));
-        b[0] = np_bin_fast((double)v.x, lo, hi, denom, rc, eps);
-        b[1] = np_bin_fast((double)v.y, lo, hi, denom, rc, eps);
-        b[2] = np_bin_fast((double)v.z, lo, hi, denom, rc, eps);
-        b[3] = np_bin_fast((double)v.w, lo, hi, denom, rc, eps);
-      }
-      // warp-aggregated increments: post-ReLU tensors pile up in bin 0
-      const unsigned int act = __ballot_sync(0xffffffffu, valid);
-      if (valid) {
-#pragma unroll
-        for (int q = 0; q < 4; ++q) {
-          const unsigned int peers = __match_any_sync(act, b[q]);
-          if (lane == __ffs(peers) - 1) atomicAdd(&sh[b[q]], __popc(peers));
-        }
-      }
+  if (vec) {
+    const int64_t nv = elems >> 2, total_v = nv * n_slots;
+    for (int64_t w = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; w < total_v; w += stride) {
+      const int j = (int)(w / nv);
+      const float4 v = __ldg(reinterpret_cast<const float4*>(x + (int64_t)slots[j] * elems) + (w - (int64_t)j * nv));
+      put(v.x);
+      put(v.y);
+      put(v.z);
+      put(v.w);
     }
-  }
-  if (!vec) {                             // scalar path (element count not a multiple of 4)
+  } else {                                // scalar path (element count not a multiple of 4)
     const int64_t total = elems * n_slots;
     for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < total; i += stride) {
       const int j = (int)(i / elems);
-      const float v = __ldg(x + (int64_t)slots[j] * elems + (i - (int64_t)j * elems));
-      atomicAdd(&sh[np_bin_fast((double)v, lo, hi, denom, rc, eps)], 1u);
+      put(__ldg(x + (int64_t)slots[j] * elems + (i - (int64_t)j * elems)));
     }
   }
+  for (int d = 16; d; d >>= 1) zc += __shfl_xor_sync(0xffffffffu, zc, d);
+  if ((threadIdx.x & 31) == 0 && zc) atomicAdd(&sh[z0], zc);
   __syncthreads();
-  for (int i = threadIdx.x; i < PTQ_NBINS; i += blockDim.x)
-    if (sh[i]) atomicAdd(counts + i, (unsigned long long)sh[i]);
+  for (int i = threadIdx.x; i < PTQ_NBINS; i += blockDim.x) {
+    const unsigned int t = sh[i] + sh[PTQ_NBINS + i] + sh[2 * PTQ_NBINS + i] + sh[3 * PTQ_NBINS + i];
+    if (t) atomicAdd(counts + i, (unsigned long long)t);
+  }
 }
 
 // ---------------------------------------------------------------- F2: KL sweep

@@ -11,8 +11,19 @@ g = build_model("resnet50", 0)
 d = make_dataset(n_calib=300, n_eval=1000, seed=0, shape=(3, 224, 224))
 ev = GpuEvaluator(g, d, 0, GENERIC)
 cfg = enumerate_space(GENERIC)[0]
+import os  # noqa: E402
+
+import torch  # noqa: E402
+
 for it in range(3):
+    prof = os.environ.get("PROFILE") and it == 2
+    if prof:
+        torch.cuda.synchronize()
+        torch.cuda.cudart().cudaProfilerStart()
     t0 = time.perf_counter()
     ev.calibrate_all()
+    if prof:
+        torch.cuda.synchronize()
+        torch.cuda.cudart().cudaProfilerStop()
     ev.correct_counts([cfg])
     print(f"iter {it}: calibrate_all + 1 config {time.perf_counter() - t0:.3f} s", file=sys.stderr)
