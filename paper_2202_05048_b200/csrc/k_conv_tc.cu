@@ -128,23 +128,31 @@ struct EpiK {
   int lo_conv, lo_add;
 };
 
-// clip(RHU(acc*m) + zp, lo, 127) on a biased accumulator: acc clamped to the layer's
+// RHU(acc*m) + zp (unclipped) on a biased accumulator: acc clamped to the layer's
 // saturation margin, then fl(fl(acc*m) + 0.5) exactly as the reference, floor and +zp in
 // one round-down add
 template <bool CLAMP>
-__device__ __forceinline__ int requant_fast(uint32_t accb, double m, const LayerRt& rt, const EpiK& k) {
+__device__ __forceinline__ int requant_raw(uint32_t accb, double m, const LayerRt& rt, const EpiK& k) {
   if (CLAMP) accb = umin(umax(accb, k.clo), k.chi);      // else |acc*m| < 2^30 already
   const double r = __dadd_rn(__dmul_rn(b2d(accb), m), 0.5);
-  return imin(imax(__double2loint(__dadd_rd(r, rt.mg_zy)), k.lo_conv), PTQ_QMAX);
+  return __double2loint(__dadd_rd(r, rt.mg_zy));
 }
-// 16 output channels of one row, fast path (no int32 saturation possible)
-// A fused residual add is one shared-memory lookup: stab[skip byte * 260 + conv code]
-// with stab pointing at column 128 of the table (built exactly by k_layer_params for the
-// config; operand order is baked in).
-template <bool WZP, bool SKIP, bool CLAMP>
-__device__ __forceinline__ void epi_chunk16(const uint32_t (&v)[16], const EpiParam* __restrict__ ep,
+// 4 int32 -> 4 saturated int8 codes in one word (byte j = x_j)
+__device__ __forceinline__ uint32_t pack4_sat(int x0, int x1, int x2, int x3) {
+  uint32_t hi, out;
+  asm("cvt.pack.sat.s8.s32.b32 %0, %1, %2, 0;" : "=r"(hi) : "r"(x3), "r"(x2));
+  asm("cvt.pack.sat.s8.s32.b32 %0, %1, %2, %3;" : "=r"(out) : "r"(x1), "r"(x0), "r"(hi));
+  return out;
+}
+// 16 output channels of one row, fast path (no int32 saturation possible).  Without a fused
+// add the clip to [-128, 127] is the saturating pack (a fused relu adds one max).  A fused
+// residual add is one shared-memory lookup: stab[skip byte * 260 + conv code] with stab
+// pointing at column 128 of the table (built exactly by k_layer_params for the config;
+// operand order is baked in).
+template <bool WZP, bool SKIP, bool CLAMP, bool RELU>
+__device__ __forceinline__ int4 epi_chunk16(const uint32_t (&v)[16], const EpiParam* __restrict__ ep,
                                             int cb, int rowsum, const LayerRt& rt, const EpiK& k,
-                                            const int8_t* __restrict__ stab, const int4 skv, int4& out) {
+                                            const int8_t* __restrict__ stab, const int4 skv) {
   uint32_t packed[4];
   const uint32_t skw[4] = {(uint32_t)skv.x, (uint32_t)skv.y, (uint32_t)skv.z, (uint32_t)skv.w};
 #pragma unroll
@@ -155,31 +163,18 @@ __device__ __forceinline__ void epi_chunk16(const uint32_t (&v)[16], const EpiPa
     int q[4];
 #pragma unroll
     for (int j = 0; j < 4; ++j) {
-      const int jj = g * 4 + j;
       const double m = __hiloint2double(raw[j].y, raw[j].x);
-      uint32_t accb = v[jj] + (uint32_t)raw[j].z;
+      uint32_t accb = v[g * 4 + j] + (uint32_t)raw[j].z;
       if (WZP) accb -= (uint32_t)(raw[j].w * rowsum);
-      q[j] = requant_fast<CLAMP>(accb, m, rt, k);
-      if (SKIP) q[j] = stab[(int)__byte_perm(skw[g], 0u, 0x4440u + j) * PTQ_ADDTAB_ROW + q[j]];
+      q[j] = requant_raw<CLAMP>(accb, m, rt, k);
+      if (RELU || SKIP) q[j] = imax(q[j], k.lo_conv);
+      if (SKIP) q[j] = stab[(int)__byte_perm(skw[g], 0u, 0x4440u + j) * PTQ_ADDTAB_ROW + imin(q[j], PTQ_QMAX)];
     }
-    packed[g] = __byte_perm(__byte_perm((uint32_t)q[0], (uint32_t)q[1], 0x0040),
-                            __byte_perm((uint32_t)q[2], (uint32_t)q[3], 0x0040), 0x5410);
+    packed[g] = SKIP ? __byte_perm(__byte_perm((uint32_t)q[0], (uint32_t)q[1], 0x0040),
+                                   __byte_perm((uint32_t)q[2], (uint32_t)q[3], 0x0040), 0x5410)
+                     : pack4_sat(q[0], q[1], q[2], q[3]);
   }
-  out = make_int4((int)packed[0], (int)packed[1], (int)packed[2], (int)packed[3]);
-}
-template <bool NOCLAMP>
-__device__ __forceinline__ void epi_dispatch(const uint32_t (&v)[16], const EpiParam* __restrict__ ep,
-                                             int cb, int rs, const LayerRt& rt, const EpiK& k,
-                                             const int8_t* __restrict__ stab, const int4 skv,
-                                             int4& res, bool skip, bool wzp) {
-  constexpr bool C = !NOCLAMP;
-  if (!skip) {
-    if (wzp) epi_chunk16<true, false, C>(v, ep, cb, rs, rt, k, stab, skv, res);
-    else epi_chunk16<false, false, C>(v, ep, cb, rs, rt, k, stab, skv, res);
-  } else {
-    if (wzp) epi_chunk16<true, true, C>(v, ep, cb, rs, rt, k, stab, skv, res);
-    else epi_chunk16<false, true, C>(v, ep, cb, rs, rt, k, stab, skv, res);
-  }
+  return make_int4((int)packed[0], (int)packed[1], (int)packed[2], (int)packed[3]);
 }
 
 // general (slow) path: 64-bit accumulator with the reference's int32 saturation
@@ -256,6 +251,71 @@ __device__ __forceinline__ RowGeo row_geo(const ConvTcArgs& a, int m, int M) {
   g.ih0 = g.oh * a.stride - a.pad + a.in.halo;
   g.iw0 = g.ow * a.stride - a.pad + a.in.halo;
   return g;
+}
+
+// what the epilogue warps share across the persistent tile loop
+struct EpiEnv {
+  uint32_t tmem;
+  uint64_t *tfull, *tempty;
+  const EpiParam* ep;
+  const int8_t* stab_c;
+  int q, grp, row, M, n_tiles, n_nt;
+};
+
+// persistent epilogue tile loop of one variant (GENERIC: runtime dispatch, slow layers and
+// the profiling ablation)
+template <int BN, bool WZP, bool SKIP, bool CLAMP, bool RELU, bool GENERIC>
+__device__ __forceinline__ void epi_tiles(const ConvTcArgs& a, const LayerRt& rt, const EpiK& k, const EpiEnv& e) {
+  constexpr int NCH = BN / 16;                       // 16-column chunks per tile
+  const int Cout = a.L.cout;
+  const bool has_skip = GENERIC ? a.skip.p != nullptr : SKIP;
+  uint32_t lt = 0;
+  for (int tile = blockIdx.x; tile < e.n_tiles; tile += gridDim.x, ++lt) {
+    const uint32_t buf = lt & 1u, uph = (lt >> 1) & 1u;
+    const int mt = (int)a.div_nt.div((uint32_t)tile);
+    const int nt = tile - mt * e.n_nt;
+    // chunks c = first, first+3, ...: the assignment rotates with the tile so the three
+    // column groups share BN/16 chunks evenly over consecutive tiles
+    const int first = (int)(((uint32_t)e.grp + 3u - lt % 3u) % 3u);
+    const RowGeo g = row_geo(a, mt * TC_BM + e.row, e.M);
+    long long rowsum = 0;
+    if ((GENERIC || WZP) && g.ok && first < NCH)
+      rowsum = a.Rpix ? (long long)a.Rpix[((int64_t)g.n * a.OHr + g.oh) * a.OWr + g.ow]
+                      : pixel_rowsum(a, g.n, g.ih0, g.iw0);
+    int8_t* orow = g.ok ? a.out.p + vpix(a.out, g.n, g.oh, g.ow) * a.out.Cp : nullptr;
+    const int8_t* srow = (g.ok && has_skip) ? a.skip.p + vpix(a.skip, g.n, g.oh, g.ow) * a.skip.Cp : nullptr;
+    // the residual operand does not depend on the accumulator: fetch it before the wait
+    // and one chunk ahead inside the loop
+    const int cb0 = nt * BN + first * 16;
+    int4 sk_next = make_int4(0, 0, 0, 0);
+    if (has_skip && srow && first < NCH && cb0 < a.out.Cp) sk_next = __ldg(reinterpret_cast<const int4*>(srow + cb0));
+    mbar_wait(&e.tfull[buf], uph);
+    tc_fence_after();
+    const uint32_t tbase = e.tmem + ((uint32_t)(e.q * 32) << 16) + buf * BN;
+#pragma unroll 1
+    for (int c = first; c < NCH; c += 3) {
+      uint32_t v[16];
+      tmem_ld16(tbase + (uint32_t)(c * 16), v);
+      const int cb = nt * BN + c * 16;
+      if (cb >= a.out.Cp) continue;              // warp-uniform: the slow path re-reads TMEM
+      int4 skv = make_int4(0, 0, 0, 0);
+      if (has_skip) {
+        skv = sk_next;
+        if (srow && c + 3 < NCH && cb + 48 < a.out.Cp) sk_next = __ldg(reinterpret_cast<const int4*>(srow + cb + 48));
+      }
+      int4 res;
+      if (GENERIC && a.ablate == 1) {
+        res = make_int4((int)v[0], (int)v[1], (int)v[2], (int)v[3]);
+      } else if (!GENERIC && cb + 16 <= Cout) {
+        res = epi_chunk16<WZP, SKIP, CLAMP, RELU>(v, e.ep, cb, (int)rowsum, rt, k, e.stab_c, skv);
+      } else {
+        res = epi_slow_chunk(tbase + (uint32_t)(c * 16), cb, rowsum, a, rt, k.lo_conv, k.lo_add, skv);
+      }
+      if (g.ok) *reinterpret_cast<int4*>(orow + cb) = res;
+    }
+    tc_fence_before();
+    mbar_arrive(&e.tempty[buf]);                     // accumulator buffer may be reused
+  }
 }
 
 template <int BN>
@@ -448,7 +508,6 @@ __global__ void __launch_bounds__(TC_THREADS, 1) k_conv_tc(const __grid_constant
     // ------------------------------------------------ epilogue warps
     const int q = warp & 3;                          // TMEM lane quarter this warp may access
     const int grp = (warp - 4) >> 2;                  // column group (3 groups per lane quarter)
-    constexpr int NCH = BN / 16;                      // 16-column chunks per tile
     const int row = q * 32 + lane;
     const LayerRt rt = *a.L.rt;
     EpiK k;
@@ -466,53 +525,27 @@ __global__ void __launch_bounds__(TC_THREADS, 1) k_conv_tc(const __grid_constant
     asm volatile("bar.sync 1, %0;" ::"n"(TC_EPI_WARPS * 32) : "memory");
     const EpiParam* ep = sparam;
     const int8_t* stab_c = stab + 128;                // column of conv code 0
-    const bool wzp = a.has_wzp != 0;
-    uint32_t lt = 0;
-    for (int tile = blockIdx.x; tile < n_tiles; tile += gridDim.x, ++lt) {
-      const uint32_t buf = lt & 1u, uph = (lt >> 1) & 1u;
-      const int mt = (int)a.div_nt.div((uint32_t)tile);
-      const int nt = tile - mt * n_nt;
-      // chunks c = first, first+3, ...: the assignment rotates with the tile so the three
-      // column groups share BN/16 chunks evenly over consecutive tiles
-      const int first = (int)(((uint32_t)grp + 3u - lt % 3u) % 3u);
-      const RowGeo g = row_geo(a, mt * TC_BM + row, M);
-      const long long rowsum =
-          (g.ok && first < NCH)
-              ? (a.Rpix ? (long long)a.Rpix[((int64_t)g.n * a.OHr + g.oh) * a.OWr + g.ow] : pixel_rowsum(a, g.n, g.ih0, g.iw0))
-              : 0;
-      int8_t* orow = g.ok ? a.out.p + vpix(a.out, g.n, g.oh, g.ow) * a.out.Cp : nullptr;
-      const int8_t* srow = (g.ok && a.skip.p) ? a.skip.p + vpix(a.skip, g.n, g.oh, g.ow) * a.skip.Cp : nullptr;
-      // the residual operand does not depend on the accumulator: fetch it before the wait
-      // and one chunk ahead inside the loop (its load latency was the top stall)
-      const int cb0 = nt * BN + first * 16;
-      int4 sk_next = (srow && first < NCH && cb0 < a.out.Cp) ? __ldg(reinterpret_cast<const int4*>(srow + cb0))
-                                                            : make_int4(0, 0, 0, 0);
-      mbar_wait(&tfull[buf], uph);
-      tc_fence_after();
-#pragma unroll 1
-      for (int c = first; c < NCH; c += 3) {
-        uint32_t v[16];
-        tmem_ld16(tmem + ((uint32_t)(q * 32) << 16) + buf * BN + (uint32_t)(c * 16), v);
-        const int cb = nt * BN + c * 16;
-        if (cb >= a.out.Cp) continue;            // warp-uniform: the slow path re-reads TMEM
-        const int4 skv = sk_next;
-        if (srow && c + 3 < NCH && cb + 48 < a.out.Cp)
-          sk_next = __ldg(reinterpret_cast<const int4*>(srow + cb + 48));
-        int4 res;
-        if (a.ablate == 1) {
-          res = make_int4((int)v[0], (int)v[1], (int)v[2], (int)v[3]);
-        } else if (!rt.slow && cb + 16 <= Cout) {
-          const int rs = (int)rowsum;
-          if (rt.noclamp) epi_dispatch<true>(v, ep, cb, rs, rt, k, stab_c, skv, res, srow != nullptr, wzp);
-          else epi_dispatch<false>(v, ep, cb, rs, rt, k, stab_c, skv, res, srow != nullptr, wzp);
-        } else {
-          res = epi_slow_chunk(tmem + ((uint32_t)(q * 32) << 16) + buf * BN + (uint32_t)(c * 16), cb, rowsum,
-                               a, rt, k.lo_conv, k.lo_add, skv);
-        }
-        if (g.ok) *reinterpret_cast<int4*>(orow + cb) = res;
-      }
-      tc_fence_before();
-      mbar_arrive(&tempty[buf]);                     // accumulator buffer may be reused
+    const EpiEnv e{tmem, tfull, tempty, ep, stab_c, q, grp, row, M, n_tiles, n_nt};
+    // one persistent tile loop per epilogue variant: the per-chunk code carries no
+    // layer-level dispatch (that overhead was ~20% of the hot loop's instructions)
+    const bool skip = a.skip.p != nullptr, wzp = a.has_wzp != 0, clamp = !rt.noclamp,
+               relu = k.lo_conv > PTQ_QMIN;
+    if (rt.slow || a.ablate == 1) epi_tiles<BN, false, false, false, false, true>(a, rt, k, e);
+    else if (skip) {
+      if (wzp) { if (clamp) epi_tiles<BN, true, true, true, false, false>(a, rt, k, e);
+                 else epi_tiles<BN, true, true, false, false, false>(a, rt, k, e); }
+      else { if (clamp) epi_tiles<BN, false, true, true, false, false>(a, rt, k, e);
+             else epi_tiles<BN, false, true, false, false, false>(a, rt, k, e); }
+    } else if (wzp) {
+      if (clamp) { if (relu) epi_tiles<BN, true, false, true, true, false>(a, rt, k, e);
+                   else epi_tiles<BN, true, false, true, false, false>(a, rt, k, e); }
+      else { if (relu) epi_tiles<BN, true, false, false, true, false>(a, rt, k, e);
+             else epi_tiles<BN, true, false, false, false, false>(a, rt, k, e); }
+    } else {
+      if (clamp) { if (relu) epi_tiles<BN, false, false, true, true, false>(a, rt, k, e);
+                   else epi_tiles<BN, false, false, true, false, false>(a, rt, k, e); }
+      else { if (relu) epi_tiles<BN, false, false, false, true, false>(a, rt, k, e);
+             else epi_tiles<BN, false, false, false, false, false>(a, rt, k, e); }
     }
   }
 
