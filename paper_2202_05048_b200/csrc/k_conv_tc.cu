@@ -36,6 +36,14 @@
 namespace ptq {
 
 constexpr int TC_BM = 128;
+// per-channel epilogue constants of the layer being run, in constant memory for the
+// fused-add layers: their shared-memory pipe is saturated by the add table, so the
+// per-output constant broadcast goes through the constant cache instead (elsewhere the
+// shared-memory copy is faster).  Written by the launcher with a stream-ordered
+// device-to-device copy before every launch.
+constexpr int TC_MAX_COUT = 2048;
+__constant__ EpiParam c_ep[TC_MAX_COUT];
+
 constexpr int TC_MAX_STAGES = 10;                 // smem pipeline depth cap (runtime depth: launcher)
 constexpr int TC_SMEM_MAX = 232448;                // 227 KB opt-in dynamic smem per CTA
 constexpr int TC_A_STAGE = TC_BM * 128;            // 16 KB: 8 chunks x 128 rows x 16 B
@@ -159,7 +167,7 @@ __device__ __forceinline__ int4 epi_chunk16(const uint32_t (&v)[16], const EpiPa
   for (int g = 0; g < 4; ++g) {
     int4 raw[4];
 #pragma unroll
-    for (int j = 0; j < 4; ++j) raw[j] = reinterpret_cast<const int4*>(ep + cb + g * 4)[j];
+    for (int j = 0; j < 4; ++j) raw[j] = reinterpret_cast<const int4*>((SKIP ? c_ep : ep) + cb + g * 4)[j];
     int q[4];
 #pragma unroll
     for (int j = 0; j < 4; ++j) {
@@ -331,8 +339,8 @@ __global__ void __launch_bounds__(TC_THREADS, 1) k_conv_tc(const __grid_constant
   uint64_t* tfull = empty + NS;
   uint64_t* tempty = tfull + 2;
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
-  EpiParam* sparam = reinterpret_cast<EpiParam*>(tempty + 4);   // [Cout] per-channel epilogue constants
-  int8_t* stab = reinterpret_cast<int8_t*>(sparam + a.L.cout);   // fused-add table (PTQ_ADDTAB_*)
+  EpiParam* sparam = reinterpret_cast<EpiParam*>(tempty + 4);   // [Cout] (layers without a fused add)
+  int8_t* stab = reinterpret_cast<int8_t*>(tempty + 4);          // fused-add table (PTQ_ADDTAB_*)
   constexpr uint32_t TMEM_COLS = (2 * BN) < 32 ? 32 : 2 * BN;
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -516,9 +524,10 @@ __global__ void __launch_bounds__(TC_THREADS, 1) k_conv_tc(const __grid_constant
     k.clo = 0x80000000u - (uint32_t)rt.aclamp;
     k.chi = 0x80000000u + (uint32_t)rt.aclamp;
     const int Cout = a.L.cout;
-    // stage the layer's per-channel epilogue constants in shared memory once (L1 misses on
-    // these broadcast loads were the top stall), then sync the 12 epilogue warps only
-    for (int i = threadIdx.x - 4 * 32; i < Cout; i += TC_EPI_WARPS * 32) sparam[i] = a.L.ep[i];
+    // stage the fused-add table (or the per-channel constants) in shared memory, then sync
+    // the 12 epilogue warps only
+    if (!a.addtab)
+      for (int i = threadIdx.x - 4 * 32; i < Cout; i += TC_EPI_WARPS * 32) sparam[i] = a.L.ep[i];
     if (a.addtab)
       for (int i = threadIdx.x - 4 * 32; i < PTQ_ADDTAB_BYTES / 16; i += TC_EPI_WARPS * 32)
         reinterpret_cast<int4*>(stab)[i] = reinterpret_cast<const int4*>(a.addtab)[i];
@@ -598,6 +607,8 @@ __global__ void k_conv_i8_ref(const ConvTcArgs a) {
   }
 }
 
+int conv_tc_max_cout() { return TC_MAX_COUT; }
+
 int conv_tc_bn_for(int cout) {
   if (cout <= 16) return 16;
   if (cout <= 32) return 32;
@@ -612,14 +623,17 @@ template <int BN>
 static void launch_bn(const ConvTcArgs& a, cudaStream_t s) {
   // fixed part: barriers, TMEM slot, per-channel constants, optional add table; the rest
   // of the 227 KB goes to pipeline stages (deeper for narrow tiles, at least 2)
-  const size_t fixed = 1024 + (2 * TC_MAX_STAGES + 4) * 8 + 16 + (size_t)a.L.cout * sizeof(EpiParam) +
-                       (a.addtab ? PTQ_ADDTAB_BYTES : 0);
+  const size_t fixed = 1024 + (2 * TC_MAX_STAGES + 4) * 8 + 16 +
+                       (a.addtab ? PTQ_ADDTAB_BYTES : (size_t)a.L.cout * sizeof(EpiParam));
   const size_t per_stage = (size_t)TC_A_STAGE + (size_t)BN * 128;
   int ns = (int)((TC_SMEM_MAX - fixed) / per_stage);
   if (ns > TC_MAX_STAGES) ns = TC_MAX_STAGES;
   if (ns < 2) ns = 2;                // does not fit: the launch fails loudly (check_launch)
   ConvTcArgs b = a;
   b.n_stages = ns;
+  // cout <= TC_MAX_COUT is checked when the graph is imported (conv_tc_max_cout)
+  if (a.addtab)
+    cudaMemcpyToSymbolAsync(c_ep, a.L.ep, (size_t)a.L.cout * sizeof(EpiParam), 0, cudaMemcpyDeviceToDevice, s);
   const size_t smem = (size_t)ns * per_stage + fixed;
   static bool configured = false;
   if (!configured) {

@@ -193,6 +193,7 @@ struct ConvTcArgs {
   int n_stages;           // smem pipeline depth (set by the launcher)
 };
 int conv_tc_bn_for(int cout);     // BN tile width the kernel uses for this Cout
+int conv_tc_max_cout();           // largest Cout the tensor-core conv supports
 void launch_conv_tc(const ConvTcArgs& a, int bn, cudaStream_t s);
 // CUDA-core reference of the same contract (tests / cross-checks only)
 void launch_conv_i8_ref(const ConvTcArgs& a, int bn, cudaStream_t s);

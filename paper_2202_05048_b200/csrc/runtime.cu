@@ -381,6 +381,7 @@ void import_graph(ptq_ctx* c, const ptq_graph_desc* g) {
         wd.q_fc_hw = kk * kk;
       }
       wd.n_kiter = (wd.n_chunks + 7) / 8;
+      REQ(wd.cout <= conv_tc_max_cout(), "conv / fc output channels exceed the tensor-core conv limit (2048)");
       wd.bn = conv_tc_bn_for(wd.cout);
       int ntiles = (wd.cout + wd.bn - 1) / wd.bn;
       wd.bytes_per_variant = (int64_t)ntiles * wd.n_kiter * 8 * wd.bn * 16;
