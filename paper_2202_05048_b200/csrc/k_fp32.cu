@@ -114,6 +114,110 @@ __global__ void __launch_bounds__(256) k_conv_f32(const float* __restrict__ x, i
   }
 }
 
+// Register-blocked implicit-GEMM conv for Cin % 8 == 0 (every layer but the RGB stem):
+// 128 x BN block tile, BK = 8 (one tap, 8 consecutive channels), 256 threads each owning
+// an 8 x (BN/16) register tile, double-buffered shared tiles with the next K slice
+// prefetched into registers (float4 global loads) while the current one is multiplied.
+template <int BN>
+__global__ void __launch_bounds__(256, 2) k_conv_f32_rb(const float* __restrict__ x, int N, int H, int W,
+                                                     int Cin, const float* __restrict__ Bw,
+                                                     const float* __restrict__ bias, int Cout, int k,
+                                                     int stride, int pad, int OH, int OW,
+                                                     float* __restrict__ y) {
+  constexpr int BM = 128, BK = 8, TN = BN / 16;   // TN = 8 (BN 128) or 4 (BN 64)
+  __shared__ __align__(16) float As[2][BK][BM + 4];
+  __shared__ __align__(16) float Bs[2][BK][BN];
+  const int tid = threadIdx.x;
+  const int64_t M = (int64_t)N * OH * OW;
+  const int K = k * k * Cin;
+  const int64_t m0 = (int64_t)blockIdx.x * BM;
+  const int n0 = blockIdx.y * BN;
+  // A loader: row ar = tid / 2, channels 4 * (tid & 1) .. +4 of the current tap
+  const int ar = tid >> 1, ah = (tid & 1) * 4;
+  const int64_t am = m0 + ar;
+  const bool aok = am < M;
+  int aih0 = 0, aiw0 = 0;
+  int64_t abase = 0;
+  {
+    const int64_t mm = aok ? am : 0;
+    const int ow = (int)(mm % OW);
+    const int64_t t = mm / OW;
+    const int oh = (int)(t % OH);
+    aih0 = oh * stride - pad;
+    aiw0 = ow * stride - pad;
+    abase = (t / OH) * H * W;
+  }
+  // B loader: k row bk, columns bc .. +4 (BN 128: 256 float4; BN 64: 128 float4)
+  const int bk = BN == 128 ? tid >> 5 : (tid >> 4) & 7, bc = BN == 128 ? (tid & 31) * 4 : (tid & 15) * 4;
+  const bool bload = BN == 128 || tid < 128;
+  const int tm = tid >> 4, tn = tid & 15;
+  float acc[8][TN];
+#pragma unroll
+  for (int i = 0; i < 8; ++i)
+#pragma unroll
+    for (int j = 0; j < TN; ++j) acc[i][j] = 0.f;
+
+  auto load_a = [&](int k0) -> float4 {
+    const int tap = k0 / Cin, ci = k0 - tap * Cin + ah;
+    const int kh = tap / k, kw = tap - kh * k;
+    const int ih = aih0 + kh, iw = aiw0 + kw;
+    if (aok && ih >= 0 && ih < H && iw >= 0 && iw < W)
+      return __ldg(reinterpret_cast<const float4*>(x + (abase + (int64_t)ih * W + iw) * Cin + ci));
+    return make_float4(0.f, 0.f, 0.f, 0.f);
+  };
+  auto load_b = [&](int k0) -> float4 {
+    const int nn = n0 + bc;
+    if (!bload || nn >= Cout) return make_float4(0.f, 0.f, 0.f, 0.f);
+    return __ldg(reinterpret_cast<const float4*>(Bw + (int64_t)(k0 + bk) * Cout + nn));
+  };
+  float4 ra = load_a(0), rb = load_b(0);
+  int buf = 0;
+  for (int k0 = 0; k0 < K; k0 += BK) {
+    As[buf][ah + 0][ar] = ra.x;
+    As[buf][ah + 1][ar] = ra.y;
+    As[buf][ah + 2][ar] = ra.z;
+    As[buf][ah + 3][ar] = ra.w;
+    if (bload) *reinterpret_cast<float4*>(&Bs[buf][bk][bc]) = rb;
+    __syncthreads();
+    if (k0 + BK < K) {                               // prefetch the next K slice
+      ra = load_a(k0 + BK);
+      rb = load_b(k0 + BK);
+    }
+#pragma unroll
+    for (int kk = 0; kk < BK; ++kk) {
+      const float4 a0 = *reinterpret_cast<const float4*>(&As[buf][kk][tm * 8]);
+      const float4 a1 = *reinterpret_cast<const float4*>(&As[buf][kk][tm * 8 + 4]);
+      const float a[8] = {a0.x, a0.y, a0.z, a0.w, a1.x, a1.y, a1.z, a1.w};
+      float b[TN];
+      const float4 b0 = *reinterpret_cast<const float4*>(&Bs[buf][kk][tn * TN]);
+      b[0] = b0.x; b[1] = b0.y; b[2] = b0.z; b[3] = b0.w;
+      if (TN == 8) {
+        const float4 b1 = *reinterpret_cast<const float4*>(&Bs[buf][kk][tn * TN + 4]);
+        b[4 % TN] = b1.x; b[5 % TN] = b1.y; b[6 % TN] = b1.z; b[7 % TN] = b1.w;
+      }
+#pragma unroll
+      for (int i = 0; i < 8; ++i)
+#pragma unroll
+        for (int j = 0; j < TN; ++j) acc[i][j] = fmaf(a[i], b[j], acc[i][j]);
+    }
+    buf ^= 1;
+  }
+  const int cn = n0 + tn * TN;
+  float bv[TN];
+#pragma unroll
+  for (int j = 0; j < TN; ++j) bv[j] = (bias && cn + j < Cout) ? __ldg(bias + cn + j) : 0.f;
+#pragma unroll
+  for (int i = 0; i < 8; ++i) {
+    const int64_t m = m0 + tm * 8 + i;
+    if (m >= M || cn >= Cout) continue;
+    float* dst = y + m * Cout + cn;
+#pragma unroll
+    for (int j = 0; j < TN; j += 4)
+      *reinterpret_cast<float4*>(dst + j) =
+          make_float4(acc[i][j] + bv[j], acc[i][j + 1] + bv[j + 1], acc[i][j + 2] + bv[j + 2], acc[i][j + 3] + bv[j + 3]);
+  }
+}
+
 // depthwise conv: w is [C][k*k]
 __global__ void k_dwconv_f32(const float* __restrict__ x, int N, int H, int W, int C,
                              const float* __restrict__ w, const float* __restrict__ bias, int k,
@@ -233,6 +337,16 @@ void launch_conv_f32(const float* x, int N, int H, int W, int Cin, const float* 
                      const float* bias, int Cout, int k, int stride, int pad, int OH, int OW,
                      float* y, cudaStream_t s) {
   int64_t M = (int64_t)N * OH * OW;
+  if (Cin % 8 == 0 && Cout % 64 == 0) {              // register-blocked path (float4 operands)
+    if (Cout % 128 == 0) {
+      dim3 g((unsigned)((M + 127) / 128), (unsigned)(Cout / 128));
+      k_conv_f32_rb<128><<<g, 256, 0, s>>>(x, N, H, W, Cin, Bw, bias, Cout, k, stride, pad, OH, OW, y);
+    } else {
+      dim3 g((unsigned)((M + 127) / 128), (unsigned)(Cout / 64));
+      k_conv_f32_rb<64><<<g, 256, 0, s>>>(x, N, H, W, Cin, Bw, bias, Cout, k, stride, pad, OH, OW, y);
+    }
+    return;
+  }
   dim3 g((unsigned)((M + CF_BM - 1) / CF_BM), (unsigned)((Cout + CF_BN - 1) / CF_BN));
   k_conv_f32<<<g, 256, 0, s>>>(x, N, H, W, Cin, Bw, bias, Cout, k, stride, pad, OH, OW, y);
 }

@@ -461,6 +461,23 @@ void launch_quant_input_s2d(const float* imgs, int64_t img0, int C0, View out, c
 // columns 2kw'+b-1; sub-pixels outside [0, k) are masked out
 __global__ void k_stem_rowsum(View in, int k, int C0, int OH, int OW, int* __restrict__ R) {
   const int k2 = (k + 1) / 2;
+  // byte masks of the real sub-pixels of every s2d tap, built once per block
+  __shared__ uint4 smask[64];
+  for (int t = threadIdx.x; t < k2 * k2 && t < 64; t += blockDim.x) {
+    const int th = t / k2, tw = t - th * k2;
+    uint32_t m[4] = {0u, 0u, 0u, 0u};
+    for (int a = 0; a < 2; ++a)
+      for (int b = 0; b < 2; ++b) {
+        const int kh = 2 * th + a - 1, kw = 2 * tw + b - 1;
+        if (kh < 0 || kh >= k || kw < 0 || kw >= k) continue;
+        for (int c = 0; c < C0; ++c) {
+          const int j = (2 * a + b) * C0 + c;
+          m[j >> 2] |= 1u << (8 * (j & 3));
+        }
+      }
+    smask[t] = make_uint4(m[0], m[1], m[2], m[3]);
+  }
+  __syncthreads();
   const int Hp = in.H + 2 * in.halo, Wp = in.W + 2 * in.halo;
   const int64_t total = (int64_t)in.N * OH * OW;
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < total;
@@ -468,24 +485,16 @@ __global__ void k_stem_rowsum(View in, int k, int C0, int OH, int OW, int* __res
     const int ow = (int)(i % OW);
     const int64_t t = i / OW;
     const int oh = (int)(t % OH), n = (int)(t / OH);
+    const int8_t* base = in.p + (((int64_t)n * Hp + oh) * Wp + ow) * in.Cp;
     int sum = 0;
     for (int th = 0; th < k2; ++th)
       for (int tw = 0; tw < k2; ++tw) {
-        const int4 v = __ldg(reinterpret_cast<const int4*>(in.p + (((int64_t)n * Hp + oh + th) * Wp + ow + tw) * in.Cp));
-        uint32_t m[4] = {0u, 0u, 0u, 0u};
-        for (int a = 0; a < 2; ++a)
-          for (int b = 0; b < 2; ++b) {
-            const int kh = 2 * th + a - 1, kw = 2 * tw + b - 1;
-            if (kh < 0 || kh >= k || kw < 0 || kw >= k) continue;
-            for (int c = 0; c < C0; ++c) {
-              const int j = (2 * a + b) * C0 + c;
-              m[j >> 2] |= 1u << (8 * (j & 3));
-            }
-          }
-        sum = __dp4a(v.x, (int)m[0], sum);
-        sum = __dp4a(v.y, (int)m[1], sum);
-        sum = __dp4a(v.z, (int)m[2], sum);
-        sum = __dp4a(v.w, (int)m[3], sum);
+        const int4 v = __ldg(reinterpret_cast<const int4*>(base + ((int64_t)th * Wp + tw) * in.Cp));
+        const uint4 m = smask[th * k2 + tw];
+        sum = __dp4a(v.x, (int)m.x, sum);
+        sum = __dp4a(v.y, (int)m.y, sum);
+        sum = __dp4a(v.z, (int)m.z, sum);
+        sum = __dp4a(v.w, (int)m.w, sum);
       }
     R[i] = sum;
   }
