@@ -264,7 +264,8 @@ __device__ __forceinline__ RowGeo row_geo(const ConvTcArgs& a, int m, int M) {
 // what the epilogue warps share across the persistent tile loop
 struct EpiEnv {
   uint32_t tmem;
-  uint64_t *tfull, *tempty;
+  uint64_t *tfull, *tempty, *rsfull;
+  const int* rsum;
   const EpiParam* ep;
   const int8_t* stab_c;
   int q, grp, row, M, n_tiles, n_nt;
@@ -287,9 +288,13 @@ __device__ __forceinline__ void epi_tiles(const ConvTcArgs& a, const LayerRt& rt
     const int first = (int)(((uint32_t)e.grp + 3u - lt % 3u) % 3u);
     const RowGeo g = row_geo(a, mt * TC_BM + e.row, e.M);
     long long rowsum = 0;
-    if ((GENERIC || WZP) && g.ok && first < NCH)
+    if ((GENERIC || WZP) && a.tma_rowsum) {
+      mbar_wait(&e.rsfull[buf], uph);
+      rowsum = e.rsum[buf * TC_BM + e.row];
+    } else if ((GENERIC || WZP) && g.ok && first < NCH) {
       rowsum = a.Rpix ? (long long)a.Rpix[((int64_t)g.n * a.OHr + g.oh) * a.OWr + g.ow]
                       : pixel_rowsum(a, g.n, g.ih0, g.iw0);
+    }
     int8_t* orow = g.ok ? a.out.p + vpix(a.out, g.n, g.oh, g.ow) * a.out.Cp : nullptr;
     const int8_t* srow = (g.ok && has_skip) ? a.skip.p + vpix(a.skip, g.n, g.oh, g.ow) * a.skip.Cp : nullptr;
     // the residual operand does not depend on the accumulator: fetch it before the wait
@@ -338,9 +343,11 @@ __global__ void __launch_bounds__(TC_THREADS, 1) k_conv_tc(const __grid_constant
   uint64_t* empty = full + NS;
   uint64_t* tfull = empty + NS;
   uint64_t* tempty = tfull + 2;
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
-  EpiParam* sparam = reinterpret_cast<EpiParam*>(tempty + 4);   // [Cout] (layers without a fused add)
-  int8_t* stab = reinterpret_cast<int8_t*>(tempty + 4);          // fused-add table (PTQ_ADDTAB_*)
+  uint64_t* rsfull = tempty + 2;                                 // row sums of tile buffer ready
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 4);
+  int* rsum = reinterpret_cast<int*>(tempty + 6);                // [2][128] A-row sums (tma_rowsum)
+  EpiParam* sparam = reinterpret_cast<EpiParam*>(rsum + 2 * TC_BM);   // [Cout] (no fused add)
+  int8_t* stab = reinterpret_cast<int8_t*>(rsum + 2 * TC_BM);          // fused-add table
   constexpr uint32_t TMEM_COLS = (2 * BN) < 32 ? 32 : 2 * BN;
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -351,9 +358,10 @@ __global__ void __launch_bounds__(TC_THREADS, 1) k_conv_tc(const __grid_constant
   if (threadIdx.x == 0) {
     for (int s = 0; s < NS; ++s) {
       mbar_init(&full[s], a.tma_a ? 2 : 64 + 1);
-      mbar_init(&empty[s], 1);
+      mbar_init(&empty[s], a.tma_rowsum ? 2 : 1);
     }
     for (int b = 0; b < 2; ++b) {
+      mbar_init(&rsfull[b], 1);
       mbar_init(&tfull[b], 1);
       mbar_init(&tempty[b], TC_EPI_WARPS * 32);
     }
@@ -418,6 +426,50 @@ __global__ void __launch_bounds__(TC_THREADS, 1) k_conv_tc(const __grid_constant
           }
           if (++s == NS) { s = 0; ph ^= 1u; }
         }
+      }
+    } else if (warp == 1 && a.tma_rowsum) {
+      // weight zero points need sum_k x[row][k] per GEMM row: sum the A rows straight from
+      // the landed stages (halo taps hold the zero point, pad channels 0), instead of a
+      // separate pixel-sum pass over the input tensor.  Lane l owns rows l + 32i; chunks are
+      // visited in a lane-rotated order so every quarter-warp hits distinct banks.
+      const int taps = a.k * a.k;
+      int s = 0;
+      uint32_t ph = 0, lt = 0;
+      for (int tile = blockIdx.x; tile < n_tiles; tile += gridDim.x, ++lt) {
+        const uint32_t buf = lt & 1u, uph = (lt >> 1) & 1u;
+        int sum[4] = {0, 0, 0, 0};
+        for (int ki = 0; ki < a.n_kiter; ++ki) {
+          mbar_wait(&full[s], ph);
+          const uint8_t* st = sA + s * TC_A_STAGE;
+          if (a.tma_a == 128) {
+#pragma unroll
+            for (int i = 0; i < 4; ++i)
+#pragma unroll
+              for (int j = 0; j < 8; ++j) {
+                const int4 v = *reinterpret_cast<const int4*>(st + (lane + 32 * i) * 128 + ((j + lane) & 7) * 16);
+                sum[i] = __dp4a(v.x, 0x01010101, __dp4a(v.y, 0x01010101, __dp4a(v.z, 0x01010101, __dp4a(v.w, 0x01010101, sum[i]))));
+              }
+          } else {
+            const int halves = 2 * ki + 1 < taps ? 2 : 1;
+            for (int hv = 0; hv < halves; ++hv)
+#pragma unroll
+              for (int i = 0; i < 4; ++i)
+#pragma unroll
+                for (int j = 0; j < 4; ++j) {
+                  const int4 v = *reinterpret_cast<const int4*>(st + hv * (TC_A_STAGE / 2) + (lane + 32 * i) * 64 +
+                                                                ((j + (lane >> 1)) & 3) * 16);
+                  sum[i] = __dp4a(v.x, 0x01010101, __dp4a(v.y, 0x01010101, __dp4a(v.z, 0x01010101, __dp4a(v.w, 0x01010101, sum[i]))));
+                }
+          }
+          __syncwarp();
+          if (lane == 0) mbar_arrive(&empty[s]);     // this stage's A bytes are no longer needed here
+          if (++s == NS) { s = 0; ph ^= 1u; }
+        }
+        mbar_wait(&tempty[buf], uph ^ 1u);           // the epilogue is done with rsum[buf]
+#pragma unroll
+        for (int i = 0; i < 4; ++i) rsum[buf * TC_BM + lane + 32 * i] = sum[i];
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&rsfull[buf]);
       }
     }
   } else if (warp < 2) {
@@ -534,7 +586,7 @@ __global__ void __launch_bounds__(TC_THREADS, 1) k_conv_tc(const __grid_constant
     asm volatile("bar.sync 1, %0;" ::"n"(TC_EPI_WARPS * 32) : "memory");
     const EpiParam* ep = sparam;
     const int8_t* stab_c = stab + 128;                // column of conv code 0
-    const EpiEnv e{tmem, tfull, tempty, ep, stab_c, q, grp, row, M, n_tiles, n_nt};
+    const EpiEnv e{tmem, tfull, tempty, rsfull, rsum, ep, stab_c, q, grp, row, M, n_tiles, n_nt};
     // one persistent tile loop per epilogue variant: the per-chunk code carries no
     // layer-level dispatch (that overhead was ~20% of the hot loop's instructions)
     const bool skip = a.skip.p != nullptr, wzp = a.has_wzp != 0, clamp = !rt.noclamp,
@@ -623,7 +675,7 @@ template <int BN>
 static void launch_bn(const ConvTcArgs& a, cudaStream_t s) {
   // fixed part: barriers, TMEM slot, per-channel constants, optional add table; the rest
   // of the 227 KB goes to pipeline stages (deeper for narrow tiles, at least 2)
-  const size_t fixed = 1024 + (2 * TC_MAX_STAGES + 4) * 8 + 16 +
+  const size_t fixed = 1024 + (2 * TC_MAX_STAGES + 8) * 8 + 2 * TC_BM * 4 + 16 +
                        (a.addtab ? PTQ_ADDTAB_BYTES : (size_t)a.L.cout * sizeof(EpiParam));
   const size_t per_stage = (size_t)TC_A_STAGE + (size_t)BN * 128;
   int ns = (int)((TC_SMEM_MAX - fixed) / per_stage);
@@ -722,10 +774,17 @@ static bool setup_tma_a(ConvTcArgs& a) {
   return true;
 }
 
+bool conv_tc_tma_rowsum(const ConvTcArgs& a0) {
+  ConvTcArgs t = a0;
+  t.tma_a = 0;
+  return setup_tma_a(t) && t.has_wzp && !t.Rpix && (t.tma_a == 64 || t.tma_a == 128);
+}
+
 void launch_conv_tc(const ConvTcArgs& a0, int bn, cudaStream_t s) {
   ConvTcArgs t = a0;
   t.tma_a = 0;
   setup_tma_a(t);
+  t.tma_rowsum = t.has_wzp && !t.Rpix && (t.tma_a == 64 || t.tma_a == 128);
   const ConvTcArgs a = with_divs(t, bn);
   switch (bn) {
     case 16: launch_bn<16>(a, s); break;

@@ -183,6 +183,8 @@ struct ConvTcArgs {
   int kreal;              // k*k*C
   const int* P;           // per-padded-input-pixel channel sums (only when has_wzp)
   const int* Rpix;        // per-output-pixel window sums (s2d stem with has_wzp) or nullptr
+  int tma_rowsum;         // set by the launcher: TMA mode with has_wzp -> row sums of the A
+                          // tiles are taken from shared memory (no pixel-sum pass)
   int has_wzp;
   LayerSt L;              // holds device pointers: mult / biasq / rt
   View skip;              // fused add operand (p == nullptr when none)
@@ -195,6 +197,8 @@ struct ConvTcArgs {
 int conv_tc_bn_for(int cout);     // BN tile width the kernel uses for this Cout
 int conv_tc_max_cout();           // largest Cout the tensor-core conv supports
 void launch_conv_tc(const ConvTcArgs& a, int bn, cudaStream_t s);
+// true when launch_conv_tc will load A with TMA and (with has_wzp) sum the rows itself
+bool conv_tc_tma_rowsum(const ConvTcArgs& a);
 // CUDA-core reference of the same contract (tests / cross-checks only)
 void launch_conv_i8_ref(const ConvTcArgs& a, int bn, cudaStream_t s);
 

@@ -884,10 +884,6 @@ void eval_one(ptq_ctx* c, const ptq_config& cfg, unsigned long long* d_correct, 
             launch_stem_rowsum(vin, n.k, c->tens[0].c, a.OH, a.OW, c->d_P, c->st);
             check_launch(c);
             a.Rpix = c->d_P;
-          } else if (a.has_wzp) {
-            launch_pixsum(vin, c->d_P, c->st);
-            check_launch(c);
-            a.P = c->d_P;
           }
           a.L = L;
           a.skip = View{nullptr, 0, 0, 0, 0, 0, 0};
@@ -898,6 +894,11 @@ void eval_one(ptq_ctx* c, const ptq_config& cfg, unsigned long long* d_correct, 
           a.addtab = L.addtab;
           a.ablate = c->ablate;
           a.allow_tma = c->tma;
+          if (a.has_wzp && !a.Rpix && (c->conv_ref || !conv_tc_tma_rowsum(a))) {
+            launch_pixsum(vin, c->d_P, c->st);       // gather-mode convs sum input pixels first
+            check_launch(c);
+            a.P = c->d_P;
+          }
           cudaEvent_t ea = nullptr, eb = nullptr;
           const bool timed = c->cur_cfg < c->time_conv;   // instrument only the leading configs
           ++c->conv_launches_total;
