@@ -63,12 +63,15 @@ def kl_window_bounds(lo: float, hi: float, i: int) -> tuple[int, int]:
     return start, start + i
 
 
-def _numpy_window_kl(counts: np.ndarray, lo: float, hi: float, i: int) -> float:
+_AR128 = np.arange(128)
+_AR2048 = np.arange(N_BINS)
+
+
+def _numpy_window_kl(counts: np.ndarray, lo: float, hi: float, i: int, _pre=None) -> float:
     """numpy evaluation of one window's KL in the reference's op order
-    (clipping.py:38-52, :77-81) -- used only to break near-ties."""
-    c = counts.astype(np.float64)
-    total = c.sum()
-    cum = np.cumsum(c)
+    (clipping.py:38-52, :77-81) -- used only to break near-ties.  `_pre` carries the
+    per-histogram (float64 counts, total, cumsum) when several windows are ranked."""
+    c, total, cum = _pre if _pre is not None else _kl_pre(counts)
     start, end = kl_window_bounds(lo, hi, i)
     win = c[start:end]
     ref = win.copy()
@@ -76,17 +79,22 @@ def _numpy_window_kl(counts: np.ndarray, lo: float, hi: float, i: int) -> float:
         ref[0] += cum[start - 1]
     ref[-1] += total - cum[end - 1]
     m = i // 128
-    starts = np.arange(128) * m
+    starts = _AR128 * m
     sums = np.add.reduceat(win, starts)
     nz = ref > 0
     nzg = np.add.reduceat(nz.astype(np.float64), starts)
-    gidx = np.minimum(np.arange(i) // m, 127)
+    gidx = np.minimum(_AR2048[:i] // m, 127)
     q = np.zeros(i)
     q[nz] = sums[gidx[nz]] / nzg[gidx[nz]]
     if np.any(nz & (q == 0.0)):
         return math.inf
     p = ref[nz]
     return float(np.sum(p * (np.log(p) - np.log(q[nz]))) / ref.sum())
+
+
+def _kl_pre(counts: np.ndarray):
+    c = counts.astype(np.float64)
+    return c, c.sum(), np.cumsum(c)
 
 
 def choose_kl_range(counts: np.ndarray, lo: float, hi: float, kl: np.ndarray) -> tuple[tuple[float, float], int]:
@@ -102,8 +110,9 @@ def choose_kl_range(counts: np.ndarray, lo: float, hi: float, kl: np.ndarray) ->
         if band.size > 1:
             reranked = int(band.size)
             best_kl = math.inf
+            pre = _kl_pre(counts)
             for w in band:
-                v = _numpy_window_kl(counts, lo, hi, int(w) + 128)
+                v = _numpy_window_kl(counts, lo, hi, int(w) + 128, pre)
                 if v < best_kl:
                     best_kl, best = v, int(w)
         start, end = kl_window_bounds(lo, hi, best + 128)

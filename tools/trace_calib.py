@@ -26,4 +26,13 @@ for it in range(3):
         torch.cuda.synchronize()
         torch.cuda.cudart().cudaProfilerStop()
     ev.correct_counts([cfg])
-    print(f"iter {it}: calibrate_all + 1 config {time.perf_counter() - t0:.3f} s", file=sys.stderr)
+    print(f"iter {it}: calibrate_all + 1 config {time.perf_counter() - t0:.3f} s, "
+          f"KL windows re-ranked on the host: {ev.kl_reranked}", file=sys.stderr)
+    if it == 0:
+        import numpy as np
+        from paper_2202_05048_b200.evaluator import TIE_BAND
+        kl = ev.kl_values.reshape(-1, ev.kl_values.shape[-1])
+        best = kl.min(axis=1)
+        band = (kl <= best[:, None] + np.abs(best)[:, None] * TIE_BAND).sum(axis=1)
+        print("band sizes > 1:", sorted(band[band > 1].tolist())[-20:], "zero-best:", int((best == 0).sum()),
+              file=sys.stderr)
