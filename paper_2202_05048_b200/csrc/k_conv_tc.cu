@@ -412,6 +412,11 @@ __global__ void __launch_bounds__(TC_THREADS, 1) k_conv_tc(const __grid_constant
             const int kk = ki * 8, tap = kk / cpc, c0 = (kk - tap * cpc) * 16;
             mbar_arrive_expect_tx(&full[s], TC_A_STAGE);
             tma_load_2d(dst, &a.tmA, c0, p0 + (tap / a.k) * Wp + tap % a.k, &full[s]);
+          } else if (a.tma_a == 66) {                // s2d stem, 64-byte window rows: two kh
+            const int t0 = 2 * ki, t1 = 2 * ki + 1;  // rows of 4 kw taps per stage
+            mbar_arrive_expect_tx(&full[s], t1 < a.k ? TC_A_STAGE : TC_A_STAGE / 2);
+            tma_load_2d(dst, &a.tmA, 0, p0 + t0 * Wp, &full[s]);
+            if (t1 < a.k) tma_load_2d(dst + TC_A_STAGE / 2, &a.tmA, 0, p0 + t1 * Wp, &full[s]);
           } else if (a.tma_a == 64) {                // Cp == 64: two taps per stage
             const int t0 = 2 * ki, t1 = 2 * ki + 1;
             mbar_arrive_expect_tx(&full[s], t1 < taps ? TC_A_STAGE : TC_A_STAGE / 2);
@@ -737,6 +742,24 @@ static bool setup_tma_a(ConvTcArgs& a) {
   EncodeTiledFn fn = encode_tiled();
   if (!fn) return false;
   if (Cp == 16 && a.k == 4 && a.OH <= Hp - 3 && a.OW <= Wp - 3) {
+    // preferred: overlapping 64-byte rows (4 consecutive 16-byte pixels) as a 2-D map with a
+    // 16-byte row stride, loaded as SWIZZLE_64B boxes like the Cp == 64 path
+    {
+      cuuint64_t gdim[2] = {64, (cuuint64_t)a.in.N * Hp * Wp - 3};
+      cuuint64_t gstride[1] = {16};
+      cuuint32_t box[2] = {64, (cuuint32_t)TC_BM};
+      cuuint32_t es[2] = {1, 1};
+      if (fn(&a.tmA, CU_TENSOR_MAP_DATA_TYPE_UINT8, 2, (void*)a.in.p, gdim, gstride, box, es,
+             CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_64B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+             CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS) {
+        a.tma_a = 66;
+        a.OHr = a.OH;
+        a.OWr = a.OW;
+        a.OH = Hp;
+        a.OW = Wp;
+        return true;
+      }
+    }
     // s2d stem: dims {16 B, pixels, 4 kw taps} with strides {16, 16} (the tap dimension
     // overlaps the pixel one): a box {16, 128, 4} lands as [tap][row][16 B], the no-swizzle
     // K-major layout of 4 K chunks, i.e. one kh row of taps for 128 GEMM rows
