@@ -338,13 +338,14 @@ __global__ void __launch_bounds__(TC_THREADS, 1) k_conv_tc(const __grid_constant
   // swizzled TMA tiles need 1024-byte aligned stages (the launcher reserves the slack)
   uint8_t* smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
   uint8_t* sA = smem;
-  uint8_t* sB = smem + NS * TC_A_STAGE;
-  uint64_t* full = reinterpret_cast<uint64_t*>(sB + NS * BN * 128);
+  uint8_t* sB = smem + NS * TC_A_STAGE;             // B ring [NS][BN][128], or resident [n_kiter][BN][128]
+  uint64_t* full = reinterpret_cast<uint64_t*>(sB + (a.b_res ? a.n_kiter : NS) * BN * 128);
   uint64_t* empty = full + NS;
   uint64_t* tfull = empty + NS;
   uint64_t* tempty = tfull + 2;
   uint64_t* rsfull = tempty + 2;                                 // row sums of tile buffer ready
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 4);
+  uint64_t* bfull = tempty + 4;                                  // resident B landed
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 5);
   int* rsum = reinterpret_cast<int*>(tempty + 6);                // [2][128] A-row sums (tma_rowsum)
   EpiParam* sparam = reinterpret_cast<EpiParam*>(rsum + 2 * TC_BM);   // [Cout] (no fused add)
   int8_t* stab = reinterpret_cast<int8_t*>(rsum + 2 * TC_BM);          // fused-add table
@@ -357,9 +358,10 @@ __global__ void __launch_bounds__(TC_THREADS, 1) k_conv_tc(const __grid_constant
 
   if (threadIdx.x == 0) {
     for (int s = 0; s < NS; ++s) {
-      mbar_init(&full[s], a.tma_a ? 2 : 64 + 1);
+      mbar_init(&full[s], (a.tma_a ? 1 : 64) + (a.b_res ? 0 : 1));
       mbar_init(&empty[s], a.tma_rowsum ? 2 : 1);
     }
+    mbar_init(bfull, 1);
     for (int b = 0; b < 2; ++b) {
       mbar_init(&rsfull[b], 1);
       mbar_init(&tfull[b], 1);
@@ -523,7 +525,11 @@ __global__ void __launch_bounds__(TC_THREADS, 1) k_conv_tc(const __grid_constant
     }
   } else if (warp == 2) {
     // ------------------------------------------------ B producer (bulk copies of pre-tiled weights)
-    if (lane == 0) {
+    if (lane == 0 && a.b_res) {                     // one n-tile: load every K stage once
+      mbar_arrive_expect_tx(bfull, (uint32_t)(a.n_kiter * BN * 128));
+      for (int ki = 0; ki < a.n_kiter; ++ki)
+        bulk_g2s(sB + ki * BN * 128, a.wB + (int64_t)ki * BN * 128, BN * 128, bfull);
+    } else if (lane == 0) {
       int s = 0;
       uint32_t ph = 0;
       for (int tile = blockIdx.x; tile < n_tiles; tile += gridDim.x) {
@@ -541,6 +547,7 @@ __global__ void __launch_bounds__(TC_THREADS, 1) k_conv_tc(const __grid_constant
     // ------------------------------------------------ MMA issuer
     if (lane == 0) {
       const uint32_t idesc = idesc_i8<BN>();
+      if (a.b_res) mbar_wait(bfull, 0);
       int s = 0;
       uint32_t ph = 0, lt = 0;
       for (int tile = blockIdx.x; tile < n_tiles; tile += gridDim.x, ++lt) {
@@ -552,7 +559,8 @@ __global__ void __launch_bounds__(TC_THREADS, 1) k_conv_tc(const __grid_constant
           mbar_wait(&full[s], ph);
           tc_fence_after();
           fence_proxy_async();
-          const uint32_t a0 = smem_u32(sA + s * TC_A_STAGE), b0 = smem_u32(sB + s * BN * 128);
+          const uint32_t a0 = smem_u32(sA + s * TC_A_STAGE),
+                         b0 = smem_u32(sB + (a.b_res ? ki : s) * BN * 128);
 #pragma unroll
           for (int ks = 0; ks < 4; ++ks) {
             const uint64_t ad =
@@ -680,14 +688,19 @@ template <int BN>
 static void launch_bn(const ConvTcArgs& a, cudaStream_t s) {
   // fixed part: barriers, TMEM slot, per-channel constants, optional add table; the rest
   // of the 227 KB goes to pipeline stages (deeper for narrow tiles, at least 2)
+  const int n_nt = (a.L.cout + BN - 1) / BN;
+  const size_t b_bytes = (size_t)a.n_kiter * BN * 128;
+  const int b_res = n_nt == 1 && b_bytes <= 64 * 1024;
   const size_t fixed = 1024 + (2 * TC_MAX_STAGES + 8) * 8 + 2 * TC_BM * 4 + 16 +
-                       (a.addtab ? PTQ_ADDTAB_BYTES : (size_t)a.L.cout * sizeof(EpiParam));
-  const size_t per_stage = (size_t)TC_A_STAGE + (size_t)BN * 128;
+                       (a.addtab ? PTQ_ADDTAB_BYTES : (size_t)a.L.cout * sizeof(EpiParam)) +
+                       (b_res ? b_bytes : 0);
+  const size_t per_stage = (size_t)TC_A_STAGE + (b_res ? 0 : (size_t)BN * 128);
   int ns = (int)((TC_SMEM_MAX - fixed) / per_stage);
   if (ns > TC_MAX_STAGES) ns = TC_MAX_STAGES;
   if (ns < 2) ns = 2;                // does not fit: the launch fails loudly (check_launch)
   ConvTcArgs b = a;
   b.n_stages = ns;
+  b.b_res = b_res;
   // cout <= TC_MAX_COUT is checked when the graph is imported (conv_tc_max_cout)
   if (a.addtab)
     cudaMemcpyToSymbolAsync(c_ep, a.L.ep, (size_t)a.L.cout * sizeof(EpiParam), 0, cudaMemcpyDeviceToDevice, s);

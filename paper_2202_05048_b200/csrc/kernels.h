@@ -193,6 +193,8 @@ struct ConvTcArgs {
   int ablate;             // profiling only: 1 = skip epilogue math, 2 = skip A gathers
   const int8_t* addtab;   // fused add lookup table (LayerSt::addtab) or nullptr
   int n_stages;           // smem pipeline depth (set by the launcher)
+  int b_res;              // set by the launcher: the whole B operand (one n-tile) stays resident
+                          // in shared memory instead of streaming with every tile
 };
 int conv_tc_bn_for(int cout);     // BN tile width the kernel uses for this Cout
 int conv_tc_max_cout();           // largest Cout the tensor-core conv supports
