@@ -61,12 +61,13 @@ __device__ __forceinline__ uint64_t umma_desc(uint32_t saddr, uint32_t lbo, uint
 
 // K-major swizzled layout (TMA-written A): rows of 64 / 128 bytes in 8-row atoms of
 // 512 / 1024 bytes (SBO), LBO unused (1), layout type 4 (SWIZZLE_64B) / 2 (SWIZZLE_128B)
-__device__ __forceinline__ uint64_t umma_desc_sw(uint32_t saddr, int swz) {
+__device__ __forceinline__ uint64_t umma_desc_sw(uint32_t saddr, int swz, uint32_t base_off = 0) {
   uint64_t d = 0;
   d |= (uint64_t)((saddr >> 4) & 0x3FFFu);
   d |= (uint64_t)1 << 16;
   d |= (uint64_t)(((uint32_t)(swz * 8) >> 4) & 0x3FFFu) << 32;
   d |= (uint64_t)1 << 46;
+  d |= (uint64_t)(base_off & 7u) << 49;                // matrix base offset (swizzle phase)
   d |= (uint64_t)(swz == 128 ? 2u : 4u) << 61;
   return d;
 }
@@ -407,7 +408,7 @@ __global__ void __launch_bounds__(TC_THREADS, 1) k_conv_tc(const __grid_constant
             p += run;
           }
         }
-        for (int ki = 0; ki < a.n_kiter; ++ki) {
+        for (int ki = 0; ki < a.a_iters; ++ki) {
           mbar_wait(&empty[s], ph ^ 1u);
           uint8_t* dst = sA + s * TC_A_STAGE;
           if (a.tma_a == 128) {                      // one tap, 128 channels per stage
@@ -419,6 +420,9 @@ __global__ void __launch_bounds__(TC_THREADS, 1) k_conv_tc(const __grid_constant
             mbar_arrive_expect_tx(&full[s], t1 < a.k ? TC_A_STAGE : TC_A_STAGE / 2);
             tma_load_2d(dst, &a.tmA, 0, p0 + t0 * Wp, &full[s]);
             if (t1 < a.k) tma_load_2d(dst + TC_A_STAGE / 2, &a.tmA, 0, p0 + t1 * Wp, &full[s]);
+          } else if (a.kwr) {                        // one 136-row slab per kh (all 3 kw taps)
+            mbar_arrive_expect_tx(&full[s], (TC_BM + 8) * 64);
+            tma_load_2d(dst, &a.tmA, 0, p0 + ki * Wp, &full[s]);
           } else if (a.tma_a == 64) {                // Cp == 64: two taps per stage
             const int t0 = 2 * ki, t1 = 2 * ki + 1;
             mbar_arrive_expect_tx(&full[s], t1 < taps ? TC_A_STAGE : TC_A_STAGE / 2);
@@ -555,12 +559,29 @@ __global__ void __launch_bounds__(TC_THREADS, 1) k_conv_tc(const __grid_constant
         mbar_wait(&tempty[buf], uph ^ 1u);           // epilogue drained this accumulator
         tc_fence_after();
         const uint32_t d = tmem + buf * BN;
-        for (int ki = 0; ki < a.n_kiter; ++ki) {
+        for (int ki = 0; ki < a.a_iters; ++ki) {
           mbar_wait(&full[s], ph);
           tc_fence_after();
           fence_proxy_async();
           const uint32_t a0 = smem_u32(sA + s * TC_A_STAGE),
                          b0 = smem_u32(sB + (a.b_res ? ki : s) * BN * 128);
+          if (a.kwr) {
+            // slab = input rows p0 + ki*Wp + [0, 136); tap (ki, kw) = the slab shifted by kw
+            // rows; B (resident, chunk-major) chunk index = ki*12 + kw*4 + 2*ks2
+            const uint32_t bb = smem_u32(sB);
+#pragma unroll
+            for (int kw = 0; kw < 3; ++kw)
+#pragma unroll
+              for (int ks2 = 0; ks2 < 2; ++ks2) {
+                const uint32_t st = a0 + kw * 64 + ks2 * 32;
+                const uint64_t ad = umma_desc_sw(st, 64, a.kwr_bo == 1 ? ((st >> 7) & 7u) : a.kwr_bo == 2 ? ((st >> 6) & 7u) : 0u);
+                const uint64_t bd = umma_desc(bb + (uint32_t)((ki * 12 + kw * 4 + ks2 * 2) * BN * 16), BN * 16, 128);
+                mma_i8(d, ad, bd, idesc, (ki | kw | ks2) != 0);
+              }
+            mma_commit(&empty[s]);
+            if (++s == NS) { s = 0; ph ^= 1u; }
+            continue;
+          }
 #pragma unroll
           for (int ks = 0; ks < 4; ++ks) {
             const uint64_t ad =
@@ -683,6 +704,8 @@ int conv_tc_bn_for(int cout) {
 }
 
 static int g_num_sms = 0;
+static int g_kwr_mode = 0;   // -1 disables the kw-reuse slabs; 0/1/2 = descriptor base-offset convention
+void conv_tc_set_kwr_mode(int m) { g_kwr_mode = m; }
 
 template <int BN>
 static void launch_bn(const ConvTcArgs& a, cudaStream_t s) {
@@ -810,17 +833,41 @@ static bool setup_tma_a(ConvTcArgs& a) {
   return true;
 }
 
-bool conv_tc_tma_rowsum(const ConvTcArgs& a0) {
-  ConvTcArgs t = a0;
+// A-operand mode of one launch: TMA map (setup_tma_a), kw-reuse slabs, in-kernel row sums
+static void plan_launch(ConvTcArgs& t, int bn) {
   t.tma_a = 0;
-  return setup_tma_a(t) && t.has_wzp && !t.Rpix && (t.tma_a == 64 || t.tma_a == 128);
+  setup_tma_a(t);
+  t.kwr = 0;
+  t.a_iters = t.n_kiter;
+  if (t.tma_a == 64 && t.k == 3 && bn == 64 && t.L.cout <= 64 && g_kwr_mode >= 0 &&
+      (size_t)t.n_kiter * 64 * 128 <= 64 * 1024) {    // needs the resident B of launch_bn
+    // re-encode A with 136-row boxes: one slab per kh row of taps
+    const int Hp = t.in.H + 2 * t.in.halo, Wp = t.in.W + 2 * t.in.halo;
+    cuuint64_t gdim[2] = {64, (cuuint64_t)t.in.N * Hp * Wp};
+    cuuint64_t gstride[1] = {64};
+    cuuint32_t box[2] = {64, (cuuint32_t)(TC_BM + 8)};
+    cuuint32_t es[2] = {1, 1};
+    EncodeTiledFn fn = encode_tiled();
+    if (fn && fn(&t.tmA, CU_TENSOR_MAP_DATA_TYPE_UINT8, 2, (void*)t.in.p, gdim, gstride, box, es,
+                 CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_64B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                 CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS) {
+      t.kwr = 1;
+      t.kwr_bo = g_kwr_mode;
+      t.a_iters = 3;                                 // A stages per tile = kh rows
+    }
+  }
+  t.tma_rowsum = t.has_wzp && !t.Rpix && (t.tma_a == 64 || t.tma_a == 128) && !t.kwr;
+}
+
+bool conv_tc_tma_rowsum(const ConvTcArgs& a0, int bn) {
+  ConvTcArgs t = a0;
+  plan_launch(t, bn);
+  return t.tma_rowsum != 0;
 }
 
 void launch_conv_tc(const ConvTcArgs& a0, int bn, cudaStream_t s) {
   ConvTcArgs t = a0;
-  t.tma_a = 0;
-  setup_tma_a(t);
-  t.tma_rowsum = t.has_wzp && !t.Rpix && (t.tma_a == 64 || t.tma_a == 128);
+  plan_launch(t, bn);
   const ConvTcArgs a = with_divs(t, bn);
   switch (bn) {
     case 16: launch_bn<16>(a, s); break;

@@ -195,12 +195,17 @@ struct ConvTcArgs {
   int n_stages;           // smem pipeline depth (set by the launcher)
   int b_res;              // set by the launcher: the whole B operand (one n-tile) stays resident
                           // in shared memory instead of streaming with every tile
+  int kwr;                // set by the launcher: 3x3 Cp=64 TMA conv loads one 136-row slab per kh
+                          // and feeds its 3 kw taps as row-shifted descriptors (A bytes / 3)
+  int kwr_bo;             // descriptor base-offset convention for the row-shifted slabs
+  int a_iters;            // A pipeline stages per tile (n_kiter, or 3 kh slabs with kwr)
 };
 int conv_tc_bn_for(int cout);     // BN tile width the kernel uses for this Cout
 int conv_tc_max_cout();           // largest Cout the tensor-core conv supports
 void launch_conv_tc(const ConvTcArgs& a, int bn, cudaStream_t s);
 // true when launch_conv_tc will load A with TMA and (with has_wzp) sum the rows itself
-bool conv_tc_tma_rowsum(const ConvTcArgs& a);
+bool conv_tc_tma_rowsum(const ConvTcArgs& a, int bn);
+void conv_tc_set_kwr_mode(int m);   // -1: no kw-reuse slabs (A/B testing)
 // CUDA-core reference of the same contract (tests / cross-checks only)
 void launch_conv_i8_ref(const ConvTcArgs& a, int bn, cudaStream_t s);
 

@@ -894,7 +894,7 @@ void eval_one(ptq_ctx* c, const ptq_config& cfg, unsigned long long* d_correct, 
           a.addtab = L.addtab;
           a.ablate = c->ablate;
           a.allow_tma = c->tma;
-          if (a.has_wzp && !a.Rpix && (c->conv_ref || !conv_tc_tma_rowsum(a))) {
+          if (a.has_wzp && !a.Rpix && (c->conv_ref || !conv_tc_tma_rowsum(a, wd.bn))) {
             launch_pixsum(vin, c->d_P, c->st);       // gather-mode convs sum input pixels first
             check_launch(c);
             a.P = c->d_P;
@@ -1304,6 +1304,7 @@ int ptq_set_option(ptq_ctx* c, const char* key, int64_t value) {
     if (k == "conv_ref") c->conv_ref = (int)value;
     else if (k == "ablate") c->ablate = (int)value;
     else if (k == "tma") c->tma = (int)value;
+    else if (k == "kwr") conv_tc_set_kwr_mode((int)value);
     else if (k == "time_conv") c->time_conv = (int)value;
     else if (k == "reset_stats") c->launches = 0;
     else if (k == "fusion") {
