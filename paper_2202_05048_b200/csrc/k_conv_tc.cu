@@ -280,14 +280,27 @@ __device__ __forceinline__ void epi_tiles(const ConvTcArgs& a, const LayerRt& rt
   const int Cout = a.L.cout;
   const bool has_skip = GENERIC ? a.skip.p != nullptr : SKIP;
   uint32_t lt = 0;
-  for (int tile = blockIdx.x; tile < e.n_tiles; tile += gridDim.x, ++lt) {
+  int rot = 0;                                       // lt % 3
+  for (int tile = blockIdx.x; tile < e.n_tiles; tile += gridDim.x, ++lt, rot = rot == 2 ? 0 : rot + 1) {
     const uint32_t buf = lt & 1u, uph = (lt >> 1) & 1u;
     const int mt = (int)a.div_nt.div((uint32_t)tile);
     const int nt = tile - mt * e.n_nt;
     // chunks c = first, first+3, ...: the assignment rotates with the tile so the three
     // column groups share BN/16 chunks evenly over consecutive tiles
-    const int first = (int)(((uint32_t)e.grp + 3u - lt % 3u) % 3u);
-    const RowGeo g = row_geo(a, mt * TC_BM + e.row, e.M);
+    const int first = e.grp >= rot ? e.grp - rot : e.grp - rot + 3;
+    const int m = mt * TC_BM + e.row;
+    RowGeo g;
+    int8_t* orow;
+    const int8_t* srow;
+    if (a.flat) {                                    // row m == flat output pixel m
+      g.ok = m < e.M;
+      orow = g.ok ? a.out.p + (int64_t)m * a.out.Cp : nullptr;
+      srow = (g.ok && has_skip) ? a.skip.p + (int64_t)m * a.skip.Cp : nullptr;
+    } else {
+      g = row_geo(a, m, e.M);
+      orow = g.ok ? a.out.p + vpix(a.out, g.n, g.oh, g.ow) * a.out.Cp : nullptr;
+      srow = (g.ok && has_skip) ? a.skip.p + vpix(a.skip, g.n, g.oh, g.ow) * a.skip.Cp : nullptr;
+    }
     long long rowsum = 0;
     if ((GENERIC || WZP) && a.tma_rowsum) {
       mbar_wait(&e.rsfull[buf], uph);
@@ -296,8 +309,6 @@ __device__ __forceinline__ void epi_tiles(const ConvTcArgs& a, const LayerRt& rt
       rowsum = a.Rpix ? (long long)a.Rpix[((int64_t)g.n * a.OHr + g.oh) * a.OWr + g.ow]
                       : pixel_rowsum(a, g.n, g.ih0, g.iw0);
     }
-    int8_t* orow = g.ok ? a.out.p + vpix(a.out, g.n, g.oh, g.ow) * a.out.Cp : nullptr;
-    const int8_t* srow = (g.ok && has_skip) ? a.skip.p + vpix(a.skip, g.n, g.oh, g.ow) * a.skip.Cp : nullptr;
     // the residual operand does not depend on the accumulator: fetch it before the wait
     // and one chunk ahead inside the loop
     const int cb0 = nt * BN + first * 16;
@@ -857,6 +868,10 @@ static void plan_launch(ConvTcArgs& t, int bn) {
     }
   }
   t.tma_rowsum = t.has_wzp && !t.Rpix && (t.tma_a == 64 || t.tma_a == 128) && !t.kwr;
+  // flat rows: halo-free input and output, no padded-grid rows, halo-free add operand, and
+  // row sums (when needed) taken in-kernel
+  t.flat = (t.tma_a == 64 || t.tma_a == 128) && t.in.halo == 0 && t.out.halo == 0 && t.OH == t.OHr &&
+           t.OW == t.OWr && (!t.skip.p || t.skip.halo == 0) && (!t.has_wzp || t.tma_rowsum);
 }
 
 bool conv_tc_tma_rowsum(const ConvTcArgs& a0, int bn) {

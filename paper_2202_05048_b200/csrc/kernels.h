@@ -199,6 +199,8 @@ struct ConvTcArgs {
                           // and feeds its 3 kw taps as row-shifted descriptors (A bytes / 3)
   int kwr_bo;             // descriptor base-offset convention for the row-shifted slabs
   int a_iters;            // A pipeline stages per tile (n_kiter, or 3 kh slabs with kwr)
+  int flat;               // set by the launcher: GEMM row m is flat pixel m of the output (and of
+                          // the add operand) -- halo-free TMA-mode layers skip the row geometry
 };
 int conv_tc_bn_for(int cout);     // BN tile width the kernel uses for this Cout
 int conv_tc_max_cout();           // largest Cout the tensor-core conv supports
