@@ -65,6 +65,32 @@ __device__ __forceinline__ int quant1_fast(float x, double r, double s64, double
   return quant1(x, s64, zp64);
 }
 
+// quant1 on the fp32 pipe with an exactness guard: t32 = fma(x, fl32(1/s), zp) is within
+// 2^-23 (2|t| + |zp|) of the reference's fl(fl(x/s) + zp).  When t32 is farther than that
+// from a half-integer, RHA of the reference value equals round-to-nearest of t32 (the
+// half-way tie rule never applies), and saturation follows from the clamp.  Otherwise
+// (rare) the exact fp64 path.  Returns the unclamped code (callers saturate).
+__device__ __forceinline__ int quant1_f32g_raw(float x, float r32, float zf, double r64, double s64, double z64) {
+  const float t = __fmaf_rn(x, r32, zf);
+  const float r = rintf(t);
+  const float lim = __fmaf_rn(-3.0e-7f, fabsf(t), 0.4999f);   // 0.5 - margin
+  if (fabsf(__fsub_rn(t, r)) < lim) return (int)r;           // exact conversion (|r| < 2^24)
+  if (fabsf(t) > 300.0f) return t > 0.0f ? PTQ_QMAX : PTQ_QMIN;
+  return quant1_fast(x, r64, s64, z64);
+}
+__device__ __forceinline__ int quant1_f32g(float x, float r32, float zf, double r64, double s64, double z64) {
+  const int q = quant1_f32g_raw(x, r32, zf, r64, s64, z64);
+  return q < PTQ_QMIN ? PTQ_QMIN : (q > PTQ_QMAX ? PTQ_QMAX : q);
+}
+
+// 4 int32 -> 4 saturated int8 codes in one word (byte j = x_j)
+__device__ __forceinline__ uint32_t pack4_sat(int x0, int x1, int x2, int x3) {
+  uint32_t hi, out;
+  asm("cvt.pack.sat.s8.s32.b32 %0, %1, %2, 0;" : "=r"(hi) : "r"(x3), "r"(x2));
+  asm("cvt.pack.sat.s8.s32.b32 %0, %1, %2, %3;" : "=r"(out) : "r"(x1), "r"(x0), "r"(hi));
+  return out;
+}
+
 // requantize an int32-clipped accumulator: clip(RHU(acc * m) + zp)   (ref intexec.py:72-85)
 __device__ __forceinline__ int requant1(long long acc, double m, int zp) {
   return clip8(rhu(__dmul_rn((double)acc, m)) + (double)zp);

@@ -146,13 +146,6 @@ __device__ __forceinline__ int requant_raw(uint32_t accb, double m, const LayerR
   const double r = __dadd_rn(__dmul_rn(b2d(accb), m), 0.5);
   return __double2loint(__dadd_rd(r, rt.mg_zy));
 }
-// 4 int32 -> 4 saturated int8 codes in one word (byte j = x_j)
-__device__ __forceinline__ uint32_t pack4_sat(int x0, int x1, int x2, int x3) {
-  uint32_t hi, out;
-  asm("cvt.pack.sat.s8.s32.b32 %0, %1, %2, 0;" : "=r"(hi) : "r"(x3), "r"(x2));
-  asm("cvt.pack.sat.s8.s32.b32 %0, %1, %2, %3;" : "=r"(out) : "r"(x1), "r"(x0), "r"(hi));
-  return out;
-}
 // 16 output channels of one row, fast path (no int32 saturation possible).  Without a fused
 // add the clip to [-128, 127] is the saturating pack (a fused relu adds one max).  A fused
 // residual add is one shared-memory lookup: stab[skip byte * 260 + conv code] with stab

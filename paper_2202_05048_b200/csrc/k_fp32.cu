@@ -218,6 +218,22 @@ __global__ void __launch_bounds__(256, 2) k_conv_f32_rb(const float* __restrict_
   }
 }
 
+// fully-connected layers with few outputs (the classifier): one warp per output element,
+// lanes stride over K (the generic tiled kernel would run a handful of CTAs over K)
+__global__ void k_fc_f32_small(const float* __restrict__ x, int64_t rows, int K, const float* __restrict__ Bw,
+                               const float* __restrict__ bias, int Cout, float* __restrict__ y) {
+  const int64_t wid = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
+  const int lane = threadIdx.x & 31;
+  if (wid >= rows * Cout) return;
+  const int64_t r = wid / Cout;
+  const int co = (int)(wid - r * Cout);
+  const float* xr = x + r * K;
+  float acc = 0.f;
+  for (int kk = lane; kk < K; kk += 32) acc = fmaf(__ldg(xr + kk), __ldg(Bw + (int64_t)kk * Cout + co), acc);
+  for (int d = 16; d; d >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, d);
+  if (lane == 0) y[wid] = acc + (bias ? __ldg(bias + co) : 0.f);
+}
+
 // depthwise conv: w is [C][k*k]
 __global__ void k_dwconv_f32(const float* __restrict__ x, int N, int H, int W, int C,
                              const float* __restrict__ w, const float* __restrict__ bias, int k,
@@ -337,6 +353,11 @@ void launch_conv_f32(const float* x, int N, int H, int W, int Cin, const float* 
                      const float* bias, int Cout, int k, int stride, int pad, int OH, int OW,
                      float* y, cudaStream_t s) {
   int64_t M = (int64_t)N * OH * OW;
+  if (k == 1 && H == 1 && W == 1 && OH == 1 && OW == 1 && Cout < 64) {
+    const int64_t warps = M * Cout;
+    k_fc_f32_small<<<(unsigned)((warps * 32 + 255) / 256), 256, 0, s>>>(x, M, Cin, Bw, bias, Cout, y);
+    return;
+  }
   if (Cin % 8 == 0 && Cout % 64 == 0) {              // register-blocked path (float4 operands)
     if (Cout % 128 == 0) {
       dim3 g((unsigned)((M + 127) / 128), (unsigned)(Cout / 128));

@@ -433,6 +433,7 @@ __global__ void k_quant_input_s2d(const float* __restrict__ imgs, int64_t img0, 
                                   const float* __restrict__ as, const int* __restrict__ az, int hist) {
   const double s = (double)as[hist], z = (double)az[hist];
   const double rs = __ddiv_rn(1.0, s);
+  const float rs32 = (float)rs, zf = (float)z;
   const int n = blockIdx.x / out.H, R = blockIdx.x - (blockIdx.x / out.H) * out.H;
   const int W0 = 2 * out.W;
   const int64_t plane = (int64_t)(2 * out.H) * W0;
@@ -444,8 +445,8 @@ __global__ void k_quant_input_s2d(const float* __restrict__ imgs, int64_t img0, 
         const float2 v = __ldg(reinterpret_cast<const float2*>(imgs + (img0 + n) * C0 * plane + (int64_t)c * plane +
                                                                (int64_t)(2 * R + a) * W0 + 2 * Q));
         const int j0 = (2 * a) * C0 + c, j1 = (2 * a + 1) * C0 + c;
-        pk[j0 >> 2] |= ((uint32_t)quant1_fast(v.x, rs, s, z) & 0xffu) << (8 * (j0 & 3));
-        pk[j1 >> 2] |= ((uint32_t)quant1_fast(v.y, rs, s, z) & 0xffu) << (8 * (j1 & 3));
+        pk[j0 >> 2] |= ((uint32_t)quant1_f32g(v.x, rs32, zf, rs, s, z) & 0xffu) << (8 * (j0 & 3));
+        pk[j1 >> 2] |= ((uint32_t)quant1_f32g(v.y, rs32, zf, rs, s, z) & 0xffu) << (8 * (j1 & 3));
       }
     *reinterpret_cast<int4*>(out.p + voff(out, n, R, Q)) = make_int4((int)pk[0], (int)pk[1], (int)pk[2], (int)pk[3]);
   }
@@ -529,8 +530,37 @@ __global__ void k_quant_nhwc(const float* __restrict__ x, View out, const float*
     *reinterpret_cast<int4*>(out.p + voff(out, n, h, w) + c0) = make_int4((int)pk[0], (int)pk[1], (int)pk[2], (int)pk[3]);
   }
 }
+// vectorised form for C % 4 == 0: one float4 -> 4 codes per thread, consecutive threads on
+// consecutive channel quads (coalesced 16-byte loads, 4-byte stores); pad channels of the
+// view are written 0 by the C..Cp tail threads
+__global__ void k_quant_nhwc4(const float* __restrict__ x, View out, const float* __restrict__ as,
+                              const int* __restrict__ az, int hist, int relu_hist) {
+  const double s = (double)as[hist], z = (double)az[hist];
+  const double rs = __ddiv_rn(1.0, s);
+  const float rs32 = (float)rs, zf = (float)z;
+  const int rz = relu_hist >= 0 ? az[relu_hist] : INT_MIN;
+  const int qp = out.Cp >> 2, qc = out.C >> 2;                // channel quads per pixel
+  const int n = blockIdx.x / out.H, h = blockIdx.x - n * out.H;   // one (image, row) per block
+  const float4* src = reinterpret_cast<const float4*>(x + ((int64_t)n * out.H + h) * out.W * out.C);
+  int8_t* dst = out.p + voff(out, n, h, 0);
+  const int per_row = out.W * qp;
+  for (int j = threadIdx.x; j < per_row; j += blockDim.x) {
+    const int w = j / qp, cq = j - w * qp;
+    uint32_t pk = 0u;
+    if (cq < qc) {
+      const float4 v = __ldg(src + w * qc + cq);
+      pk = pack4_sat(max(quant1_f32g_raw(v.x, rs32, zf, rs, s, z), rz), max(quant1_f32g_raw(v.y, rs32, zf, rs, s, z), rz),
+                     max(quant1_f32g_raw(v.z, rs32, zf, rs, s, z), rz), max(quant1_f32g_raw(v.w, rs32, zf, rs, s, z), rz));
+    }
+    *reinterpret_cast<uint32_t*>(dst + (int64_t)w * out.Cp + cq * 4) = pk;
+  }
+}
 void launch_quant_nhwc(const float* x, View out, const float* as, const int* az, int hist,
                        int relu_hist, cudaStream_t s) {
+  if ((out.C & 3) == 0) {
+    k_quant_nhwc4<<<out.N * out.H, 256, 0, s>>>(x, out, as, az, hist, relu_hist);
+    return;
+  }
   const int per_row = out.W * (out.Cp >> 4);
   dim3 g(out.N * out.H, (per_row + 127) / 128);
   k_quant_nhwc<<<g, 128, 0, s>>>(x, out, as, az, hist, relu_hist);
