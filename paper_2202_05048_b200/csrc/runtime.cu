@@ -157,6 +157,10 @@ struct ptq_ctx {
   std::vector<int> halo, cpad;
   std::vector<float*> d_f32;             // per tensor fp32 eval buffer (mixed tail)
   float* d_prefix = nullptr;             // mixed: fp32 output of the first compute node, all eval imgs
+  // mixed + first compute -> relu -> maxpool: maxpool(relu(prefix)) in fp32, config-invariant;
+  // quantization is monotone, so quantizing it equals max-pooling the relu'd codes
+  int pool_fold = -1;                    // the folded maxpool node, or -1
+  float* d_prefix_pool = nullptr;
   int* d_P = nullptr;                    // pixel sums scratch
   int8_t* d_im2col = nullptr;            // packed im2col scratch (few-channel convs)
   int64_t P_cap = 0;
@@ -754,6 +758,30 @@ void prepare(ptq_ctx* c) {
     }
     for (int t : need)
       if (t != tout) c->dfree(bufs[t]);
+    // fold relu + maxpool into the prefix (see pool_fold)
+    c->pool_fold = -1;
+    const TensorI& t1 = c->tens[tout];
+    if (t1.consumers.size() == 1 && c->nodes[t1.consumers[0]].kind == PTQ_RELU) {
+      const NodeI& r = c->nodes[t1.consumers[0]];
+      const TensorI& t2 = c->tens[r.out];
+      if (t2.consumers.size() == 1 && c->nodes[t2.consumers[0]].kind == PTQ_MAXPOOL) {
+        const int pi = t2.consumers[0];
+        const NodeI& pn = c->nodes[pi];
+        const TensorI& tp = c->tens[pn.out];
+        if (!c->d_prefix_pool) c->d_prefix_pool = c->dalloc<float>((size_t)c->n_eval * tp.elems);
+        for (int64_t s0 = 0; s0 < c->n_eval; s0 += pc) {
+          const int nn = (int)std::min<int64_t>(pc, c->n_eval - s0);
+          launch_pool_f32(c->d_prefix + s0 * t1.elems, nn, t1.h, t1.w, t1.c, pn.k, pn.stride, tp.h, tp.w, 0,
+                          c->d_prefix_pool + s0 * tp.elems, c->st);
+          check_launch(c);
+        }
+        // relu after the max (both monotone: relu(max x) == max relu(x)); d_prefix stays
+        // intact for probes of the unfolded tensors
+        launch_relu_f32(c->d_prefix_pool, c->d_prefix_pool, (int64_t)c->n_eval * tp.elems, c->st);
+        check_launch(c);
+        c->pool_fold = pi;
+      }
+    }
   }
   CK(cudaStreamSynchronize(c->st));
   c->prepared = true;
@@ -831,12 +859,24 @@ void eval_one(ptq_ctx* c, const ptq_config& cfg, unsigned long long* d_correct, 
     } else {
       const int fc_ = c->first_compute;
       const int mt = P.mat[fc_];
-      launch_quant_nhwc(c->d_prefix + img0 * c->tens[c->nodes[fc_].out].elems, V(mt), as, az,
-                        P.psrc[c->nodes[fc_].out], P.relu_hist[fc_], c->st);
-      check_launch(c);
-      halo_fill(mt);
-      probe(mt);
-      start = fc_ + 1;
+      const int pf = c->pool_fold;
+      if (pf >= 0 && P.psrc[c->nodes[pf].out] == P.psrc[c->nodes[fc_].out] && probe_t < 0) {
+        // quantize maxpool(relu(prefix)) straight into the maxpool's output codes
+        const int tp = c->nodes[pf].out;
+        launch_quant_nhwc(c->d_prefix_pool + img0 * c->tens[tp].elems, V(tp), as, az,
+                          P.psrc[c->nodes[fc_].out], -1, c->st);
+        check_launch(c);
+        halo_fill(tp);
+        probe(tp);
+        start = pf + 1;
+      } else {
+        launch_quant_nhwc(c->d_prefix + img0 * c->tens[c->nodes[fc_].out].elems, V(mt), as, az,
+                          P.psrc[c->nodes[fc_].out], P.relu_hist[fc_], c->st);
+        check_launch(c);
+        halo_fill(mt);
+        probe(mt);
+        start = fc_ + 1;
+      }
     }
     for (int i = start; i < N; ++i) {
       if (P.skip[i]) continue;
