@@ -94,3 +94,39 @@ def test_top1_matches_oracle(name, ds64):
         else:                                     # fp32 first/last layer: ulp-level drift allowed
             assert abs(int(c) - want) <= 1, (name, space[i])
     ev.close()
+
+
+def test_input_quantizer_at_rounding_boundaries():
+    """The s2d input quantizer runs on the fp32 pipe with an fp64 guard: eval images whose
+    values sit exactly on, and one fp32 ulp either side of, the reference's RHA rounding
+    points (x/s + zp = k + 0.5) must quantize exactly like quantize_array (schemes.py:145-150)."""
+    from paper_2202_05048_b200.dataset import Dataset
+    from paper_2202_05048_b200.evaluator import GpuEvaluator
+    base = make_dataset(n_calib=300, n_eval=12, seed=0, shape=SHAPE)
+    g = build_model("resnet50", seed=0, shape=SHAPE)
+    space = enumerate_space(GENERIC)
+    cfg = space[2]                                 # Asym / Max / Channel, Mixed=Off
+    ev = GpuEvaluator(g, base, 0, GENERIC)
+    caches = {sc: {t: O.Hist(t, float(ev.cache_ranges[k, i, 0]), float(ev.cache_ranges[k, i, 1]),
+                             ev.cache_counts[k, i], int(ev.cache_nsamp[k, i]))
+                   for i, t in enumerate(ev.lowered.tensor_names)}
+              for k, sc in enumerate(("S1", "S2", "S3"))}
+    ev.close()
+    qp = O.quantize_model(g, caches[cfg.cache], cfg).act["input"]
+    s, z = float(qp.scale), float(qp.zp)
+    rng = np.random.default_rng(1)
+    n_img = 12
+    k = rng.integers(-140, 140, size=(n_img,) + SHAPE)
+    x = ((k + 0.5 - z) * s).astype(np.float32)     # on (or next to) the rounding points
+    step = rng.integers(-1, 2, size=x.shape)
+    x = np.where(step > 0, np.nextafter(x, np.float32(np.inf)),
+                 np.where(step < 0, np.nextafter(x, np.float32(-np.inf)), x)).astype(np.float32)
+    imgs = np.concatenate([base.images[:base.n_calib], x]).astype(np.float32)
+    d = Dataset(images=imgs, labels=np.concatenate([base.labels[:base.n_calib], base.labels[:n_img]]),
+                n_calib=base.n_calib)
+    ev = GpuEvaluator(g, d, 0, GENERIC)
+    ev.set_option("fusion", 0)
+    got = ev.probe_codes(cfg, "input").reshape(x.shape)
+    want = O.quantize_array(x, qp).astype(np.int8)
+    assert np.array_equal(got, want)
+    ev.close()
