@@ -397,21 +397,6 @@ __global__ void __launch_bounds__(TC_THREADS, 1) k_conv_tc(const __grid_constant
       uint32_t ph = 0;
       for (int tile = blockIdx.x; tile < n_tiles; tile += gridDim.x) {
         const int p0 = (int)a.div_nt.div((uint32_t)tile) * TC_BM;
-        if (a.skip.p) {
-          // the fused add's operand pixels of this tile (runs along image rows) into L2, paced
-          // by the A pipeline so they arrive a few tiles before the epilogue reads them
-          for (int p = p0; p < p0 + TC_BM && p < M;) {
-            const uint32_t t = a.div_ow.div((uint32_t)p);
-            const int wp = p - (int)t * a.OW;
-            const uint32_t nn = a.div_oh.div(t);
-            const int hp = (int)t - (int)nn * a.OH;
-            const int run = min(a.OW - wp, p0 + TC_BM - p);
-            const int cnt = min(wp + run, a.OWr) - wp;
-            if (hp < a.OHr && cnt > 0)
-              bulk_prefetch_l2(a.skip.p + vpix(a.skip, (int)nn, hp, wp) * a.skip.Cp, (uint32_t)(cnt * a.skip.Cp));
-            p += run;
-          }
-        }
         for (int ki = 0; ki < a.a_iters; ++ki) {
           mbar_wait(&empty[s], ph ^ 1u);
           uint8_t* dst = sA + s * TC_A_STAGE;
