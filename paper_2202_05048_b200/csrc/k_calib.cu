@@ -116,6 +116,19 @@ __device__ __forceinline__ int np_bin_fast(double x, double lo, double hi, doubl
   return np_bin(x, lo, hi, denom);
 }
 
+// fp32 pre-filter: fe32 = fl32(fl32(x - lo) * fl32(2048 / (hi - lo))) is within 4e-4 bins
+// of the true position (three fp32 roundings on a value < 2048); when its fractional part
+// keeps a 1e-3 margin from both neighbouring integers the bin is settled on the fp32 pipe,
+// otherwise np_bin_fast decides in fp64.
+__device__ __forceinline__ int np_bin_f32g(float x, float lo32, float rc32, double lo, double hi, double denom,
+                                           double rc, double eps) {
+  const float fe = __fmul_rn(__fsub_rn(x, lo32), rc32);
+  const int k = (int)fe;
+  const float frac = __fsub_rn(fe, (float)k);
+  if (k < PTQ_NBINS && frac > 1.0e-3f && frac < 0.999f) return k;
+  return np_bin_fast((double)x, lo, hi, denom, rc, eps);
+}
+
 // x: [n_img_total][elems]; slots: image slots of this cache; range: lo, hi (fp32 values).
 // counts: [2048] int64 (accumulated).  Four shared sub-histograms (one per warp % 4) spread
 // the atomics; exact zeros (post-ReLU tensors pile up there) are counted in registers and
@@ -140,9 +153,10 @@ __global__ void __launch_bounds__(512) k_histogram(const float* __restrict__ x, 
   const int z0 = (lo <= 0.0 && 0.0 <= hi) ? np_bin(0.0, lo, hi, denom) : -1;
   unsigned int* my = sh + ((threadIdx.x >> 5) & 3) * PTQ_NBINS;
   unsigned int zc = 0;
+  const float lo32 = range[0], rc32 = (float)rc;
   auto put = [&](float v) {
     if (v == 0.0f && z0 >= 0) ++zc;
-    else atomicAdd(&my[np_bin_fast((double)v, lo, hi, denom, rc, eps)], 1u);
+    else atomicAdd(&my[np_bin_f32g(v, lo32, rc32, lo, hi, denom, rc, eps)], 1u);
   };
   const int64_t stride = (int64_t)gridDim.x * blockDim.x;
   // every per-image slice is 16-byte aligned (elems % 4 == 0) except for tiny tensors:
