@@ -77,29 +77,6 @@ __global__ void k_init_minmax(unsigned int* p, int n) {
   int i = blockIdx.x * blockDim.x + threadIdx.x;
   if (i < n) { p[2 * i] = 0xffffffffu; p[2 * i + 1] = 0u; }
 }
-void launch_weight_minmax(const float* w, int cout, int64_t per_ch, int per_channel,
-                          unsigned int* mnmx, cudaStream_t s) {
-  int npairs = per_channel ? cout : 1;
-  k_init_minmax<<<(npairs + 255) / 256, 256, 0, s>>>(mnmx, npairs);
-  if (per_channel)
-    k_weight_minmax<<<cout, 256, 0, s>>>(w, cout, per_ch, 1, mnmx);
-  else
-    k_weight_minmax<<<nblk(per_ch * cout), 256, 0, s>>>(w, cout, per_ch, 0, mnmx);
-}
-
-// params per channel; per-tensor params are broadcast to every channel slot
-__global__ void k_weight_params(const unsigned int* __restrict__ mnmx, int cout, int per_channel,
-                                int scheme, float* __restrict__ scale, int* __restrict__ zp) {
-  int o = blockIdx.x * blockDim.x + threadIdx.x;
-  if (o >= cout) return;
-  const unsigned int* q = mnmx + (per_channel ? 2 * o : 0);
-  params_for_range(scheme, (double)ord2f(q[0]), (double)ord2f(q[1]), scale + o, zp + o);
-}
-void launch_weight_params(const unsigned int* mnmx, int cout, int per_channel, int scheme,
-                          float* scale, int* zp, cudaStream_t s) {
-  k_weight_params<<<(cout + 127) / 128, 128, 0, s>>>(mnmx, cout, per_channel, scheme, scale, zp);
-}
-
 // value of the weight element feeding GEMM column o, K byte position kb (padded layout)
 __device__ __forceinline__ bool wsrc(int o, int64_t kb, int cin, int k, int fc_hw, int cin_p,
                                      int64_t* src_idx) {
@@ -126,56 +103,6 @@ __device__ __forceinline__ bool wsrc(int o, int64_t kb, int cin, int k, int fc_h
   int kh = (int)(tap / k), kw = (int)(tap - (int64_t)kh * k);
   *src_idx = (((int64_t)o * cin + c) * k + kh) * k + kw;
   return true;
-}
-
-// tiled B operand: [nt][it][j(8)][row(bn)][16 bytes]
-__global__ void k_weight_quant_tc(const float* __restrict__ w, int cout, int cin, int k, int fc_hw,
-                                  int cin_p, const float* __restrict__ scale,
-                                  const int* __restrict__ zp, int bn, int n_kiter,
-                                  int8_t* __restrict__ out, int64_t total) {
-  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < total;
-       i += (int64_t)gridDim.x * blockDim.x) {
-    int b = (int)(i & 15);
-    int64_t r = i >> 4;
-    int row = (int)(r % bn); r /= bn;
-    int j = (int)(r & 7); r >>= 3;
-    int it = (int)(r % n_kiter);
-    int nt = (int)(r / n_kiter);
-    int o = nt * bn + row;
-    int64_t kb = ((int64_t)it * 8 + j) * 16 + b;
-    int8_t code = 0;
-    int64_t si;
-    if (o < cout && wsrc(o, kb, cin, k, fc_hw, cin_p, &si))
-      code = (int8_t)quant1(__ldg(w + si), (double)scale[o], (double)zp[o]);
-    out[i] = code;
-  }
-}
-// wsum[o] = sum of real weight codes of column o (used by the zero-point correction)
-__global__ void k_weight_sum(const float* __restrict__ w, int64_t per_ch, const float* __restrict__ scale,
-                             const int* __restrict__ zp, int* __restrict__ wsum) {
-  int o = blockIdx.x;
-  double s = (double)scale[o], z = (double)zp[o];
-  int acc = 0;
-  for (int64_t i = threadIdx.x; i < per_ch; i += blockDim.x) acc += quant1(__ldg(w + (int64_t)o * per_ch + i), s, z);
-  for (int d = 16; d; d >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, d);
-  __shared__ int red[32];
-  if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = acc;
-  __syncthreads();
-  if (threadIdx.x == 0) {
-    int t = 0;
-    for (int q = 0; q < (int)(blockDim.x >> 5); ++q) t += red[q];
-    wsum[o] = t;
-  }
-}
-void launch_weight_quant_tc(const float* w, int cout, int cin, int k, int fc_hw, int cin_p,
-                            const float* scale, const int* zp, int bn, int n_kiter, int8_t* out,
-                            int* wsum, cudaStream_t s) {
-  int nt = (cout + bn - 1) / bn;
-  int64_t total = (int64_t)nt * n_kiter * 8 * bn * 16;
-  k_weight_quant_tc<<<nblk(total), 256, 0, s>>>(w, cout, cin, k, fc_hw, cin_p, scale, zp, bn,
-                                                n_kiter, out, total);
-  int64_t per_ch = fc_hw > 0 ? (int64_t)cin * fc_hw : (int64_t)cin * k * k;   // s2d: fc_hw < 0
-  k_weight_sum<<<cout, 128, 0, s>>>(w, per_ch, scale, zp, wsum);
 }
 
 // ---------------------------------------------------------------- all 8 weight variants at once
@@ -274,21 +201,6 @@ void launch_weight_prepare8(const float* w, int cout, int64_t per_ch, bool depth
         w, cout, cin, k, fc_hw, cin_p, scale, zp, bn, n_kiter, codes, bytes_per_variant);
     k_weight_sum8<<<dim3(cout, 8), 128, 0, s>>>(w, per_ch, cout, scale, zp, wsum);
   }
-}
-
-// depthwise: out [c][k*k] codes
-__global__ void k_weight_quant_dw(const float* __restrict__ w, int c, int kk,
-                                  const float* __restrict__ scale, const int* __restrict__ zp,
-                                  int8_t* __restrict__ out) {
-  int i = blockIdx.x * blockDim.x + threadIdx.x;
-  if (i >= c * kk) return;
-  int ch = i / kk;
-  out[i] = (int8_t)quant1(__ldg(w + i), (double)scale[ch], (double)zp[ch]);
-}
-void launch_weight_quant_dw(const float* w, int c, int k, const float* scale, const int* zp,
-                            int8_t* out, cudaStream_t s) {
-  int n = c * k * k;
-  k_weight_quant_dw<<<(n + 255) / 256, 256, 0, s>>>(w, c, k * k, scale, zp, out);
 }
 
 // ---------------------------------------------------------------- per-config layer params

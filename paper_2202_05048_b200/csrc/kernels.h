@@ -94,25 +94,11 @@ void launch_softmax_f32(const float* x, int64_t rows, int C, float* y, cudaStrea
 // ---------------------------------------------------------------- F3 (k_quant.cu)
 void launch_act_params(const double* ranges /*[n_var][T][2]*/, const int* var_scheme, int n_var,
                        int T, float* scale, int* zp, cudaStream_t s);
-// per-channel (or per-tensor) min/max of a weight tensor -> ordered-uint pairs [cout][2]
-void launch_weight_minmax(const float* w, int cout, int64_t per_ch, int per_channel,
-                          unsigned int* mnmx, cudaStream_t s);
-void launch_weight_params(const unsigned int* mnmx, int cout, int per_channel, int scheme,
-                          float* scale, int* zp, cudaStream_t s);
-// quantize conv/fc weights [cout][cin][k][k] into the tcgen05 B tile layout
-// conv: w [cout][cin][k][k]; fc: w [cout][cin*fc_hw] (NCHW flatten) treated as a 1x1 conv over
-// an NHWC-flattened input of fc_hw pixels x cin_p channels; fc_hw = -k' selects the
-// space-to-depth stem layout (k'xk' taps of 16-byte s2d pixels).  Output: tiled B operand.
-void launch_weight_quant_tc(const float* w, int cout, int cin, int k, int fc_hw, int cin_p,
-                            const float* scale, const int* zp, int bn, int n_kiter, int8_t* out,
-                            int* wsum, cudaStream_t s);
 // all 8 (scheme, granularity) variants of one weight tensor: params, codes, code sums
 void launch_weight_prepare8(const float* w, int cout, int64_t per_ch, bool depthwise, int cin, int k,
                             int fc_hw, int cin_p, int bn, int n_kiter, int64_t bytes_per_variant,
                             unsigned int* mnmx, float* scale, int* zp, int8_t* codes, int* wsum,
                             cudaStream_t s);
-void launch_weight_quant_dw(const float* w, int c, int k, const float* scale, const int* zp,
-                            int8_t* out, cudaStream_t s);
 void launch_layer_params(const LayerSt* d_layers, int n_layers, const float* act_scale,
                          const int* act_zp, int wvar, cudaStream_t s);
 void launch_quant_input(const float* imgs_nchw, int64_t img0, View out, const float* act_scale,
