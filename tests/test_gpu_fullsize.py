@@ -1,0 +1,67 @@
+"""Full-size (BASELINE.json configs[1]: ResNet-50 IR, 224x224, 1000 eval images) GPU
+properties.  The numpy oracle cannot run this size in test time, so these check
+size-independent invariants of the path on the exact workload the bench measures:
+
+* histogram count conservation: every cache/tensor histogram holds n_images x elems
+  samples (calibration.py:81-93 bins every value; lo == hi puts all in bin 0);
+* the optimised A-operand paths (TMA tiles, kw-reuse slabs) and the fused epilogues
+  (relu / residual-add tables) give exactly the top-1 counts of the plain cp.async
+  gather path without fusion;
+* the tcgen05 conv equals a CUDA-core reference conv of the same contract on two
+  configurations (one with weight zero points) over the whole evaluation set.
+
+Every int8 tensor is already bit-exact against the oracle at 64x64
+(test_gpu_imagenet.py); these tests tie the full-size measurement to those paths.
+"""
+import numpy as np
+import pytest
+
+from paper_2202_05048_b200 import GENERIC, build_model, enumerate_space, make_dataset
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module")
+def ev224():
+    from paper_2202_05048_b200.evaluator import GpuEvaluator
+    g = build_model("resnet50", 0)
+    d = make_dataset(n_calib=300, n_eval=1000, seed=0, shape=(3, 224, 224))
+    ev = GpuEvaluator(g, d, 0, GENERIC)
+    yield ev
+    ev.close()
+
+
+def test_histogram_count_conservation(ev224):
+    counts = ev224.cache_counts.sum(axis=-1)
+    assert np.array_equal(counts, ev224.cache_nsamp)
+    lo, hi = ev224.cache_ranges[..., 0], ev224.cache_ranges[..., 1]
+    assert np.all(lo <= hi)
+
+
+def test_fast_paths_equal_plain_path(ev224):
+    space = enumerate_space(GENERIC)
+    picks = [space[i] for i in (0, 2, 12, 20, 45, 54, 67, 90)]   # Off + FirstLastFp32, zw = 0 / != 0
+    fast = ev224.correct_counts(picks)
+    try:
+        ev224.set_option("tma", 0)
+        ev224.set_option("kwr", -1)
+        ev224.set_option("fusion", 0)
+        plain = ev224.correct_counts(picks)
+    finally:
+        ev224.set_option("tma", 1)
+        ev224.set_option("kwr", 0)
+        ev224.set_option("fusion", 1)
+    assert np.array_equal(fast, plain)
+    assert np.all((fast >= 0) & (fast <= 1000))
+
+
+def test_tc_conv_equals_reference_conv_fullsize(ev224):
+    space = enumerate_space(GENERIC)
+    picks = [space[12], space[2]]                  # Sym/KL/Tensor and Asym/Max/Channel (zw != 0)
+    tc = ev224.correct_counts(picks)
+    try:
+        ev224.set_option("conv_ref", 1)
+        ref = ev224.correct_counts(picks)
+    finally:
+        ev224.set_option("conv_ref", 0)
+    assert np.array_equal(tc, ref)
