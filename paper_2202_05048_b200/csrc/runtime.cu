@@ -151,6 +151,9 @@ struct ptq_ctx {
   float* d_act_scale = nullptr;          // [24][T]
   int* d_act_zp = nullptr;
   bool prepared = false;
+  bool static_ready = false;             // weight variants + eval buffers + mixed prefix enqueued
+  bool wzp_pending = false;              // h_zp holds weight zero points not yet scanned
+  int* h_zp = nullptr;                   // pinned [sum of 8*cout] weight zero points
   // eval buffers
   int64_t chunk = 0;
   std::vector<int8_t*> d_codes;          // per tensor int8 view buffer (or null)
@@ -673,6 +676,8 @@ void ensure_eval_buffers(ptq_ctx* c) {
 }
 
 // ---------------------------------------------------------------- prepare
+void prepare_static(ptq_ctx* c);
+
 void prepare(ptq_ctx* c) {
   if (c->prepared) return;
   Trace tr("prepare");
@@ -698,6 +703,30 @@ void prepare(ptq_ctx* c) {
   }
   launch_act_params(d_r, d_vs, 24, T, c->d_act_scale, c->d_act_zp, c->st);
   check_launch(c);
+  prepare_static(c);
+  CK(cudaStreamSynchronize(c->st));
+  if (c->wzp_pending) {
+    size_t off = 0;
+    for (auto& wd : c->W) {
+      if (!wd.cout) continue;
+      for (int v = 0; v < 8; ++v) {
+        wd.has_wzp[v] = false;
+        for (int o = 0; o < wd.cout; ++o) wd.has_wzp[v] |= c->h_zp[off + (size_t)v * wd.cout + o] != 0;
+      }
+      off += (size_t)8 * wd.cout;
+    }
+    c->wzp_pending = false;
+  }
+  c->dfree(d_r);
+  c->dfree(d_vs);
+  c->prepared = true;
+}
+
+// clip-range independent part of prepare(): weight variants, eval buffers, the mixed
+// prefix.  Only enqueued (no sync), so ptq_kl_sweep can start it while the host picks the
+// KL windows.
+void prepare_static(ptq_ctx* c) {
+  if (c->static_ready) return;
   // weights: 8 variants (scheme, granularity) per compute node
   Trace trw("prepare.weights");
   unsigned int* d_mm = nullptr;
@@ -716,19 +745,18 @@ void prepare(ptq_ctx* c) {
                            wd.zp, wd.codes, wd.wsum, c->st);
     check_launch(c);
   }
-  CK(cudaStreamSynchronize(c->st));
+  // weight zero points to the host asynchronously (scanned for has_wzp in prepare())
+  size_t nzp = 0;
+  for (auto& wd : c->W) nzp += (size_t)8 * wd.cout;
+  if (!c->h_zp) CK(cudaMallocHost(&c->h_zp, std::max<size_t>(nzp, 1) * sizeof(int)));
+  size_t off = 0;
   for (auto& wd : c->W) {
     if (!wd.cout) continue;
-    std::vector<int> hz((size_t)8 * wd.cout);
-    CK(cudaMemcpy(hz.data(), wd.zp, hz.size() * sizeof(int), cudaMemcpyDeviceToHost));
-    for (int v = 0; v < 8; ++v) {
-      wd.has_wzp[v] = false;
-      for (int o = 0; o < wd.cout; ++o) wd.has_wzp[v] |= hz[(size_t)v * wd.cout + o] != 0;
-    }
+    CK(cudaMemcpyAsync(c->h_zp + off, wd.zp, (size_t)8 * wd.cout * sizeof(int), cudaMemcpyDeviceToHost, c->st));
+    off += (size_t)8 * wd.cout;
   }
+  c->wzp_pending = true;
   c->dfree(d_mm);
-  c->dfree(d_r);
-  c->dfree(d_vs);
   ensure_eval_buffers(c);
   // mixed prefix: config-invariant fp32 output of the first compute node for all eval images
   {
@@ -783,8 +811,7 @@ void prepare(ptq_ctx* c) {
       }
     }
   }
-  CK(cudaStreamSynchronize(c->st));
-  c->prepared = true;
+  c->static_ready = true;
 }
 
 // ---------------------------------------------------------------- one config
@@ -1086,6 +1113,7 @@ int ptq_destroy(ptq_ctx* c) {
   for (void* p : c->allocs) cudaFreeAsync(p, c->st);
   if (c->st) cudaStreamSynchronize(c->st);
   for (auto e : c->ev_pool) cudaEventDestroy(e);
+  if (c->h_zp) cudaFreeHost(c->h_zp);
   if (c->st) cudaStreamDestroy(c->st);
   delete c;
   return PTQ_OK;
@@ -1103,6 +1131,7 @@ int ptq_calib_forward(ptq_ctx* c, int32_t n_caches, const int32_t* sizes, const 
     Trace tr("calib_forward");
     REQ(c && n_caches >= 1 && sizes, "null argument");
     CK(cudaSetDevice(c->dev));
+    c->static_ready = false;                     // a new calibration rebuilds the evaluator state
     for (auto p : c->cal_bufs) c->dfree(p);
     for (auto p : c->cal_slots) c->dfree(p);
     c->cal_bufs.clear();
@@ -1232,8 +1261,14 @@ int ptq_kl_sweep(ptq_ctx* c, int32_t n_hist, const int64_t* counts, const float*
     launch_kl_sweep(d_c, d_r, n_hist, d_cum, d_nz, d_log, d_kl, c->st);
     check_launch(c);
     CK(cudaMemcpyAsync(kl, d_kl, (size_t)n_hist * PTQ_NWINDOWS * 8, cudaMemcpyDeviceToHost, c->st));
-    CK(cudaStreamSynchronize(c->st));
+    cudaEvent_t done;
+    CK(cudaEventCreateWithFlags(&done, cudaEventDisableTiming));
+    CK(cudaEventRecord(done, c->st));
     for (void* p : {(void*)d_c, (void*)d_r, (void*)d_cum, (void*)d_nz, (void*)d_log, (void*)d_kl}) c->dfree(p);
+    // the clip-range independent preparation runs on the GPU while the caller picks windows
+    if (!c->static_ready && c->W.size()) prepare_static(c);
+    CK(cudaEventSynchronize(done));
+    CK(cudaEventDestroy(done));
   });
 }
 
@@ -1353,9 +1388,13 @@ int ptq_set_option(ptq_ctx* c, const char* key, int64_t value) {
         for (auto& P : c->plans) { if (P.d_layers) c->dfree(P.d_layers); P = Plan{}; }
         for (auto p : c->d_codes) c->dfree(p);
         c->d_codes.clear();
+        c->static_ready = false;
+        c->prepared = false;
       }
     } else if (k == "eval_chunk") {
       c->opt_chunk = value;
+      c->static_ready = false;
+      c->prepared = false;
     } else {
       REQ(false, "unknown option " + k);
     }
