@@ -563,7 +563,7 @@ __global__ void __launch_bounds__(TC_THREADS, 1) k_conv_tc(const __grid_constant
 #pragma unroll
               for (int ks2 = 0; ks2 < 2; ++ks2) {
                 const uint32_t st = a0 + kw * 64 + ks2 * 32;
-                const uint64_t ad = umma_desc_sw(st, 64, a.kwr_bo == 1 ? ((st >> 7) & 7u) : a.kwr_bo == 2 ? ((st >> 6) & 7u) : 0u);
+                const uint64_t ad = umma_desc_sw(st, 64);   // swizzle on absolute address bits
                 const uint64_t bd = umma_desc(bb + (uint32_t)((ki * 12 + kw * 4 + ks2 * 2) * BN * 16), BN * 16, 128);
                 mma_i8(d, ad, bd, idesc, (ki | kw | ks2) != 0);
               }
@@ -693,7 +693,7 @@ int conv_tc_bn_for(int cout) {
 }
 
 static int g_num_sms = 0;
-static int g_kwr_mode = 0;   // -1 disables the kw-reuse slabs; 0/1/2 = descriptor base-offset convention
+static int g_kwr_mode = 0;   // -1 disables the kw-reuse slabs (A/B testing)
 void conv_tc_set_kwr_mode(int m) { g_kwr_mode = m; }
 
 template <int BN>
@@ -841,7 +841,6 @@ static void plan_launch(ConvTcArgs& t, int bn) {
                  CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_64B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
                  CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS) {
       t.kwr = 1;
-      t.kwr_bo = g_kwr_mode;
       t.a_iters = 3;                                 // A stages per tile = kh rows
     }
   }

@@ -183,7 +183,6 @@ struct ConvTcArgs {
                           // in shared memory instead of streaming with every tile
   int kwr;                // set by the launcher: 3x3 Cp=64 TMA conv loads one 136-row slab per kh
                           // and feeds its 3 kw taps as row-shifted descriptors (A bytes / 3)
-  int kwr_bo;             // descriptor base-offset convention for the row-shifted slabs
   int a_iters;            // A pipeline stages per tile (n_kiter, or 3 kh slabs with kwr)
   int flat;               // set by the launcher: GEMM row m is flat pixel m of the output (and of
                           // the add operand) -- halo-free TMA-mode layers skip the row geometry
