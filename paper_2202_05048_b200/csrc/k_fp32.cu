@@ -118,13 +118,15 @@ __global__ void __launch_bounds__(256) k_conv_f32(const float* __restrict__ x, i
 // 128 x BN block tile, BK = 8 (one tap, 8 consecutive channels), 256 threads each owning
 // an 8 x (BN/16) register tile, double-buffered shared tiles with the next K slice
 // prefetched into registers (float4 global loads) while the current one is multiplied.
-template <int BN>
+template <int BN, int BK>
 __global__ void __launch_bounds__(256, 2) k_conv_f32_rb(const float* __restrict__ x, int N, int H, int W,
                                                      int Cin, const float* __restrict__ Bw,
                                                      const float* __restrict__ bias, int Cout, int k,
                                                      int stride, int pad, int OH, int OW,
                                                      float* __restrict__ y) {
-  constexpr int BM = 128, BK = 8, TN = BN / 16;   // TN = 8 (BN 128) or 4 (BN 64)
+  constexpr int BM = 128, TN = BN / 16;           // TN = 8 (BN 128) or 4 (BN 64)
+  constexpr int NA = BK / 8;                       // float4 A loads per thread per K slice
+  constexpr int NB = (BK * BN / 4 + 255) / 256;    // float4 B loads per thread per K slice
   __shared__ __align__(16) float As[2][BK][BM + 4];
   __shared__ __align__(16) float Bs[2][BK][BN];
   const int tid = threadIdx.x;
@@ -132,7 +134,7 @@ __global__ void __launch_bounds__(256, 2) k_conv_f32_rb(const float* __restrict_
   const int K = k * k * Cin;
   const int64_t m0 = (int64_t)blockIdx.x * BM;
   const int n0 = blockIdx.y * BN;
-  // A loader: row ar = tid / 2, channels 4 * (tid & 1) .. +4 of the current tap
+  // A loader: row ar = tid / 2, channels 4 * (tid & 1) + 8 j .. +4 of the current tap
   const int ar = tid >> 1, ah = (tid & 1) * 4;
   const int64_t am = m0 + ar;
   const bool aok = am < M;
@@ -147,9 +149,7 @@ __global__ void __launch_bounds__(256, 2) k_conv_f32_rb(const float* __restrict_
     aiw0 = ow * stride - pad;
     abase = (t / OH) * H * W;
   }
-  // B loader: k row bk, columns bc .. +4 (BN 128: 256 float4; BN 64: 128 float4)
-  const int bk = BN == 128 ? tid >> 5 : (tid >> 4) & 7, bc = BN == 128 ? (tid & 31) * 4 : (tid & 15) * 4;
-  const bool bload = BN == 128 || tid < 128;
+  // B loader: float4 index q = tid + 256 i over the BK x BN slice
   const int tm = tid >> 4, tn = tid & 15;
   float acc[8][TN];
 #pragma unroll
@@ -157,31 +157,45 @@ __global__ void __launch_bounds__(256, 2) k_conv_f32_rb(const float* __restrict_
 #pragma unroll
     for (int j = 0; j < TN; ++j) acc[i][j] = 0.f;
 
-  auto load_a = [&](int k0) -> float4 {
+  auto load_a = [&](int k0, float4 (&r)[NA]) {
     const int tap = k0 / Cin, ci = k0 - tap * Cin + ah;
     const int kh = tap / k, kw = tap - kh * k;
     const int ih = aih0 + kh, iw = aiw0 + kw;
-    if (aok && ih >= 0 && ih < H && iw >= 0 && iw < W)
-      return __ldg(reinterpret_cast<const float4*>(x + (abase + (int64_t)ih * W + iw) * Cin + ci));
-    return make_float4(0.f, 0.f, 0.f, 0.f);
+    const bool ok = aok && ih >= 0 && ih < H && iw >= 0 && iw < W;
+    const float4* src = reinterpret_cast<const float4*>(x + (abase + (int64_t)ih * W + iw) * Cin + ci);
+#pragma unroll
+    for (int j = 0; j < NA; ++j) r[j] = ok ? __ldg(src + 2 * j) : make_float4(0.f, 0.f, 0.f, 0.f);
   };
-  auto load_b = [&](int k0) -> float4 {
-    const int nn = n0 + bc;
-    if (!bload || nn >= Cout) return make_float4(0.f, 0.f, 0.f, 0.f);
-    return __ldg(reinterpret_cast<const float4*>(Bw + (int64_t)(k0 + bk) * Cout + nn));
+  auto load_b = [&](int k0, float4 (&r)[NB]) {
+#pragma unroll
+    for (int i = 0; i < NB; ++i) {
+      const int q = tid + 256 * i, bk = q / (BN / 4), bc = (q % (BN / 4)) * 4;
+      const int nn = n0 + bc;
+      r[i] = (bk < BK && nn < Cout) ? __ldg(reinterpret_cast<const float4*>(Bw + (int64_t)(k0 + bk) * Cout + nn))
+                                    : make_float4(0.f, 0.f, 0.f, 0.f);
+    }
   };
-  float4 ra = load_a(0), rb = load_b(0);
+  float4 ra[NA], rb[NB];
+  load_a(0, ra);
+  load_b(0, rb);
   int buf = 0;
   for (int k0 = 0; k0 < K; k0 += BK) {
-    As[buf][ah + 0][ar] = ra.x;
-    As[buf][ah + 1][ar] = ra.y;
-    As[buf][ah + 2][ar] = ra.z;
-    As[buf][ah + 3][ar] = ra.w;
-    if (bload) *reinterpret_cast<float4*>(&Bs[buf][bk][bc]) = rb;
+#pragma unroll
+    for (int j = 0; j < NA; ++j) {
+      As[buf][ah + 8 * j + 0][ar] = ra[j].x;
+      As[buf][ah + 8 * j + 1][ar] = ra[j].y;
+      As[buf][ah + 8 * j + 2][ar] = ra[j].z;
+      As[buf][ah + 8 * j + 3][ar] = ra[j].w;
+    }
+#pragma unroll
+    for (int i = 0; i < NB; ++i) {
+      const int q = tid + 256 * i, bk = q / (BN / 4), bc = (q % (BN / 4)) * 4;
+      if (bk < BK) *reinterpret_cast<float4*>(&Bs[buf][bk][bc]) = rb[i];
+    }
     __syncthreads();
     if (k0 + BK < K) {                               // prefetch the next K slice
-      ra = load_a(k0 + BK);
-      rb = load_b(k0 + BK);
+      load_a(k0 + BK, ra);
+      load_b(k0 + BK, rb);
     }
 #pragma unroll
     for (int kk = 0; kk < BK; ++kk) {
@@ -359,12 +373,15 @@ void launch_conv_f32(const float* x, int N, int H, int W, int Cin, const float* 
     return;
   }
   if (Cin % 8 == 0 && Cout % 64 == 0) {              // register-blocked path (float4 operands)
+    const bool bk16 = Cin % 16 == 0;                 // 16-deep K slices: half the barriers
     if (Cout % 128 == 0) {
       dim3 g((unsigned)((M + 127) / 128), (unsigned)(Cout / 128));
-      k_conv_f32_rb<128><<<g, 256, 0, s>>>(x, N, H, W, Cin, Bw, bias, Cout, k, stride, pad, OH, OW, y);
+      if (bk16) k_conv_f32_rb<128, 16><<<g, 256, 0, s>>>(x, N, H, W, Cin, Bw, bias, Cout, k, stride, pad, OH, OW, y);
+      else k_conv_f32_rb<128, 8><<<g, 256, 0, s>>>(x, N, H, W, Cin, Bw, bias, Cout, k, stride, pad, OH, OW, y);
     } else {
       dim3 g((unsigned)((M + 127) / 128), (unsigned)(Cout / 64));
-      k_conv_f32_rb<64><<<g, 256, 0, s>>>(x, N, H, W, Cin, Bw, bias, Cout, k, stride, pad, OH, OW, y);
+      if (bk16) k_conv_f32_rb<64, 16><<<g, 256, 0, s>>>(x, N, H, W, Cin, Bw, bias, Cout, k, stride, pad, OH, OW, y);
+      else k_conv_f32_rb<64, 8><<<g, 256, 0, s>>>(x, N, H, W, Cin, Bw, bias, Cout, k, stride, pad, OH, OW, y);
     }
     return;
   }
