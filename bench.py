@@ -238,8 +238,17 @@ def run_b200(args):
     bf16 = peaks.get("bf16_tflops")
     peak = 2.0 * bf16 if bf16 else 2.0 * 1590.0
     achieved = (conv_ops / (conv_ms / 1000.0)) / 1e12 if conv_ms > 0 else 0.0
+    # DRAM traffic per k_conv_tc launch from the committed ncu capture of one config's 54
+    # conv launches (profiles/r1/conv_dram_per_launch.csv), mean over launches
+    traffic = None
+    tpath = os.path.join(ROOT, "profiles", "r1", "conv_dram_per_launch.csv")
+    if os.path.exists(tpath):
+        rows = [ln.split(",") for ln in open(tpath).read().strip().splitlines()[1:]]
+        if rows:
+            traffic = sum(int(r[2]) + int(r[3]) for r in rows) / len(rows)
     roofline = {"bound": "tensor", "achieved": achieved, "peak": peak, "unit": "TOP/s",
-                "frac": achieved / peak if peak else None, "traffic": None,
+                "frac": achieved / peak if peak else None, "traffic": traffic,
+                "traffic_unit": "bytes per launch (ncu dram__bytes_read+write, mean of one config's 54 launches)",
                 "kernel": "k_conv_tc (tcgen05.mma.kind::i8)",
                 "timed_launches": conv_n, "timed_ms": conv_ms,
                 "avg_launch_ms": conv_ms / conv_n if conv_n else None,

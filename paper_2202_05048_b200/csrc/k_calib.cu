@@ -133,7 +133,7 @@ __device__ __forceinline__ int np_bin_f32g(float x, float lo32, float rc32, doub
 // counts: [2048] int64 (accumulated).  Four shared sub-histograms (one per warp % 4) spread
 // the atomics; exact zeros (post-ReLU tensors pile up there) are counted in registers and
 // added to the zero bin once per warp.
-__global__ void __launch_bounds__(512) k_histogram(const float* __restrict__ x, int64_t elems,
+__global__ void __launch_bounds__(256) k_histogram(const float* __restrict__ x, int64_t elems,
                                                    const int* __restrict__ slots, int n_slots,
                                                    const float* __restrict__ range,
                                                    unsigned long long* __restrict__ counts) {
@@ -164,13 +164,22 @@ __global__ void __launch_bounds__(512) k_histogram(const float* __restrict__ x, 
   const bool vec = (elems & 3) == 0 && ((((uintptr_t)x) & 15) == 0);
   if (vec) {
     const int64_t nv = elems >> 2, total_v = nv * n_slots;
-    for (int64_t w = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; w < total_v; w += stride) {
+    auto ld = [&](int64_t w) -> float4 {
       const int j = (int)(w / nv);
-      const float4 v = __ldg(reinterpret_cast<const float4*>(x + (int64_t)slots[j] * elems) + (w - (int64_t)j * nv));
-      put(v.x);
-      put(v.y);
-      put(v.z);
-      put(v.w);
+      return __ldg(reinterpret_cast<const float4*>(x + (int64_t)slots[j] * elems) + (w - (int64_t)j * nv));
+    };
+    // four loads in flight per thread before binning (the pass was load-latency bound)
+    int64_t w = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    for (; w + 3 * stride < total_v; w += 4 * stride) {
+      const float4 v0 = ld(w), v1 = ld(w + stride), v2 = ld(w + 2 * stride), v3 = ld(w + 3 * stride);
+      put(v0.x); put(v0.y); put(v0.z); put(v0.w);
+      put(v1.x); put(v1.y); put(v1.z); put(v1.w);
+      put(v2.x); put(v2.y); put(v2.z); put(v2.w);
+      put(v3.x); put(v3.y); put(v3.z); put(v3.w);
+    }
+    for (; w < total_v; w += stride) {
+      const float4 v = ld(w);
+      put(v.x); put(v.y); put(v.z); put(v.w);
     }
   } else {                                // scalar path (element count not a multiple of 4)
     const int64_t total = elems * n_slots;
@@ -377,7 +386,7 @@ void launch_minmax_reduce_cache(const unsigned int* per_img, int n_tensors, int 
 void launch_histogram(const float* x, int64_t elems, const int* slots, int n_slots,
                       const float* range, unsigned long long* counts, cudaStream_t s) {
   int64_t total = elems * n_slots;
-  k_histogram<<<nblocks(total, 512, 148 * 4), 512, 0, s>>>(x, elems, slots, n_slots, range, counts);
+  k_histogram<<<nblocks(total, 256, 148 * 8), 256, 0, s>>>(x, elems, slots, n_slots, range, counts);
 }
 void launch_kl_sweep(const long long* counts, const float* ranges, int n_hist, double* cum,
                      int* nzc, double* logc, double* kl_out, cudaStream_t s) {
