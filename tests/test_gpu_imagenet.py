@@ -130,3 +130,36 @@ def test_input_quantizer_at_rounding_boundaries():
     want = O.quantize_array(x, qp).astype(np.int8)
     assert np.array_equal(got, want)
     ev.close()
+
+
+def test_integer_only_profile(ds64):
+    """IntegerOnly profile (power-of-two scales, per-tensor, Mixed=Off, optional fusion;
+    tuner.py:75-80): the requant multiplier is 2^-s, so the fp64 epilogue equals the
+    reference's shift form (intexec.py:80-84).  Every code bit-exact for two configs and the
+    top-1 of the whole 12-config IntegerOnly space equal to the oracle's."""
+    from paper_2202_05048_b200 import INTEGER_ONLY
+    from paper_2202_05048_b200.evaluator import GpuEvaluator
+    g = build_model("resnet50", seed=0, shape=SHAPE)
+    ev = GpuEvaluator(g, ds64, 0, INTEGER_ONLY)
+    caches = {sc: {t: O.Hist(t, float(ev.cache_ranges[k, i, 0]), float(ev.cache_ranges[k, i, 1]),
+                             ev.cache_counts[k, i], int(ev.cache_nsamp[k, i]))
+                   for i, t in enumerate(ev.lowered.tensor_names)}
+              for k, sc in enumerate(("S1", "S2", "S3"))}
+    space = enumerate_space(INTEGER_ONLY)
+    assert len(space) == 12 and all(c.scheme.value == "SymmetricPower2" for c in space)
+    ev.set_option("fusion", 0)
+    try:
+        for cfg in (space[0], space[-1]):
+            qm = O.quantize_model(g, caches[cfg.cache], cfg)
+            seen = {}
+            O.run_quantized(qm, ds64.eval_images, sink=lambda t, v: seen.__setitem__(t, v))
+            for t, v in seen.items():
+                if t in qm.act:
+                    assert np.array_equal(ev.probe_codes(cfg, t).reshape(v.shape), v.astype(np.int8)), (cfg, t)
+    finally:
+        ev.set_option("fusion", 1)
+    got = ev.correct_counts(space)
+    oev = O.make_accuracy_evaluator(g, ds64, 0, caches=caches)
+    want = [round(oev(c) * len(ds64.eval_labels)) for c in space]
+    assert [int(x) for x in got] == want
+    ev.close()
