@@ -267,6 +267,15 @@ class GpuEvaluator:
             _lib.check(self.lib.ptq_probe_codes(self._ctx, C.byref(cd), tid, _lib.ptr(out), C.byref(n)))
         return out
 
+    def save_cache(self, path: str, size_class: str, meta: dict | None = None) -> None:
+        """Write one calibration cache of this evaluator as the reference's ``.qcal``
+        (calibration.py:115-134), byte-identical to ptqtune.save_cache of the same cache."""
+        from .artifacts import save_qcal
+        k = CACHE_SIZES.index(size_class)
+        ids = self.image_ids[k] if getattr(self, "image_ids", None) else select_images(self.n_calib, size_class, self.seed)
+        save_qcal(path, getattr(self.graph, "name", "model"), size_class, ids, self.lowered.tensor_names,
+                  self.cache_ranges[k], self.cache_counts[k], self.cache_nsamp[k], meta)
+
     def act_params(self, cache: int, scheme: int, clipping: int):
         s = np.zeros(self.T, dtype=np.float32)
         z = np.zeros(self.T, dtype=np.int32)

@@ -214,3 +214,18 @@ def test_end_to_end_gpu_calibration(golden, ds, toys, rec):
     assert np.max(np.abs(got - want)) <= 0.02
     assert got.max() == want.max()
     ev.close()
+
+
+@pytest.mark.parametrize("rec", TOYS)
+def test_save_cache_matches_reference_file(injected, rec, tmp_path):
+    """GpuEvaluator.save_cache writes the evaluator's caches as the
+    reference's .qcal, byte-identical to ptqtune.save_cache (tests/golden/ref_qcal.json)."""
+    import hashlib
+    import json
+    import os
+    ref = json.load(open(os.path.join(os.path.dirname(__file__), "golden", "ref_qcal.json")))
+    ev = injected[rec]
+    for sc in ("S1", "S2", "S3"):
+        path = tmp_path / f"{sc}.qcal"
+        ev.save_cache(str(path), sc)
+        assert hashlib.sha256(path.read_bytes()).hexdigest() == ref["qcal"][f"{rec}/{sc}/plain"]["sha256"]
