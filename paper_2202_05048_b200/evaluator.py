@@ -134,6 +134,60 @@ def _linspace_edge(lo: float, hi: float, k: int) -> float:
     return k * step + lo
 
 
+# ---------------------------------------------------------------- call coalescing
+class Coalescer:
+    """Batches concurrent single-item calls: the first caller becomes the leader and runs
+    ``batch_fn`` on everything queued (repeating while new requests arrive); the others
+    wait for their slot.  Results and exceptions go back to the caller that asked."""
+
+    def __init__(self, batch_fn):
+        self._fn = batch_fn
+        self._cv = threading.Condition()
+        self._queue: list = []
+        self._busy = False
+        self.batches: list[int] = []          # sizes of the batches run (for tests / stats)
+
+    def __call__(self, item):
+        slot = {"done": False}
+        with self._cv:
+            self._queue.append((item, slot))
+            if self._busy:
+                while not slot["done"]:
+                    self._cv.wait()
+                return self._result(slot)
+            self._busy = True
+        try:
+            while True:
+                with self._cv:
+                    batch, self._queue = self._queue, []
+                    if not batch:
+                        self._busy = False
+                        self._cv.notify_all()
+                        break
+                try:
+                    out = list(self._fn([b[0] for b in batch]))
+                    err = None
+                except Exception as e:  # noqa: BLE001 - handed to every caller of the batch
+                    out, err = [None] * len(batch), e
+                with self._cv:
+                    self.batches.append(len(batch))
+                    for (_, sl), r in zip(batch, out):
+                        sl.update(done=True, value=r, error=err)
+                    self._cv.notify_all()
+        finally:
+            with self._cv:
+                if self._busy and not self._queue:
+                    self._busy = False
+                self._cv.notify_all()
+        return self._result(slot)
+
+    @staticmethod
+    def _result(slot):
+        if slot.get("error") is not None:
+            raise slot["error"]
+        return slot["value"]
+
+
 # ---------------------------------------------------------------- evaluator
 
 class GpuEvaluator:
@@ -150,6 +204,7 @@ class GpuEvaluator:
         if self.n_eval <= 0:
             raise ValueError("empty evaluation set")
         self._lock = threading.Lock()
+        self._coalescer = None
         imgs = np.ascontiguousarray(np.asarray(d.images, dtype=np.float32))
         labels = np.ascontiguousarray(np.asarray(d.labels[d.n_calib:], dtype=np.int64))
         if tuple(imgs.shape[1:]) != tuple(int(v) for v in g.input_shape):
@@ -251,7 +306,11 @@ class GpuEvaluator:
         return [int(c) / float(self.n_eval) for c in self.correct_counts(cfgs)]
 
     def __call__(self, cfg) -> float:
-        return self.evaluate_many([cfg])[0]
+        # concurrent callers (measure_many's thread pool, tuner.py:192-203) are coalesced
+        # into one evaluate_many batch
+        if self._coalescer is None:
+            self._coalescer = Coalescer(self.evaluate_many)
+        return self._coalescer(cfg)
 
     # ------------------------------------------------------------ probes / options
     def set_option(self, key: str, value: int) -> None:
