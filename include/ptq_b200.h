@@ -132,6 +132,13 @@ int ptq_eval_configs(ptq_ctx* ctx, const ptq_config* cfgs, int32_t n_cfg, int64_
 /* Parity probes (tests): int8 codes of tensor `tensor` for one config over the
  * eval set in NCHW order [n_eval][C][H][W] (fp32-domain tensors return
  * PTQ_EINVAL).  Returns the element count through *n_out when out == NULL. */
+/* Quantized state of one int8 compute node under `cfg`, in the reference's layouts, for the
+ * .qtm8 emitter (replaces the QuantizedGraph fields quantize.py:133-211 builds and
+ * save_quantized, quantize.py:254-300, writes): weight codes [cout][cin][k][k] (depthwise
+ * [C][1][k][k], fc [cout][features]), per-output-channel weight scale / zero point (the same
+ * value repeated for per-tensor granularity) and int32 bias codes (if the node has a bias). */
+int ptq_export_layer(ptq_ctx* ctx, const ptq_config* cfg, int32_t node, int8_t* codes, float* wscale,
+                     int32_t* wzp, int32_t* bias);
 int ptq_probe_codes(ptq_ctx* ctx, const ptq_config* cfg, int32_t tensor, int8_t* out,
                     int64_t* n_out);
 /* Activation params the device derived for one variant: scale/zp [T]. */

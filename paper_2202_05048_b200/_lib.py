@@ -25,6 +25,7 @@ KINDS = {"conv2d": 0, "depthwise_conv2d": 1, "pointwise_conv2d": 2, "fully_conne
 EXPORTS = ("ptq_last_error", "ptq_version", "ptq_create", "ptq_destroy", "ptq_num_tensors",
            "ptq_calibrate", "ptq_kl_sweep", "ptq_set_clip_ranges", "ptq_prepare",
            "ptq_eval_configs", "ptq_probe_codes", "ptq_probe_act_params", "ptq_histogram_host",
+           "ptq_export_layer",
            "ptq_set_option", "ptq_last_stats", "ptq_calib_forward", "ptq_calib_histogram",
            "ptq_stream", "ptq_conv_timings")
 
@@ -85,6 +86,7 @@ def load() -> C.CDLL:
         "ptq_probe_codes": [P, C.POINTER(ConfigDesc), i32, P, C.POINTER(i64)],
         "ptq_probe_act_params": [P, i32, i32, i32, P, P],
         "ptq_histogram_host": [P, P, i64, C.c_float, C.c_float, P],
+        "ptq_export_layer": [P, C.POINTER(ConfigDesc), i32, P, P, P, P],
         "ptq_set_option": [P, C.c_char_p, i64],
         "ptq_last_stats": [P, C.POINTER(i64), C.POINTER(C.c_double), C.POINTER(C.c_double),
                            C.POINTER(i64), C.POINTER(i64)],

@@ -1350,6 +1350,62 @@ int ptq_probe_act_params(ptq_ctx* c, int32_t cache, int32_t scheme, int32_t clip
   });
 }
 
+int ptq_export_layer(ptq_ctx* c, const ptq_config* cfg, int32_t node, int8_t* codes, float* wscale,
+                     int32_t* wzp, int32_t* bias) {
+  return guarded([&] {
+    REQ(c && cfg && codes && wscale && wzp, "null argument");
+    REQ(node >= 0 && node < (int)c->nodes.size() && is_compute(c->nodes[node].kind), "not a compute node");
+    CK(cudaSetDevice(c->dev));
+    prepare(c);
+    Plan& P = c->plans[cfg->mixed];
+    REQ(!P.fp32node[node], "node runs in fp32 under this config");
+    const NodeI& n = c->nodes[node];
+    WeightsDev& wd = c->W[node];
+    const int wv = cfg->scheme * 2 + cfg->granularity;
+    const int v = (cfg->cache * 4 + cfg->scheme) * 2 + cfg->clipping;
+    // per-config layer constants (bias codes) exactly as an evaluation computes them
+    launch_layer_params(P.d_layers, (int)P.h_layers.size(), c->d_act_scale + (size_t)v * c->T,
+                        c->d_act_zp + (size_t)v * c->T, wv, c->st);
+    check_launch(c);
+    CK(cudaMemcpyAsync(wscale, wd.scale + (size_t)wv * wd.cout, wd.cout * sizeof(float), cudaMemcpyDeviceToHost, c->st));
+    CK(cudaMemcpyAsync(wzp, wd.zp + (size_t)wv * wd.cout, wd.cout * sizeof(int), cudaMemcpyDeviceToHost, c->st));
+    if (bias && wd.f32_bias)
+      CK(cudaMemcpyAsync(bias, wd.biasq, wd.cout * sizeof(int), cudaMemcpyDeviceToHost, c->st));
+    std::vector<int8_t> tiled((size_t)wd.bytes_per_variant);
+    CK(cudaMemcpyAsync(tiled.data(), wd.codes + (size_t)wv * wd.bytes_per_variant, tiled.size(),
+                       cudaMemcpyDeviceToHost, c->st));
+    CK(cudaStreamSynchronize(c->st));
+    if (n.kind == PTQ_DWCONV) {                      // [C][k*k], stored as is
+      std::memcpy(codes, tiled.data(), (size_t)wd.cout * wd.k * wd.k);
+      return;
+    }
+    // inverse of the B-tile layout [nt][ki][8][BN][16] (see wsrc in k_quant.cu)
+    const int k = n.kind == PTQ_FC ? 1 : n.k, cin = wd.cin;
+    const int64_t per_o = n.kind == PTQ_FC ? (int64_t)cin * wd.q_fc_hw : (int64_t)cin * k * k;
+    for (int o = 0; o < wd.cout; ++o)
+      for (int64_t e = 0; e < per_o; ++e) {
+        int64_t kb;
+        if (n.kind == PTQ_FC) {                      // e = ch*hw + pix  ->  kb = pix*cin_p + ch
+          const int64_t ch = e / wd.q_fc_hw, pix = e - ch * wd.q_fc_hw;
+          kb = pix * wd.q_cin_p + ch;
+        } else {
+          const int ch = (int)(e / (k * k)), t = (int)(e % (k * k)), kh = t / k, kw = t % k;
+          if (wd.q_fc_hw < 0) {                      // s2d stem: tap (kh', kw'), sub-pixel (a, b)
+            const int k2 = -wd.q_fc_hw, a = (kh + 1) & 1, b = (kw + 1) & 1;
+            kb = (((kh + 1) >> 1) * k2 + ((kw + 1) >> 1)) * 16 + (2 * a + b) * cin + ch;
+          } else if (wd.im2col) {                    // packed (kh, kw, c) row
+            kb = (int64_t)(kh * k + kw) * cin + ch;
+          } else {
+            kb = (int64_t)(kh * k + kw) * wd.cin_p + ch;
+          }
+        }
+        const int nt = o / wd.bn, row = o % wd.bn;
+        const int64_t it = kb >> 7, j = (kb >> 4) & 7, b = kb & 15;
+        codes[(int64_t)o * per_o + e] = tiled[(size_t)((((int64_t)nt * wd.n_kiter + it) * 8 + j) * wd.bn + row) * 16 + b];
+      }
+  });
+}
+
 int ptq_histogram_host(ptq_ctx* c, const float* x, int64_t n, float lo, float hi, int64_t* counts) {
   return guarded([&] {
     REQ(c && x && counts && n > 0, "bad argument");

@@ -229,3 +229,29 @@ def test_save_cache_matches_reference_file(injected, rec, tmp_path):
         path = tmp_path / f"{sc}.qcal"
         ev.save_cache(str(path), sc)
         assert hashlib.sha256(path.read_bytes()).hexdigest() == ref["qcal"][f"{rec}/{sc}/plain"]["sha256"]
+
+
+@pytest.mark.parametrize("rec", TOYS)
+def test_save_qtm8_matches_reference_file(injected, rec, tmp_path):
+    """The quantized model of a config written from device state (artifacts.save_qtm8:
+    weight codes / params and int32 bias codes via ptq_export_layer, activation params
+    from the device table) is byte-identical to ptqtune.save_quantized
+    (tests/golden/ref_qcal.json "qtm8": Generic configs incl. FirstLastFp32 and an
+    IntegerOnly config with fusion)."""
+    import hashlib
+    import json
+    import os
+
+    from paper_2202_05048_b200.artifacts import save_qtm8
+    from paper_2202_05048_b200.config import QuantConfig
+    ref = json.load(open(os.path.join(os.path.dirname(__file__), "golden", "ref_qcal.json")))
+    ev = injected[rec]
+    keys = [k for k in ref["qtm8"] if k.startswith(rec + "/")]
+    assert keys
+    for key in keys:
+        cfg = QuantConfig.from_dict(ref["qtm8"][key]["config"])
+        path = tmp_path / "m.qtm8"
+        save_qtm8(str(path), ev, cfg)
+        blob = path.read_bytes()
+        assert len(blob) == ref["qtm8"][key]["bytes"], key
+        assert hashlib.sha256(blob).hexdigest() == ref["qtm8"][key]["sha256"], key
