@@ -116,29 +116,37 @@ __device__ __forceinline__ int np_bin_fast(double x, double lo, double hi, doubl
   return np_bin(x, lo, hi, denom);
 }
 
-// fp32 pre-filter: fe32 = fl32(fl32(x - lo) * fl32(2048 / (hi - lo))) is within 4e-4 bins
-// of the true position (three fp32 roundings on a value < 2048); when its fractional part
-// keeps a 1e-3 margin from both neighbouring integers the bin is settled on the fp32 pipe,
-// otherwise np_bin_fast decides in fp64.
+// fp32 pre-filter: fe32 = fl32(fl32(x - lo) * fl32(2048 / (hi - lo))) is within
+// 3 * 2^-24 * 2048 = 3.7e-4 bins of the true position (three relative fp32 roundings on a
+// value <= 2048; numpy's own fp64 position and edges are 1e-12 away); when its fractional
+// part keeps a 5e-4 margin from both neighbouring integers the bin is settled on the fp32
+// pipe, otherwise np_bin_fast decides in fp64.
+__device__ __forceinline__ bool f32_bin_ok(float fe, int k) {
+  // |frac - 0.5| < 0.4995  <=>  5e-4 < frac < 0.9995 (frac = fe - k is exact).  k == 2048
+  // needs fe >= 2048, which for x <= hi is within 3.7e-4 of 2048 and fails the margin.
+  return fabsf(__fsub_rn(__fsub_rn(fe, (float)k), 0.5f)) < 0.4995f;
+}
 __device__ __forceinline__ int np_bin_f32g(float x, float lo32, float rc32, double lo, double hi, double denom,
                                            double rc, double eps) {
   const float fe = __fmul_rn(__fsub_rn(x, lo32), rc32);
   const int k = (int)fe;
-  const float frac = __fsub_rn(fe, (float)k);
-  if (k < PTQ_NBINS && frac > 1.0e-3f && frac < 0.999f) return k;
+  if (f32_bin_ok(fe, k)) return k;
   return np_bin_fast((double)x, lo, hi, denom, rc, eps);
 }
 
 // x: [n_img_total][elems]; slots: image slots of this cache; range: lo, hi (fp32 values).
-// counts: [2048] int64 (accumulated).  Four shared sub-histograms (one per warp % 4) spread
-// the atomics; exact zeros (post-ReLU tensors pile up there) are counted in registers and
-// added to the zero bin once per warp.
+// counts: [2048] int64 (accumulated).  One shared sub-histogram per warp keeps the atomics
+// warp-private; exact zeros (post-ReLU tensors pile up there) go straight to the zero bin.
+#ifndef HIST_COPIES
+#define HIST_COPIES 8              // one private sub-histogram per warp: no cross-warp atomics
+#endif
+#define HIST_BLOCKS_PER_SM (HIST_COPIES == 8 ? 3 : 8)
 __global__ void __launch_bounds__(256) k_histogram(const float* __restrict__ x, int64_t elems,
                                                    const int* __restrict__ slots, int n_slots,
                                                    const float* __restrict__ range,
                                                    unsigned long long* __restrict__ counts) {
-  __shared__ unsigned int sh[4 * PTQ_NBINS];
-  for (int i = threadIdx.x; i < 4 * PTQ_NBINS; i += blockDim.x) sh[i] = 0;
+  extern __shared__ unsigned int sh[];       // HIST_COPIES sub-histograms, one per warp
+  for (int i = threadIdx.x; i < HIST_COPIES * PTQ_NBINS; i += blockDim.x) sh[i] = 0;
   __syncthreads();
   const double lo = (double)range[0], hi = (double)range[1];
   const double denom = __dsub_rn(hi, lo);
@@ -151,7 +159,7 @@ __global__ void __launch_bounds__(256) k_histogram(const float* __restrict__ x, 
     return;
   }
   const int z0 = (lo <= 0.0 && 0.0 <= hi) ? np_bin(0.0, lo, hi, denom) : -1;
-  unsigned int* my = sh + ((threadIdx.x >> 5) & 3) * PTQ_NBINS;
+  unsigned int* my = sh + ((threadIdx.x >> 5) % HIST_COPIES) * PTQ_NBINS;
   unsigned int zc = 0;
   const float lo32 = range[0], rc32 = (float)rc;
   auto put = [&](float v) {
@@ -163,22 +171,59 @@ __global__ void __launch_bounds__(256) k_histogram(const float* __restrict__ x, 
   // flatten (image, float4) work items so small tensors still spread over all blocks
   const bool vec = (elems & 3) == 0 && ((((uintptr_t)x) & 15) == 0);
   if (vec) {
-    const int64_t nv = elems >> 2, total_v = nv * n_slots;
-    auto ld = [&](int64_t w) -> float4 {
-      const int j = (int)(w / nv);
-      return __ldg(reinterpret_cast<const float4*>(x + (int64_t)slots[j] * elems) + (w - (int64_t)j * nv));
+    // (image, float4) cursors advanced by the grid stride with 32-bit adds (the flat index
+    // split costs one 64-bit division per thread, not one per load)
+    const int64_t nv = elems >> 2;
+    const unsigned nvu = (unsigned)nv;           // < 2^31: r + sr never wraps
+    const int sj = (int)(stride / nv);
+    const unsigned sr = (unsigned)(stride % nv);
+    const int64_t w0 = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    int j = (int)(w0 / nv);
+    unsigned r = (unsigned)(w0 % nv);
+    auto adv = [&](int& jj, unsigned& rr) {
+      rr += sr;
+      jj += sj;
+      if (rr >= nvu) { rr -= nvu; ++jj; }
     };
-    // four loads in flight per thread before binning (the pass was load-latency bound)
-    int64_t w = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-    for (; w + 3 * stride < total_v; w += 4 * stride) {
-      const float4 v0 = ld(w), v1 = ld(w + stride), v2 = ld(w + 2 * stride), v3 = ld(w + 3 * stride);
-      put(v0.x); put(v0.y); put(v0.z); put(v0.w);
-      put(v1.x); put(v1.y); put(v1.z); put(v1.w);
-      put(v2.x); put(v2.y); put(v2.z); put(v2.w);
-      put(v3.x); put(v3.y); put(v3.z); put(v3.w);
+    auto at = [&](int jj, unsigned rr) -> float4 {
+      return __ldg(reinterpret_cast<const float4*>(x + (int64_t)__ldg(slots + jj) * elems) + rr);
+    };
+    // four loads in flight per thread, then 16 values binned without branches: the fp32
+    // bin and a needs-fp64 mask for all 16, one (rarely taken) branch for the near-edge
+    // values, then 16 unconditional shared atomics
+    const bool zero_in = z0 >= 0;
+    for (;;) {
+      int j1 = j, j2, j3;
+      unsigned r1 = r, r2, r3;
+      adv(j1, r1); j2 = j1; r2 = r1; adv(j2, r2); j3 = j2; r3 = r2; adv(j3, r3);
+      if (j3 >= n_slots) break;
+      const float4 q0 = at(j, r), q1 = at(j1, r1), q2 = at(j2, r2), q3 = at(j3, r3);
+      j = j3; r = r3;
+      adv(j, r);
+      const float v[16] = {q0.x, q0.y, q0.z, q0.w, q1.x, q1.y, q1.z, q1.w,
+                           q2.x, q2.y, q2.z, q2.w, q3.x, q3.y, q3.z, q3.w};
+      int k[16];
+      unsigned slow = 0;
+#pragma unroll
+      for (int e = 0; e < 16; ++e) {
+        const float fe = __fmul_rn(__fsub_rn(v[e], lo32), rc32);
+        k[e] = (int)fe;
+        const bool ok = f32_bin_ok(fe, k[e]);
+        const bool z = zero_in && v[e] == 0.0f;   // exact zeros: the zero bin, no fp64
+        if (z) k[e] = z0;
+        slow |= (unsigned)(!ok && !z) << e;
+      }
+      if (slow) {
+#pragma unroll
+        for (int e = 0; e < 16; ++e)
+          if (slow & (1u << e)) k[e] = np_bin_fast((double)v[e], lo, hi, denom, rc, eps);
+      }
+#pragma unroll
+      for (int e = 0; e < 16; ++e)
+        atomicAdd(&my[k[e]], 1u);      // ATOMS.POPC.INC: same-address lanes aggregate
     }
-    for (; w < total_v; w += stride) {
-      const float4 v = ld(w);
+    for (; j < n_slots; adv(j, r)) {
+      const float4 v = at(j, r);
       put(v.x); put(v.y); put(v.z); put(v.w);
     }
   } else {                                // scalar path (element count not a multiple of 4)
@@ -192,7 +237,9 @@ __global__ void __launch_bounds__(256) k_histogram(const float* __restrict__ x, 
   if ((threadIdx.x & 31) == 0 && zc) atomicAdd(&sh[z0], zc);
   __syncthreads();
   for (int i = threadIdx.x; i < PTQ_NBINS; i += blockDim.x) {
-    const unsigned int t = sh[i] + sh[PTQ_NBINS + i] + sh[2 * PTQ_NBINS + i] + sh[3 * PTQ_NBINS + i];
+    unsigned int t = 0;
+#pragma unroll
+    for (int c = 0; c < HIST_COPIES; ++c) t += sh[c * PTQ_NBINS + i];
     if (t) atomicAdd(counts + i, (unsigned long long)t);
   }
 }
@@ -386,7 +433,14 @@ void launch_minmax_reduce_cache(const unsigned int* per_img, int n_tensors, int 
 void launch_histogram(const float* x, int64_t elems, const int* slots, int n_slots,
                       const float* range, unsigned long long* counts, cudaStream_t s) {
   int64_t total = elems * n_slots;
-  k_histogram<<<nblocks(total, 256, 148 * 8), 256, 0, s>>>(x, elems, slots, n_slots, range, counts);
+  constexpr int smem = HIST_COPIES * PTQ_NBINS * 4;
+  static bool attr = false;
+  if (!attr) {
+    cudaFuncSetAttribute(k_histogram, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+    attr = true;
+  }
+  k_histogram<<<nblocks(total, 256, 148 * HIST_BLOCKS_PER_SM), 256, smem, s>>>(x, elems, slots, n_slots, range,
+                                                                               counts);
 }
 void launch_kl_sweep(const long long* counts, const float* ranges, int n_hist, double* cum,
                      int* nzc, double* logc, double* kl_out, cudaStream_t s) {

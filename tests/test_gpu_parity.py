@@ -76,6 +76,29 @@ def test_histogram_exact_adversarial(injected):
         assert np.array_equal(got, want), trial
 
 
+def test_histogram_exact_adversarial_large(injected):
+    """Arrays large enough for the 16-value batched binning loop (every thread runs several
+    4 x float4 rounds): edge points, their fp32 neighbours, exact zeros and the range ends
+    mixed into uniform values; counts must equal numpy's histogram exactly."""
+    ev = injected["lenet-ish"]
+    rng = np.random.default_rng(11)
+    for lo, hi in ((-1.3, 2.7), (0.0, 5.0e-3), (-40.0, -0.5)):
+        lo, hi = np.float32(lo), np.float32(hi)
+        edges = np.linspace(float(lo), float(hi), 2049)
+        pts = np.concatenate([edges, np.nextafter(edges, -np.inf), np.nextafter(edges, np.inf)]).astype(np.float32)
+        n = 9_000_004
+        x = rng.uniform(float(lo), float(hi), n).astype(np.float32)
+        x[rng.integers(0, n, 600_000)] = rng.choice(pts, 600_000)
+        if lo <= 0 <= hi:
+            x[rng.integers(0, n, 2_000_000)] = 0.0
+        x[:2] = lo, hi
+        x = np.clip(x, lo, hi)
+        for m in (n, n - 1):                       # float4 path and scalar path
+            want = O.histogram_counts(x[:m], float(lo), float(hi))
+            got = ev.histogram_array(x[:m], float(lo), float(hi))
+            assert np.array_equal(got, want), (lo, hi, m)
+
+
 def test_histogram_degenerate(injected):
     ev = injected["lenet-ish"]
     x = np.full(1000, 3.5, np.float32)
