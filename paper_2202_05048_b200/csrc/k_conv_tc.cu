@@ -135,7 +135,16 @@ __device__ __forceinline__ double b2d(uint32_t accb) {
 struct EpiK {
   uint32_t clo, chi;   // biased acc clamp bounds 2^31 -/+ aclamp
   int lo_conv, lo_add;
+  // fused add on the fp64 pipe: conv / skip operand (zero point as a 2^31 bias, ratio)
+  uint32_t zc_bias, zs_bias;
+  double rc, rs;
 };
+// 4-channel groups of a 16-channel chunk whose fused add runs on the fp64 pipe instead of
+// the shared-memory table: one group of four balances the L1 (table) and fp64 pipes (A/B
+// on ResNet-50: 0x0 13.7 ms, 0x8 13.4 ms, 0xC 14.0 ms of conv per config)
+#ifndef PTQ_ADD_ALU_MASK
+#define PTQ_ADD_ALU_MASK 0x8
+#endif
 
 // RHU(acc*m) + zp (unclipped) on a biased accumulator: acc clamped to the layer's
 // saturation margin, then fl(fl(acc*m) + 0.5) exactly as the reference, floor and +zp in
@@ -170,7 +179,18 @@ __device__ __forceinline__ int4 epi_chunk16(const uint32_t (&v)[16], const EpiPa
       if (WZP) accb -= (uint32_t)(raw[j].w * rowsum);
       q[j] = requant_raw<CLAMP>(accb, m, rt, k);
       if (RELU || SKIP) q[j] = imax(q[j], k.lo_conv);
-      if (SKIP) q[j] = stab[(int)__byte_perm(skw[g], 0u, 0x4440u + j) * PTQ_ADDTAB_ROW + imin(q[j], PTQ_QMAX)];
+      if (SKIP) {
+        if ((PTQ_ADD_ALU_MASK >> g) & 1) {
+          // the table entry computed in place: fl(fl((xc - zc) rc) + fl((xs - zs) rs)) (the sum
+          // is commutative, so the operand order needs no branch), RHU + zo, clip, relu floor
+          const int skc = (int)(int8_t)(skw[g] >> (8 * j));
+          const double t2 = __dadd_rn(__dmul_rn(b2d((uint32_t)imin(q[j], PTQ_QMAX) + k.zc_bias), k.rc),
+                                      __dmul_rn(b2d((uint32_t)skc + k.zs_bias), k.rs));
+          q[j] = imin(imax(__double2loint(__dadd_rd(__dadd_rn(t2, 0.5), rt.mg_zo)), k.lo_add), PTQ_QMAX);
+        } else {
+          q[j] = stab[(int)__byte_perm(skw[g], 0u, 0x4440u + j) * PTQ_ADDTAB_ROW + imin(q[j], PTQ_QMAX)];
+        }
+      }
     }
     packed[g] = SKIP ? __byte_perm(__byte_perm((uint32_t)q[0], (uint32_t)q[1], 0x0040),
                                    __byte_perm((uint32_t)q[2], (uint32_t)q[3], 0x0040), 0x5410)
@@ -390,7 +410,7 @@ __global__ void __launch_bounds__(TC_THREADS, 1) k_conv_tc(const __grid_constant
     // the padded output grid, so tap (kh, kw) of 128 consecutive output positions is 128
     // consecutive flat input pixels at offset kh*Wp + kw -- one tensor-map tile per tap slice
     if (warp == 0 && lane == 0) {
-      prefetch_tmap(&a.tmA);
+      if (a.tma_a != 67) prefetch_tmap(&a.tmA);
       const int Wp = a.in.W + 2 * a.in.halo;
       const int cpc = a.in.Cp >> 4, taps = a.k * a.k;
       int s = 0;
@@ -404,6 +424,13 @@ __global__ void __launch_bounds__(TC_THREADS, 1) k_conv_tc(const __grid_constant
             const int kk = ki * 8, tap = kk / cpc, c0 = (kk - tap * cpc) * 16;
             mbar_arrive_expect_tx(&full[s], TC_A_STAGE);
             tma_load_2d(dst, &a.tmA, c0, p0 + (tap / a.k) * Wp + tap % a.k, &full[s]);
+          } else if (a.tma_a == 67) {                // s2d stem: one contiguous slab per stage
+            // input pixels p0 + 2ki*Wp + [0, Wp + 131): both kh rows of the stage and their 4 kw
+            // taps are this slab shifted by kh*Wp + kw pixels (16 bytes each) -- one bulk copy
+            const int kh0 = 2 * ki;
+            const uint32_t bytes = (uint32_t)((kh0 + 1 < a.k ? Wp : 0) + TC_BM + 3) * 16u;
+            mbar_arrive_expect_tx(&full[s], bytes);
+            bulk_g2s(dst, a.in.p + ((int64_t)p0 + (int64_t)kh0 * Wp) * 16, bytes, &full[s]);
           } else if (a.tma_a == 66) {                // s2d stem, 64-byte window rows: two kh
             const int t0 = 2 * ki, t1 = 2 * ki + 1;  // rows of 4 kw taps per stage
             mbar_arrive_expect_tx(&full[s], t1 < a.k ? TC_A_STAGE : TC_A_STAGE / 2);
@@ -571,6 +598,22 @@ __global__ void __launch_bounds__(TC_THREADS, 1) k_conv_tc(const __grid_constant
             if (++s == NS) { s = 0; ph ^= 1u; }
             continue;
           }
+          if (a.tma_a == 67) {
+            // no-swizzle K-major views of the slab: row r of tap (kh, kw) is slab pixel
+            // kh*Wp + kw + r, so rows are 16 bytes apart (SBO 128 per 8 rows) and the second
+            // 16-byte K chunk of an MMA (tap kw + 1) is the next pixel (LBO 16)
+            const int Wp = a.in.W + 2 * a.in.halo;
+#pragma unroll
+            for (int ks = 0; ks < 4; ++ks) {
+              if ((ks >> 1) + 2 * ki >= a.k) break;
+              const uint64_t ad = umma_desc(a0 + (uint32_t)(((ks >> 1) * Wp + (ks & 1) * 2) * 16), 16, 128);
+              const uint64_t bd = umma_desc(b0 + ks * 2 * (BN * 16), BN * 16, 128);
+              mma_i8(d, ad, bd, idesc, (ki | ks) != 0);
+            }
+            mma_commit(&empty[s]);
+            if (++s == NS) { s = 0; ph ^= 1u; }
+            continue;
+          }
 #pragma unroll
           for (int ks = 0; ks < 4; ++ks) {
             const uint64_t ad =
@@ -598,6 +641,10 @@ __global__ void __launch_bounds__(TC_THREADS, 1) k_conv_tc(const __grid_constant
     k.lo_add = rt.add_relu_zp > PTQ_QMIN ? rt.add_relu_zp : PTQ_QMIN;
     k.clo = 0x80000000u - (uint32_t)rt.aclamp;
     k.chi = 0x80000000u + (uint32_t)rt.aclamp;
+    k.zc_bias = 0x80000000u - (uint32_t)(a.conv_is_a ? rt.za : rt.zb);
+    k.zs_bias = 0x80000000u - (uint32_t)(a.conv_is_a ? rt.zb : rt.za);
+    k.rc = a.conv_is_a ? rt.ra : rt.rb;
+    k.rs = a.conv_is_a ? rt.rb : rt.ra;
     const int Cout = a.L.cout;
     // stage the fused-add table (or the per-channel constants) in shared memory, then sync
     // the 12 epilogue warps only
@@ -693,7 +740,7 @@ int conv_tc_bn_for(int cout) {
 }
 
 static int g_num_sms = 0;
-static int g_kwr_mode = 0;   // -1 disables the kw-reuse slabs (A/B testing)
+static int g_kwr_mode = 0;   // -1 disables the kw-reuse slabs and the stem slab (A/B testing)
 void conv_tc_set_kwr_mode(int m) { g_kwr_mode = m; }
 
 template <int BN>
@@ -767,6 +814,16 @@ static bool setup_tma_a(ConvTcArgs& a) {
   EncodeTiledFn fn = encode_tiled();
   if (!fn) return false;
   if (Cp == 16 && a.k == 4 && a.OH <= Hp - 3 && a.OW <= Wp - 3) {
+    if (g_kwr_mode >= 0 && (Wp + TC_BM + 3) * 16 <= TC_A_STAGE) {
+      // preferred: one contiguous bulk copy per stage (the input buffer carries the slack
+      // the last tiles read past the grid; those rows only feed masked outputs)
+      a.tma_a = 67;
+      a.OHr = a.OH;
+      a.OWr = a.OW;
+      a.OH = Hp;
+      a.OW = Wp;
+      return true;
+    }
     // preferred: overlapping 64-byte rows (4 consecutive 16-byte pixels) as a 2-D map with a
     // 16-byte row stride, loaded as SWIZZLE_64B boxes like the Cp == 64 path
     {

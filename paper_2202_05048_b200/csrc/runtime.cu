@@ -652,7 +652,11 @@ void ensure_eval_buffers(ptq_ctx* c) {
     const TensorI& x = c->tens[t];
     const int h = (t == 0 && c->s2d_node >= 0) ? x.h / 2 : x.h, w = (t == 0 && c->s2d_node >= 0) ? x.w / 2 : x.w;
     int64_t bytes = chunk * (int64_t)(h + 2 * c->halo[t]) * (w + 2 * c->halo[t]) * c->cpad[t];
-    c->d_codes[t] = c->dalloc<int8_t>(bytes);
+    // the stem's slab copies (k_conv_tc A mode 67) of the last tile read up to one tile plus
+    // k-1 padded rows past the grid
+    const int64_t slack = (t == 0 && c->s2d_node >= 0)
+                              ? ((int64_t)c->s2d_k * (w + 2 * c->halo[t]) + 2 * 128) * c->cpad[t] : 0;
+    c->d_codes[t] = c->dalloc<int8_t>(bytes + slack);
     CK(cudaMemsetAsync(c->d_codes[t], 0, bytes, c->st));
     maxP = std::max<int64_t>(maxP, chunk * (int64_t)(h + 2 * c->halo[t]) * (w + 2 * c->halo[t]));
   }
