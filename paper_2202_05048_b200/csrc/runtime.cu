@@ -150,6 +150,10 @@ struct ptq_ctx {
   std::vector<char> clip_set;            // [3][2]
   float* d_act_scale = nullptr;          // [24][T]
   int* d_act_zp = nullptr;
+  uint64_t act_gen = 0;                  // bumped whenever the activation-parameter table is rewritten
+  // the graph input's codes currently in d_codes[0]: (variant, act_gen, first image, images,
+  // buffer) -- configs that share the input's quantization parameters reuse them
+  struct { int v = -1; uint64_t gen = 0; int64_t img0 = -1; int B = -1; const int8_t* buf = nullptr; } inq;
   bool prepared = false;
   bool static_ready = false;             // weight variants + eval buffers + mixed prefix enqueued
   bool wzp_pending = false;              // h_zp holds weight zero points not yet scanned
@@ -706,6 +710,7 @@ void prepare(ptq_ctx* c) {
     c->d_act_zp = c->dalloc<int>((size_t)24 * T);
   }
   launch_act_params(d_r, d_vs, 24, T, c->d_act_scale, c->d_act_zp, c->st);
+  ++c->act_gen;
   check_launch(c);
   prepare_static(c);
   CK(cudaStreamSynchronize(c->st));
@@ -880,12 +885,19 @@ void eval_one(ptq_ctx* c, const ptq_config& cfg, unsigned long long* d_correct, 
     // graph input / mixed prefix
     int start = 0;
     if (!cfg.mixed) {
-      if (c->s2d_node >= 0)
-        launch_quant_input_s2d(c->d_imgs, c->n_calib + img0, c->tens[0].c, V(0), as, az, P.psrc[0], c->st);
-      else
-        launch_quant_input(c->d_imgs, c->n_calib + img0, V(0), as, az, P.psrc[0], c->st);
-      check_launch(c);
-      halo_fill(0);
+      // the input codes depend only on the activation-parameter variant (its input entry):
+      // consecutive Mixed=Off configs of one (cache, scheme, clipping) quantize it once
+      const bool reuse = c->inq.v == v && c->inq.gen == c->act_gen && c->inq.img0 == img0 && c->inq.B == B &&
+                         c->inq.buf == c->d_codes[0] && P.psrc[0] == 0;
+      if (!reuse) {
+        if (c->s2d_node >= 0)
+          launch_quant_input_s2d(c->d_imgs, c->n_calib + img0, c->tens[0].c, V(0), as, az, P.psrc[0], c->st);
+        else
+          launch_quant_input(c->d_imgs, c->n_calib + img0, V(0), as, az, P.psrc[0], c->st);
+        check_launch(c);
+        halo_fill(0);
+        c->inq.v = v; c->inq.gen = c->act_gen; c->inq.img0 = img0; c->inq.B = B; c->inq.buf = c->d_codes[0];
+      }
       probe(0);
     } else {
       const int fc_ = c->first_compute;
