@@ -153,7 +153,9 @@ struct ptq_ctx {
   uint64_t act_gen = 0;                  // bumped whenever the activation-parameter table is rewritten
   // the graph input's codes currently in d_codes[0]: (variant, act_gen, first image, images,
   // buffer) -- configs that share the input's quantization parameters reuse them
-  struct { int v = -1; uint64_t gen = 0; int64_t img0 = -1; int B = -1; const int8_t* buf = nullptr; } inq;
+  struct CodesKey { int v = -1; uint64_t gen = 0; int64_t img0 = -1; int B = -1; const int8_t* buf = nullptr; };
+  CodesKey inq;
+  CodesKey pq;                           // the same for the folded FirstLastFp32 prefix codes
   bool prepared = false;
   bool static_ready = false;             // weight variants + eval buffers + mixed prefix enqueued
   bool wzp_pending = false;              // h_zp holds weight zero points not yet scanned
@@ -898,6 +900,7 @@ void eval_one(ptq_ctx* c, const ptq_config& cfg, unsigned long long* d_correct, 
         halo_fill(0);
         c->inq.v = v; c->inq.gen = c->act_gen; c->inq.img0 = img0; c->inq.B = B; c->inq.buf = c->d_codes[0];
       }
+      c->pq.v = -1;                                // this plan writes the prefix's pooled codes
       probe(0);
     } else {
       const int fc_ = c->first_compute;
@@ -906,13 +909,18 @@ void eval_one(ptq_ctx* c, const ptq_config& cfg, unsigned long long* d_correct, 
       if (pf >= 0 && P.psrc[c->nodes[pf].out] == P.psrc[c->nodes[fc_].out] && probe_t < 0) {
         // quantize maxpool(relu(prefix)) straight into the maxpool's output codes
         const int tp = c->nodes[pf].out;
-        launch_quant_nhwc(c->d_prefix_pool + img0 * c->tens[tp].elems, V(tp), as, az,
-                          P.psrc[c->nodes[fc_].out], -1, c->st);
-        check_launch(c);
-        halo_fill(tp);
+        const View vt = V(tp);
+        if (!(c->pq.v == v && c->pq.gen == c->act_gen && c->pq.img0 == img0 && c->pq.B == B && c->pq.buf == vt.p)) {
+          launch_quant_nhwc(c->d_prefix_pool + img0 * c->tens[tp].elems, vt, as, az,
+                            P.psrc[c->nodes[fc_].out], -1, c->st);
+          check_launch(c);
+          halo_fill(tp);
+          c->pq.v = v; c->pq.gen = c->act_gen; c->pq.img0 = img0; c->pq.B = B; c->pq.buf = vt.p;
+        }
         probe(tp);
         start = pf + 1;
       } else {
+        c->pq.v = -1;
         launch_quant_nhwc(c->d_prefix + img0 * c->tens[c->nodes[fc_].out].elems, V(mt), as, az,
                           P.psrc[c->nodes[fc_].out], P.relu_hist[fc_], c->st);
         check_launch(c);
@@ -1319,7 +1327,16 @@ int ptq_eval_configs(ptq_ctx* c, const ptq_config* cfgs, int32_t n_cfg, int64_t*
     for (int32_t b0 = 0; b0 < n_cfg; b0 += 4096) {
       const int nb = std::min<int32_t>(4096, n_cfg - b0);
       CK(cudaMemsetAsync(c->d_correct, 0, nb * sizeof(unsigned long long), c->st));
-      for (int i = 0; i < nb; ++i) {
+      // evaluation order: grouped by (mixed, cache, scheme, clipping) so configs that share
+      // the quantized graph input / prefix reuse it (results land in the caller's order)
+      std::vector<int> order(nb);
+      for (int i = 0; i < nb; ++i) order[i] = i;
+      auto key = [&](int i) {
+        const ptq_config& f = cfgs[b0 + i];
+        return ((f.mixed * 3 + f.cache) * 4 + f.scheme) * 2 + f.clipping;
+      };
+      std::stable_sort(order.begin(), order.end(), [&](int x, int y) { return key(x) < key(y); });
+      for (int i : order) {
         c->cur_cfg = b0 + i;
         eval_one(c, cfgs[b0 + i], c->d_correct + i, -1, nullptr);
       }

@@ -163,3 +163,21 @@ def test_integer_only_profile(ds64):
     want = [round(oev(c) * len(ds64.eval_labels)) for c in space]
     assert [int(x) for x in got] == want
     ev.close()
+
+
+def test_grid_batch_equals_isolated_configs(ds64):
+    """evaluate_many reorders a batch by (mixed, cache, scheme, clipping) and reuses the
+    quantized graph input / folded FirstLastFp32 prefix across configs that share them: the
+    whole grid in one batch must count exactly like every config evaluated on its own right
+    after a config of a different parameter variant (nothing left to reuse)."""
+    from paper_2202_05048_b200.evaluator import GpuEvaluator
+    g = build_model("resnet50", seed=0, shape=SHAPE)
+    ev = GpuEvaluator(g, ds64, 0, GENERIC)
+    space = enumerate_space(GENERIC)
+    batch = ev.correct_counts(space)
+    for i, cfg in enumerate(space):
+        other = next(c for c in space if (c.cache, c.scheme, c.clipping) != (cfg.cache, cfg.scheme, cfg.clipping)
+                     and c.mixed == cfg.mixed)
+        ev.correct_counts([other])
+        assert int(ev.correct_counts([cfg])[0]) == int(batch[i]), cfg
+    ev.close()
