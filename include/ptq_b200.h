@@ -115,6 +115,17 @@ int ptq_calib_histogram(ptq_ctx* ctx, const float* ranges, int64_t* counts);
 int ptq_kl_sweep(ptq_ctx* ctx, int32_t n_hist, const int64_t* counts, const float* ranges,
                  double* kl);
 
+/* EXTENSION (not in the reference: clipped_range rejects "Percentile", clipping.py:91-92;
+ * parity unpinned -- checked against oracle.percentile_range only).  Percentile clipping
+ * of n_hist histograms on the device, one CTA per histogram: out[h] = (edge[lo_idx],
+ * edge[hi_idx + 1]) with hi_idx = first bin whose cumulative count >= fl(q N), lo_idx =
+ * first bin whose cumulative count > fl(fl(1 - q) N), q = pct / 100, edges as numpy's
+ * histogram (calibration.py:81-91); lo == hi or empty histograms keep (lo, hi).  counts
+ * [n_hist][2048], ranges [n_hist][2] fp32, out [n_hist][2] fp64 -- the format
+ * ptq_set_clip_ranges takes. */
+int ptq_percentile_ranges(ptq_ctx* ctx, int32_t n_hist, const int64_t* counts, const float* ranges,
+                          double pct, double* out);
+
 /* Install the clipped ranges (clipped_range, clipping.py:89-96) for
  * (cache, clipping): ranges [T][2] fp64 (lo, hi). */
 int ptq_set_clip_ranges(ptq_ctx* ctx, int32_t cache, int32_t clipping, const double* ranges);

@@ -373,6 +373,28 @@ def clipped_range(h: Hist, mode: str) -> tuple[float, float]:
     return h.memo[mode]
 
 
+def percentile_range(counts, lo: float, hi: float, pct: float) -> tuple[float, float]:
+    """EXTENSION, not a restatement: the reference rejects "Percentile" clipping
+    (clipping.py:91-92), so this definition is ours and parity is unpinned (include/ptq_b200.h,
+    ptq_percentile_ranges).  With N = sum(counts), q = pct / 100 and cum the running count:
+    hi_idx = first bin with cum >= q N, lo_idx = first bin with cum > (1 - q) N; the range is
+    (edge[lo_idx], edge[hi_idx + 1]) on numpy's histogram edges (calibration.py:81-91).
+    Histograms the KL sweep skips (lo == hi or empty) keep (lo, hi)."""
+    counts = np.asarray(counts, dtype=np.int64).ravel()
+    lo, hi = float(lo), float(hi)
+    total = int(counts.sum())
+    if total == 0 or not lo < hi:
+        return (lo, hi)
+    q = float(pct) / 100.0
+    cum = np.cumsum(counts).astype(np.float64)
+    li = np.flatnonzero(cum > (1.0 - q) * float(total))
+    hj = np.flatnonzero(cum >= q * float(total))
+    li = int(li[0]) if li.size else N_BINS - 1
+    hj = int(hj[0]) if hj.size else N_BINS - 1
+    edges = np.linspace(lo, hi, N_BINS + 1)
+    return (float(edges[li]), float(edges[hj + 1]))
+
+
 # ---------------------------------------------------------------- quantize_model
 # ref: quantize.py:99-211
 

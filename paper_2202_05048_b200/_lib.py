@@ -25,7 +25,7 @@ KINDS = {"conv2d": 0, "depthwise_conv2d": 1, "pointwise_conv2d": 2, "fully_conne
 EXPORTS = ("ptq_last_error", "ptq_version", "ptq_create", "ptq_destroy", "ptq_num_tensors",
            "ptq_calibrate", "ptq_kl_sweep", "ptq_set_clip_ranges", "ptq_prepare",
            "ptq_eval_configs", "ptq_probe_codes", "ptq_probe_act_params", "ptq_histogram_host",
-           "ptq_export_layer",
+           "ptq_export_layer", "ptq_percentile_ranges",
            "ptq_set_option", "ptq_last_stats", "ptq_calib_forward", "ptq_calib_histogram",
            "ptq_stream", "ptq_conv_timings")
 
@@ -81,6 +81,7 @@ def load() -> C.CDLL:
         "ptq_calibrate": [P, i32, P, P, P, P, P],
         "ptq_kl_sweep": [P, i32, P, P, P],
         "ptq_set_clip_ranges": [P, i32, i32, P],
+        "ptq_percentile_ranges": [P, i32, P, P, C.c_double, P],
         "ptq_prepare": [P],
         "ptq_eval_configs": [P, C.POINTER(ConfigDesc), i32, P],
         "ptq_probe_codes": [P, C.POINTER(ConfigDesc), i32, P, C.POINTER(i64)],

@@ -442,6 +442,64 @@ void launch_histogram(const float* x, int64_t elems, const int* slots, int n_slo
   k_histogram<<<nblocks(total, 256, 148 * HIST_BLOCKS_PER_SM), 256, smem, s>>>(x, elems, slots, n_slots, range,
                                                                                counts);
 }
+// ---------------------------------------------------------------- F2b: percentile clipping
+// Extension (not in the reference, which rejects "Percentile": clipping.py:91-92): the
+// clipped range of a histogram keeps the central q = pct/100 of its mass.  With N = sum(c),
+// cum_i = c_0 + ... + c_i (exact int64):  hi_idx = first i with cum_i >= fl(q N),
+// lo_idx = first i with cum_i > fl(fl(1 - q) N);  range = (edge[lo_idx], edge[hi_idx + 1])
+// on numpy's linspace edges.  Histograms the KL sweep skips (lo == hi, N == 0) keep (lo, hi).
+// One CTA per histogram: 256 threads own 8 consecutive bins each, a block scan of the
+// per-thread sums, then each thread scans its bins and offers candidates by atomicMin.
+__global__ void __launch_bounds__(256) k_percentile(const long long* __restrict__ counts,
+                                                    const float* __restrict__ ranges, double q,
+                                                    double* __restrict__ out) {
+  __shared__ long long part[256];
+  __shared__ int idx[2];
+  const int h = blockIdx.x, t = threadIdx.x;
+  const long long* c = counts + (int64_t)h * PTQ_NBINS;
+  const double lo = (double)ranges[2 * h], hi = (double)ranges[2 * h + 1];
+  long long v[8], s = 0;
+#pragma unroll
+  for (int j = 0; j < 8; ++j) { v[j] = c[t * 8 + j]; s += v[j]; }
+  part[t] = s;
+  if (t == 0) { idx[0] = PTQ_NBINS; idx[1] = PTQ_NBINS; }
+  __syncthreads();
+  for (int d = 1; d < 256; d <<= 1) {                 // inclusive Hillis-Steele scan
+    const long long a = t >= d ? part[t - d] : 0;
+    __syncthreads();
+    part[t] += a;
+    __syncthreads();
+  }
+  const long long total = part[255];
+  if (total == 0 || !(lo < hi)) {
+    if (t == 0) { out[2 * h] = lo; out[2 * h + 1] = hi; }
+    return;
+  }
+  const double thr_hi = __dmul_rn(q, (double)total);
+  const double thr_lo = __dmul_rn(__dsub_rn(1.0, q), (double)total);
+  long long cum = part[t] - s;
+  bool got_lo = false, got_hi = false;
+#pragma unroll
+  for (int j = 0; j < 8; ++j) {
+    cum += v[j];
+    const double cd = (double)cum;                   // exact: total < 2^53
+    if (!got_lo && cd > thr_lo) { atomicMin(&idx[0], t * 8 + j); got_lo = true; }
+    if (!got_hi && cd >= thr_hi) { atomicMin(&idx[1], t * 8 + j); got_hi = true; }
+  }
+  __syncthreads();
+  if (t == 0) {
+    const int li = idx[0] < PTQ_NBINS ? idx[0] : PTQ_NBINS - 1;
+    const int hj = idx[1] < PTQ_NBINS ? idx[1] : PTQ_NBINS - 1;
+    out[2 * h] = hist_edge(lo, hi, li);
+    out[2 * h + 1] = hist_edge(lo, hi, hj + 1);
+  }
+}
+void launch_percentile(const long long* counts, const float* ranges, int n_hist, double q, double* out,
+                       cudaStream_t s) {
+  if (n_hist <= 0) return;
+  k_percentile<<<n_hist, 256, 0, s>>>(counts, ranges, q, out);
+}
+
 void launch_kl_sweep(const long long* counts, const float* ranges, int n_hist, double* cum,
                      int* nzc, double* logc, double* kl_out, cudaStream_t s) {
   if (n_hist <= 0) return;

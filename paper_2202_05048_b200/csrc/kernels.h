@@ -70,6 +70,8 @@ void launch_minmax_reduce_cache(const unsigned int* per_img, int n_tensors, int 
                                 const int* slots, int n_slots, float* ranges, cudaStream_t s);
 void launch_histogram(const float* x, int64_t elems, const int* slots, int n_slots,
                       const float* range, unsigned long long* counts, cudaStream_t s);
+void launch_percentile(const long long* counts, const float* ranges, int n_hist, double q, double* out,
+                       cudaStream_t s);
 void launch_kl_sweep(const long long* counts, const float* ranges, int n_hist, double* cum,
                      int* nzc, double* logc, double* kl_out, cudaStream_t s);
 

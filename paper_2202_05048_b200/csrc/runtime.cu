@@ -1296,6 +1296,26 @@ int ptq_kl_sweep(ptq_ctx* c, int32_t n_hist, const int64_t* counts, const float*
   });
 }
 
+int ptq_percentile_ranges(ptq_ctx* c, int32_t n_hist, const int64_t* counts, const float* ranges, double pct,
+                          double* out) {
+  return guarded([&] {
+    REQ(c && counts && ranges && out && n_hist >= 0, "null argument");
+    REQ(pct > 0.0 && pct <= 100.0, "percentile must be in (0, 100]");
+    if (n_hist == 0) return;
+    CK(cudaSetDevice(c->dev));
+    long long* d_c = c->dalloc<long long>((size_t)n_hist * PTQ_NBINS);
+    float* d_r = c->dalloc<float>((size_t)n_hist * 2);
+    double* d_o = c->dalloc<double>((size_t)n_hist * 2);
+    CK(cudaMemcpyAsync(d_c, counts, (size_t)n_hist * PTQ_NBINS * 8, cudaMemcpyHostToDevice, c->st));
+    CK(cudaMemcpyAsync(d_r, ranges, (size_t)n_hist * 2 * sizeof(float), cudaMemcpyHostToDevice, c->st));
+    launch_percentile(d_c, d_r, n_hist, pct / 100.0, d_o, c->st);
+    check_launch(c);
+    CK(cudaMemcpyAsync(out, d_o, (size_t)n_hist * 2 * sizeof(double), cudaMemcpyDeviceToHost, c->st));
+    CK(cudaStreamSynchronize(c->st));
+    for (void* p : {(void*)d_c, (void*)d_r, (void*)d_o}) c->dfree(p);
+  });
+}
+
 int ptq_set_clip_ranges(ptq_ctx* c, int32_t cache, int32_t clipping, const double* ranges) {
   return guarded([&] {
     REQ(c && ranges && cache >= 0 && cache < 3 && clipping >= 0 && clipping < 2, "bad argument");

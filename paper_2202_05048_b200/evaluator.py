@@ -283,6 +283,31 @@ class GpuEvaluator:
         with _trace("prepare"):
             _lib.check(self.lib.ptq_prepare(self._ctx))
 
+    # ------------------------------------------------------------ extension: percentile clipping
+    def percentile_ranges(self, pct: float) -> np.ndarray:
+        """EXTENSION, not in the reference (clipped_range rejects "Percentile",
+        clipping.py:91-92; parity unpinned, checked against oracle.percentile_range): the
+        device percentile clipping of every cache/tensor histogram, [3, T, 2] fp64."""
+        out = np.zeros((3 * self.T, 2), dtype=np.float64)
+        _lib.check(self.lib.ptq_percentile_ranges(self._ctx, 3 * self.T, _lib.ptr(self.cache_counts),
+                                                  _lib.ptr(self.cache_ranges), float(pct), _lib.ptr(out)))
+        return out.reshape(3, self.T, 2)
+
+    def correct_counts_percentile(self, cfgs, pct: float) -> np.ndarray:
+        """EXTENSION: evaluate configs with percentile-clipped activation ranges in place of
+        the clipping each config names (the KL slot is borrowed and restored afterwards)."""
+        import dataclasses
+        pr = self.percentile_ranges(pct)
+        cfgs = [dataclasses.replace(c, clipping="KL") for c in cfgs]
+        try:
+            for k in range(3):
+                _lib.check(self.lib.ptq_set_clip_ranges(self._ctx, k, 1, _lib.ptr(np.ascontiguousarray(pr[k]))))
+            return self.correct_counts(cfgs)
+        finally:
+            for k in range(3):
+                _lib.check(self.lib.ptq_set_clip_ranges(self._ctx, k, 1,
+                                                        _lib.ptr(np.ascontiguousarray(self.kl_ranges[k]))))
+
     # ------------------------------------------------------------ evaluation
     def _check_cfg(self, cfg) -> None:
         if not isinstance(cfg, QuantConfig):

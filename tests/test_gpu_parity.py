@@ -278,3 +278,33 @@ def test_save_qtm8_matches_reference_file(injected, rec, tmp_path):
         blob = path.read_bytes()
         assert len(blob) == ref["qtm8"][key]["bytes"], key
         assert hashlib.sha256(blob).hexdigest() == ref["qtm8"][key]["sha256"], key
+
+
+@pytest.mark.parametrize("rec", TOYS)
+def test_percentile_matches_oracle(injected, golden, ds, toys, rec):
+    """EXTENSION (the reference rejects "Percentile", clipping.py:91-92; parity unpinned):
+    the device percentile clipping equals oracle.percentile_range bit-for-bit on the
+    reference's histograms, and top-1 with those ranges equals the oracle's (Mixed=Off);
+    the KL slot the extension borrows is restored afterwards."""
+    arrs, meta = golden
+    ev = injected[rec]
+    T, ranges, counts, _, _ = golden_caches(golden, rec)
+    for pct in (90.0, 99.0, 99.9, 99.99, 100.0):
+        got = ev.percentile_ranges(pct)
+        for k in range(3):
+            for i in range(T):
+                want = O.percentile_range(counts[k, i], ranges[k, i, 0], ranges[k, i, 1], pct)
+                assert (float(got[k, i, 0]), float(got[k, i, 1])) == want, (pct, k, i)
+    space = [c for c in enumerate_space(GENERIC) if c.clipping == "KL" and c.mixed == "Off"]
+    kl_before = ev.correct_counts(space)
+    pr = ev.percentile_ranges(99.9)
+    caches = oracle_caches(golden, rec)
+    for k, sc in enumerate(CACHE_SIZES):
+        for i, t in enumerate(meta["cache_tensors"][f"{rec}/{sc}"]):
+            caches[sc][t].memo["KL"] = (float(pr[k, i, 0]), float(pr[k, i, 1]))
+    oev = O.make_accuracy_evaluator(toys[rec], ds, 0, caches=caches)
+    got = ev.correct_counts_percentile(space, 99.9)
+    n = len(ds.eval_labels)
+    for c, g in zip(space[::4], got[::4]):
+        assert int(g) == round(oev(c) * n), c
+    assert np.array_equal(ev.correct_counts(space), kl_before)
