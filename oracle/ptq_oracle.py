@@ -635,3 +635,147 @@ def make_accuracy_evaluator(g, d, seed: int, caches: dict | None = None):
 
     evaluate.caches = caches
     return evaluate
+
+
+# ---------------------------------------------------------------- integer-only executor
+# ref: intexec.py:40-64 (OpTrace), :88-92 (_exact_log2), :115-145, :354-359,
+# :369-398 (fuse_conv_relu); pinned by tests/golden/gen_intonly_golden.py
+
+FLOAT_CATS = ("float_mul", "float_add", "float_kernel")
+
+
+class IntegerOnlyError(ValueError):
+    """ref: intexec.py:43."""
+
+
+@dataclass
+class OpTrace:
+    """(node id, op category) events in execution order (ref: intexec.py:47-64)."""
+    events: list = field(default_factory=list)
+
+    def add(self, node_id, *cats):
+        self.events.extend((node_id, c) for c in cats)
+
+    def float_ops(self) -> int:
+        return sum(1 for _, c in self.events if c in FLOAT_CATS)
+
+    def to_csv(self) -> str:
+        return "\n".join(["node,category"] + [f"{n},{c}" for n, c in self.events]) + "\n"
+
+
+@dataclass
+class _N:
+    id: str
+    kind: str
+    inputs: list
+    output: str
+    attrs: dict
+
+
+@dataclass
+class _G:
+    nodes: list
+    weights: dict
+
+
+def fuse_graph(g):
+    """Compute -> sole-relu pairs merged into one node with fused_relu (ref: intexec.py:369-398)."""
+    fuse = {}
+    for n in g.nodes:
+        if n.kind in COMPUTE_KINDS:
+            cons = _consumers(g, n.output)
+            if len(cons) == 1 and cons[0].kind == "relu":
+                fuse[n.id] = cons[0]
+    drop = {r.id for r in fuse.values()}
+    nodes = [_N(n.id, n.kind, list(n.inputs), fuse[n.id].output if n.id in fuse else n.output,
+                {**dict(n.attrs), **({"fused_relu": True} if n.id in fuse else {})})
+             for n in g.nodes if n.id not in drop]
+    return _G(nodes, g.weights)
+
+
+def exact_log2(scale: float) -> int:
+    """ref: intexec.py:88-92."""
+    k = ceil_log2(scale)
+    if 2.0 ** k != scale:
+        raise IntegerOnlyError(f"scale {scale} is not a power of two")
+    return k
+
+
+def check_integer_only(qm: QModel) -> None:
+    """ref: intexec.py:132-145."""
+    cfg = qm.cfg
+    scheme = _scheme_name(cfg.scheme)
+    if scheme != "SymmetricPower2" or cfg.granularity != "Tensor" or cfg.mixed != "Off":
+        raise IntegerOnlyError(
+            "integer-only execution requires scheme=SymmetricPower2, granularity=Tensor, mixed=Off; "
+            f"got {scheme}/{cfg.granularity}/{cfg.mixed}")
+    for n in qm.graph.nodes:
+        if n.kind == "avgpool":
+            area = int(n.attrs["kernel"]) ** 2
+            if area & (area - 1):
+                raise IntegerOnlyError(f"avgpool {n.id}: area {area} not a power of two")
+
+
+def run_integer_only(qm: QModel, batch, trace: OpTrace | None = None) -> np.ndarray:
+    """Strict integer program: mul/add/shift/clamp only (ref: intexec.py:148-359 with
+    integer_only=True).  ``qm.graph`` is the graph as executed (pass a fuse_graph()
+    graph for fusion=True).  Returns int8 output codes."""
+    check_integer_only(qm)
+    g = qm.graph
+    tr = trace if trace is not None else OpTrace()
+    env = {INPUT: quantize_array(np.asarray(batch, dtype=np.float32), qm.act[INPUT]).astype(np.int64)}
+    for n in g.nodes:
+        x = env[n.inputs[0]]
+        k = n.kind
+        if k in COMPUTE_KINDS:                         # ref: intexec.py:170-211
+            wid = n.inputs[1]
+            pw, pin, pout = qm.wparams[wid], qm.act[n.inputs[0]], qm.act[n.output]
+            ws = qm.wcodes[wid].astype(np.int64) - int(np.asarray(pw.zp))
+            acc = int_conv(k, x - int(pin.zp), ws, int(n.attrs.get("stride", 1)), int(n.attrs.get("padding", 0)))
+            tr.add(n.id, "int_mul", "int_add")
+            if len(n.inputs) > 2:
+                b = qm.bias[n.inputs[2]].astype(np.int64)
+                acc = acc + (_pc(b, acc.ndim) if acc.ndim == 4 else b)
+                tr.add(n.id, "int_add")
+            acc = np.clip(acc, INT32_MIN, INT32_MAX)
+            s = exact_log2(float(pout.scale)) - exact_log2(float(pin.scale)) - exact_log2(float(pw.scale))
+            out = requantize_shift(acc, s, int(pout.zp))
+            tr.add(n.id, "int_add", "shift", "clamp")
+            if n.attrs.get("fused_relu"):
+                out = np.maximum(out, np.int8(pout.zp))
+                tr.add(n.id, "clamp")
+            out = out.astype(np.int64)
+        elif k == "relu":
+            out = np.maximum(x, int(qm.act[n.output].zp))
+            tr.add(n.id, "clamp")
+        elif k == "maxpool":
+            ks = int(n.attrs["kernel"])
+            out = _win(x, ks, int(n.attrs.get("stride", ks)), 0).max(axis=(-1, -2))
+        elif k == "avgpool":                           # ref: intexec.py:225-243
+            ks = int(n.attrs["kernel"])
+            zp = int(qm.act[n.output].zp)
+            tot = _win(x, ks, int(n.attrs.get("stride", ks)), 0).sum(axis=(-1, -2))
+            out = requantize_shift(tot - zp * ks * ks, exact_log2(float(ks * ks)), zp).astype(np.int64)
+            tr.add(n.id, "int_add", "shift", "clamp")
+        elif k == "add":                               # ref: intexec.py:256-265
+            y = env[n.inputs[1]]
+            po, pa, pb = qm.act[n.output], qm.act[n.inputs[0]], qm.act[n.inputs[1]]
+            ka, kb, ko = exact_log2(float(pa.scale)), exact_log2(float(pb.scale)), exact_log2(float(po.scale))
+            kmin = min(ka, kb)
+            acc = ((x - int(pa.zp)) << (ka - kmin)) + ((y - int(pb.zp)) << (kb - kmin))
+            out = requantize_shift(acc, ko - kmin, int(po.zp)).astype(np.int64)
+            tr.add(n.id, "int_add", "shift", "int_add", "shift", "int_add", "shift", "clamp")
+        elif k == "concat":                            # ref: intexec.py:115-129
+            po = qm.act[n.output]
+            parts = []
+            for t in n.inputs:
+                s = exact_log2(float(po.scale)) - exact_log2(float(qm.act[t].scale))
+                parts.append(requantize_shift(env[t] - int(qm.act[t].zp), s, int(po.zp)).astype(np.int64))
+                tr.add(n.id, "int_add", "shift", "clamp")
+            out = np.concatenate(parts, axis=1)
+        elif k == "softmax":
+            out = x
+        else:
+            raise ValueError(k)
+        env[n.output] = out
+    return env[_output_tensor(g)].astype(np.int8)

@@ -35,6 +35,17 @@ def shard(seq, rank: int, n: int):
     return list(seq)[rank::n]
 
 
+def eval_slice(n_eval: int, rank: int, n: int) -> tuple[int, int]:
+    """Contiguous [lo, hi) share of the eval split for image-sharded evaluation
+    (the sequential xgb / GA searches, tuner.py:251-281, evaluate one
+    config at a time, so their ranks split the eval images and SUM the correct
+    counts)."""
+    lo, hi = n_eval * rank // n, n_eval * (rank + 1) // n
+    if hi <= lo:
+        raise ValueError(f"rank {rank} of {n} has no eval images (n_eval={n_eval})")
+    return lo, hi
+
+
 def _tensor(a: np.ndarray):
     import torch
     import torch.distributed as dist

@@ -194,7 +194,7 @@ class GpuEvaluator:
     """Callable ``QuantConfig -> top-1`` backed by one B200 context."""
 
     def __init__(self, g, d, seed: int, profile: TargetProfile | None = None, *, device: int = 0,
-                 eval_chunk: int | None = None, calibrate: bool = True):
+                 eval_chunk: int | None = None, calibrate: bool = True, image_sharded: bool = False):
         self.lib = _lib.load()
         self.graph, self.profile, self.seed = g, profile, seed
         self.lowered = LoweredGraph(g)
@@ -207,6 +207,20 @@ class GpuEvaluator:
         self._coalescer = None
         imgs = np.ascontiguousarray(np.asarray(d.images, dtype=np.float32))
         labels = np.ascontiguousarray(np.asarray(d.labels[d.n_calib:], dtype=np.int64))
+        # image-sharded mode (sequential xgb / GA search): every rank keeps all
+        # calibration images and a contiguous slice of the eval split; correct counts are
+        # SUM-allreduced per config, so each config costs 1/world of the images per GPU
+        self.image_sharded = False
+        if image_sharded:
+            from . import dist
+            rank, world = dist.world()
+            if world > 1:
+                lo, hi = dist.eval_slice(self.n_eval, rank, world)
+                imgs = np.ascontiguousarray(np.concatenate([imgs[: self.n_calib],
+                                                            imgs[self.n_calib + lo: self.n_calib + hi]]))
+                labels = np.ascontiguousarray(labels[lo:hi])
+                self.image_sharded = True
+        self.n_eval_local = int(len(labels))
         if tuple(imgs.shape[1:]) != tuple(int(v) for v in g.input_shape):
             raise ValueError(f"dataset shape {imgs.shape[1:]} does not match graph input {g.input_shape}")
         self._ctx = C.c_void_p()
@@ -328,7 +342,11 @@ class GpuEvaluator:
         return out[: len(cfgs)]
 
     def evaluate_many(self, cfgs) -> list[float]:
-        return [int(c) / float(self.n_eval) for c in self.correct_counts(cfgs)]
+        counts = self.correct_counts(cfgs)
+        if self.image_sharded:
+            from . import dist
+            counts = dist.allreduce(counts, "sum")
+        return [int(c) / float(self.n_eval) for c in counts]
 
     def __call__(self, cfg) -> float:
         # concurrent callers (measure_many's thread pool, tuner.py:192-203) are coalesced
@@ -351,6 +369,16 @@ class GpuEvaluator:
             _lib.check(self.lib.ptq_probe_codes(self._ctx, C.byref(cd), tid, _lib.ptr(out), C.byref(n)))
         return out
 
+    def run_quantized_codes(self, cfg) -> np.ndarray:
+        """Output codes of the eval set (intexec.run_quantized(..., return_codes=True))."""
+        from .intonly import run_quantized_codes
+        return run_quantized_codes(self, cfg)
+
+    def run_integer_only(self, cfg, trace=None) -> np.ndarray:
+        """intexec.run_integer_only (intexec.py:354-359) from device state; see intonly.py."""
+        from .intonly import run_integer_only
+        return run_integer_only(self, cfg, trace)
+
     def save_cache(self, path: str, size_class: str, meta: dict | None = None) -> None:
         """Write one calibration cache of this evaluator as the reference's ``.qcal``
         (calibration.py:115-134), byte-identical to ptqtune.save_cache of the same cache."""
@@ -370,6 +398,8 @@ class GpuEvaluator:
         """Correct counts of every config, configs dealt round-robin over ranks."""
         from . import dist
         cfgs = list(cfgs)
+        if self.image_sharded:
+            return dist.allreduce(self.correct_counts(cfgs), "sum")
         rank, n = dist.world()
         mine = self.correct_counts(dist.shard(cfgs, rank, n))
         return dist.gather_counts(mine, len(cfgs))
@@ -413,6 +443,11 @@ class GpuEvaluator:
 
 
 def make_accuracy_evaluator(g, d, seed: int, profile: TargetProfile | None = None, *,
-                            device: int = 0, eval_chunk: int | None = None) -> GpuEvaluator:
-    """Drop-in for ptqtune.tuner.make_accuracy_evaluator (tuner.py:434-444)."""
-    return GpuEvaluator(g, d, seed, profile, device=device, eval_chunk=eval_chunk)
+                            device: int = 0, eval_chunk: int | None = None,
+                            image_sharded: bool = False) -> GpuEvaluator:
+    """Drop-in for ptqtune.tuner.make_accuracy_evaluator (tuner.py:434-444).
+    ``image_sharded=True`` under torch.distributed splits the eval images over the ranks
+    (for the one-config-at-a-time xgb / GA searches); every rank must then evaluate the
+    same configs in the same order."""
+    return GpuEvaluator(g, d, seed, profile, device=device, eval_chunk=eval_chunk,
+                        image_sharded=image_sharded)
