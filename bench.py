@@ -142,6 +142,59 @@ def cpu_baseline(g, d, n_imgs: int) -> dict:
             "extrapolated_step_s": total}
 
 
+def _reference_pkg():
+    """The unmodified reference (ptqtune) from the offline install in baseline/_ref, or None."""
+    ref = os.path.join(os.path.dirname(os.path.abspath(__file__)), "baseline", "_ref")
+    if not os.path.isdir(os.path.join(ref, "ptqtune")):
+        return None
+    if ref not in sys.path:
+        sys.path.insert(0, ref)
+    import ptqtune
+    return ptqtune
+
+
+def cpu_baseline_reference(g, d, n_imgs: int) -> dict | None:
+    """The same bounded sample as cpu_baseline, run through the REFERENCE's own functions
+    (ptqtune.calibration.calibrate, clipping.clip_range_kl, quantize.quantize_model,
+    intexec.run_quantized) from baseline/_ref, extrapolated the same way."""
+    R = _reference_pkg()
+    if R is None:
+        return None
+    from ptqtune import calibration as RC
+    from ptqtune import clipping as RK
+    from ptqtune import intexec as RI
+    from ptqtune import quantize as RQ
+    from ptqtune import tuner as RT
+    space = RT.enumerate_space(RT.TargetProfile("Generic"))
+    n_union = len(set(np.concatenate([RC.select_images(d.calib_images, sc, 0) for sc in ("S1", "S2", "S3")])))
+    t0 = time.perf_counter()
+    cache = RC.calibrate(g, d.images[:n_imgs], model_name=g.name)
+    t_cal_img = (time.perf_counter() - t0) / n_imgs
+    hs = [h for h in cache.histograms.values() if h.min_seen != h.max_seen][:6]
+    t0 = time.perf_counter()
+    for h in hs:
+        RK.clip_range_kl(h)
+    t_kl = (time.perf_counter() - t0) / max(1, len(hs))
+    T = len(cache.histograms)
+    cfg = space[2]                                           # S1 / Asymmetric / Max / Channel / Off
+    t0 = time.perf_counter()
+    qg = RQ.quantize_model(g, cache, cfg)
+    t_q = time.perf_counter() - t0
+    t0 = time.perf_counter()
+    RI.run_quantized(qg, d.eval_images[:n_imgs])
+    t_eval_img = (time.perf_counter() - t0) / n_imgs
+    n_eval = len(d.eval_images)
+    total = n_union * t_cal_img + 3 * T * t_kl + len(space) * (t_q + n_eval * t_eval_img)
+    return {"value": len(space) / total, "unit": UNIT, "cores": os.cpu_count(), "kind": "reference",
+            "sample": (f"reference ptqtune (baseline/_ref, numpy/OpenBLAS, {os.cpu_count()} threads): "
+                       f"calibrate() of {n_imgs} images ({t_cal_img:.2f} s/img), clip_range_kl of "
+                       f"{len(hs)} histograms ({t_kl:.3f} s each), quantize_model of 1 config "
+                       f"({t_q:.2f} s), run_quantized of {n_imgs} eval images ({t_eval_img:.3f} s/img); "
+                       f"extrapolated linearly to {n_union} calibration images, {3 * T} histograms, "
+                       f"{len(space)} configs x {n_eval} images = {total:.0f} s per full grid"),
+            "extrapolated_step_s": total}
+
+
 # ---------------------------------------------------------------- reference arm
 def run_reference(args):
     import torch.distributed as dist
@@ -151,7 +204,8 @@ def run_reference(args):
     g, d = workload(args.model, args.n_eval)
     vals = []
     for _ in range(max(1, args.steps)):
-        vals.append(cpu_baseline(g, d, args.cpu_sample_imgs))
+        vals.append(cpu_baseline_reference(g, d, args.cpu_sample_imgs)
+                    or cpu_baseline(g, d, args.cpu_sample_imgs))
     v = float(np.median([x["value"] for x in vals]))
     cb = dict(vals[-1])
     cb["value"] = v
@@ -282,7 +336,7 @@ def run_b200(args):
     if rank == 0:
         cb = None
         if world == 1 and not args.no_cpu_baseline:
-            cb = cpu_baseline(g, d, args.cpu_sample_imgs)
+            cb = cpu_baseline_reference(g, d, args.cpu_sample_imgs) or cpu_baseline(g, d, args.cpu_sample_imgs)
             cb.pop("extrapolated_step_s", None)
         best = int(np.argmax(counts))
         line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
