@@ -46,11 +46,13 @@ def test_fast_paths_equal_plain_path(ev224):
         ev224.set_option("tma", 0)
         ev224.set_option("kwr", -1)
         ev224.set_option("fusion", 0)
+        ev224.set_option("subsample", 0)
         plain = ev224.correct_counts(picks)
     finally:
         ev224.set_option("tma", 1)
         ev224.set_option("kwr", 0)
         ev224.set_option("fusion", 1)
+        ev224.set_option("subsample", 1)
     assert np.array_equal(fast, plain)
     assert np.all((fast >= 0) & (fast <= 1000))
 
@@ -65,3 +67,22 @@ def test_tc_conv_equals_reference_conv_fullsize(ev224):
     finally:
         ev224.set_option("conv_ref", 0)
     assert np.array_equal(tc, ref)
+
+
+def test_strided_1x1_subsample_codes_bit_exact(ev224):
+    """The downsample shortcuts (1x1, stride 2) run as subsample + pointwise TMA GEMM; their
+    output codes must equal the direct strided gather path bit for bit (zw = 0 and != 0)."""
+    space = enumerate_space(GENERIC)
+    g = ev224.graph
+    shortcuts = [n for n in g.nodes if n.kind == "conv2d" and int(n.attrs.get("kernel", 0) or
+                 np.asarray(g.weights[n.inputs[1]]).shape[-1]) == 1 and int(n.attrs.get("stride", 1)) > 1]
+    assert len(shortcuts) == 3
+    for ci in (0, 2):
+        for n in shortcuts:
+            fast = ev224.probe_codes(space[ci], n.output)
+            try:
+                ev224.set_option("subsample", 0)
+                plain = ev224.probe_codes(space[ci], n.output)
+            finally:
+                ev224.set_option("subsample", 1)
+            assert np.array_equal(fast, plain), (ci, n.id)
