@@ -730,10 +730,30 @@ __global__ void k_im2col_ck(View in, int stride, int pad, int OH, int OW, int8_t
   }
 }
 
+// strided 1x1 conv input (the ResNet downsample shortcuts): subsample the pixel grid into a
+// dense halo-free [pixels][C] buffer, one thread per 16-byte chunk, so the conv runs as a
+// stride-1 pointwise GEMM on the TMA path (int4 loads / stores, coalesced per pixel row)
+__global__ void k_subsample(View in, int stride, int OH, int OW, int8_t* __restrict__ out, int nch,
+                            int64_t total) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < total;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    const int j = (int)(i % nch);
+    const int64_t m = i / nch;
+    const int ow = (int)(m % OW);
+    const int64_t t = m / OW;
+    const int oh = (int)(t % OH), n = (int)(t / OH);
+    const int4 v = __ldg(reinterpret_cast<const int4*>(in.p + voff(in, n, oh * stride, ow * stride) + j * 16));
+    *reinterpret_cast<int4*>(out + m * (int64_t)nch * 16 + j * 16) = v;
+  }
+}
+
 void launch_im2col(View in, int k, int stride, int pad, int OH, int OW, int8_t* out, int out_cp,
                    cudaStream_t s) {
   const int64_t pixels = (int64_t)in.N * OH * OW;
-  if (in.C == 3 && k == 7) {
+  if (k == 1 && pad == 0 && in.C % 16 == 0 && out_cp == in.C && in.Cp % 16 == 0) {
+    const int64_t total = pixels * (in.C >> 4);
+    k_subsample<<<nblk(total), 256, 0, s>>>(in, stride, OH, OW, out, in.C >> 4, total);
+  } else if (in.C == 3 && k == 7) {
     k_im2col_ck<3, 7><<<nblk(pixels, 128), 128, 0, s>>>(in, stride, pad, OH, OW, out, pixels);
   } else if (in.C == 3 && k == 3) {
     k_im2col_ck<3, 3><<<nblk(pixels, 128), 128, 0, s>>>(in, stride, pad, OH, OW, out, pixels);

@@ -92,6 +92,7 @@ struct WeightsDev {
   int cout = 0, cin = 0, k = 1, fc_hw = 0, cin_p = 0;
   int bn = 0, n_kiter = 0, n_chunks = 0, kreal = 0;
   bool im2col = false;          // few-channel conv: packed im2col + 1x1 tensor-core GEMM
+  bool sub1x1 = false;          // strided 1x1 conv: subsampled input + stride-1 pointwise GEMM
   int im_cp = 0;                // im2col row pitch (k*k*Cin rounded up to 16)
   int q_cin_p = 0, q_k = 1, q_fc_hw = 0;   // weight-quantizer view of the K layout
   float* f32_gemm = nullptr;    // [K][cout] fp32 (NHWC K order) for the fp32 path, or dw [C][k*k]
@@ -180,7 +181,7 @@ struct ptq_ctx {
   std::vector<int*> cal_slots;
   std::vector<int> cal_sizes;
   // options
-  int conv_ref = 0, fusion = 1, time_conv = 0, ablate = 0, tma = 1;
+  int conv_ref = 0, fusion = 1, time_conv = 0, ablate = 0, tma = 1, subsample = 1;
   int64_t opt_chunk = 0;
   // stats
   int64_t launches = 0;
@@ -392,6 +393,12 @@ void import_graph(ptq_ctx* c, const ptq_graph_desc* g) {
         wd.q_cin_p = x.c;
         wd.q_k = 1;
         wd.q_fc_hw = kk * kk;
+      }
+      if (!s2d && !wd.im2col && n.kind == PTQ_CONV && kk == 1 && n.stride > 1 && n.pad == 0 &&
+          x.c % 16 == 0 && wd.cin_p == x.c) {
+        // same K layout as a pointwise conv (kb = ch), so the weight tiles need no change
+        wd.sub1x1 = true;
+        wd.im_cp = x.c;
       }
       wd.n_kiter = (wd.n_chunks + 7) / 8;
       REQ(wd.cout <= conv_tc_max_cout(), "conv / fc output channels exceed the tensor-core conv limit (2048)");
@@ -673,13 +680,13 @@ void ensure_eval_buffers(ptq_ctx* c) {
   for (int t : need32) c->d_f32[t] = c->dalloc<float>(chunk * c->tens[t].elems);
   int64_t im_bytes = 0;
   for (int i = 0; i < (int)c->nodes.size(); ++i)
-    if (c->W[i].im2col)
+    if (c->W[i].im2col || c->W[i].sub1x1)
       im_bytes = std::max<int64_t>(im_bytes, chunk * (int64_t)c->tens[c->nodes[i].out].h *
                                                  c->tens[c->nodes[i].out].w * c->W[i].im_cp);
   c->dfree(c->d_im2col);
   c->d_im2col = im_bytes ? c->dalloc<int8_t>(im_bytes) : nullptr;
   for (int i = 0; i < (int)c->nodes.size(); ++i)
-    if (c->W[i].im2col)
+    if (c->W[i].im2col || c->W[i].sub1x1)
       maxP = std::max<int64_t>(maxP, chunk * (int64_t)c->tens[c->nodes[i].out].h * c->tens[c->nodes[i].out].w);
   c->d_P = c->dalloc<int>(maxP);
   c->P_cap = maxP;
@@ -948,7 +955,7 @@ void eval_one(ptq_ctx* c, const ptq_config& cfg, unsigned long long* d_correct, 
           if (n.kind == PTQ_FC) {
             vin.H = 1; vin.W = 1; vin.C = x.h * x.w * vin.Cp; vin.Cp = vin.C; vin.halo = 0;
             a.k = 1; a.stride = 1; a.pad = 0; a.OH = 1; a.OW = 1;
-          } else if (wd.im2col) {
+          } else if (wd.im2col || (wd.sub1x1 && c->subsample)) {
             const TensorI& y = c->tens[n.out];
             launch_im2col(vin, n.k, n.stride, n.pad, y.h, y.w, c->d_im2col, wd.im_cp, c->st);
             check_launch(c);
@@ -1488,6 +1495,7 @@ int ptq_set_option(ptq_ctx* c, const char* key, int64_t value) {
     if (k == "conv_ref") c->conv_ref = (int)value;
     else if (k == "ablate") c->ablate = (int)value;
     else if (k == "tma") c->tma = (int)value;
+    else if (k == "subsample") c->subsample = (int)value;
     else if (k == "kwr") conv_tc_set_kwr_mode((int)value);
     else if (k == "time_conv") c->time_conv = (int)value;
     else if (k == "reset_stats") c->launches = 0;

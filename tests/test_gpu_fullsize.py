@@ -77,12 +77,20 @@ def test_strided_1x1_subsample_codes_bit_exact(ev224):
     shortcuts = [n for n in g.nodes if n.kind == "conv2d" and int(n.attrs.get("kernel", 0) or
                  np.asarray(g.weights[n.inputs[1]]).shape[-1]) == 1 and int(n.attrs.get("stride", 1)) > 1]
     assert len(shortcuts) == 3
+    def after_add(t):                      # the shortcut feeds an add (+ relu): probe its end
+        add = next(m for m in g.nodes if m.kind == "add" and t in m.inputs)
+        relu = [m for m in g.nodes if m.kind == "relu" and m.inputs[0] == add.output]
+        return relu[0].output if relu else add.output
+
     for ci in (0, 2):
         for n in shortcuts:
-            fast = ev224.probe_codes(space[ci], n.output)
-            try:
-                ev224.set_option("subsample", 0)
-                plain = ev224.probe_codes(space[ci], n.output)
-            finally:
-                ev224.set_option("subsample", 1)
-            assert np.array_equal(fast, plain), (ci, n.id)
+            for fusion, t in ((0, n.output), (1, after_add(n.output))):
+                ev224.set_option("fusion", fusion)
+                try:
+                    fast = ev224.probe_codes(space[ci], t)
+                    ev224.set_option("subsample", 0)
+                    plain = ev224.probe_codes(space[ci], t)
+                finally:
+                    ev224.set_option("subsample", 1)
+                    ev224.set_option("fusion", 1)
+                assert np.array_equal(fast, plain), (ci, n.id, fusion)
