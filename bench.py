@@ -42,7 +42,7 @@ def parse():
     ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
     ap.add_argument("--model", default="resnet50")
     ap.add_argument("--n-eval", type=int, default=1000)
-    ap.add_argument("--e2e-steps", type=int, default=2)
+    ap.add_argument("--e2e-steps", type=int, default=3)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-sample-imgs", type=int, default=4)
     ap.add_argument("--configs", type=int, default=96, help="profiling only: first N configs")
