@@ -388,9 +388,52 @@ void launch_conv_f32(const float* x, int N, int H, int W, int Cin, const float* 
   dim3 g((unsigned)((M + CF_BM - 1) / CF_BM), (unsigned)((Cout + CF_BN - 1) / CF_BN));
   k_conv_f32<<<g, 256, 0, s>>>(x, N, H, W, Cin, Bw, bias, Cout, k, stride, pad, OH, OW, y);
 }
+// four channels per thread (float4 loads / stores); per channel the same fmaf chain in the
+// same (kh, kw) order as k_dwconv_f32, so the results are bit-identical
+__global__ void k_dwconv_f32_v4(const float* __restrict__ x, int N, int H, int W, int C,
+                                const float* __restrict__ w, const float* __restrict__ bias, int k,
+                                int stride, int pad, int OH, int OW, float* __restrict__ y) {
+  const int cq = C >> 2;
+  const int64_t total = (int64_t)N * OH * OW * cq;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < total;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    const int c0 = (int)(i % cq) * 4;
+    const int p = (int)(i / cq);
+    const int ow = p % OW, t = p / OW;
+    const int oh = t % OH, n = t / OH;
+    float a0 = 0.f, a1 = 0.f, a2 = 0.f, a3 = 0.f;
+    for (int kh = 0; kh < k; ++kh) {
+      const int ih = oh * stride - pad + kh;
+      if (ih < 0 || ih >= H) continue;
+      for (int kw = 0; kw < k; ++kw) {
+        const int iw = ow * stride - pad + kw;
+        if (iw < 0 || iw >= W) continue;
+        const float4 v = __ldg(reinterpret_cast<const float4*>(x + (((int64_t)n * H + ih) * W + iw) * C + c0));
+        const int tap = kh * k + kw;
+        a0 = fmaf(v.x, __ldg(w + (c0 + 0) * k * k + tap), a0);
+        a1 = fmaf(v.y, __ldg(w + (c0 + 1) * k * k + tap), a1);
+        a2 = fmaf(v.z, __ldg(w + (c0 + 2) * k * k + tap), a2);
+        a3 = fmaf(v.w, __ldg(w + (c0 + 3) * k * k + tap), a3);
+      }
+    }
+    if (bias) {
+      a0 += __ldg(bias + c0); a1 += __ldg(bias + c0 + 1);
+      a2 += __ldg(bias + c0 + 2); a3 += __ldg(bias + c0 + 3);
+    } else {
+      a0 += 0.f; a1 += 0.f; a2 += 0.f; a3 += 0.f;
+    }
+    *reinterpret_cast<float4*>(y + (int64_t)p * C + c0) = make_float4(a0, a1, a2, a3);
+  }
+}
+
 void launch_dwconv_f32(const float* x, int N, int H, int W, int C, const float* w,
                        const float* bias, int k, int stride, int pad, int OH, int OW, float* y,
                        cudaStream_t s) {
+  if (C % 4 == 0 && ((uintptr_t)x & 15) == 0 && ((uintptr_t)y & 15) == 0) {
+    k_dwconv_f32_v4<<<gblk((int64_t)N * OH * OW * (C / 4)), 256, 0, s>>>(x, N, H, W, C, w, bias, k,
+                                                                        stride, pad, OH, OW, y);
+    return;
+  }
   k_dwconv_f32<<<gblk((int64_t)N * OH * OW * C), 256, 0, s>>>(x, N, H, W, C, w, bias, k, stride,
                                                              pad, OH, OW, y);
 }

@@ -790,6 +790,10 @@ void launch_pixsum(View in, int* P, cudaStream_t s) {
 
 // ---------------------------------------------------------------- depthwise int8 conv (CUDA cores)
 // acc = sum_taps (x - zx)(w - zw[c]) + bias[c]; clip int32; requant; fused relu.
+static int g_dwconv_v4 = 1;
+void set_dwconv_v4(int v) { g_dwconv_v4 = v; }
+static bool dwconv_v4_enabled() { return g_dwconv_v4 != 0; }
+
 __global__ void k_dwconv_i8(View in, View out, const int8_t* __restrict__ w,
                             const int* __restrict__ wzp, int k, int stride, int pad, LayerSt L) {
   const LayerRt r = *L.rt;
@@ -818,8 +822,55 @@ __global__ void k_dwconv_i8(View in, View out, const int8_t* __restrict__ w,
     out.p[voff(out, n, oh, ow) + c] = res;
   }
 }
+// four channels of one output pixel per thread: one 4-byte load per tap (coalesced across the
+// channel-fastest threads), int32 tap sums (|sum| <= k*k*255*255 < 2^31), one packed 4-byte
+// store; same arithmetic per channel as k_dwconv_i8 (bit-identical)
+__global__ void k_dwconv_i8_v4(View in, View out, const int8_t* __restrict__ w,
+                               const int* __restrict__ wzp, int k, int stride, int pad, LayerSt L) {
+  const LayerRt r = *L.rt;
+  const int cq = out.Cp >> 2, kk = k * k;
+  const int64_t rowp = (int64_t)(in.W + 2 * in.halo) * in.Cp;
+  const int64_t total = (int64_t)out.N * out.H * out.W * cq;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < total;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    const int c0 = (int)(i % cq) * 4;
+    const int p = (int)(i / cq);
+    const int ow = p % out.W, t = p / out.W;
+    const int oh = t % out.H, n = t / out.H;
+    int acc[4] = {0, 0, 0, 0}, zw[4];
+#pragma unroll
+    for (int j = 0; j < 4; ++j) zw[j] = c0 + j < out.C ? __ldg(wzp + c0 + j) : 0;
+    const int8_t* base = in.p + voff(in, n, oh * stride - pad, ow * stride - pad) + c0;
+    for (int kh = 0; kh < k; ++kh)
+      for (int kw = 0; kw < k; ++kw) {
+        const uint32_t xv = __ldg(reinterpret_cast<const uint32_t*>(base + kh * rowp + (int64_t)kw * in.Cp));
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+          const int wv = c0 + j < out.C ? (int)__ldg(w + (c0 + j) * kk + kh * k + kw) : 0;
+          acc[j] += ((int)(int8_t)(xv >> (8 * j)) - r.zx) * (wv - zw[j]);
+        }
+      }
+    uint32_t packed = 0u;
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      if (c0 + j < out.C) {
+        const long long a = clip32((long long)acc[j] + L.biasq[c0 + j]);
+        int q = requant1(a, L.mult[c0 + j], r.zy);
+        if (q < r.relu_zp) q = r.relu_zp;
+        packed |= ((uint32_t)q & 0xffu) << (8 * j);
+      }
+    }
+    *reinterpret_cast<uint32_t*>(out.p + voff(out, n, oh, ow) + c0) = packed;
+  }
+}
+
 void launch_dwconv_i8(View in, View out, const int8_t* w, const int* wzp, int k, int stride, int pad,
                       LayerSt L, cudaStream_t s) {
+  if (in.Cp % 4 == 0 && out.Cp % 4 == 0 && dwconv_v4_enabled()) {
+    k_dwconv_i8_v4<<<nblk((int64_t)out.N * out.H * out.W * (out.Cp / 4)), 256, 0, s>>>(
+        in, out, w, wzp, k, stride, pad, L);
+    return;
+  }
   k_dwconv_i8<<<nblk((int64_t)out.N * out.H * out.W * out.Cp), 256, 0, s>>>(in, out, w, wzp, k,
                                                                              stride, pad, L);
 }

@@ -121,6 +121,7 @@ void launch_add_codes(View a, View b, View out, const float* act_scale, const in
 void launch_concat_codes(View in, View out, int coff, const float* act_scale, const int* act_zp,
                          int hin, int hout, cudaStream_t s);
 void launch_pixsum(View in, int* P, cudaStream_t s);
+void set_dwconv_v4(int v);
 void launch_dwconv_i8(View in, View out, const int8_t* w, const int* wzp, int k, int stride,
                       int pad, LayerSt L, cudaStream_t s);
 void launch_argmax_codes(View in, const long long* labels, unsigned long long* correct,

@@ -181,3 +181,28 @@ def test_grid_batch_equals_isolated_configs(ds64):
         ev.correct_counts([other])
         assert int(ev.correct_counts([cfg])[0]) == int(batch[i]), cfg
     ev.close()
+
+
+def test_dwconv_vectorized_equals_scalar(ds64):
+    """k_dwconv_i8_v4 (4 channels per thread) vs the scalar k_dwconv_i8: every depthwise
+    output of MobileNet-v2 bit-identical, for zw = 0 and zw != 0 configs."""
+    from paper_2202_05048_b200.evaluator import GpuEvaluator
+    g = build_model("mobilenet_v2", seed=0, shape=SHAPE)
+    ev = GpuEvaluator(g, ds64, 0, GENERIC)
+    try:
+        ev.set_option("fusion", 0)
+        dw = [n.output for n in g.nodes if n.kind == "depthwise_conv2d"]
+        assert len(dw) == 17
+        for ci in (0, 2, 14):
+            cfg = enumerate_space(GENERIC)[ci]
+            fast = [ev.probe_codes(cfg, t) for t in dw]
+            ev.set_option("dwconv_v4", 0)
+            try:
+                slow = [ev.probe_codes(cfg, t) for t in dw]
+            finally:
+                ev.set_option("dwconv_v4", 1)
+            for t, a, b in zip(dw, fast, slow):
+                assert np.array_equal(a, b), (ci, t)
+    finally:
+        ev.set_option("fusion", 1)
+        ev.close()

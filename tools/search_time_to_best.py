@@ -7,8 +7,8 @@ reference IR) and on ResNet-18.
     python tools/search_time_to_best.py [--models squeezenet resnet18] [--n-eval 1000]
 
 Prints one JSON line per (model, strategy).  Times are host wall clock around the
-driver call (the driver itself is host Python); the evaluator is built once per model
-(its calibration time is reported separately).
+driver call (the driver itself is host Python); the evaluator is built once per model after one warm-up
+construction (its calibration time is reported separately).
 """
 
 from __future__ import annotations
@@ -41,6 +41,7 @@ def main() -> int:
     space = RT.enumerate_space(RT.TargetProfile("Generic"))
     for name in args.models:
         g = build_model(name, seed=0)
+        make_accuracy_evaluator(g, d, 0).close()        # warm-up: CUDA context, library, allocator
         t0 = time.perf_counter()
         ev = make_accuracy_evaluator(g, d, 0)
         t_cal = time.perf_counter() - t0
