@@ -23,6 +23,11 @@ static inline int nblk(int64_t n, int t = 256, int cap = 148 * 32) {
   return (int)(b < 1 ? 1 : (b > cap ? cap : b));
 }
 
+static int g_concat_v16 = 1;
+void set_concat_v16(int v) { g_concat_v16 = v; }
+static bool concat_v16_enabled() { return g_concat_v16 != 0; }
+static int g_dwconv_v4 = 2;   // 2: k x k register-weight kernel, 1: 4-channel, 0: scalar
+
 __device__ __forceinline__ int64_t voff(const View& v, int n, int h, int w) {
   const int Hp = v.H + 2 * v.halo, Wp = v.W + 2 * v.halo;
   return (((int64_t)n * Hp + h + v.halo) * Wp + w + v.halo) * v.Cp;
@@ -659,8 +664,47 @@ __global__ void k_concat_codes(View in, View out, int coff, const float* __restr
     out.p[voff(out, n, h, w) + coff + c] = (int8_t)requant1((long long)(v - zi), m, zo);
   }
 }
+// the requantization of a concat input depends only on the int8 code, so each block builds
+// the 256-entry table with the same requant1 (bit-identical) and maps 16 codes per thread
+// through it: int4 loads / stores instead of one fp64 requant and an int64 index chain per byte
+__global__ void k_concat_codes_v16(View in, View out, int coff, const float* __restrict__ as,
+                                   const int* __restrict__ az, int hin, int hout) {
+  __shared__ uint8_t lut[256];
+  const double m = __ddiv_rn((double)as[hin], (double)as[hout]);
+  const int zi = az[hin], zo = az[hout];
+  for (int v = threadIdx.x; v < 256; v += blockDim.x)
+    lut[v] = (uint8_t)requant1((long long)(v - 128 - zi), m, zo);
+  __syncthreads();
+  const int cq = in.C >> 4;
+  const int64_t total = (int64_t)in.N * in.H * in.W * cq;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < total;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    const int j = (int)(i % cq);
+    const int64_t p = i / cq;
+    const int w = (int)(p % in.W);
+    const int64_t t = p / in.W;
+    const int h = (int)(t % in.H), n = (int)(t / in.H);
+    const int4 v = __ldg(reinterpret_cast<const int4*>(in.p + voff(in, n, h, w) + j * 16));
+    uint32_t x[4] = {(uint32_t)v.x, (uint32_t)v.y, (uint32_t)v.z, (uint32_t)v.w}, y[4];
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      y[q] = 0u;
+#pragma unroll
+      for (int b = 0; b < 4; ++b)
+        y[q] |= (uint32_t)lut[((x[q] >> (8 * b)) & 0xffu) ^ 0x80u] << (8 * b);
+    }
+    *reinterpret_cast<int4*>(out.p + voff(out, n, h, w) + coff + j * 16) =
+        make_int4((int)y[0], (int)y[1], (int)y[2], (int)y[3]);
+  }
+}
+
 void launch_concat_codes(View in, View out, int coff, const float* as, const int* az, int hin,
                          int hout, cudaStream_t s) {
+  if (in.C % 16 == 0 && in.Cp % 16 == 0 && out.Cp % 16 == 0 && coff % 16 == 0 && concat_v16_enabled()) {
+    k_concat_codes_v16<<<nblk((int64_t)in.N * in.H * in.W * (in.C / 16)), 256, 0, s>>>(
+        in, out, coff, as, az, hin, hout);
+    return;
+  }
   k_concat_codes<<<nblk((int64_t)in.N * in.H * in.W * in.C), 256, 0, s>>>(in, out, coff, as, az,
                                                                           hin, hout);
 }
@@ -790,7 +834,7 @@ void launch_pixsum(View in, int* P, cudaStream_t s) {
 
 // ---------------------------------------------------------------- depthwise int8 conv (CUDA cores)
 // acc = sum_taps (x - zx)(w - zw[c]) + bias[c]; clip int32; requant; fused relu.
-static int g_dwconv_v4 = 1;
+
 void set_dwconv_v4(int v) { g_dwconv_v4 = v; }
 static bool dwconv_v4_enabled() { return g_dwconv_v4 != 0; }
 
@@ -864,8 +908,68 @@ __global__ void k_dwconv_i8_v4(View in, View out, const int8_t* __restrict__ w,
   }
 }
 
+// k x k specialisation: the 4 channels' (w - zw) taps stay in registers and each thread walks
+// PX consecutive output pixels of one row, amortising the weight loads and index math
+template <int K, int PX>
+__global__ void k_dwconv_i8_k(View in, View out, const int8_t* __restrict__ w,
+                              const int* __restrict__ wzp, int stride, int pad, LayerSt L) {
+  const LayerRt r = *L.rt;
+  const int cq = out.Cp >> 2, owq = (out.W + PX - 1) / PX;
+  const int64_t rowp = (int64_t)(in.W + 2 * in.halo) * in.Cp;
+  const int64_t total = (int64_t)out.N * out.H * owq * cq;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < total;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    const int c0 = (int)(i % cq) * 4;
+    const int64_t p = i / cq;
+    const int ow0 = (int)(p % owq) * PX, t = (int)(p / owq);
+    const int oh = t % out.H, n = t / out.H;
+    int wr[K * K][4];
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      const bool ok = c0 + j < out.C;
+      const int zw = ok ? __ldg(wzp + c0 + j) : 0;
+#pragma unroll
+      for (int tap = 0; tap < K * K; ++tap)
+        wr[tap][j] = ok ? (int)__ldg(w + (c0 + j) * K * K + tap) - zw : 0;
+    }
+    const int8_t* base = in.p + voff(in, n, oh * stride - pad, ow0 * stride - pad) + c0;
+    int8_t* obase = out.p + voff(out, n, oh, ow0) + c0;
+#pragma unroll 1
+    for (int px = 0; px < PX && ow0 + px < out.W; ++px) {
+      const int8_t* b = base + (int64_t)px * stride * in.Cp;
+      int acc[4] = {0, 0, 0, 0};
+#pragma unroll
+      for (int kh = 0; kh < K; ++kh)
+#pragma unroll
+        for (int kw = 0; kw < K; ++kw) {
+          const uint32_t xv = __ldg(reinterpret_cast<const uint32_t*>(b + kh * rowp + (int64_t)kw * in.Cp));
+#pragma unroll
+          for (int j = 0; j < 4; ++j)
+            acc[j] += ((int)(int8_t)(xv >> (8 * j)) - r.zx) * wr[kh * K + kw][j];
+        }
+      uint32_t packed = 0u;
+#pragma unroll
+      for (int j = 0; j < 4; ++j) {
+        if (c0 + j < out.C) {
+          const long long a = clip32((long long)acc[j] + L.biasq[c0 + j]);
+          int q = requant1(a, L.mult[c0 + j], r.zy);
+          if (q < r.relu_zp) q = r.relu_zp;
+          packed |= ((uint32_t)q & 0xffu) << (8 * j);
+        }
+      }
+      *reinterpret_cast<uint32_t*>(obase + (int64_t)px * out.Cp) = packed;
+    }
+  }
+}
+
 void launch_dwconv_i8(View in, View out, const int8_t* w, const int* wzp, int k, int stride, int pad,
                       LayerSt L, cudaStream_t s) {
+  if (k == 3 && in.Cp % 4 == 0 && out.Cp % 4 == 0 && g_dwconv_v4 == 2) {
+    constexpr int PX = 4;
+    const int64_t total = (int64_t)out.N * out.H * ((out.W + PX - 1) / PX) * (out.Cp / 4);
+    k_dwconv_i8_k<3, PX><<<nblk(total), 256, 0, s>>>(in, out, w, wzp, stride, pad, L);
+    return;
+  }
   if (in.Cp % 4 == 0 && out.Cp % 4 == 0 && dwconv_v4_enabled()) {
     k_dwconv_i8_v4<<<nblk((int64_t)out.N * out.H * out.W * (out.Cp / 4)), 256, 0, s>>>(
         in, out, w, wzp, k, stride, pad, L);

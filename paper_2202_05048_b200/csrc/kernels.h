@@ -122,6 +122,7 @@ void launch_concat_codes(View in, View out, int coff, const float* act_scale, co
                          int hin, int hout, cudaStream_t s);
 void launch_pixsum(View in, int* P, cudaStream_t s);
 void set_dwconv_v4(int v);
+void set_concat_v16(int v);
 void launch_dwconv_i8(View in, View out, const int8_t* w, const int* wzp, int k, int stride,
                       int pad, LayerSt L, cudaStream_t s);
 void launch_argmax_codes(View in, const long long* labels, unsigned long long* correct,

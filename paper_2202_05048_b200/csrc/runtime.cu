@@ -1497,6 +1497,7 @@ int ptq_set_option(ptq_ctx* c, const char* key, int64_t value) {
     else if (k == "tma") c->tma = (int)value;
     else if (k == "subsample") c->subsample = (int)value;
     else if (k == "dwconv_v4") set_dwconv_v4((int)value);
+    else if (k == "concat_v16") set_concat_v16((int)value);
     else if (k == "kwr") conv_tc_set_kwr_mode((int)value);
     else if (k == "time_conv") c->time_conv = (int)value;
     else if (k == "reset_stats") c->launches = 0;

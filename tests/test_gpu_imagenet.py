@@ -195,13 +195,40 @@ def test_dwconv_vectorized_equals_scalar(ds64):
         assert len(dw) == 17
         for ci in (0, 2, 14):
             cfg = enumerate_space(GENERIC)[ci]
-            fast = [ev.probe_codes(cfg, t) for t in dw]
-            ev.set_option("dwconv_v4", 0)
+            got = {}
             try:
-                slow = [ev.probe_codes(cfg, t) for t in dw]
+                for mode in (2, 1, 0):          # register-weight k x k, 4-channel, scalar
+                    ev.set_option("dwconv_v4", mode)
+                    got[mode] = [ev.probe_codes(cfg, t) for t in dw]
             finally:
-                ev.set_option("dwconv_v4", 1)
-            for t, a, b in zip(dw, fast, slow):
+                ev.set_option("dwconv_v4", 2)
+            for mode in (2, 1):
+                for t, a, b in zip(dw, got[mode], got[0]):
+                    assert np.array_equal(a, b), (ci, mode, t)
+    finally:
+        ev.set_option("fusion", 1)
+        ev.close()
+
+
+def test_concat_lut_equals_scalar(ds64):
+    """k_concat_codes_v16 (per-block 256-entry requant table, 16 codes per thread) vs the
+    per-byte fp64 k_concat_codes: every SqueezeNet concat output bit-identical."""
+    from paper_2202_05048_b200.evaluator import GpuEvaluator
+    g = build_model("squeezenet", seed=0, shape=SHAPE)
+    ev = GpuEvaluator(g, ds64, 0, GENERIC)
+    try:
+        ev.set_option("fusion", 0)
+        cat = [n.output for n in g.nodes if n.kind == "concat"]
+        assert len(cat) == 8
+        for ci in (0, 2, 14, 30):
+            cfg = enumerate_space(GENERIC)[ci]
+            fast = [ev.probe_codes(cfg, t) for t in cat]
+            ev.set_option("concat_v16", 0)
+            try:
+                slow = [ev.probe_codes(cfg, t) for t in cat]
+            finally:
+                ev.set_option("concat_v16", 1)
+            for t, a, b in zip(cat, fast, slow):
                 assert np.array_equal(a, b), (ci, t)
     finally:
         ev.set_option("fusion", 1)
