@@ -932,12 +932,20 @@ __global__ void k_dwconv_i8_k(View in, View out, const int8_t* __restrict__ w,
       for (int tap = 0; tap < K * K; ++tap)
         wr[tap][j] = ok ? (int)__ldg(w + (c0 + j) * K * K + tap) - zw : 0;
     }
+    int zsum[4];                                   // zx * sum(w - zw): sum (x - zx)(w - zw) = sum x(w - zw) - zsum
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      int sw = 0;
+#pragma unroll
+      for (int tap = 0; tap < K * K; ++tap) sw += wr[tap][j];
+      zsum[j] = r.zx * sw;
+    }
     const int8_t* base = in.p + voff(in, n, oh * stride - pad, ow0 * stride - pad) + c0;
     int8_t* obase = out.p + voff(out, n, oh, ow0) + c0;
 #pragma unroll 1
     for (int px = 0; px < PX && ow0 + px < out.W; ++px) {
       const int8_t* b = base + (int64_t)px * stride * in.Cp;
-      int acc[4] = {0, 0, 0, 0};
+      int acc[4] = {-zsum[0], -zsum[1], -zsum[2], -zsum[3]};
 #pragma unroll
       for (int kh = 0; kh < K; ++kh)
 #pragma unroll
@@ -945,7 +953,7 @@ __global__ void k_dwconv_i8_k(View in, View out, const int8_t* __restrict__ w,
           const uint32_t xv = __ldg(reinterpret_cast<const uint32_t*>(b + kh * rowp + (int64_t)kw * in.Cp));
 #pragma unroll
           for (int j = 0; j < 4; ++j)
-            acc[j] += ((int)(int8_t)(xv >> (8 * j)) - r.zx) * wr[kh * K + kw][j];
+            acc[j] += (int)(int8_t)(xv >> (8 * j)) * wr[kh * K + kw][j];
         }
       uint32_t packed = 0u;
 #pragma unroll
