@@ -163,7 +163,10 @@ int ptq_histogram_host(ptq_ctx* ctx, const float* x, int64_t n, float lo, float 
  * "eval_chunk" (images per eval pass; default = whole eval set), "time_conv" (N =
  * record CUDA events around the int8 conv launches of the first N configs of each
  * ptq_eval_configs call, for ptq_last_stats),
- * "reset_stats" (zero the cumulative kernel-launch counter). */
+ * "reset_stats" (zero the cumulative kernel-launch counter).  A/B switches for tests, each
+ * path bit-identical to its fallback: "tma" (0 = gather A operand), "kwr" (kw-reuse slabs),
+ * "subsample" (0 = strided 1x1 convs gather directly), "dwconv_v4" (2 register-tap 3x3,
+ * 1 four-channel, 0 scalar depthwise), "concat_v16" (0 = per-byte concat requant). */
 int ptq_set_option(ptq_ctx* ctx, const char* key, int64_t value);
 /* Statistics: cumulative kernel launches (option "reset_stats" zeroes it) and, for the
  * last ptq_eval_configs call, the summed CUDA-event time of the int8 conv launches of
