@@ -152,6 +152,30 @@ int ptq_export_layer(ptq_ctx* ctx, const ptq_config* cfg, int32_t node, int8_t* 
                      int32_t* wzp, int32_t* bias);
 int ptq_probe_codes(ptq_ctx* ctx, const ptq_config* cfg, int32_t tensor, int8_t* out,
                     int64_t* n_out);
+/* Parity probes over a subset of eval images (imgs: eval-set indices, n_imgs of them); every
+ * output is in the reference's NCHW layout, image-major in the order of imgs.
+ *  ptq_probe_tensors  int8 codes of n_tensors tensors after one evaluation of cfg (the codes the
+ *                     reference's run_quantized sink sees, intexec.py:148-301): out holds
+ *                     [n_imgs][C][H][W] per tensor, back to back; found[k] = 0 for tensors the
+ *                     fused epilogues never materialise (fusion option on).
+ *  ptq_probe_acc      the int32-saturated accumulator acc + bias of int8 compute node `node`
+ *                     (intexec.py:177-190), taken from the same tcgen05 / depthwise kernel launch
+ *                     with an accumulator-storing epilogue: [n_imgs][Cout][OH][OW] ([n_imgs][Cout]
+ *                     for fc).
+ *  ptq_probe_output   run_quantized's return value (intexec.py:337-351): dequantize_array of the
+ *                     output codes (schemes.py:153-155, on the device) or the fp32 scores when
+ *                     the last layer runs in fp32: [n_imgs][classes].
+ *  ptq_probe_f32      an fp32-domain tensor of cfg (FirstLastFp32 layers, intexec.py:304-334).
+ *  ptq_minmax_host    the calibration min/max kernels (calibration.py:67-76) over a host array
+ *                     [n_img][elems]: range = (min, max) as fp32. */
+int ptq_probe_tensors(ptq_ctx* ctx, const ptq_config* cfg, int32_t n_tensors, const int32_t* tensors,
+                      int32_t n_imgs, const int64_t* imgs, int8_t* out, int32_t* found);
+int ptq_probe_acc(ptq_ctx* ctx, const ptq_config* cfg, int32_t node, int32_t n_imgs, const int64_t* imgs,
+                  int32_t* out);
+int ptq_probe_output(ptq_ctx* ctx, const ptq_config* cfg, int32_t n_imgs, const int64_t* imgs, float* out);
+int ptq_probe_f32(ptq_ctx* ctx, const ptq_config* cfg, int32_t tensor, int32_t n_imgs, const int64_t* imgs,
+                  float* out);
+int ptq_minmax_host(ptq_ctx* ctx, const float* x, int32_t n_img, int64_t elems, float* range);
 /* Activation params the device derived for one variant: scale/zp [T]. */
 int ptq_probe_act_params(ptq_ctx* ctx, int32_t cache, int32_t scheme, int32_t clipping,
                          float* scale, int32_t* zp);

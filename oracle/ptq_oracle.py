@@ -9,8 +9,8 @@ missing; it has no CPU fallback).
 Parity is PINNED: tests/test_oracle_golden.py checks every function here
 against golden vectors that tests/golden/gen_golden.py produced by importing
 the reference itself (/root/reference/pkg/src/ptqtune) in the build
-container, plus the reference's own known-answer tests (schemes, requantize,
-KL brute force) restated in tests/test_oracle_kat.py.
+container (scheme / quantize / requantize known answers, caches, KL windows
+and the App. B grids of the three fixtures).
 
 Each function cites the reference file:line it restates ("ref:" below is
 /root/reference/pkg/src/ptqtune/).  Graph and dataset arguments are
@@ -514,13 +514,16 @@ def _pc(v, ndim):
     return np.asarray(v).reshape(shape)
 
 
-def run_quantized(qm: QModel, batch, sink=None, accs=None):
+def run_quantized(qm: QModel, batch, sink=None, accs=None, inject=None):
     """Simulated-int8 forward (ref: intexec.py:148-351).
 
     Returns fp32 scores (dequantized output codes, or fp32 logits when the
     last layer is kept in fp32).  ``sink(t, v)`` sees codes (int64) for
     quantized tensors and fp32 values otherwise; ``accs`` (dict) collects
-    each int8 compute node's clipped int32 accumulator."""
+    each int8 compute node's clipped int32 accumulator.  ``inject`` (test
+    staging only) replaces a node's output by the given values, e.g. the
+    device's codes at the boundary after an fp32 first layer, so everything
+    downstream is compared on identical int8 inputs."""
     g = qm.graph
     batch = np.asarray(batch, dtype=np.float32)
     env = {}
@@ -586,6 +589,8 @@ def run_quantized(qm: QModel, batch, sink=None, accs=None):
             out = x if n.output in qm.act else _softmax(x)
         else:
             raise ValueError(k)
+        if inject is not None and n.output in inject:
+            out = np.asarray(inject[n.output]).astype(out.dtype if hasattr(out, "dtype") else np.int64)
         env[n.output] = out
         if sink is not None:
             sink(n.output, out)

@@ -27,7 +27,8 @@ EXPORTS = ("ptq_last_error", "ptq_version", "ptq_create", "ptq_destroy", "ptq_nu
            "ptq_eval_configs", "ptq_probe_codes", "ptq_probe_act_params", "ptq_histogram_host",
            "ptq_export_layer", "ptq_percentile_ranges",
            "ptq_set_option", "ptq_last_stats", "ptq_calib_forward", "ptq_calib_histogram",
-           "ptq_stream", "ptq_conv_timings")
+           "ptq_stream", "ptq_conv_timings", "ptq_probe_tensors", "ptq_probe_acc",
+           "ptq_probe_output", "ptq_probe_f32", "ptq_minmax_host")
 
 
 class NodeDesc(C.Structure):
@@ -95,6 +96,11 @@ def load() -> C.CDLL:
         "ptq_calib_histogram": [P, P, P],
         "ptq_stream": [P, C.POINTER(P)],
         "ptq_conv_timings": [P, P, i64, C.POINTER(i64)],
+        "ptq_probe_tensors": [P, C.POINTER(ConfigDesc), i32, P, i32, P, P, P],
+        "ptq_probe_acc": [P, C.POINTER(ConfigDesc), i32, i32, P, P],
+        "ptq_probe_output": [P, C.POINTER(ConfigDesc), i32, P, P],
+        "ptq_probe_f32": [P, C.POINTER(ConfigDesc), i32, i32, P, P],
+        "ptq_minmax_host": [P, P, i32, i64, P],
     }
     for name, args in sig.items():
         f = getattr(lib, name)

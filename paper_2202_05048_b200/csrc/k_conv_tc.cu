@@ -246,6 +246,25 @@ __device__ __forceinline__ int4 epi_slow_chunk(uint32_t taddr, int cb, long long
   return make_int4((int)(uint32_t)lo, (int)(uint32_t)(lo >> 32), (int)(uint32_t)hi, (int)(uint32_t)(hi >> 32));
 }
 
+// parity probe (ptq_probe_acc): the exact accumulators of a 16-channel chunk, acc + bias
+// saturated to int32 as the reference does before requantizing (intexec.py:177-190), stored to
+// dst[c] (dst = this pixel's [cout] row, or nullptr for rows outside the real output).  The
+// warp-uniform loop re-reads one TMEM column per step (tcgen05.ld is .sync.aligned).
+__device__ __forceinline__ void epi_acc_chunk(uint32_t taddr, int cb, long long rowsum, const ConvTcArgs& a,
+                                              const LayerRt& rt, int* dst) {
+#pragma unroll 1
+  for (int j = 0; j < 16; ++j) {
+    const uint32_t x = tmem_ld1(taddr + (uint32_t)j);
+    const int c = cb + j;
+    if (dst && c < a.L.cout) {
+      const long long zw = a.wzp[c];
+      const long long acc = (long long)(int)x - zw * rowsum - (long long)rt.zx * a.wsum[c] +
+                            (long long)a.kreal * rt.zx * zw;
+      dst[c] = (int)clip32(acc + a.L.biasq[c]);
+    }
+  }
+}
+
 __device__ __forceinline__ long long pixel_rowsum(const ConvTcArgs& a, int n, int ih0, int iw0) {
   if (!a.has_wzp) return 0;
   const int Wp = a.in.W + 2 * a.in.halo, Hp = a.in.H + 2 * a.in.halo;
@@ -287,7 +306,7 @@ struct EpiEnv {
 
 // persistent epilogue tile loop of one variant (GENERIC: runtime dispatch, slow layers and
 // the profiling ablation)
-template <int BN, bool WZP, bool SKIP, bool CLAMP, bool RELU, bool GENERIC>
+template <int BN, bool WZP, bool SKIP, bool CLAMP, bool RELU, bool GENERIC, bool ACC = false>
 __device__ __forceinline__ void epi_tiles(const ConvTcArgs& a, const LayerRt& rt, const EpiK& k, const EpiEnv& e) {
   constexpr int NCH = BN / 16;                       // 16-column chunks per tile
   const int Cout = a.L.cout;
@@ -332,6 +351,13 @@ __device__ __forceinline__ void epi_tiles(const ConvTcArgs& a, const LayerRt& rt
     const uint32_t tbase = e.tmem + ((uint32_t)(e.q * 32) << 16) + buf * BN;
 #pragma unroll 1
     for (int c = first; c < NCH; c += 3) {
+      if (ACC) {
+        const int cb = nt * BN + c * 16;
+        if (cb >= Cout) continue;                  // warp-uniform
+        const int64_t pix = a.flat ? (int64_t)m : ((int64_t)g.n * a.OHr + g.oh) * a.OWr + g.ow;
+        epi_acc_chunk(tbase + (uint32_t)(c * 16), cb, rowsum, a, rt, g.ok ? a.acc_out + pix * Cout : nullptr);
+        continue;
+      }
       uint32_t v[16];
       tmem_ld16(tbase + (uint32_t)(c * 16), v);
       const int cb = nt * BN + c * 16;
@@ -661,7 +687,8 @@ __global__ void __launch_bounds__(TC_THREADS, 1) k_conv_tc(const __grid_constant
     // layer-level dispatch (that overhead was ~20% of the hot loop's instructions)
     const bool skip = a.skip.p != nullptr, wzp = a.has_wzp != 0, clamp = !rt.noclamp,
                relu = k.lo_conv > PTQ_QMIN;
-    if (rt.slow || a.ablate == 1) epi_tiles<BN, false, false, false, false, true>(a, rt, k, e);
+    if (a.acc_out) epi_tiles<BN, false, false, false, false, true, true>(a, rt, k, e);
+    else if (rt.slow || a.ablate == 1) epi_tiles<BN, false, false, false, false, true>(a, rt, k, e);
     else if (skip) {
       if (wzp) { if (clamp) epi_tiles<BN, true, true, true, false, false>(a, rt, k, e);
                  else epi_tiles<BN, true, true, false, false, false>(a, rt, k, e); }

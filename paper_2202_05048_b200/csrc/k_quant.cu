@@ -839,7 +839,8 @@ void set_dwconv_v4(int v) { g_dwconv_v4 = v; }
 static bool dwconv_v4_enabled() { return g_dwconv_v4 != 0; }
 
 __global__ void k_dwconv_i8(View in, View out, const int8_t* __restrict__ w,
-                            const int* __restrict__ wzp, int k, int stride, int pad, LayerSt L) {
+                            const int* __restrict__ wzp, int k, int stride, int pad, LayerSt L,
+                            int* __restrict__ acc_out) {
   const LayerRt r = *L.rt;
   const int64_t total = (int64_t)out.N * out.H * out.W * out.Cp;
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < total;
@@ -859,6 +860,7 @@ __global__ void k_dwconv_i8(View in, View out, const int8_t* __restrict__ w,
           acc += (long long)(xv - r.zx) * (int)(w[c * k * k + kh * k + kw] - zw);
         }
       acc = clip32(acc + L.biasq[c]);
+      if (acc_out) acc_out[((int64_t)(n * out.H + oh) * out.W + ow) * out.C + c] = (int)acc;
       int q = requant1(acc, L.mult[c], r.zy);
       if (q < r.relu_zp) q = r.relu_zp;
       res = (int8_t)q;
@@ -870,7 +872,8 @@ __global__ void k_dwconv_i8(View in, View out, const int8_t* __restrict__ w,
 // channel-fastest threads), int32 tap sums (|sum| <= k*k*255*255 < 2^31), one packed 4-byte
 // store; same arithmetic per channel as k_dwconv_i8 (bit-identical)
 __global__ void k_dwconv_i8_v4(View in, View out, const int8_t* __restrict__ w,
-                               const int* __restrict__ wzp, int k, int stride, int pad, LayerSt L) {
+                               const int* __restrict__ wzp, int k, int stride, int pad, LayerSt L,
+                               int* __restrict__ acc_out) {
   const LayerRt r = *L.rt;
   const int cq = out.Cp >> 2, kk = k * k;
   const int64_t rowp = (int64_t)(in.W + 2 * in.halo) * in.Cp;
@@ -899,6 +902,7 @@ __global__ void k_dwconv_i8_v4(View in, View out, const int8_t* __restrict__ w,
     for (int j = 0; j < 4; ++j) {
       if (c0 + j < out.C) {
         const long long a = clip32((long long)acc[j] + L.biasq[c0 + j]);
+        if (acc_out) acc_out[((int64_t)(n * out.H + oh) * out.W + ow) * out.C + c0 + j] = (int)a;
         int q = requant1(a, L.mult[c0 + j], r.zy);
         if (q < r.relu_zp) q = r.relu_zp;
         packed |= ((uint32_t)q & 0xffu) << (8 * j);
@@ -912,7 +916,8 @@ __global__ void k_dwconv_i8_v4(View in, View out, const int8_t* __restrict__ w,
 // PX consecutive output pixels of one row, amortising the weight loads and index math
 template <int K, int PX>
 __global__ void k_dwconv_i8_k(View in, View out, const int8_t* __restrict__ w,
-                              const int* __restrict__ wzp, int stride, int pad, LayerSt L) {
+                              const int* __restrict__ wzp, int stride, int pad, LayerSt L,
+                              int* __restrict__ acc_out) {
   const LayerRt r = *L.rt;
   const int cq = out.Cp >> 2, owq = (out.W + PX - 1) / PX;
   const int64_t rowp = (int64_t)(in.W + 2 * in.halo) * in.Cp;
@@ -960,6 +965,7 @@ __global__ void k_dwconv_i8_k(View in, View out, const int8_t* __restrict__ w,
       for (int j = 0; j < 4; ++j) {
         if (c0 + j < out.C) {
           const long long a = clip32((long long)acc[j] + L.biasq[c0 + j]);
+          if (acc_out) acc_out[((int64_t)(n * out.H + oh) * out.W + ow0 + px) * out.C + c0 + j] = (int)a;
           int q = requant1(a, L.mult[c0 + j], r.zy);
           if (q < r.relu_zp) q = r.relu_zp;
           packed |= ((uint32_t)q & 0xffu) << (8 * j);
@@ -971,20 +977,20 @@ __global__ void k_dwconv_i8_k(View in, View out, const int8_t* __restrict__ w,
 }
 
 void launch_dwconv_i8(View in, View out, const int8_t* w, const int* wzp, int k, int stride, int pad,
-                      LayerSt L, cudaStream_t s) {
+                      LayerSt L, cudaStream_t s, int* acc_out) {
   if (k == 3 && in.Cp % 4 == 0 && out.Cp % 4 == 0 && g_dwconv_v4 == 2) {
     constexpr int PX = 4;
     const int64_t total = (int64_t)out.N * out.H * ((out.W + PX - 1) / PX) * (out.Cp / 4);
-    k_dwconv_i8_k<3, PX><<<nblk(total), 256, 0, s>>>(in, out, w, wzp, stride, pad, L);
+    k_dwconv_i8_k<3, PX><<<nblk(total), 256, 0, s>>>(in, out, w, wzp, stride, pad, L, acc_out);
     return;
   }
   if (in.Cp % 4 == 0 && out.Cp % 4 == 0 && dwconv_v4_enabled()) {
     k_dwconv_i8_v4<<<nblk((int64_t)out.N * out.H * out.W * (out.Cp / 4)), 256, 0, s>>>(
-        in, out, w, wzp, k, stride, pad, L);
+        in, out, w, wzp, k, stride, pad, L, acc_out);
     return;
   }
   k_dwconv_i8<<<nblk((int64_t)out.N * out.H * out.W * out.Cp), 256, 0, s>>>(in, out, w, wzp, k,
-                                                                             stride, pad, L);
+                                                                             stride, pad, L, acc_out);
 }
 
 // ---------------------------------------------------------------- top-1

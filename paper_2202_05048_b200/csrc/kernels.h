@@ -124,7 +124,7 @@ void launch_pixsum(View in, int* P, cudaStream_t s);
 void set_dwconv_v4(int v);
 void set_concat_v16(int v);
 void launch_dwconv_i8(View in, View out, const int8_t* w, const int* wzp, int k, int stride,
-                      int pad, LayerSt L, cudaStream_t s);
+                      int pad, LayerSt L, cudaStream_t s, int* acc_out = nullptr);
 void launch_argmax_codes(View in, const long long* labels, unsigned long long* correct,
                          cudaStream_t s);
 void launch_argmax_f32(const float* x, int64_t rows, int C, const long long* labels,
@@ -190,6 +190,9 @@ struct ConvTcArgs {
   int a_iters;            // A pipeline stages per tile (n_kiter, or 3 kh slabs with kwr)
   int flat;               // set by the launcher: GEMM row m is flat pixel m of the output (and of
                           // the add operand) -- halo-free TMA-mode layers skip the row geometry
+  int* acc_out;           // parity probe (ptq_probe_acc): when set, the epilogue stores the exact
+                          // int32-clipped accumulator acc + bias (intexec.py:177-190) of every real
+                          // output as [pixel][cout] int32 instead of requantized codes
 };
 int conv_tc_bn_for(int cout);     // BN tile width the kernel uses for this Cout
 int conv_tc_max_cout();           // largest Cout the tensor-core conv supports

@@ -833,9 +833,50 @@ void prepare_static(ptq_ctx* c) {
 }
 
 // ---------------------------------------------------------------- one config
-// probe_t >= 0: after the tensor is produced, copy its codes to probe_out (NCHW)
-void eval_one(ptq_ctx* c, const ptq_config& cfg, unsigned long long* d_correct, int probe_t,
-              int8_t* probe_out) {
+// Parity probes (tests only; the timed path passes pr == nullptr).  Images `imgs` (eval-set
+// indices) of one evaluation are copied to the host in the reference's NCHW layouts:
+//   codes   int8 codes of each tensor in `tensors` ([n_imgs][C][H][W] at code_out[k]); found[k]
+//           = 1 when the tensor was materialised (fused-away tensors stay 0)
+//   acc     the clipped int32 accumulator of compute node acc_node ([n_imgs][Cout][OH][OW])
+//   logits  what run_quantized returns (intexec.py:337-351): dequantized output codes, or the
+//           fp32 output when the last layer runs in fp32 ([n_imgs][classes])
+//   f32     an fp32-domain tensor (FirstLastFp32 layers) ([n_imgs][C][H][W])
+struct ProbeReq {
+  std::vector<int64_t> imgs;
+  std::vector<int> tensors;
+  std::vector<int8_t*> code_out;
+  std::vector<int> found;
+  int acc_node = -1;
+  int32_t* acc_out = nullptr;
+  bool acc_found = false;
+  float* logit_out = nullptr;
+  int f32_tensor = -1;
+  float* f32_out = nullptr;
+  bool f32_found = false;
+};
+
+// host copy of the selected images of a [B][h][w][c] device array (element size E) into
+// out[j] = image imgs[j] in NCHW order; sel = (output slot j, local image index)
+template <typename T>
+void copy_nchw(ptq_ctx* c, const T* dev, int64_t img_stride, int h, int w, int ch, int64_t pitch_px,
+               int halo, int cp, const std::vector<std::pair<int, int>>& sel, T* out) {
+  const int Hp = h + 2 * halo, Wp = w + 2 * halo;
+  std::vector<T> tmp((size_t)Hp * Wp * cp);
+  for (auto [j, n] : sel) {
+    CK(cudaMemcpyAsync(tmp.data(), dev + (int64_t)n * img_stride, tmp.size() * sizeof(T), cudaMemcpyDeviceToHost,
+                       c->st));
+    CK(cudaStreamSynchronize(c->st));
+    T* o = out + (size_t)j * ch * h * w;
+    for (int k = 0; k < ch; ++k)
+      for (int y = 0; y < h; ++y)
+        for (int x = 0; x < w; ++x)
+          o[((size_t)k * h + y) * w + x] = tmp[((size_t)(y + halo) * Wp + x + halo) * cp + k];
+    (void)pitch_px;
+  }
+}
+
+// ---------------------------------------------------------------- one config
+void eval_one(ptq_ctx* c, const ptq_config& cfg, unsigned long long* d_correct, ProbeReq* pr) {
   REQ(cfg.cache >= 0 && cfg.cache < 3 && cfg.scheme >= 0 && cfg.scheme < 4 && cfg.clipping >= 0 &&
           cfg.clipping < 2 && cfg.granularity >= 0 && cfg.granularity < 2 && cfg.mixed >= 0 &&
           cfg.mixed < 2,
@@ -850,39 +891,41 @@ void eval_one(ptq_ctx* c, const ptq_config& cfg, unsigned long long* d_correct, 
   const int N = (int)c->nodes.size();
   std::vector<int> alias(c->T);
   for (int t = 0; t < c->T; ++t) alias[t] = t;
-  cudaEvent_t e0 = nullptr, e1 = nullptr;
 
   for (int64_t img0 = 0; img0 < c->n_eval; img0 += c->chunk) {
     const int B = (int)std::min<int64_t>(c->chunk, c->n_eval - img0);
     auto V = [&](int t) { return view_of(c, alias[t], B); };
+    std::vector<std::pair<int, int>> sel;          // (probe slot, local image) in this chunk
+    if (pr)
+      for (int j = 0; j < (int)pr->imgs.size(); ++j)
+        if (pr->imgs[j] >= img0 && pr->imgs[j] < img0 + B) sel.push_back({j, (int)(pr->imgs[j] - img0)});
     auto probe = [&](int t) {
-      if (t != probe_t || !probe_out) return;
+      if (!pr || sel.empty()) return;
+      int k = -1;
+      for (int q = 0; q < (int)pr->tensors.size(); ++q)
+        if (pr->tensors[q] == t) k = q;
+      if (k < 0) return;
+      pr->found[k] = 1;
       View pv = V(t);
       const TensorI& x = c->tens[t];
-      if (t == 0 && c->s2d_node >= 0) {
-        std::vector<int8_t> h2((size_t)B * (pv.H + 2 * pv.halo) * (pv.W + 2 * pv.halo) * pv.Cp);
-        CK(cudaMemcpyAsync(h2.data(), pv.p, h2.size(), cudaMemcpyDeviceToHost, c->st));
-        CK(cudaStreamSynchronize(c->st));
+      int8_t* out = pr->code_out[k];
+      if (t == 0 && c->s2d_node >= 0) {                // space-to-depth input view
         const int Wq = pv.W + 2 * pv.halo, Hq = pv.H + 2 * pv.halo;
-        for (int n = 0; n < B; ++n)
+        std::vector<int8_t> h2((size_t)Hq * Wq * pv.Cp);
+        for (auto [j, n] : sel) {
+          CK(cudaMemcpyAsync(h2.data(), pv.p + (size_t)n * h2.size(), h2.size(), cudaMemcpyDeviceToHost, c->st));
+          CK(cudaStreamSynchronize(c->st));
+          int8_t* o = out + (size_t)j * x.elems;
           for (int ch = 0; ch < x.c; ++ch)
             for (int y = 0; y < x.h; ++y)
               for (int xx = 0; xx < x.w; ++xx)
-                probe_out[((((size_t)(img0 + n) * x.c + ch) * x.h + y) * x.w) + xx] =
-                    h2[(((size_t)n * Hq + y / 2 + pv.halo) * Wq + xx / 2 + pv.halo) * pv.Cp +
-                       ((y & 1) * 2 + (xx & 1)) * x.c + ch];
+                o[((size_t)ch * x.h + y) * x.w + xx] =
+                    h2[((size_t)(y / 2 + pv.halo) * Wq + xx / 2 + pv.halo) * pv.Cp + ((y & 1) * 2 + (xx & 1)) * x.c + ch];
+        }
         return;
       }
-      std::vector<int8_t> h((size_t)B * (x.h + 2 * pv.halo) * (x.w + 2 * pv.halo) * pv.Cp);
-      CK(cudaMemcpyAsync(h.data(), pv.p, h.size(), cudaMemcpyDeviceToHost, c->st));
-      CK(cudaStreamSynchronize(c->st));
-      const int Wp = x.w + 2 * pv.halo, Hp = x.h + 2 * pv.halo;
-      for (int n = 0; n < B; ++n)
-        for (int ch = 0; ch < x.c; ++ch)
-          for (int y = 0; y < x.h; ++y)
-            for (int xx = 0; xx < x.w; ++xx)
-              probe_out[((((size_t)(img0 + n) * x.c + ch) * x.h + y) * x.w) + xx] =
-                  h[(((size_t)n * Hp + y + pv.halo) * Wp + xx + pv.halo) * pv.Cp + ch];
+      const int64_t per_img = (int64_t)(x.h + 2 * pv.halo) * (x.w + 2 * pv.halo) * pv.Cp;
+      copy_nchw<int8_t>(c, pv.p, per_img, x.h, x.w, x.c, 0, pv.halo, pv.Cp, sel, out);
     };
     auto halo_fill = [&](int t) {
       View vv = V(t);
@@ -913,7 +956,7 @@ void eval_one(ptq_ctx* c, const ptq_config& cfg, unsigned long long* d_correct, 
       const int fc_ = c->first_compute;
       const int mt = P.mat[fc_];
       const int pf = c->pool_fold;
-      if (pf >= 0 && P.psrc[c->nodes[pf].out] == P.psrc[c->nodes[fc_].out] && probe_t < 0) {
+      if (pf >= 0 && P.psrc[c->nodes[pf].out] == P.psrc[c->nodes[fc_].out] && !pr) {
         // quantize maxpool(relu(prefix)) straight into the maxpool's output codes
         const int tp = c->nodes[pf].out;
         const View vt = V(tp);
@@ -944,9 +987,12 @@ void eval_one(ptq_ctx* c, const ptq_config& cfg, unsigned long long* d_correct, 
         WeightsDev& wd = c->W[i];
         const int tout = P.mat[i];
         const LayerSt& L = P.h_layers[P.layer_of[i]];
+        const TensorI& yo = c->tens[n.out];
+        const bool acc_probe = pr && pr->acc_node == i && !sel.empty();
+        int* d_acc = acc_probe ? c->dalloc<int>((size_t)B * yo.elems) : nullptr;
         if (n.kind == PTQ_DWCONV) {
           launch_dwconv_i8(V(tin), V(tout), wd.codes + (size_t)wv * wd.bytes_per_variant,
-                           wd.zp + (size_t)wv * wd.cout, n.k, n.stride, n.pad, L, c->st);
+                           wd.zp + (size_t)wv * wd.cout, n.k, n.stride, n.pad, L, c->st, d_acc);
           check_launch(c);
         } else {
           ConvTcArgs a{};
@@ -1013,10 +1059,22 @@ void eval_one(ptq_ctx* c, const ptq_config& cfg, unsigned long long* d_correct, 
           if (c->conv_ref) launch_conv_i8_ref(a, wd.bn, c->st);
           else launch_conv_tc(a, wd.bn, c->st);
           check_launch(c);
+          if (d_acc) {                               // probe: the same tcgen05 launch, acc epilogue
+            REQ(!c->conv_ref, "accumulator probes need the tensor-core conv");
+            ConvTcArgs b = a;
+            b.acc_out = d_acc;
+            launch_conv_tc(b, wd.bn, c->st);
+            check_launch(c);
+          }
           if (timed) {
             CK(cudaEventRecord(eb, c->st));
             c->conv_ops += 2.0 * (double)B * a.OH * a.OW * (double)wd.cout * (double)wd.kreal;
           }
+        }
+        if (d_acc) {
+          copy_nchw<int>(c, d_acc, yo.elems, yo.h, yo.w, yo.c, 0, 0, yo.c, sel, pr->acc_out);
+          pr->acc_found = true;
+          c->dfree(d_acc);
         }
         halo_fill(tout);
         probe(tout);
@@ -1079,8 +1137,30 @@ void eval_one(ptq_ctx* c, const ptq_config& cfg, unsigned long long* d_correct, 
     if (P.psrc[ot] >= 0) launch_argmax_codes(V(ot), c->d_labels + img0, d_correct, c->st);
     else launch_argmax_f32(c->d_f32[ot], B, c->tens[ot].c, c->d_labels + img0, d_correct, c->st);
     check_launch(c);
+    if (pr && !sel.empty() && pr->logit_out) {       // run_quantized's return value
+      const TensorI& o = c->tens[ot];
+      if (P.psrc[ot] >= 0) {                         // dequantize_array of the output codes (F3)
+        float* d_y = c->dalloc<float>((size_t)B * o.elems);
+        launch_dequant(V(ot), as, az, P.psrc[ot], d_y, c->st);
+        check_launch(c);
+        copy_nchw<float>(c, d_y, o.elems, 1, 1, o.c, 0, 0, o.c, sel, pr->logit_out);
+        c->dfree(d_y);
+      } else {
+        copy_nchw<float>(c, c->d_f32[ot], o.elems, 1, 1, o.c, 0, 0, o.c, sel, pr->logit_out);
+      }
+    }
+    if (pr && !sel.empty() && pr->f32_tensor >= 0) { // an fp32-domain tensor of this config
+      const int t = pr->f32_tensor;
+      const TensorI& x = c->tens[t];
+      const float* src = nullptr;
+      int64_t stride = x.elems;
+      if (cfg.mixed && t == c->nodes[c->first_compute].out) src = c->d_prefix + img0 * x.elems;
+      else if (P.psrc[t] < 0 && c->d_f32[t]) src = c->d_f32[t];
+      REQ(src, "tensor is not an fp32-domain tensor of this config");
+      copy_nchw<float>(c, src, stride, x.h, x.w, x.c, 0, 0, x.c, sel, pr->f32_out);
+      pr->f32_found = true;
+    }
   }
-  (void)e0; (void)e1;
 }
 
 }  // namespace
@@ -1365,7 +1445,7 @@ int ptq_eval_configs(ptq_ctx* c, const ptq_config* cfgs, int32_t n_cfg, int64_t*
       std::stable_sort(order.begin(), order.end(), [&](int x, int y) { return key(x) < key(y); });
       for (int i : order) {
         c->cur_cfg = b0 + i;
-        eval_one(c, cfgs[b0 + i], c->d_correct + i, -1, nullptr);
+        eval_one(c, cfgs[b0 + i], c->d_correct + i, nullptr);
       }
       c->cur_cfg = 0;
       std::vector<unsigned long long> h(nb);
@@ -1392,9 +1472,124 @@ int ptq_probe_codes(ptq_ctx* c, const ptq_config* cfg, int32_t tensor, int8_t* o
     ensure_eval_buffers(c);
     REQ(c->plans[cfg->mixed].psrc[tensor] >= 0, "tensor is in the fp32 domain for this config");
     REQ(c->d_codes[tensor], "tensor is fused away (set option fusion=0 to probe it)");
+    ProbeReq pr;
+    for (int64_t i = 0; i < c->n_eval; ++i) pr.imgs.push_back(i);
+    pr.tensors = {tensor};
+    pr.code_out = {out};
+    pr.found = {0};
     CK(cudaMemsetAsync(c->d_correct, 0, 8, c->st));
-    eval_one(c, *cfg, c->d_correct, tensor, out);
+    eval_one(c, *cfg, c->d_correct, &pr);
     CK(cudaStreamSynchronize(c->st));
+    REQ(pr.found[0], "tensor is fused away (set option fusion=0 to probe it)");
+  });
+}
+
+static void probe_images(ptq_ctx* c, ProbeReq& pr, int32_t n_imgs, const int64_t* imgs) {
+  REQ(n_imgs > 0 && imgs, "no probe images");
+  for (int i = 0; i < n_imgs; ++i) {
+    REQ(imgs[i] >= 0 && imgs[i] < c->n_eval, "probe image out of range");
+    pr.imgs.push_back(imgs[i]);
+  }
+}
+
+int ptq_probe_tensors(ptq_ctx* c, const ptq_config* cfg, int32_t n_tensors, const int32_t* tensors,
+                      int32_t n_imgs, const int64_t* imgs, int8_t* out, int32_t* found) {
+  return guarded([&] {
+    REQ(c && cfg && tensors && out && found && n_tensors > 0, "null argument");
+    CK(cudaSetDevice(c->dev));
+    prepare(c);
+    ensure_eval_buffers(c);
+    ProbeReq pr;
+    probe_images(c, pr, n_imgs, imgs);
+    int64_t off = 0;
+    for (int k = 0; k < n_tensors; ++k) {
+      REQ(tensors[k] >= 0 && tensors[k] < c->T, "bad tensor id");
+      pr.tensors.push_back(tensors[k]);
+      pr.code_out.push_back(out + off);
+      pr.found.push_back(0);
+      off += (int64_t)n_imgs * c->tens[tensors[k]].elems;
+    }
+    CK(cudaMemsetAsync(c->d_correct, 0, 8, c->st));
+    eval_one(c, *cfg, c->d_correct, &pr);
+    CK(cudaStreamSynchronize(c->st));
+    for (int k = 0; k < n_tensors; ++k) found[k] = pr.found[k];
+  });
+}
+
+int ptq_probe_acc(ptq_ctx* c, const ptq_config* cfg, int32_t node, int32_t n_imgs, const int64_t* imgs,
+                  int32_t* out) {
+  return guarded([&] {
+    REQ(c && cfg && out, "null argument");
+    REQ(node >= 0 && node < (int)c->nodes.size() && is_compute(c->nodes[node].kind), "not a compute node");
+    CK(cudaSetDevice(c->dev));
+    prepare(c);
+    ensure_eval_buffers(c);
+    REQ(!c->plans[cfg->mixed].fp32node[node], "node runs in fp32 under this config");
+    ProbeReq pr;
+    probe_images(c, pr, n_imgs, imgs);
+    pr.acc_node = node;
+    pr.acc_out = out;
+    CK(cudaMemsetAsync(c->d_correct, 0, 8, c->st));
+    eval_one(c, *cfg, c->d_correct, &pr);
+    CK(cudaStreamSynchronize(c->st));
+    REQ(pr.acc_found, "accumulator probe did not run");
+  });
+}
+
+int ptq_probe_output(ptq_ctx* c, const ptq_config* cfg, int32_t n_imgs, const int64_t* imgs, float* out) {
+  return guarded([&] {
+    REQ(c && cfg && out, "null argument");
+    CK(cudaSetDevice(c->dev));
+    prepare(c);
+    ensure_eval_buffers(c);
+    ProbeReq pr;
+    probe_images(c, pr, n_imgs, imgs);
+    pr.logit_out = out;
+    CK(cudaMemsetAsync(c->d_correct, 0, 8, c->st));
+    eval_one(c, *cfg, c->d_correct, &pr);
+    CK(cudaStreamSynchronize(c->st));
+  });
+}
+
+int ptq_probe_f32(ptq_ctx* c, const ptq_config* cfg, int32_t tensor, int32_t n_imgs, const int64_t* imgs,
+                  float* out) {
+  return guarded([&] {
+    REQ(c && cfg && out && tensor >= 0 && tensor < c->T, "bad argument");
+    CK(cudaSetDevice(c->dev));
+    prepare(c);
+    ensure_eval_buffers(c);
+    ProbeReq pr;
+    probe_images(c, pr, n_imgs, imgs);
+    pr.f32_tensor = tensor;
+    pr.f32_out = out;
+    CK(cudaMemsetAsync(c->d_correct, 0, 8, c->st));
+    eval_one(c, *cfg, c->d_correct, &pr);
+    CK(cudaStreamSynchronize(c->st));
+    REQ(pr.f32_found, "tensor is not an fp32-domain tensor of this config");
+  });
+}
+
+int ptq_minmax_host(ptq_ctx* c, const float* x, int32_t n_img, int64_t elems, float* range) {
+  return guarded([&] {
+    REQ(c && x && range && n_img > 0 && elems > 0, "bad argument");
+    CK(cudaSetDevice(c->dev));
+    float* d_x = c->dalloc<float>((size_t)n_img * elems);
+    unsigned int* d_mm = c->dalloc<unsigned int>((size_t)n_img * 2);
+    int* d_s = c->dalloc<int>(n_img);
+    float* d_r = c->dalloc<float>(2);
+    std::vector<int> sl(n_img);
+    for (int i = 0; i < n_img; ++i) sl[i] = i;
+    CK(cudaMemcpyAsync(d_x, x, (size_t)n_img * elems * sizeof(float), cudaMemcpyHostToDevice, c->st));
+    CK(cudaMemcpyAsync(d_s, sl.data(), n_img * sizeof(int), cudaMemcpyHostToDevice, c->st));
+    launch_fill_minmax(d_mm, n_img, c->st);
+    check_launch(c);
+    launch_minmax_per_image(d_x, elems, n_img, d_mm, c->st);   // F1a, as in ptq_calib_forward
+    check_launch(c);
+    launch_minmax_reduce_cache(d_mm, 1, n_img, d_s, n_img, d_r, c->st);
+    check_launch(c);
+    CK(cudaMemcpyAsync(range, d_r, 2 * sizeof(float), cudaMemcpyDeviceToHost, c->st));
+    CK(cudaStreamSynchronize(c->st));
+    for (void* p : {(void*)d_x, (void*)d_mm, (void*)d_s, (void*)d_r}) c->dfree(p);
   });
 }
 

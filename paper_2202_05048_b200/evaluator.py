@@ -369,6 +369,73 @@ class GpuEvaluator:
             _lib.check(self.lib.ptq_probe_codes(self._ctx, C.byref(cd), tid, _lib.ptr(out), C.byref(n)))
         return out
 
+    # ------------------------------------------------------------ parity probes (image subsets)
+    def _imgs(self, imgs) -> np.ndarray:
+        return np.ascontiguousarray(np.asarray(imgs, dtype=np.int64).ravel())
+
+    def probe_tensors(self, cfg, tensors, imgs) -> dict:
+        """int8 codes {tensor: [n_imgs, C, H, W]} of every requested tensor the evaluation of
+        ``cfg`` materialises, for eval images ``imgs`` (one device evaluation)."""
+        from .ir import tensor_shapes
+        shapes = tensor_shapes(self.graph)
+        imgs = self._imgs(imgs)
+        tids = np.asarray([self.lowered.tensor_ids[t] for t in tensors], dtype=np.int32)
+        sizes = [len(imgs) * int(np.prod(shapes[t])) for t in tensors]
+        out = np.zeros(max(1, sum(sizes)), dtype=np.int8)
+        found = np.zeros(len(tids), dtype=np.int32)
+        cd = _lib.ConfigDesc(*config_key(cfg))
+        with self._lock:
+            _lib.check(self.lib.ptq_probe_tensors(self._ctx, C.byref(cd), len(tids), _lib.ptr(tids), len(imgs),
+                                                  _lib.ptr(imgs), _lib.ptr(out), _lib.ptr(found)))
+        res, off = {}, 0
+        for t, n, f in zip(tensors, sizes, found):
+            if f:
+                res[t] = out[off:off + n].reshape((len(imgs),) + tuple(shapes[t]))
+            off += n
+        return res
+
+    def probe_acc(self, cfg, node_id: str, imgs) -> np.ndarray:
+        """Clipped int32 accumulators of one int8 compute node, [n_imgs, Cout, OH, OW]."""
+        from .ir import tensor_shapes
+        node = next(i for i, n in enumerate(self.graph.nodes) if n.id == node_id)
+        shape = tuple(tensor_shapes(self.graph)[self.graph.nodes[node].output])
+        imgs = self._imgs(imgs)
+        out = np.zeros((len(imgs),) + shape, dtype=np.int32)
+        cd = _lib.ConfigDesc(*config_key(cfg))
+        with self._lock:
+            _lib.check(self.lib.ptq_probe_acc(self._ctx, C.byref(cd), node, len(imgs), _lib.ptr(imgs),
+                                              _lib.ptr(out)))
+        return out
+
+    def probe_output(self, cfg, imgs) -> np.ndarray:
+        """run_quantized's return value for eval images ``imgs`` (intexec.py:337-351)."""
+        imgs = self._imgs(imgs)
+        out = np.zeros((len(imgs), int(self.graph.output_classes)), dtype=np.float32)
+        cd = _lib.ConfigDesc(*config_key(cfg))
+        with self._lock:
+            _lib.check(self.lib.ptq_probe_output(self._ctx, C.byref(cd), len(imgs), _lib.ptr(imgs), _lib.ptr(out)))
+        return out
+
+    def probe_f32(self, cfg, tensor: str, imgs) -> np.ndarray:
+        """An fp32-domain tensor of ``cfg`` (FirstLastFp32 layers), [n_imgs, C, H, W]."""
+        from .ir import tensor_shapes
+        shape = tuple(tensor_shapes(self.graph)[tensor])
+        imgs = self._imgs(imgs)
+        out = np.zeros((len(imgs),) + shape, dtype=np.float32)
+        cd = _lib.ConfigDesc(*config_key(cfg))
+        with self._lock:
+            _lib.check(self.lib.ptq_probe_f32(self._ctx, C.byref(cd), self.lowered.tensor_ids[tensor], len(imgs),
+                                              _lib.ptr(imgs), _lib.ptr(out)))
+        return out
+
+    def minmax_array(self, x: np.ndarray) -> tuple[float, float]:
+        """Device min/max of a host array [n_img, ...] through the calibration kernels."""
+        x = np.ascontiguousarray(np.asarray(x, dtype=np.float32))
+        x = x.reshape(x.shape[0], -1)
+        r = np.zeros(2, dtype=np.float32)
+        _lib.check(self.lib.ptq_minmax_host(self._ctx, _lib.ptr(x), x.shape[0], x.shape[1], _lib.ptr(r)))
+        return float(r[0]), float(r[1])
+
     def run_quantized_codes(self, cfg) -> np.ndarray:
         """Output codes of the eval set (intexec.run_quantized(..., return_codes=True))."""
         from .intonly import run_quantized_codes

@@ -194,6 +194,26 @@ def test_codes_every_tensor_bit_exact(injected, golden, ds, toys, rec, ci):
 
 
 @pytest.mark.parametrize("rec", TOYS)
+@pytest.mark.parametrize("ci", [2, 12, 50, 92])
+def test_accumulators_and_logits_bit_exact(injected, golden, ds, toys, rec, ci):
+    """int32-saturated accumulators acc + bias of every int8 compute node (intexec.py:177-190),
+    read from the tcgen05 / depthwise launches' accumulator epilogue, and run_quantized's
+    dequantized output (intexec.py:346-348, schemes.py:153-155): bit-exact on all eval images
+    with the reference's caches (zw != 0 and zw == 0, per-tensor and per-channel)."""
+    ev = injected[rec]
+    cfg = enumerate_space(GENERIC)[ci]
+    qm = O.quantize_model(toys[rec], oracle_caches(golden, rec)[cfg.cache], cfg)
+    accs = {}
+    out = O.run_quantized(qm, ds.eval_images, accs=accs)
+    imgs = np.arange(len(ds.eval_images))
+    assert accs
+    for node_id, want in accs.items():
+        got = ev.probe_acc(cfg, node_id, imgs)
+        assert np.array_equal(got, want.reshape(got.shape)), (rec, ci, node_id)
+    assert np.array_equal(ev.probe_output(cfg, imgs), np.asarray(out, dtype=np.float32)), (rec, ci)
+
+
+@pytest.mark.parametrize("rec", TOYS)
 def test_grid_matches_reference(injected, golden, rec):
     """Full 96-config grid with the reference's caches: top-1 bit-exact vs App. B."""
     arrs, _ = golden
