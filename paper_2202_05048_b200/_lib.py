@@ -14,7 +14,8 @@ import os
 import numpy as np
 
 HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(HERE, "libptq_b200.so")
+# PTQ_B200_LIB: an alternative build of the same library (kernel A/B experiments only)
+LIB_PATH = os.environ.get("PTQ_B200_LIB") or os.path.join(HERE, "libptq_b200.so")
 
 PTQ_NBINS = 2048
 PTQ_NWINDOWS = 1921

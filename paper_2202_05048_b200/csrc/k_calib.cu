@@ -13,6 +13,8 @@
 // order (8 strided accumulators per <=128-element leaf, halving splits rounded
 // to multiples of 8), so it is bit-identical to numpy whenever the log values
 // agree; the host re-ranks near-ties with numpy (evaluator.py).
+#include <atomic>
+
 #include "common.cuh"
 #include "kernels.h"
 
@@ -434,11 +436,14 @@ void launch_histogram(const float* x, int64_t elems, const int* slots, int n_slo
                       const float* range, unsigned long long* counts, cudaStream_t s) {
   int64_t total = elems * n_slots;
   constexpr int smem = HIST_COPIES * PTQ_NBINS * 4;
-  static bool attr = false;
-  if (!attr) {
-    cudaFuncSetAttribute(k_histogram, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
-    attr = true;
-  }
+  // per-device function attribute, raised once per device (a failure surfaces as a failed launch)
+  static std::atomic<uint64_t> attr{0};
+  int dev = 0;
+  cudaGetDevice(&dev);
+  const uint64_t bit = 1ull << (dev & 63);
+  if (!(attr.load() & bit) &&
+      cudaFuncSetAttribute(k_histogram, cudaFuncAttributeMaxDynamicSharedMemorySize, smem) == cudaSuccess)
+    attr.fetch_or(bit);
   k_histogram<<<nblocks(total, 256, 148 * HIST_BLOCKS_PER_SM), 256, smem, s>>>(x, elems, slots, n_slots, range,
                                                                                counts);
 }

@@ -28,7 +28,9 @@
 //               add as a 64 KB shared-memory lookup table, 16-byte code stores.
 // The smem pipeline depth is chosen at launch from what the per-channel constants
 // and the add table leave of the 227 KB.
+#include <atomic>
 #include <climits>
+#include <mutex>
 
 #include "common.cuh"
 #include "kernels.h"
@@ -36,19 +38,24 @@
 namespace ptq {
 
 constexpr int TC_BM = 128;
-// per-channel epilogue constants of the layer being run, in constant memory for the
-// fused-add layers: their shared-memory pipe is saturated by the add table, so the
-// per-output constant broadcast goes through the constant cache instead (elsewhere the
-// shared-memory copy is faster).  Written by the launcher with a stream-ordered
+// per-channel epilogue constants of the layer being run, in constant memory: the epilogue
+// indexes them with warp-uniform channel bases, so they load into uniform registers through
+// the constant cache and never touch the L1 data pipe (shared-memory broadcasts of these
+// 16-byte records were the L1 limiter).  Written by the launcher with a stream-ordered
 // device-to-device copy before every launch.
 constexpr int TC_MAX_COUT = 2048;
-__constant__ EpiParam c_ep[TC_MAX_COUT];
+__constant__ EpiParam c_ep[TC_MAX_COUT];    // SoA image, see ep_soa() in kernels.h
 
 constexpr int TC_MAX_STAGES = 10;                 // smem pipeline depth cap (runtime depth: launcher)
 constexpr int TC_SMEM_MAX = 232448;                // 227 KB opt-in dynamic smem per CTA
 constexpr int TC_A_STAGE = TC_BM * 128;            // 16 KB: 8 chunks x 128 rows x 16 B
-constexpr int TC_EPI_WARPS = 12;                   // 3 per SM sub-partition (register budget: no spills)
-constexpr int TC_THREADS = (4 + TC_EPI_WARPS) * 32;    // 16 warps: 4 per SM sub-partition
+#ifndef PTQ_EPI_GROUPS
+#define PTQ_EPI_GROUPS 3
+#endif
+constexpr int TC_NG = PTQ_EPI_GROUPS;               // epilogue column groups per TMEM lane quarter
+constexpr int TC_EPI_WARPS = 4 * TC_NG;             // NG per SM sub-partition
+constexpr int TC_THREADS = (4 + TC_EPI_WARPS) * 32;    // + producer / MMA warps 0-3
+
 
 __device__ __forceinline__ uint64_t umma_desc(uint32_t saddr, uint32_t lbo, uint32_t sbo) {
   uint64_t d = 0;
@@ -138,6 +145,10 @@ struct EpiK {
   // fused add on the fp64 pipe: conv / skip operand (zero point as a 2^31 bias, ratio)
   uint32_t zc_bias, zs_bias;
   double rc, rs;
+  // per-tensor weight granularity (rt.uni): the requant multiplier and the weight zero point
+  // are the same for every channel and live in registers; only cc is loaded per channel
+  double m0;
+  int zw0;
 };
 // 4-channel groups of a 16-channel chunk whose fused add runs on the fp64 pipe instead of
 // the shared-memory table: one group of four balances the L1 (table) and fp64 pipes (A/B
@@ -160,24 +171,51 @@ __device__ __forceinline__ int requant_raw(uint32_t accb, double m, const LayerR
 // residual add is one shared-memory lookup: stab[skip byte * 260 + conv code] with stab
 // pointing at column 128 of the table (built exactly by k_layer_params for the config;
 // operand order is baked in).
-template <bool WZP, bool SKIP, bool CLAMP, bool RELU>
-__device__ __forceinline__ int4 epi_chunk16(const uint32_t (&v)[16], const EpiParam* __restrict__ ep,
+template <bool WZP, bool SKIP, bool CLAMP, bool RELU, bool PT>
+__device__ __forceinline__ int4 epi_chunk16(const uint32_t (&v)[16], const uint8_t* __restrict__ sp, int cs,
                                             int cb, int rowsum, const LayerRt& rt, const EpiK& k,
                                             const int8_t* __restrict__ stab, const int4 skv) {
+  // per-channel constants, structure of arrays (m[cs] fp64, cc[cs], zw[cs]): from shared
+  // memory (sp), or from __constant__ c_ep for the fused-add layers whose shared-memory pipe
+  // the add table saturates.  Each broadcast 16-byte load costs the L1 data pipe several
+  // wavefronts, so only what the variant needs is loaded: cc always, m and zw per channel
+  // unless the weights are per-tensor (PT).
+  const uint8_t* cbase = SKIP ? reinterpret_cast<const uint8_t*>(c_ep) : sp;
   uint32_t packed[4];
   const uint32_t skw[4] = {(uint32_t)skv.x, (uint32_t)skv.y, (uint32_t)skv.z, (uint32_t)skv.w};
 #pragma unroll
   for (int g = 0; g < 4; ++g) {
-    int4 raw[4];
-#pragma unroll
-    for (int j = 0; j < 4; ++j) raw[j] = reinterpret_cast<const int4*>((SKIP ? c_ep : ep) + cb + g * 4)[j];
+    int4 cc4, zw4;
+    double2 m01, m23;
+    if (SKIP) {
+      cc4 = reinterpret_cast<const int4*>(reinterpret_cast<const uint8_t*>(c_ep) + 8 * cs)[(cb >> 2) + g];
+      if (WZP && !PT) zw4 = reinterpret_cast<const int4*>(reinterpret_cast<const uint8_t*>(c_ep) + 12 * cs)[(cb >> 2) + g];
+      if (!PT) {
+        m01 = reinterpret_cast<const double2*>(c_ep)[(cb >> 1) + 2 * g];
+        m23 = reinterpret_cast<const double2*>(c_ep)[(cb >> 1) + 2 * g + 1];
+      }
+    } else {
+      cc4 = reinterpret_cast<const int4*>(sp + 8 * cs)[(cb >> 2) + g];
+      if (WZP && !PT) zw4 = reinterpret_cast<const int4*>(sp + 12 * cs)[(cb >> 2) + g];
+      if (!PT) {
+        m01 = reinterpret_cast<const double2*>(sp)[(cb >> 1) + 2 * g];
+        m23 = reinterpret_cast<const double2*>(sp)[(cb >> 1) + 2 * g + 1];
+      }
+    }
+    (void)cbase;
+    const int ccv[4] = {cc4.x, cc4.y, cc4.z, cc4.w};
+    int zwv[4] = {0, 0, 0, 0};
+    double mv[4] = {k.m0, k.m0, k.m0, k.m0};
+    if (!PT) {
+      mv[0] = m01.x; mv[1] = m01.y; mv[2] = m23.x; mv[3] = m23.y;
+      if (WZP) { zwv[0] = zw4.x; zwv[1] = zw4.y; zwv[2] = zw4.z; zwv[3] = zw4.w; }
+    }
     int q[4];
 #pragma unroll
     for (int j = 0; j < 4; ++j) {
-      const double m = __hiloint2double(raw[j].y, raw[j].x);
-      uint32_t accb = v[g * 4 + j] + (uint32_t)raw[j].z;
-      if (WZP) accb -= (uint32_t)(raw[j].w * rowsum);
-      q[j] = requant_raw<CLAMP>(accb, m, rt, k);
+      uint32_t accb = v[g * 4 + j] + (uint32_t)ccv[j];
+      if (WZP) accb -= (uint32_t)((PT ? k.zw0 : zwv[j]) * rowsum);
+      q[j] = requant_raw<CLAMP>(accb, mv[j], rt, k);
       if (RELU || SKIP) q[j] = imax(q[j], k.lo_conv);
       if (SKIP) {
         if ((PTQ_ADD_ALU_MASK >> g) & 1) {
@@ -299,27 +337,34 @@ struct EpiEnv {
   uint32_t tmem;
   uint64_t *tfull, *tempty, *rsfull;
   const int* rsum;
-  const EpiParam* ep;
+  const uint8_t* sp;                                 // shared-memory constants (non-add layers), SoA
+  int cs;                                            // SoA channel stride = roundup(Cout, 16)
   const int8_t* stab_c;
   int q, grp, row, M, n_tiles, n_nt;
 };
 
 // persistent epilogue tile loop of one variant (GENERIC: runtime dispatch, slow layers and
-// the profiling ablation)
-template <int BN, bool WZP, bool SKIP, bool CLAMP, bool RELU, bool GENERIC, bool ACC = false>
+// the profiling ablation).  q / grp come from a warp-uniform (shuffled) warp index, so the
+// chunk loop and the channel base cb are uniform: the per-channel constants c_ep[cb + j] are
+// loaded into uniform registers through the constant cache (LDCU) and used as operands
+// directly -- no shared-memory loads (each broadcast LDS.128 costs 4 L1 wavefronts per warp,
+// which saturated the L1 data pipe) and no vector registers.
+template <int BN, bool WZP, bool SKIP, bool CLAMP, bool RELU, bool GENERIC, bool ACC = false, bool PT = false>
 __device__ __forceinline__ void epi_tiles(const ConvTcArgs& a, const LayerRt& rt, const EpiK& k, const EpiEnv& e) {
   constexpr int NCH = BN / 16;                       // 16-column chunks per tile
   const int Cout = a.L.cout;
   const bool has_skip = GENERIC ? a.skip.p != nullptr : SKIP;
   uint32_t lt = 0;
-  int rot = 0;                                       // lt % 3
-  for (int tile = blockIdx.x; tile < e.n_tiles; tile += gridDim.x, ++lt, rot = rot == 2 ? 0 : rot + 1) {
+  int rot = 0;                                       // lt % TC_NG
+  for (int tile = blockIdx.x; tile < e.n_tiles; tile += gridDim.x, ++lt, rot = rot == TC_NG - 1 ? 0 : rot + 1) {
     const uint32_t buf = lt & 1u, uph = (lt >> 1) & 1u;
     const int mt = (int)a.div_nt.div((uint32_t)tile);
-    const int nt = tile - mt * e.n_nt;
+    // n-tile (warp-uniform; the shuffle lets ptxas keep it, and every channel index derived
+    // from it, in uniform registers)
+    const int nt = __shfl_sync(0xffffffffu, tile - mt * e.n_nt, 0);
     // chunks c = first, first+3, ...: the assignment rotates with the tile so the three
     // column groups share BN/16 chunks evenly over consecutive tiles
-    const int first = e.grp >= rot ? e.grp - rot : e.grp - rot + 3;
+    const int first = e.grp >= rot ? e.grp - rot : e.grp - rot + TC_NG;
     const int m = mt * TC_BM + e.row;
     RowGeo g;
     int8_t* orow;
@@ -350,28 +395,28 @@ __device__ __forceinline__ void epi_tiles(const ConvTcArgs& a, const LayerRt& rt
     tc_fence_after();
     const uint32_t tbase = e.tmem + ((uint32_t)(e.q * 32) << 16) + buf * BN;
 #pragma unroll 1
-    for (int c = first; c < NCH; c += 3) {
+    for (int c = first; c < NCH; c += TC_NG) {
+      const int cb = nt * BN + c * 16;
       if (ACC) {
-        const int cb = nt * BN + c * 16;
-        if (cb >= Cout) continue;                  // warp-uniform
+        if (cb >= Cout) continue;                    // warp-uniform
         const int64_t pix = a.flat ? (int64_t)m : ((int64_t)g.n * a.OHr + g.oh) * a.OWr + g.ow;
         epi_acc_chunk(tbase + (uint32_t)(c * 16), cb, rowsum, a, rt, g.ok ? a.acc_out + pix * Cout : nullptr);
         continue;
       }
       uint32_t v[16];
       tmem_ld16(tbase + (uint32_t)(c * 16), v);
-      const int cb = nt * BN + c * 16;
-      if (cb >= a.out.Cp) continue;              // warp-uniform: the slow path re-reads TMEM
+      if (cb >= a.out.Cp) continue;                  // warp-uniform: the slow path re-reads TMEM
       int4 skv = make_int4(0, 0, 0, 0);
       if (has_skip) {
         skv = sk_next;
-        if (srow && c + 3 < NCH && cb + 48 < a.out.Cp) sk_next = __ldg(reinterpret_cast<const int4*>(srow + cb + 48));
+        if (srow && c + TC_NG < NCH && cb + 16 * TC_NG < a.out.Cp)
+          sk_next = __ldg(reinterpret_cast<const int4*>(srow + cb + 16 * TC_NG));
       }
       int4 res;
       if (GENERIC && a.ablate == 1) {
         res = make_int4((int)v[0], (int)v[1], (int)v[2], (int)v[3]);
       } else if (!GENERIC && cb + 16 <= Cout) {
-        res = epi_chunk16<WZP, SKIP, CLAMP, RELU>(v, e.ep, cb, (int)rowsum, rt, k, e.stab_c, skv);
+        res = epi_chunk16<WZP, SKIP, CLAMP, RELU, PT>(v, e.sp, e.cs, cb, (int)rowsum, rt, k, e.stab_c, skv);
       } else {
         res = epi_slow_chunk(tbase + (uint32_t)(c * 16), cb, rowsum, a, rt, k.lo_conv, k.lo_add, skv);
       }
@@ -380,6 +425,14 @@ __device__ __forceinline__ void epi_tiles(const ConvTcArgs& a, const LayerRt& rt
     tc_fence_before();
     mbar_arrive(&e.tempty[buf]);                     // accumulator buffer may be reused
   }
+}
+
+// per-tensor weights (rt.uni: one requant multiplier and weight zero point for the layer)
+// take the PT variant, which loads only cc per channel
+template <int BN, bool WZP, bool SKIP, bool CLAMP, bool RELU>
+__device__ __forceinline__ void epi_pt(const ConvTcArgs& a, const LayerRt& rt, const EpiK& k, const EpiEnv& e) {
+  if (rt.uni) epi_tiles<BN, WZP, SKIP, CLAMP, RELU, false, false, true>(a, rt, k, e);
+  else epi_tiles<BN, WZP, SKIP, CLAMP, RELU, false, false, false>(a, rt, k, e);
 }
 
 template <int BN>
@@ -658,8 +711,11 @@ __global__ void __launch_bounds__(TC_THREADS, 1) k_conv_tc(const __grid_constant
     __syncwarp();
   } else {
     // ------------------------------------------------ epilogue warps
-    const int q = warp & 3;                          // TMEM lane quarter this warp may access
-    const int grp = (warp - 4) >> 2;                  // column group (3 groups per lane quarter)
+    // warp-uniform warp index (a shuffle from lane 0): q, grp, the chunk loop and the channel
+    // base become uniform values, so the per-channel constants load into uniform registers
+    const int wu = __shfl_sync(0xffffffffu, warp, 0);
+    const int q = wu & 3;                            // TMEM lane quarter this warp may access
+    const int grp = (wu - 4) >> 2;                   // column group (TC_NG groups per lane quarter)
     const int row = q * 32 + lane;
     const LayerRt rt = *a.L.rt;
     EpiK k;
@@ -673,16 +729,19 @@ __global__ void __launch_bounds__(TC_THREADS, 1) k_conv_tc(const __grid_constant
     k.rs = a.conv_is_a ? rt.rb : rt.ra;
     const int Cout = a.L.cout;
     // stage the fused-add table (or the per-channel constants) in shared memory, then sync
-    // the 12 epilogue warps only
+    // the epilogue warps only (add layers read their constants from __constant__ c_ep)
+    const int cs = (a.L.cout + 15) & ~15;
     if (!a.addtab)
-      for (int i = threadIdx.x - 4 * 32; i < Cout; i += TC_EPI_WARPS * 32) sparam[i] = a.L.ep[i];
+      for (int i = threadIdx.x - 4 * 32; i < cs; i += TC_EPI_WARPS * 32) sparam[i] = a.L.ep[i];
     if (a.addtab)
       for (int i = threadIdx.x - 4 * 32; i < PTQ_ADDTAB_BYTES / 16; i += TC_EPI_WARPS * 32)
         reinterpret_cast<int4*>(stab)[i] = reinterpret_cast<const int4*>(a.addtab)[i];
     asm volatile("bar.sync 1, %0;" ::"n"(TC_EPI_WARPS * 32) : "memory");
-    const EpiParam* ep = sparam;
     const int8_t* stab_c = stab + 128;                // column of conv code 0
-    const EpiEnv e{tmem, tfull, tempty, rsfull, rsum, ep, stab_c, q, grp, row, M, n_tiles, n_nt};
+    k.m0 = rt.m0;
+    k.zw0 = rt.zw0;
+    const EpiEnv e{tmem, tfull, tempty, rsfull, rsum, reinterpret_cast<const uint8_t*>(sparam), cs, stab_c,
+                   q, grp, row, M, n_tiles, n_nt};
     // one persistent tile loop per epilogue variant: the per-chunk code carries no
     // layer-level dispatch (that overhead was ~20% of the hot loop's instructions)
     const bool skip = a.skip.p != nullptr, wzp = a.has_wzp != 0, clamp = !rt.noclamp,
@@ -690,20 +749,20 @@ __global__ void __launch_bounds__(TC_THREADS, 1) k_conv_tc(const __grid_constant
     if (a.acc_out) epi_tiles<BN, false, false, false, false, true, true>(a, rt, k, e);
     else if (rt.slow || a.ablate == 1) epi_tiles<BN, false, false, false, false, true>(a, rt, k, e);
     else if (skip) {
-      if (wzp) { if (clamp) epi_tiles<BN, true, true, true, false, false>(a, rt, k, e);
-                 else epi_tiles<BN, true, true, false, false, false>(a, rt, k, e); }
-      else { if (clamp) epi_tiles<BN, false, true, true, false, false>(a, rt, k, e);
-             else epi_tiles<BN, false, true, false, false, false>(a, rt, k, e); }
+      if (wzp) { if (clamp) epi_pt<BN, true, true, true, false>(a, rt, k, e);
+                 else epi_pt<BN, true, true, false, false>(a, rt, k, e); }
+      else { if (clamp) epi_pt<BN, false, true, true, false>(a, rt, k, e);
+             else epi_pt<BN, false, true, false, false>(a, rt, k, e); }
     } else if (wzp) {
-      if (clamp) { if (relu) epi_tiles<BN, true, false, true, true, false>(a, rt, k, e);
-                   else epi_tiles<BN, true, false, true, false, false>(a, rt, k, e); }
-      else { if (relu) epi_tiles<BN, true, false, false, true, false>(a, rt, k, e);
-             else epi_tiles<BN, true, false, false, false, false>(a, rt, k, e); }
+      if (clamp) { if (relu) epi_pt<BN, true, false, true, true>(a, rt, k, e);
+                   else epi_pt<BN, true, false, true, false>(a, rt, k, e); }
+      else { if (relu) epi_pt<BN, true, false, false, true>(a, rt, k, e);
+             else epi_pt<BN, true, false, false, false>(a, rt, k, e); }
     } else {
-      if (clamp) { if (relu) epi_tiles<BN, false, false, true, true, false>(a, rt, k, e);
-                   else epi_tiles<BN, false, false, true, false, false>(a, rt, k, e); }
-      else { if (relu) epi_tiles<BN, false, false, false, true, false>(a, rt, k, e);
-             else epi_tiles<BN, false, false, false, false, false>(a, rt, k, e); }
+      if (clamp) { if (relu) epi_pt<BN, false, false, true, true>(a, rt, k, e);
+                   else epi_pt<BN, false, false, true, false>(a, rt, k, e); }
+      else { if (relu) epi_pt<BN, false, false, false, true>(a, rt, k, e);
+             else epi_pt<BN, false, false, false, false>(a, rt, k, e); }
     }
   }
 
@@ -766,19 +825,16 @@ int conv_tc_bn_for(int cout) {
   return 256;
 }
 
-static int g_num_sms = 0;
-static int g_kwr_mode = 0;   // -1 disables the kw-reuse slabs and the stem slab (A/B testing)
-void conv_tc_set_kwr_mode(int m) { g_kwr_mode = m; }
 
 template <int BN>
 static void launch_bn(const ConvTcArgs& a, cudaStream_t s) {
-  // fixed part: barriers, TMEM slot, per-channel constants, optional add table; the rest
-  // of the 227 KB goes to pipeline stages (deeper for narrow tiles, at least 2)
+  // fixed part: barriers, TMEM slot, optional add table, resident B; the rest of the 227 KB
+  // goes to pipeline stages (deeper for narrow tiles, at least 2)
   const int n_nt = (a.L.cout + BN - 1) / BN;
   const size_t b_bytes = (size_t)a.n_kiter * BN * 128;
   const int b_res = n_nt == 1 && b_bytes <= 64 * 1024;
   const size_t fixed = 1024 + (2 * TC_MAX_STAGES + 8) * 8 + 2 * TC_BM * 4 + 16 +
-                       (a.addtab ? PTQ_ADDTAB_BYTES : (size_t)a.L.cout * sizeof(EpiParam)) +
+                       (a.addtab ? PTQ_ADDTAB_BYTES : (size_t)((a.L.cout + 15) & ~15) * sizeof(EpiParam)) +
                        (b_res ? b_bytes : 0);
   const size_t per_stage = (size_t)TC_A_STAGE + (b_res ? 0 : (size_t)BN * 128);
   int ns = (int)((TC_SMEM_MAX - fixed) / per_stage);
@@ -787,24 +843,39 @@ static void launch_bn(const ConvTcArgs& a, cudaStream_t s) {
   ConvTcArgs b = a;
   b.n_stages = ns;
   b.b_res = b_res;
-  // cout <= TC_MAX_COUT is checked when the graph is imported (conv_tc_max_cout)
-  if (a.addtab)
-    cudaMemcpyToSymbolAsync(c_ep, a.L.ep, (size_t)a.L.cout * sizeof(EpiParam), 0, cudaMemcpyDeviceToDevice, s);
   const size_t smem = (size_t)ns * per_stage + fixed;
-  static bool configured = false;
-  if (!configured) {
-    cudaFuncSetAttribute(k_conv_tc<BN>, cudaFuncAttributeMaxDynamicSharedMemorySize, TC_SMEM_MAX);
-    configured = true;
-  }
-  if (!g_num_sms) {
-    int dev = 0;
-    cudaGetDevice(&dev);
-    cudaDeviceGetAttribute(&g_num_sms, cudaDevAttrMultiProcessorCount, dev);
-  }
+  int dev = 0;
+  cudaGetDevice(&dev);
+  // the opt-in shared-memory limit is a per-device function attribute: raise it once per
+  // device (a failure leaves the launch to fail loudly in check_launch)
+  static std::atomic<uint64_t> configured{0};
+  const uint64_t bit = 1ull << (dev & 63);
+  if (!(configured.load() & bit) &&
+      cudaFuncSetAttribute(k_conv_tc<BN>, cudaFuncAttributeMaxDynamicSharedMemorySize, TC_SMEM_MAX) == cudaSuccess)
+    configured.fetch_or(bit);
+  int num_sms = 0;
+  cudaDeviceGetAttribute(&num_sms, cudaDevAttrMultiProcessorCount, dev);
   const int64_t M = (int64_t)a.in.N * a.OH * a.OW;
   const int64_t tiles = ((M + TC_BM - 1) / TC_BM) * ((a.L.cout + BN - 1) / BN);
-  const int grid = (int)(tiles < g_num_sms ? tiles : g_num_sms);   // persistent: one CTA per SM
+  const int grid = (int)(tiles < num_sms ? tiles : num_sms);   // persistent: one CTA per SM
+  // per-channel epilogue constants -> __constant__ c_ep with a stream-ordered copy right
+  // before the launch.  c_ep is one per device, so launches of several contexts on one
+  // device (other streams) are ordered through a per-device event: each copy waits for the
+  // previous conv launch on that device to finish reading the constants.
+  // cout <= TC_MAX_COUT is checked when the graph is imported (conv_tc_max_cout)
+  static std::mutex mu;
+  static cudaEvent_t last[64] = {};
+  static cudaStream_t last_stream[64] = {};
+  std::lock_guard<std::mutex> lk(mu);
+  const int d = dev & 63;
+  if (!last[d]) cudaEventCreateWithFlags(&last[d], cudaEventDisableTiming);
+  if (last_stream[d] && last_stream[d] != s) cudaStreamWaitEvent(s, last[d], 0);
+  if (a.addtab)
+    cudaMemcpyToSymbolAsync(c_ep, a.L.ep, (size_t)((a.L.cout + 15) & ~15) * sizeof(EpiParam), 0,
+                            cudaMemcpyDeviceToDevice, s);
   k_conv_tc<BN><<<grid, TC_THREADS, smem, s>>>(b);
+  cudaEventRecord(last[d], s);
+  last_stream[d] = s;
 }
 
 static ConvTcArgs with_divs(const ConvTcArgs& a0, int bn) {
@@ -841,7 +912,7 @@ static bool setup_tma_a(ConvTcArgs& a) {
   EncodeTiledFn fn = encode_tiled();
   if (!fn) return false;
   if (Cp == 16 && a.k == 4 && a.OH <= Hp - 3 && a.OW <= Wp - 3) {
-    if (g_kwr_mode >= 0 && (Wp + TC_BM + 3) * 16 <= TC_A_STAGE) {
+    if (a.kwr_mode >= 0 && (Wp + TC_BM + 3) * 16 <= TC_A_STAGE) {
       // preferred: one contiguous bulk copy per stage (the input buffer carries the slack
       // the last tiles read past the grid; those rows only feed masked outputs)
       a.tma_a = 67;
@@ -912,7 +983,7 @@ static void plan_launch(ConvTcArgs& t, int bn) {
   setup_tma_a(t);
   t.kwr = 0;
   t.a_iters = t.n_kiter;
-  if (t.tma_a == 64 && t.k == 3 && bn == 64 && t.L.cout <= 64 && g_kwr_mode >= 0 &&
+  if (t.tma_a == 64 && t.k == 3 && bn == 64 && t.L.cout <= 64 && t.kwr_mode >= 0 &&
       (size_t)t.n_kiter * 64 * 128 <= 64 * 1024) {    // needs the resident B of launch_bn
     // re-encode A with 136-row boxes: one slab per kh row of taps
     const int Hp = t.in.H + 2 * t.in.halo, Wp = t.in.W + 2 * t.in.halo;

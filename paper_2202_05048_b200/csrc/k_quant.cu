@@ -23,10 +23,6 @@ static inline int nblk(int64_t n, int t = 256, int cap = 148 * 32) {
   return (int)(b < 1 ? 1 : (b > cap ? cap : b));
 }
 
-static int g_concat_v16 = 1;
-void set_concat_v16(int v) { g_concat_v16 = v; }
-static bool concat_v16_enabled() { return g_concat_v16 != 0; }
-static int g_dwconv_v4 = 2;   // 2: k x k register-weight kernel, 1: 4-channel, 0: scalar
 
 __device__ __forceinline__ int64_t voff(const View& v, int n, int h, int w) {
   const int Hp = v.H + 2 * v.halo, Wp = v.W + 2 * v.halo;
@@ -215,14 +211,20 @@ __global__ void k_layer_params(const LayerSt* __restrict__ layers, const float* 
   const double sx = (double)as[L.in_hist], sy = (double)as[L.out_hist];
   const float* ws = L.wscale + (int64_t)wvar * L.cout;
   const long long zx = az[L.in_hist];
-  __shared__ int slow;
+  __shared__ int slow, zw_min, zw_max;
   __shared__ unsigned long long m_max_bits, m_min_bits;   // m > 0: bit order == value order
   __shared__ LayerRt srt;
   if (threadIdx.x == 0) {
     slow = 0;
     m_max_bits = 0ull;
     m_min_bits = ~0ull;
+    zw_min = INT_MAX;
+    zw_max = INT_MIN;
   }
+  const int cs = (L.cout + 15) & ~15;                    // SoA stride (kernels.h EpiParam)
+  double* ep_m = reinterpret_cast<double*>(L.ep);
+  int* ep_cc = reinterpret_cast<int*>(ep_m + cs);
+  int* ep_zw = ep_cc + cs;
   __syncthreads();
   for (int o = threadIdx.x; o < L.cout; o += blockDim.x) {
     double sw = (double)ws[o];
@@ -237,11 +239,11 @@ __global__ void k_layer_params(const LayerSt* __restrict__ layers, const float* 
       const long long cc = (long long)bq - zx * sw8 + (long long)L.kreal * zx * zw;
       const bool big = cc >= (1LL << 30) || cc <= -(1LL << 30);
       if (big) atomicOr(&slow, 1);
-      EpiParam e;
-      e.m = m;
-      e.cc = (int)((uint32_t)(big ? 0 : (int)cc) ^ 0x80000000u);   // biased by 2^31 (see i2d)
-      e.zw = (int)zw;
-      L.ep[o] = e;
+      ep_m[o] = m;
+      ep_cc[o] = (int)((uint32_t)(big ? 0 : (int)cc) ^ 0x80000000u);   // biased by 2^31 (see i2d)
+      ep_zw[o] = (int)zw;
+      atomicMin(&zw_min, (int)zw);
+      atomicMax(&zw_max, (int)zw);
       if (!(m > 0.0) || !isfinite(m)) atomicOr(&slow, 1);
       atomicMax(&m_max_bits, (unsigned long long)__double_as_longlong(m));
       atomicMin(&m_min_bits, (unsigned long long)__double_as_longlong(m));
@@ -263,6 +265,9 @@ __global__ void k_layer_params(const LayerSt* __restrict__ layers, const float* 
       else slow = 1;
       r.noclamp = mmax < 0.5;
     }
+    r.uni = L.ep && m_max_bits == m_min_bits && zw_min == zw_max;
+    r.m0 = L.ep ? __longlong_as_double((long long)m_max_bits) : 0.0;
+    r.zw0 = L.ep ? zw_max : 0;
     r.zx = az[L.in_hist];
     r.zy = az[L.out_hist];
     r.relu_zp = L.relu_hist >= 0 ? az[L.relu_hist] : INT_MIN;
@@ -699,8 +704,8 @@ __global__ void k_concat_codes_v16(View in, View out, int coff, const float* __r
 }
 
 void launch_concat_codes(View in, View out, int coff, const float* as, const int* az, int hin,
-                         int hout, cudaStream_t s) {
-  if (in.C % 16 == 0 && in.Cp % 16 == 0 && out.Cp % 16 == 0 && coff % 16 == 0 && concat_v16_enabled()) {
+                         int hout, cudaStream_t s, int v16) {
+  if (in.C % 16 == 0 && in.Cp % 16 == 0 && out.Cp % 16 == 0 && coff % 16 == 0 && v16) {
     k_concat_codes_v16<<<nblk((int64_t)in.N * in.H * in.W * (in.C / 16)), 256, 0, s>>>(
         in, out, coff, as, az, hin, hout);
     return;
@@ -835,8 +840,6 @@ void launch_pixsum(View in, int* P, cudaStream_t s) {
 // ---------------------------------------------------------------- depthwise int8 conv (CUDA cores)
 // acc = sum_taps (x - zx)(w - zw[c]) + bias[c]; clip int32; requant; fused relu.
 
-void set_dwconv_v4(int v) { g_dwconv_v4 = v; }
-static bool dwconv_v4_enabled() { return g_dwconv_v4 != 0; }
 
 __global__ void k_dwconv_i8(View in, View out, const int8_t* __restrict__ w,
                             const int* __restrict__ wzp, int k, int stride, int pad, LayerSt L,
@@ -977,14 +980,14 @@ __global__ void k_dwconv_i8_k(View in, View out, const int8_t* __restrict__ w,
 }
 
 void launch_dwconv_i8(View in, View out, const int8_t* w, const int* wzp, int k, int stride, int pad,
-                      LayerSt L, cudaStream_t s, int* acc_out) {
-  if (k == 3 && in.Cp % 4 == 0 && out.Cp % 4 == 0 && g_dwconv_v4 == 2) {
+                      LayerSt L, cudaStream_t s, int* acc_out, int variant) {
+  if (k == 3 && in.Cp % 4 == 0 && out.Cp % 4 == 0 && variant == 2) {
     constexpr int PX = 4;
     const int64_t total = (int64_t)out.N * out.H * ((out.W + PX - 1) / PX) * (out.Cp / 4);
     k_dwconv_i8_k<3, PX><<<nblk(total), 256, 0, s>>>(in, out, w, wzp, stride, pad, L, acc_out);
     return;
   }
-  if (in.Cp % 4 == 0 && out.Cp % 4 == 0 && dwconv_v4_enabled()) {
+  if (in.Cp % 4 == 0 && out.Cp % 4 == 0 && variant != 0) {
     k_dwconv_i8_v4<<<nblk((int64_t)out.N * out.H * out.W * (out.Cp / 4)), 256, 0, s>>>(
         in, out, w, wzp, k, stride, pad, L, acc_out);
     return;

@@ -30,14 +30,20 @@ struct LayerRt {
                        // saturates (|acc*m| > 300) and |acc*m| stays < 2^30 for the floor trick
   double mg_zy, mg_zo; // 1.5*2^52 + zp: floor(r) + zp via one round-down add
   int noclamp;         // max m < 0.5: |acc*m| < 2^30 for any int32 acc, no clamp needed
+  int uni;             // every channel has the same m and zw (per-tensor weights): m0 / zw0
+  double m0;
+  int zw0;
 };
 
 // per-config, per-output-channel epilogue constants of the tensor-core conv:
 //   acc = dot - zw*rowsum + cc  (cc = bias - zx*sum(w) + K*zx*zw), out = requant(acc, m)
+// stored as a structure of arrays in a block of cs = roundup(cout, 16) EpiParam slots
+// (16 * cs bytes): m[cs] fp64 at byte 0, cc[cs] at byte 8*cs, zw[cs] at byte 12*cs.
+//   cc is cc + 2^31 (mod 2^32); valid when the layer's rt.slow == 0 (|cc| < 2^30, no int32
+//   clip possible).  The bias lets acc + 2^31 feed i2d directly.
 struct alignas(16) EpiParam {
   double m;
-  int cc;              // cc + 2^31 (mod 2^32); valid when the layer's rt.slow == 0 (|cc| < 2^30,
-                       // no int32 clip possible).  The bias lets acc + 2^31 feed i2d directly.
+  int cc;
   int zw;
 };
 
@@ -56,7 +62,7 @@ struct LayerSt {
   const int* wzp8;              // [8][cout] weight zero points (tensor-core layers)
   const int* wsum8;             // [8][cout] sum of weight codes
   int kreal;                    // real K = k*k*Cin
-  EpiParam* ep;                 // [cout] per-config epilogue constants (out), or nullptr
+  EpiParam* ep;                 // [roundup(cout,16)] per-config epilogue constants (SoA, out), or nullptr
   int8_t* addtab;               // fused residual add: [256 skip codes][260: conv code + 128]
                                 // -> add output code (out, per config), or nullptr
   int add_conv_is_a;            // 1 if the conv output is operand 0 of the fused add
@@ -118,13 +124,13 @@ void launch_pool_codes(View in, View out, int k, int stride, int mode, const int
                        int hist, cudaStream_t s);
 void launch_add_codes(View a, View b, View out, const float* act_scale, const int* act_zp,
                       int ha, int hb, int ho, cudaStream_t s);
+// v16: 1 = per-block 256-entry requant table, 16 codes per thread; 0 = per-byte fp64 (A/B)
 void launch_concat_codes(View in, View out, int coff, const float* act_scale, const int* act_zp,
-                         int hin, int hout, cudaStream_t s);
+                         int hin, int hout, cudaStream_t s, int v16 = 1);
 void launch_pixsum(View in, int* P, cudaStream_t s);
-void set_dwconv_v4(int v);
-void set_concat_v16(int v);
+// variant: 2 = k x k register-tap kernel, 1 = four channels per thread, 0 = scalar (A/B)
 void launch_dwconv_i8(View in, View out, const int8_t* w, const int* wzp, int k, int stride,
-                      int pad, LayerSt L, cudaStream_t s, int* acc_out = nullptr);
+                      int pad, LayerSt L, cudaStream_t s, int* acc_out = nullptr, int variant = 2);
 void launch_argmax_codes(View in, const long long* labels, unsigned long long* correct,
                          cudaStream_t s);
 void launch_argmax_f32(const float* x, int64_t rows, int C, const long long* labels,
@@ -190,6 +196,7 @@ struct ConvTcArgs {
   int a_iters;            // A pipeline stages per tile (n_kiter, or 3 kh slabs with kwr)
   int flat;               // set by the launcher: GEMM row m is flat pixel m of the output (and of
                           // the add operand) -- halo-free TMA-mode layers skip the row geometry
+  int kwr_mode;           // runtime option: -1 disables the kw-reuse slabs and the stem slab
   int* acc_out;           // parity probe (ptq_probe_acc): when set, the epilogue stores the exact
                           // int32-clipped accumulator acc + bias (intexec.py:177-190) of every real
                           // output as [pixel][cout] int32 instead of requantized codes
@@ -199,7 +206,6 @@ int conv_tc_max_cout();           // largest Cout the tensor-core conv supports
 void launch_conv_tc(const ConvTcArgs& a, int bn, cudaStream_t s);
 // true when launch_conv_tc will load A with TMA and (with has_wzp) sum the rows itself
 bool conv_tc_tma_rowsum(const ConvTcArgs& a, int bn);
-void conv_tc_set_kwr_mode(int m);   // -1: no kw-reuse slabs (A/B testing)
 // CUDA-core reference of the same contract (tests / cross-checks only)
 void launch_conv_i8_ref(const ConvTcArgs& a, int bn, cudaStream_t s);
 

@@ -182,6 +182,7 @@ struct ptq_ctx {
   std::vector<int> cal_sizes;
   // options
   int conv_ref = 0, fusion = 1, time_conv = 0, ablate = 0, tma = 1, subsample = 1;
+  int dwconv_variant = 2, concat_v16 = 1, kwr = 0;   // A/B switches (per context)
   int64_t opt_chunk = 0;
   // stats
   int64_t launches = 0;
@@ -413,7 +414,7 @@ void import_graph(ptq_ctx* c, const ptq_graph_desc* g) {
     wd.mult = c->dalloc<double>(wd.cout);
     wd.biasq = c->dalloc<int>(wd.cout);
     wd.rt = c->dalloc<LayerRt>(1);
-    wd.ep = c->dalloc<EpiParam>(wd.cout);
+    wd.ep = c->dalloc<EpiParam>(rup(wd.cout, 16));   // SoA block (kernels.h EpiParam)
   }
 }
 
@@ -992,7 +993,8 @@ void eval_one(ptq_ctx* c, const ptq_config& cfg, unsigned long long* d_correct, 
         int* d_acc = acc_probe ? c->dalloc<int>((size_t)B * yo.elems) : nullptr;
         if (n.kind == PTQ_DWCONV) {
           launch_dwconv_i8(V(tin), V(tout), wd.codes + (size_t)wv * wd.bytes_per_variant,
-                           wd.zp + (size_t)wv * wd.cout, n.k, n.stride, n.pad, L, c->st, d_acc);
+                           wd.zp + (size_t)wv * wd.cout, n.k, n.stride, n.pad, L, c->st, d_acc,
+                           c->dwconv_variant);
           check_launch(c);
         } else {
           ConvTcArgs a{};
@@ -1038,6 +1040,7 @@ void eval_one(ptq_ctx* c, const ptq_config& cfg, unsigned long long* d_correct, 
           a.addtab = L.addtab;
           a.ablate = c->ablate;
           a.allow_tma = c->tma;
+          a.kwr_mode = c->kwr;
           if (a.has_wzp && !a.Rpix && (c->conv_ref || !conv_tc_tma_rowsum(a, wd.bn))) {
             launch_pixsum(vin, c->d_P, c->st);       // gather-mode convs sum input pixels first
             check_launch(c);
@@ -1118,7 +1121,7 @@ void eval_one(ptq_ctx* c, const ptq_config& cfg, unsigned long long* d_correct, 
         case PTQ_CONCAT: {
           int coff = 0;
           for (int t : n.in) {
-            launch_concat_codes(V(t), V(tout), coff, as, az, P.psrc[t], P.psrc[tout], c->st);
+            launch_concat_codes(V(t), V(tout), coff, as, az, P.psrc[t], P.psrc[tout], c->st, c->concat_v16);
             check_launch(c);
             coff += c->tens[t].c;
           }
@@ -1691,9 +1694,9 @@ int ptq_set_option(ptq_ctx* c, const char* key, int64_t value) {
     else if (k == "ablate") c->ablate = (int)value;
     else if (k == "tma") c->tma = (int)value;
     else if (k == "subsample") c->subsample = (int)value;
-    else if (k == "dwconv_v4") set_dwconv_v4((int)value);
-    else if (k == "concat_v16") set_concat_v16((int)value);
-    else if (k == "kwr") conv_tc_set_kwr_mode((int)value);
+    else if (k == "dwconv_v4") c->dwconv_variant = (int)value;
+    else if (k == "concat_v16") c->concat_v16 = (int)value;
+    else if (k == "kwr") c->kwr = (int)value;
     else if (k == "time_conv") c->time_conv = (int)value;
     else if (k == "reset_stats") c->launches = 0;
     else if (k == "fusion") {

@@ -7,9 +7,15 @@ statistic is an order-independent reduction, so
   (min, max) are combined with an allreduce MIN/MAX (exact), then every rank
   bins its own images with the global range and the int64 histograms are
   combined with an allreduce SUM (exact) -- bit-identical to one GPU;
-* the KL sweep is replicated (deterministic, milliseconds);
-* grid configurations are dealt round-robin and the int64 correct-counts are
-  all-gathered.
+* the KL sweep is sharded by histogram: each rank sweeps a contiguous share of the
+  3 x T histograms and the chosen (lo, hi) windows are SUM-allreduced (each slot is
+  written by exactly one rank, so the sum is exact);
+* grid configurations are split into contiguous blocks of whole parameter variants
+  (cache, scheme, clipping) in (cache, scheme, clipping, mixed, granularity) order,
+  so every rank holds the same mix of Mixed=Off / FirstLastFp32 and per-tensor /
+  per-channel configs (equal cost) and the variant's quantized graph input and
+  folded prefix codes are reused inside the rank; the int64 correct-counts are
+  reassembled with one SUM allreduce.
 
 The protocol functions take a small "backend" object so the same code runs
 with the CUDA library (GpuEvaluator) on NCCL and with the CPU oracle on gloo
@@ -31,8 +37,44 @@ def world():
 
 
 def shard(seq, rank: int, n: int):
-    """Round-robin shard (rank r takes items r, r+n, ...)."""
+    """Round-robin shard (rank r takes items r, r+n, ...): calibration image ids."""
     return list(seq)[rank::n]
+
+
+def _variant_key(cfg):
+    from .config import config_key
+    c = config_key(cfg)
+    return (c[0], c[1], c[2]), (c[4], c[3])        # (cache, scheme, clipping), (mixed, granularity)
+
+
+def config_cost(cfg) -> float:
+    """Relative evaluation cost used to balance config shards: FirstLastFp32 skips the int8
+    first and last layers; weight zero points (Asymmetric / SymmetricUint8 per-channel) add
+    the row-sum correction."""
+    from .config import config_key
+    cache, scheme, clip, gran, mixed, _ = config_key(cfg)
+    return (0.94 if mixed else 1.0) + (0.03 if scheme in (0, 2) and gran == 1 else 0.0)
+
+
+def shard_plan(cfgs, n: int) -> list[list[int]]:
+    """Config indices of every rank: contiguous blocks of whole (cache, scheme, clipping)
+    variants in variant order, cut where the cumulative cost crosses k / n of the total."""
+    cfgs = list(cfgs)
+    order = sorted(range(len(cfgs)), key=lambda i: _variant_key(cfgs[i]))
+    groups: list[list[int]] = []
+    for i in order:
+        if groups and _variant_key(cfgs[groups[-1][0]])[0] == _variant_key(cfgs[i])[0]:
+            groups[-1].append(i)
+        else:
+            groups.append([i])
+    total = sum(config_cost(cfgs[i]) for i in order) or 1.0
+    plan: list[list[int]] = [[] for _ in range(n)]
+    acc = 0.0
+    for grp in groups:
+        c = sum(config_cost(cfgs[i]) for i in grp)
+        plan[min(n - 1, int((acc + c / 2) * n / total))].extend(grp)   # the rank owning the group's midpoint
+        acc += c
+    return plan
 
 
 def eval_slice(n_eval: int, rank: int, n: int) -> tuple[int, int]:
@@ -84,9 +126,13 @@ def sharded_calibration(backend, n_calib: int, seed: int, T: int):
     return ranges, counts, np.asarray([len(i) for i in ids], dtype=np.int64)
 
 
-def gather_counts(local_counts: np.ndarray, n_total: int) -> np.ndarray:
-    """Reassemble round-robin config shards: rank r's j-th result is config r + j*n."""
-    rank, n = world()
+def gather_counts(local_counts: np.ndarray, idx, n_total: int) -> np.ndarray:
+    """Reassemble config shards: this rank's results belong at positions ``idx``."""
     full = np.zeros(n_total, dtype=np.int64)
-    full[rank::n] = local_counts
+    full[np.asarray(idx, dtype=np.int64)] = local_counts
     return allreduce(full, "sum")
+
+
+def kl_slice(n_hist: int, rank: int, n: int) -> tuple[int, int]:
+    """Contiguous [lo, hi) share of the 3 x T histograms whose KL sweep this rank runs."""
+    return n_hist * rank // n, n_hist * (rank + 1) // n

@@ -138,7 +138,9 @@ def _linspace_edge(lo: float, hi: float, k: int) -> float:
 class Coalescer:
     """Batches concurrent single-item calls: the first caller becomes the leader and runs
     ``batch_fn`` on everything queued (repeating while new requests arrive); the others
-    wait for their slot.  Results and exceptions go back to the caller that asked."""
+    wait for their slot.  Results and exceptions go back to the caller that asked: when a
+    batch raises, its items are re-run one at a time, so only the offending caller sees the
+    error (the reference's _safe_eval fails one trial, not its neighbours, tuner.py:173-177)."""
 
     def __init__(self, batch_fn):
         self._fn = batch_fn
@@ -165,13 +167,20 @@ class Coalescer:
                         self._cv.notify_all()
                         break
                 try:
-                    out = list(self._fn([b[0] for b in batch]))
-                    err = None
-                except Exception as e:  # noqa: BLE001 - handed to every caller of the batch
-                    out, err = [None] * len(batch), e
+                    res = [(r, None) for r in self._fn([b[0] for b in batch])]
+                except Exception as e:  # noqa: BLE001 - isolate the failing item(s)
+                    if len(batch) == 1:
+                        res = [(None, e)]
+                    else:
+                        res = []
+                        for item, _ in batch:
+                            try:
+                                res.append((self._fn([item])[0], None))
+                            except Exception as e1:  # noqa: BLE001 - this caller's error
+                                res.append((None, e1))
                 with self._cv:
                     self.batches.append(len(batch))
-                    for (_, sl), r in zip(batch, out):
+                    for (_, sl), (r, err) in zip(batch, res):
                         sl.update(done=True, value=r, error=err)
                     self._cv.notify_all()
         finally:
@@ -203,7 +212,7 @@ class GpuEvaluator:
         self.n_eval = int(len(d.images) - d.n_calib)
         if self.n_eval <= 0:
             raise ValueError("empty evaluation set")
-        self._lock = threading.Lock()
+        self._lock = threading.RLock()
         self._coalescer = None
         imgs = np.ascontiguousarray(np.asarray(d.images, dtype=np.float32))
         labels = np.ascontiguousarray(np.asarray(d.labels[d.n_calib:], dtype=np.int64))
@@ -275,19 +284,29 @@ class GpuEvaluator:
         self.cache_ranges, self.cache_counts = ranges, counts
         self.cache_nsamp = nsamp
         if kl_ranges is None:
-            kl = np.zeros((3 * T, _lib.PTQ_NWINDOWS), dtype=np.float64)
-            _lib.check(self.lib.ptq_kl_sweep(self._ctx, 3 * T, _lib.ptr(counts), _lib.ptr(ranges),
-                                             _lib.ptr(kl)))
+            # under torch.distributed each rank sweeps a contiguous share of the 3 x T
+            # histograms; every (lo, hi) slot is written by one rank, so a SUM allreduce
+            # assembles the exact table (dist.py)
+            from . import dist
+            rank, world = dist.world()
+            lo, hi = dist.kl_slice(3 * T, rank, world)
+            flat_c = counts.reshape(3 * T, N_BINS)
+            flat_r = ranges.reshape(3 * T, 2)
+            kl = np.full((3 * T, _lib.PTQ_NWINDOWS), np.inf, dtype=np.float64)
+            if hi > lo:
+                part = np.zeros((hi - lo, _lib.PTQ_NWINDOWS), dtype=np.float64)
+                _lib.check(self.lib.ptq_kl_sweep(self._ctx, hi - lo, _lib.ptr(np.ascontiguousarray(flat_c[lo:hi])),
+                                                 _lib.ptr(np.ascontiguousarray(flat_r[lo:hi])), _lib.ptr(part)))
+                kl[lo:hi] = part
             self.kl_values = kl.reshape(3, T, -1)
-            kl_ranges = np.zeros((3, T, 2), dtype=np.float64)
+            chosen = np.zeros((3 * T, 2), dtype=np.float64)
             self.kl_reranked = 0
             with _trace("choose_kl_ranges"):
-                for k in range(3):
-                    for t in range(T):
-                        (lo, hi), nr = choose_kl_range(counts[k, t], ranges[k, t, 0], ranges[k, t, 1],
-                                                       self.kl_values[k, t])
-                        kl_ranges[k, t] = (lo, hi)
-                        self.kl_reranked += nr
+                for h in range(lo, hi):
+                    (a, b), nr = choose_kl_range(flat_c[h], flat_r[h, 0], flat_r[h, 1], kl[h])
+                    chosen[h] = (a, b)
+                    self.kl_reranked += nr
+            kl_ranges = dist.allreduce(chosen, "sum") if world > 1 else chosen
         self.kl_ranges = np.ascontiguousarray(kl_ranges, dtype=np.float64).reshape(3, T, 2)
         for k in range(3):
             mx = np.ascontiguousarray(ranges[k].astype(np.float64))
@@ -313,14 +332,15 @@ class GpuEvaluator:
         import dataclasses
         pr = self.percentile_ranges(pct)
         cfgs = [dataclasses.replace(c, clipping="KL") for c in cfgs]
-        try:
-            for k in range(3):
-                _lib.check(self.lib.ptq_set_clip_ranges(self._ctx, k, 1, _lib.ptr(np.ascontiguousarray(pr[k]))))
-            return self.correct_counts(cfgs)
-        finally:
-            for k in range(3):
-                _lib.check(self.lib.ptq_set_clip_ranges(self._ctx, k, 1,
-                                                        _lib.ptr(np.ascontiguousarray(self.kl_ranges[k]))))
+        with self._lock:          # no other thread may evaluate KL configs while the slot is borrowed
+            try:
+                for k in range(3):
+                    _lib.check(self.lib.ptq_set_clip_ranges(self._ctx, k, 1, _lib.ptr(np.ascontiguousarray(pr[k]))))
+                return self.correct_counts(cfgs)
+            finally:
+                for k in range(3):
+                    _lib.check(self.lib.ptq_set_clip_ranges(self._ctx, k, 1,
+                                                            _lib.ptr(np.ascontiguousarray(self.kl_ranges[k]))))
 
     # ------------------------------------------------------------ evaluation
     def _check_cfg(self, cfg) -> None:
@@ -349,6 +369,13 @@ class GpuEvaluator:
         return [int(c) / float(self.n_eval) for c in counts]
 
     def __call__(self, cfg) -> float:
+        # an invalid config fails its own caller only, before it can join a batch
+        self._check_cfg(cfg)
+        if self.image_sharded:
+            # every rank must all-reduce the same configs in the same order: no coalescing
+            # (batches would form differently on each rank)
+            with self._lock:
+                return self.evaluate_many([cfg])[0]
         # concurrent callers (measure_many's thread pool, tuner.py:192-203) are coalesced
         # into one evaluate_many batch
         if self._coalescer is None:
@@ -462,14 +489,19 @@ class GpuEvaluator:
         return s, z
 
     def evaluate_grid(self, cfgs) -> np.ndarray:
-        """Correct counts of every config, configs dealt round-robin over ranks."""
+        """Correct counts of every config; under torch.distributed each rank evaluates its
+        block of whole parameter variants (dist.shard_plan) and one SUM allreduce
+        reassembles the counts in the caller's order."""
         from . import dist
         cfgs = list(cfgs)
         if self.image_sharded:
             return dist.allreduce(self.correct_counts(cfgs), "sum")
         rank, n = dist.world()
-        mine = self.correct_counts(dist.shard(cfgs, rank, n))
-        return dist.gather_counts(mine, len(cfgs))
+        if n == 1:
+            return self.correct_counts(cfgs)
+        idx = dist.shard_plan(cfgs, n)[rank]
+        mine = self.correct_counts([cfgs[i] for i in idx]) if idx else np.zeros(0, np.int64)
+        return dist.gather_counts(mine, idx, len(cfgs))
 
     def histogram_array(self, x: np.ndarray, lo: float, hi: float) -> np.ndarray:
         x = np.ascontiguousarray(np.asarray(x, dtype=np.float32).ravel())

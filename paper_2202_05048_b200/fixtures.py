@@ -296,6 +296,26 @@ def macs_per_image(g) -> int:
     return total
 
 
+def int8_traffic_per_image(g) -> int:
+    """Minimal HBM bytes of one image's int8 forward (SURVEY.md 8(d) whole-path roofline): every
+    weighted layer reads its int8 input and writes its int8 output once, a residual add's second
+    operand is read once (in the producing conv's epilogue), pools / concats read their inputs
+    and write their output once, and the fp32 image is read once (4 bytes per value)."""
+    shapes = tensor_shapes(g)
+
+    def el(t):
+        return int(np.prod(shapes[t]))
+    b = 0
+    for n in g.nodes:
+        if n.kind in ("conv2d", "pointwise_conv2d", "depthwise_conv2d", "fully_connected"):
+            b += el(n.inputs[0]) + el(n.output)
+        elif n.kind == "add":
+            b += el(n.inputs[1])
+        elif n.kind in ("maxpool", "avgpool", "concat"):
+            b += sum(el(t) for t in n.inputs) + el(n.output)
+    return b + 3 * int(np.prod(g.input_shape))          # fp32 image: 4 bytes, 1 already counted
+
+
 # --------------------------------------------------------------------------
 # planted head: host fp32 forward of the class templates (model construction
 # only; the evaluator's own fp32 forward runs on the GPU)

@@ -1,6 +1,7 @@
 """Call coalescing for the reference's threaded measure_many (tuner.py:192-203; SURVEY
 8(f) item 1): concurrent evaluate(cfg) calls are served by fewer, larger batches and every
-caller gets its own result (or its batch's exception)."""
+caller gets its own result or its own exception -- a failing item never fails the callers
+that happened to share its batch (the reference's _safe_eval fails one trial, tuner.py:173-177)."""
 import threading
 import time
 
@@ -54,6 +55,31 @@ def test_errors_reach_every_caller_of_the_batch():
     for t in ts:
         t.join()
     assert errs == ["bad config"] * 8
+
+
+def test_one_bad_item_fails_only_its_caller():
+    def batch(items):
+        time.sleep(0.01)
+        if any(x < 0 for x in items):
+            raise ValueError("bad config")
+        return [x * 2 for x in items]
+
+    co = Coalescer(batch)
+    out, errs = {}, {}
+
+    def worker(i):
+        try:
+            out[i] = co(i)
+        except ValueError as e:
+            errs[i] = str(e)
+
+    ts = [threading.Thread(target=worker, args=(i,)) for i in range(-2, 14)]
+    for t in ts:
+        t.start()
+    for t in ts:
+        t.join()
+    assert errs == {-2: "bad config", -1: "bad config"}
+    assert out == {i: 2 * i for i in range(14)}
 
 
 def test_sequential_calls_still_work():

@@ -2,7 +2,7 @@
 paper_2202_05048_b200/dist.py: calibration images of every cache dealt over
 ranks, MIN/MAX allreduce of the local ranges, local histograms with the global
 range, SUM allreduce -- must equal single-process calibration bit for bit; and
-round-robin config shards must reassemble in order.  The per-rank "device" is
+config shards (dist.shard_plan) must reassemble in order.  The per-rank "device" is
 the numpy oracle here (the GPU path implements the same two calls through
 ptq_calib_forward / ptq_calib_histogram)."""
 import os
@@ -61,7 +61,10 @@ def _worker(rank, world, port, q):
         g = generate_fixture("lenet-ish", 1)
         d = make_dataset(n_calib=40, n_eval=8, seed=0)
         ranges, counts, n_img = D.sharded_calibration(OracleBackend(g, d), d.n_calib, 0, len(g.nodes) + 1)
-        got = D.gather_counts(np.arange(rank, 10, world, dtype=np.int64) * 7, 10)
+        from paper_2202_05048_b200 import GENERIC, enumerate_space
+        space = enumerate_space(GENERIC)
+        idx = D.shard_plan(space, world)[rank]
+        got = D.gather_counts(np.asarray(idx, dtype=np.int64) * 7, idx, len(space))
         if rank == 0:
             q.put((ranges, counts, n_img, got))
     finally:
@@ -86,7 +89,7 @@ def test_sharded_calibration_matches_single_process(monkeypatch):
     for p in procs:
         p.join(timeout=60)
         assert p.exitcode == 0
-    assert got.tolist() == [7 * i for i in range(10)]
+    assert got.tolist() == [7 * i for i in range(96)]
     g = generate_fixture("lenet-ish", 1)
     d = make_dataset(n_calib=40, n_eval=8, seed=0)
     for k, sc in enumerate(("S1", "S2", "S3")):
@@ -96,3 +99,27 @@ def test_sharded_calibration_matches_single_process(monkeypatch):
         for t, h in enumerate(ref.values()):
             assert (ranges[k, t, 0], ranges[k, t, 1]) == (np.float32(h.lo), np.float32(h.hi))
             assert np.array_equal(counts[k, t], h.counts)
+
+
+def test_shard_plan_balanced_contiguous_variants():
+    """dist.shard_plan: every config exactly once; each rank's block is whole (cache, scheme,
+    clipping) variants, contiguous in variant order, with equal counts of Mixed=Off /
+    FirstLastFp32 and per-tensor / per-channel configs at 2, 4 and 8 ranks."""
+    from paper_2202_05048_b200 import GENERIC, enumerate_space
+    from paper_2202_05048_b200 import dist as D
+    from paper_2202_05048_b200.config import config_key
+    space = enumerate_space(GENERIC)
+    for n in (1, 2, 3, 4, 8):
+        plan = D.shard_plan(space, n)
+        assert sorted(i for p in plan for i in p) == list(range(len(space)))
+        seen = {}
+        for r, p in enumerate(plan):
+            for i in p:
+                v = config_key(space[i])[:3]
+                assert seen.setdefault(v, r) == r          # a variant never straddles ranks
+        if n in (2, 4, 8):
+            assert len({len(p) for p in plan}) == 1
+            for p in plan:
+                keys = [config_key(space[i]) for i in p]
+                assert sum(k[4] for k in keys) * 2 == len(p)     # half FirstLastFp32
+                assert sum(k[3] for k in keys) * 2 == len(p)     # half per-channel

@@ -1,5 +1,6 @@
 """Per-layer timing of the tcgen05 conv kernel on one config (CUDA events around each
-launch).  Usage: python tools/conv_layers.py [model] [config_index] [n_eval]"""
+launch).  Usage: python tools/conv_layers.py [model] [config_index] [n_eval] [ablate]
+[key=value runtime options ...]"""
 import sys
 import time
 
@@ -20,6 +21,9 @@ cfg = enumerate_space(GENERIC)[ci]
 ev.set_option("time_conv", 1)
 ablate = int(sys.argv[4]) if len(sys.argv) > 4 else 0
 ev.set_option("ablate", ablate)
+for kv in sys.argv[5:]:
+    k, v = kv.split("=")
+    ev.set_option(k, int(v))
 for _ in range(3):
     ev.correct_counts([cfg])
 t0 = time.perf_counter()
