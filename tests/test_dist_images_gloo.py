@@ -92,18 +92,21 @@ def test_gpu_image_sharded_slices_sum_to_full(monkeypatch, golden, ds, toys):
     cfgs = enumerate_space(GENERIC)[:96:7]
     _, ranges, counts, nsamp, _ = golden_caches(golden, "resnet-toy")
 
-    def make(**kw):
+    def make(kl=None, **kw):
         ev = GpuEvaluator(toys["resnet-toy"], ds, 0, GENERIC, calibrate=False, **kw)
-        ev.install_caches(ranges, counts, nsamp)
+        ev.install_caches(ranges, counts, nsamp, kl_ranges=kl)
         return ev
 
     full = make()
     want = full.correct_counts(cfgs)
+    # the patched world would also shard the KL sweep by histogram (reassembled by a SUM
+    # allreduce that needs a process group): hand the "ranks" the full KL table instead
+    kl = full.kl_ranges.copy()
     full.close()
     got = np.zeros_like(want)
     for r in range(2):
         monkeypatch.setattr(D, "world", lambda r=r: (r, 2))
-        ev = make(image_sharded=True)
+        ev = make(kl, image_sharded=True)
         assert ev.image_sharded and ev.n_eval_local == D.eval_slice(ev.n_eval, r, 2)[1] - D.eval_slice(ev.n_eval, r, 2)[0]
         got += ev.correct_counts(cfgs)
         ev.close()
