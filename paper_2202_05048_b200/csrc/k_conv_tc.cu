@@ -93,6 +93,62 @@ __device__ __forceinline__ void mma_i8(uint32_t tmem_d, uint64_t adesc, uint64_t
       "tcgen05.mma.cta_group::1.kind::i8 [%0], %1, %2, %3, p;\n\t}" ::"r"(tmem_d),
       "l"(adesc), "l"(bdesc), "r"(idesc), "r"(accumulate));
 }
+// One 128-byte K stage in one asm block, executed by the whole (convergent) MMA warp: an
+// elected lane issues the stage's K=32 MMAs and commits the stage's smem barrier.  The k-step
+// offsets (descriptor units = 16 bytes) are added to the start-address field (smem addresses
+// are < 256 KB, so the 14-bit field never carries).  One uniform-issue region per stage instead
+// of one per MMA: the single issuing warp was the pacing resource of every narrow (BN <= 128)
+// layer -- ~34-46 issued instructions per MMA before, the MMA itself takes 32 cycles at N=64.
+// MMAs 2 and 3 are skipped when `full` is 0 (a half stage of the s2d slab with odd k).
+__device__ __forceinline__ void mma4_commit(uint32_t d, uint64_t ad, uint64_t bd, uint64_t a1, uint64_t a2,
+                                            uint64_t a3, uint64_t b1, uint32_t idesc, uint32_t acc,
+                                            uint32_t full, uint32_t bar) {
+  asm volatile(
+      "{\n\t.reg .pred e, q, t, f;\n\t.reg .b64 xa, xb;\n\t"
+      "elect.sync _|e, 0xffffffff;\n\t"
+      "setp.ne.b32 q, %8, 0;\n\t"
+      "setp.eq.b32 t, %8, %8;\n\t"
+      "setp.ne.and.b32 f, %9, 0, e;\n\t"
+      "@e tcgen05.mma.cta_group::1.kind::i8 [%0], %1, %2, %7, q;\n\t"
+      "add.s64 xa, %1, %3;\n\tadd.s64 xb, %2, %6;\n\t"
+      "@e tcgen05.mma.cta_group::1.kind::i8 [%0], xa, xb, %7, t;\n\t"
+      "add.s64 xa, %1, %4;\n\tadd.s64 xb, xb, %6;\n\t"
+      "@f tcgen05.mma.cta_group::1.kind::i8 [%0], xa, xb, %7, t;\n\t"
+      "add.s64 xa, %1, %5;\n\tadd.s64 xb, xb, %6;\n\t"
+      "@f tcgen05.mma.cta_group::1.kind::i8 [%0], xa, xb, %7, t;\n\t"
+      "@e tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%10];\n\t}" ::"r"(d),
+      "l"(ad), "l"(bd), "l"(a1), "l"(a2), "l"(a3), "l"(b1), "r"(idesc), "r"(acc), "r"(full), "r"(bar)
+      : "memory");
+}
+// kw-reuse stage: 6 MMAs (3 kw taps x 2 K=32 halves), A and B both arithmetic sequences
+__device__ __forceinline__ void mma6_commit(uint32_t d, uint64_t ad, uint64_t bd, uint64_t astep, uint64_t bstep,
+                                            uint32_t idesc, uint32_t acc, uint32_t bar) {
+  asm volatile(
+      "{\n\t.reg .pred e, q, t;\n\t.reg .b64 xa, xb;\n\t"
+      "elect.sync _|e, 0xffffffff;\n\t"
+      "setp.ne.b32 q, %6, 0;\n\t"
+      "setp.eq.b32 t, %6, %6;\n\t"
+      "@e tcgen05.mma.cta_group::1.kind::i8 [%0], %1, %2, %5, q;\n\t"
+      "add.s64 xa, %1, %3;\n\tadd.s64 xb, %2, %4;\n\t"
+      "@e tcgen05.mma.cta_group::1.kind::i8 [%0], xa, xb, %5, t;\n\t"
+      "add.s64 xa, xa, %3;\n\tadd.s64 xb, xb, %4;\n\t"
+      "@e tcgen05.mma.cta_group::1.kind::i8 [%0], xa, xb, %5, t;\n\t"
+      "add.s64 xa, xa, %3;\n\tadd.s64 xb, xb, %4;\n\t"
+      "@e tcgen05.mma.cta_group::1.kind::i8 [%0], xa, xb, %5, t;\n\t"
+      "add.s64 xa, xa, %3;\n\tadd.s64 xb, xb, %4;\n\t"
+      "@e tcgen05.mma.cta_group::1.kind::i8 [%0], xa, xb, %5, t;\n\t"
+      "add.s64 xa, xa, %3;\n\tadd.s64 xb, xb, %4;\n\t"
+      "@e tcgen05.mma.cta_group::1.kind::i8 [%0], xa, xb, %5, t;\n\t"
+      "@e tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%7];\n\t}" ::"r"(d),
+      "l"(ad), "l"(bd), "l"(astep), "l"(bstep), "r"(idesc), "r"(acc), "r"(bar)
+      : "memory");
+}
+__device__ __forceinline__ void commit_elect(uint64_t* bar) {
+  asm volatile(
+      "{\n\t.reg .pred e;\n\telect.sync _|e, 0xffffffff;\n\t"
+      "@e tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];\n\t}" ::"r"(smem_u32(bar))
+      : "memory");
+}
 __device__ __forceinline__ void mma_commit(uint64_t* bar) {
   asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(
                    smem_u32(bar))
@@ -644,8 +700,32 @@ __global__ void __launch_bounds__(TC_THREADS, 1) k_conv_tc(const __grid_constant
     }
   } else if (warp == 3) {
     // ------------------------------------------------ MMA issuer
-    if (lane == 0) {
+    // The whole warp walks the pipeline (uniform control flow: descriptors and stage indices
+    // stay in uniform registers); one elected lane issues each stage (mma4/6_commit).
+    // Descriptors are a per-mode template plus the stage's smem address; k-steps within a
+    // stage are constant offsets (16-byte units):
+    //   gather / s2d 3-D TMA (no swizzle, LBO = one 16-byte K plane of 128 rows): 256
+    //   SWIZZLE_128B: 2          SWIZZLE_64B (two taps per stage): 0, 2, 512, 514
+    //   s2d slab (no swizzle, LBO 16: the next K chunk is the next pixel): 0, 2, Wp, Wp + 2
+    //   kw-reuse: A slab shifted by kw rows (4 units per kw), B resident chunk-major
+    // B: no swizzle, LBO = one K plane of BN rows; K=32 step = 2 planes = 2*BN units.
+    {
       const uint32_t idesc = idesc_i8<BN>();
+      const int mode = a.tma_a;
+      const uint32_t sa = smem_u32(sA), sb = smem_u32(sB);
+      const bool nosw = mode == 0 || mode == 65;
+      const uint64_t adt = a.kwr ? umma_desc_sw(0, 64)
+                           : nosw ? umma_desc(0, TC_BM * 16, 128)
+                           : mode == 67 ? umma_desc(0, 16, 128)
+                           : mode == 128 ? umma_desc_sw(0, 128) : umma_desc_sw(0, 64);
+      const uint64_t bdt = umma_desc(0, BN * 16, 128);
+      const int Wp = a.in.W + 2 * a.in.halo;
+      uint64_t a1, a2, a3;
+      if (nosw) { a1 = 256; a2 = 512; a3 = 768; }
+      else if (mode == 67) { a1 = 2; a2 = (uint64_t)Wp; a3 = (uint64_t)Wp + 2; }
+      else if (mode == 128) { a1 = 2; a2 = 4; a3 = 6; }
+      else { a1 = 2; a2 = 512; a3 = 514; }
+      const uint64_t bstep = 2 * BN;
       if (a.b_res) mbar_wait(bfull, 0);
       int s = 0;
       uint32_t ph = 0, lt = 0;
@@ -657,55 +737,20 @@ __global__ void __launch_bounds__(TC_THREADS, 1) k_conv_tc(const __grid_constant
         for (int ki = 0; ki < a.a_iters; ++ki) {
           mbar_wait(&full[s], ph);
           tc_fence_after();
-          fence_proxy_async();
-          const uint32_t a0 = smem_u32(sA + s * TC_A_STAGE),
-                         b0 = smem_u32(sB + (a.b_res ? ki : s) * BN * 128);
+          if (mode == 0) fence_proxy_async();          // cp.async-written A -> async proxy
+          const uint64_t ad = adt + ((sa + (uint32_t)s * TC_A_STAGE) >> 4);
+          const uint32_t bar = smem_u32(&empty[s]);    // freed when the stage's MMAs land
           if (a.kwr) {
             // slab = input rows p0 + ki*Wp + [0, 136); tap (ki, kw) = the slab shifted by kw
-            // rows; B (resident, chunk-major) chunk index = ki*12 + kw*4 + 2*ks2
-            const uint32_t bb = smem_u32(sB);
-#pragma unroll
-            for (int kw = 0; kw < 3; ++kw)
-#pragma unroll
-              for (int ks2 = 0; ks2 < 2; ++ks2) {
-                const uint32_t st = a0 + kw * 64 + ks2 * 32;
-                const uint64_t ad = umma_desc_sw(st, 64);   // swizzle on absolute address bits
-                const uint64_t bd = umma_desc(bb + (uint32_t)((ki * 12 + kw * 4 + ks2 * 2) * BN * 16), BN * 16, 128);
-                mma_i8(d, ad, bd, idesc, (ki | kw | ks2) != 0);
-              }
-            mma_commit(&empty[s]);
-            if (++s == NS) { s = 0; ph ^= 1u; }
-            continue;
+            // rows (A: +4 units per kw, +2 per K half); B chunk ki*12 + kw*4 + 2*ks2
+            mma6_commit(d, ad, bdt + (sb >> 4) + (uint64_t)(ki * 12 * BN), 2, bstep, idesc, ki != 0, bar);
+          } else {
+            const uint64_t bd = bdt + ((sb + (uint32_t)((a.b_res ? ki : s) * BN * 128)) >> 4);
+            mma4_commit(d, ad, bd, a1, a2, a3, bstep, idesc, ki != 0, mode != 67 || 2 * ki + 1 < a.k, bar);
           }
-          if (a.tma_a == 67) {
-            // no-swizzle K-major views of the slab: row r of tap (kh, kw) is slab pixel
-            // kh*Wp + kw + r, so rows are 16 bytes apart (SBO 128 per 8 rows) and the second
-            // 16-byte K chunk of an MMA (tap kw + 1) is the next pixel (LBO 16)
-            const int Wp = a.in.W + 2 * a.in.halo;
-#pragma unroll
-            for (int ks = 0; ks < 4; ++ks) {
-              if ((ks >> 1) + 2 * ki >= a.k) break;
-              const uint64_t ad = umma_desc(a0 + (uint32_t)(((ks >> 1) * Wp + (ks & 1) * 2) * 16), 16, 128);
-              const uint64_t bd = umma_desc(b0 + ks * 2 * (BN * 16), BN * 16, 128);
-              mma_i8(d, ad, bd, idesc, (ki | ks) != 0);
-            }
-            mma_commit(&empty[s]);
-            if (++s == NS) { s = 0; ph ^= 1u; }
-            continue;
-          }
-#pragma unroll
-          for (int ks = 0; ks < 4; ++ks) {
-            const uint64_t ad =
-                (a.tma_a == 0 || a.tma_a == 65) ? umma_desc(a0 + ks * 2 * (TC_BM * 16), TC_BM * 16, 128)
-                : a.tma_a == 128 ? umma_desc_sw(a0 + ks * 32, 128)
-                                 : umma_desc_sw(a0 + (ks >> 1) * (TC_A_STAGE / 2) + (ks & 1) * 32, 64);
-            const uint64_t bd = umma_desc(b0 + ks * 2 * (BN * 16), BN * 16, 128);
-            mma_i8(d, ad, bd, idesc, (ki | ks) != 0);
-          }
-          mma_commit(&empty[s]);                     // frees the smem stage when the MMAs land
           if (++s == NS) { s = 0; ph ^= 1u; }
         }
-        mma_commit(&tfull[buf]);                     // accumulator ready for the epilogue
+        commit_elect(&tfull[buf]);                   // accumulator ready for the epilogue
       }
     }
     __syncwarp();
