@@ -205,6 +205,7 @@ struct EpiK {
   // are the same for every channel and live in registers; only cc is loaded per channel
   double m0;
   int zw0;
+  int fxm0, fxs;       // FX: per-tensor M and the shift S - 32
 };
 // 4-channel groups of a 16-channel chunk whose fused add runs on the fp64 pipe instead of
 // the shared-memory table: one group of four balances the L1 (table) and fp64 pipes (A/B
@@ -277,6 +278,60 @@ __device__ __forceinline__ int4 epi_chunk16(const uint32_t (&v)[16], const uint8
         if ((PTQ_ADD_ALU_MASK >> g) & 1) {
           // the table entry computed in place: fl(fl((xc - zc) rc) + fl((xs - zs) rs)) (the sum
           // is commutative, so the operand order needs no branch), RHU + zo, clip, relu floor
+          const int skc = (int)(int8_t)(skw[g] >> (8 * j));
+          const double t2 = __dadd_rn(__dmul_rn(b2d((uint32_t)imin(q[j], PTQ_QMAX) + k.zc_bias), k.rc),
+                                      __dmul_rn(b2d((uint32_t)skc + k.zs_bias), k.rs));
+          q[j] = imin(imax(__double2loint(__dadd_rd(__dadd_rn(t2, 0.5), rt.mg_zo)), k.lo_add), PTQ_QMAX);
+        } else {
+          q[j] = stab[(int)__byte_perm(skw[g], 0u, 0x4440u + j) * PTQ_ADDTAB_ROW + imin(q[j], PTQ_QMAX)];
+        }
+      }
+    }
+    packed[g] = SKIP ? __byte_perm(__byte_perm((uint32_t)q[0], (uint32_t)q[1], 0x0040),
+                                   __byte_perm((uint32_t)q[2], (uint32_t)q[3], 0x0040), 0x5410)
+                     : pack4_sat(q[0], q[1], q[2], q[3]);
+  }
+  return make_int4((int)packed[0], (int)packed[1], (int)packed[2], (int)packed[3]);
+}
+
+// 16 output channels of one row, exact fixed-point requant (rt.fx, k_layer_params): code =
+// hi32(v'*M_c + B'_c) >> (S - 32) with v' = dot - zw*rowsum -- one IMAD.WIDE and one shift per
+// output, no fp64 and no clamp (|v'| < 2^28.5, |B'| < 2^62: the 64-bit sum cannot wrap).  The
+// per-channel constants (SoA: B'[cs] int64, M[cs], zw[cs]) come from shared memory, or from
+// __constant__ c_ep on the fused-add layers; per-tensor layers (PT) hold M in a register and
+// fold zw*rowsum into the per-row zr.
+template <bool WZP, bool SKIP, bool RELU, bool PT>
+__device__ __forceinline__ int4 epi_chunk16_fx(const uint32_t (&v)[16], const uint8_t* __restrict__ sp, int cs,
+                                               int cb, int rowsum, int zr, const LayerRt& rt, const EpiK& k,
+                                               const int8_t* __restrict__ stab, const int4 skv) {
+  const uint8_t* base = SKIP ? reinterpret_cast<const uint8_t*>(c_ep) : sp;
+  uint32_t packed[4];
+  const uint32_t skw[4] = {(uint32_t)skv.x, (uint32_t)skv.y, (uint32_t)skv.z, (uint32_t)skv.w};
+#pragma unroll
+  for (int g = 0; g < 4; ++g) {
+    const longlong2 b01 = reinterpret_cast<const longlong2*>(base)[(cb >> 1) + 2 * g];
+    const longlong2 b23 = reinterpret_cast<const longlong2*>(base)[(cb >> 1) + 2 * g + 1];
+    const long long bv[4] = {b01.x, b01.y, b23.x, b23.y};
+    int mv[4] = {k.fxm0, k.fxm0, k.fxm0, k.fxm0};
+    int zwv[4] = {0, 0, 0, 0};
+    if (!PT) {
+      const int4 m4 = reinterpret_cast<const int4*>(base + 8 * cs)[(cb >> 2) + g];
+      mv[0] = m4.x; mv[1] = m4.y; mv[2] = m4.z; mv[3] = m4.w;
+      if (WZP) {
+        const int4 z4 = reinterpret_cast<const int4*>(base + 12 * cs)[(cb >> 2) + g];
+        zwv[0] = z4.x; zwv[1] = z4.y; zwv[2] = z4.z; zwv[3] = z4.w;
+      }
+    }
+    int q[4];
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      int a = (int)v[g * 4 + j];
+      if (WZP) a = PT ? a - zr : a - zwv[j] * rowsum;
+      const long long X = (long long)a * (long long)mv[j] + bv[j];
+      q[j] = (int)(X >> 32) >> k.fxs;
+      if (RELU || SKIP) q[j] = imax(q[j], k.lo_conv);
+      if (SKIP) {
+        if ((PTQ_ADD_ALU_MASK >> g) & 1) {
           const int skc = (int)(int8_t)(skw[g] >> (8 * j));
           const double t2 = __dadd_rn(__dmul_rn(b2d((uint32_t)imin(q[j], PTQ_QMAX) + k.zc_bias), k.rc),
                                       __dmul_rn(b2d((uint32_t)skc + k.zs_bias), k.rs));
@@ -405,7 +460,8 @@ struct EpiEnv {
 // loaded into uniform registers through the constant cache (LDCU) and used as operands
 // directly -- no shared-memory loads (each broadcast LDS.128 costs 4 L1 wavefronts per warp,
 // which saturated the L1 data pipe) and no vector registers.
-template <int BN, bool WZP, bool SKIP, bool CLAMP, bool RELU, bool GENERIC, bool ACC = false, bool PT = false>
+template <int BN, bool WZP, bool SKIP, bool CLAMP, bool RELU, bool GENERIC, bool ACC = false, bool PT = false,
+          bool FX = false>
 __device__ __forceinline__ void epi_tiles(const ConvTcArgs& a, const LayerRt& rt, const EpiK& k, const EpiEnv& e) {
   constexpr int NCH = BN / 16;                       // 16-column chunks per tile
   const int Cout = a.L.cout;
@@ -442,6 +498,7 @@ __device__ __forceinline__ void epi_tiles(const ConvTcArgs& a, const LayerRt& rt
       rowsum = a.Rpix ? (long long)a.Rpix[((int64_t)g.n * a.OHr + g.oh) * a.OWr + g.ow]
                       : pixel_rowsum(a, g.n, g.ih0, g.iw0);
     }
+    const int zr = (FX && PT && WZP) ? k.zw0 * (int)rowsum : 0;   // per-tensor zw * rowsum
     // the residual operand does not depend on the accumulator: fetch it before the wait
     // and one chunk ahead inside the loop
     const int cb0 = nt * BN + first * 16;
@@ -471,7 +528,9 @@ __device__ __forceinline__ void epi_tiles(const ConvTcArgs& a, const LayerRt& rt
       int4 res;
       if (GENERIC && a.ablate == 1) {
         res = make_int4((int)v[0], (int)v[1], (int)v[2], (int)v[3]);
-      } else if (!GENERIC && cb + 16 <= Cout) {
+      } else if (FX && cb + 16 <= Cout) {
+        res = epi_chunk16_fx<WZP, SKIP, RELU, PT>(v, e.sp, e.cs, cb, (int)rowsum, zr, rt, k, e.stab_c, skv);
+      } else if (!GENERIC && !FX && cb + 16 <= Cout) {
         res = epi_chunk16<WZP, SKIP, CLAMP, RELU, PT>(v, e.sp, e.cs, cb, (int)rowsum, rt, k, e.stab_c, skv);
       } else {
         res = epi_slow_chunk(tbase + (uint32_t)(c * 16), cb, rowsum, a, rt, k.lo_conv, k.lo_add, skv);
@@ -489,6 +548,11 @@ template <int BN, bool WZP, bool SKIP, bool CLAMP, bool RELU>
 __device__ __forceinline__ void epi_pt(const ConvTcArgs& a, const LayerRt& rt, const EpiK& k, const EpiEnv& e) {
   if (rt.uni) epi_tiles<BN, WZP, SKIP, CLAMP, RELU, false, false, true>(a, rt, k, e);
   else epi_tiles<BN, WZP, SKIP, CLAMP, RELU, false, false, false>(a, rt, k, e);
+}
+template <int BN, bool WZP, bool SKIP, bool RELU>
+__device__ __forceinline__ void epi_fx(const ConvTcArgs& a, const LayerRt& rt, const EpiK& k, const EpiEnv& e) {
+  if (rt.uni) epi_tiles<BN, WZP, SKIP, false, RELU, false, false, true, true>(a, rt, k, e);
+  else epi_tiles<BN, WZP, SKIP, false, RELU, false, false, false, true>(a, rt, k, e);
 }
 
 template <int BN>
@@ -785,6 +849,8 @@ __global__ void __launch_bounds__(TC_THREADS, 1) k_conv_tc(const __grid_constant
     const int8_t* stab_c = stab + 128;                // column of conv code 0
     k.m0 = rt.m0;
     k.zw0 = rt.zw0;
+    k.fxm0 = rt.fx_m0;
+    k.fxs = rt.fx_s;
     const EpiEnv e{tmem, tfull, tempty, rsfull, rsum, reinterpret_cast<const uint8_t*>(sparam), cs, stab_c,
                    q, grp, row, M, n_tiles, n_nt};
     // one persistent tile loop per epilogue variant: the per-chunk code carries no
@@ -792,6 +858,14 @@ __global__ void __launch_bounds__(TC_THREADS, 1) k_conv_tc(const __grid_constant
     const bool skip = a.skip.p != nullptr, wzp = a.has_wzp != 0, clamp = !rt.noclamp,
                relu = k.lo_conv > PTQ_QMIN;
     if (a.acc_out) epi_tiles<BN, false, false, false, false, true, true>(a, rt, k, e);
+    else if (rt.fx && a.ablate != 1) {
+      if (skip) { if (wzp) epi_fx<BN, true, true, false>(a, rt, k, e);
+                  else epi_fx<BN, false, true, false>(a, rt, k, e); }
+      else if (wzp) { if (relu) epi_fx<BN, true, false, true>(a, rt, k, e);
+                      else epi_fx<BN, true, false, false>(a, rt, k, e); }
+      else { if (relu) epi_fx<BN, false, false, true>(a, rt, k, e);
+             else epi_fx<BN, false, false, false>(a, rt, k, e); }
+    }
     else if (rt.slow || a.ablate == 1) epi_tiles<BN, false, false, false, false, true>(a, rt, k, e);
     else if (skip) {
       if (wzp) { if (clamp) epi_pt<BN, true, true, true, false>(a, rt, k, e);

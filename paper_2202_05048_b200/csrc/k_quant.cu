@@ -205,13 +205,64 @@ void launch_weight_prepare8(const float* w, int cout, int64_t per_ch, bool depth
 }
 
 // ---------------------------------------------------------------- per-config layer params
-__global__ void k_layer_params(const LayerSt* __restrict__ layers, const float* __restrict__ as,
-                               const int* __restrict__ az, int wvar) {
+// Exact fixed-point requantization ("FX").  For one channel with multiplier m > 0 and output
+// zero point zy, the reference's code is clip(h(acc) + zy) with h(acc) = floor(fl(fl(acc*m) +
+// 0.5)) (intexec.py:72-85), a monotone step function of the int32 accumulator.  With a layer-wide
+// S >= 32 and per-channel integers (M < 2^31, B), g(acc) = floor((acc*M + B) / 2^S) is monotone too, so
+// clip(g) == clip(h + zy) for EVERY acc iff the two agree on each level's threshold:
+//   t_k = min{acc : h(acc) + zy >= k},  k = lo+1 .. 127  (lo = the relu / int8 floor)
+//   g(t_k) >= k  and  g(t_k - 1) < k   <=>   L_k <= B < L_k + M,   L_k = k*2^S - t_k*M.
+// The thresholds are found with the reference's own fp64 arithmetic (estimate, then step until
+// the exact predicate flips), so the integer map reproduces its rounding bit for bit, including
+// fp64 ties.  M starts at round(m*2^S) and may move by +-2; B = max_k L_k when max - min < M.
+// One warp per channel, lanes over levels.  Returns false when no (M, B) fits.
+__device__ bool fx_channel(double m, int zy, int lo, int S, long long& Mo, long long& Bo) {
+  const int lane = threadIdx.x & 31;
+  long long t[8];
+  int nk = 0;
+  bool ok = true;
+  for (int k = lo + 1 + lane; k <= PTQ_QMAX; k += 32) {
+    const double j = (double)(k - zy);                    // h(acc) >= j
+    const double x0 = __ddiv_rn(__dsub_rn(j, 0.5), m);
+    if (!(fabs(x0) < 1073741824.0)) { ok = false; break; }
+    long long a = (long long)ceil(x0);
+    auto pred = [&](long long v) { return __dadd_rn(__dmul_rn((double)v, m), 0.5) >= j; };
+    int guard = 0;
+    while (pred(a - 1) && ++guard < 64) --a;
+    while (!pred(a) && ++guard < 64) ++a;
+    if (guard >= 64) ok = false;
+    t[nk++] = a;
+  }
+  if (!__all_sync(0xffffffffu, ok)) return false;
+  const long long M0 = __double2ll_rn(ldexp(m, S));
+  for (int d = 0; d < 5; ++d) {
+    const long long M = M0 + ((d & 1) ? (d + 1) / 2 : -(d / 2));
+    if (M <= 0 || M >= (1LL << 31)) continue;
+    long long lmax = LLONG_MIN, lmin = LLONG_MAX;
+    for (int i = 0; i < nk; ++i) {
+      const int k = lo + 1 + lane + 32 * i;
+      const long long L = (long long)k * (1LL << S) - t[i] * M;
+      lmax = L > lmax ? L : lmax;
+      lmin = L < lmin ? L : lmin;
+    }
+    for (int o = 16; o; o >>= 1) {
+      const long long a = __shfl_xor_sync(0xffffffffu, lmax, o), b = __shfl_xor_sync(0xffffffffu, lmin, o);
+      lmax = a > lmax ? a : lmax;
+      lmin = b < lmin ? b : lmin;
+    }
+    if (lmax == LLONG_MIN) { Mo = M; Bo = 0; return true; }   // no level to match (lo >= 127)
+    if (lmax - lmin < M) { Mo = M; Bo = lmax; return true; }
+  }
+  return false;
+}
+
+__global__ void __launch_bounds__(512) k_layer_params(const LayerSt* __restrict__ layers, const float* __restrict__ as,
+                                                      const int* __restrict__ az, int wvar, int fx_enable) {
   const LayerSt L = layers[blockIdx.x];
   const double sx = (double)as[L.in_hist], sy = (double)as[L.out_hist];
   const float* ws = L.wscale + (int64_t)wvar * L.cout;
   const long long zx = az[L.in_hist];
-  __shared__ int slow, zw_min, zw_max;
+  __shared__ int slow, slow_base, zw_min, zw_max, fx_S, fx_ok;
   __shared__ unsigned long long m_max_bits, m_min_bits;   // m > 0: bit order == value order
   __shared__ LayerRt srt;
   if (threadIdx.x == 0) {
@@ -251,6 +302,7 @@ __global__ void k_layer_params(const LayerSt* __restrict__ layers, const float* 
   }
   __syncthreads();
   if (threadIdx.x == 0) {
+    slow_base = slow;                                    // cc beyond 2^30 or a bad multiplier
     LayerRt r;
     // fast-path acc clamp: |A*m| <= 2^30 for every channel, and A*m > 300 for every channel
     // (so clamped accumulators still saturate exactly as the unclamped ones would)
@@ -279,7 +331,7 @@ __global__ void k_layer_params(const LayerSt* __restrict__ layers, const float* 
       r.ra = __ddiv_rn((double)as[L.add_a_hist], so);
       r.rb = __ddiv_rn((double)as[L.add_b_hist], so);
       // the fast add path floors via a 2^52 magic add: needs |xs*ra + ys*rb| < 2^50
-      if (!(r.ra + r.rb < 1e12)) slow = 1;
+      if (!(r.ra + r.rb < 1e12)) { slow = 1; slow_base = 1; }
     } else {
       r.za = r.zb = r.zo = 0;
       r.ra = r.rb = 0.0;
@@ -288,9 +340,62 @@ __global__ void k_layer_params(const LayerSt* __restrict__ layers, const float* 
     r.slow = slow;
     r.mg_zy = 6755399441055744.0 + (double)r.zy;
     r.mg_zo = 6755399441055744.0 + (double)r.zo;
-    *L.rt = r;
+    // FX: S from the largest multiplier (M_max in [2^30, 2^31)); needs S in [32, 52] so that
+    // code = hi32(v*M + B') >> (S - 32) and |v'*M + B'| < 2^62.5 (|t|, |cc| < 2^30, |v'| < 2^28.5)
+    r.fx = 0;
+    r.fx_s = 0;
+    r.fx_m0 = 0;
+    fx_S = 0;
+    if (fx_enable && L.ep && !slow_base) {
+      int e = 0;
+      frexp(__longlong_as_double((long long)m_max_bits), &e);
+      const int S = 31 - e;
+      if (S >= 32 && S <= 52) fx_S = S;
+    }
+    fx_ok = fx_S != 0;
     srt = r;
   }
+  __syncthreads();
+  if (fx_S) {
+    // per-channel (M, B') into the second half of the ep block (scratch), committed below
+    const int S = fx_S;
+    const int lo = srt.relu_zp > PTQ_QMIN ? srt.relu_zp : PTQ_QMIN;
+    long long* fx_b = reinterpret_cast<long long*>(L.ep + cs);
+    int* fx_m = reinterpret_cast<int*>(fx_b + cs);
+    for (int o = threadIdx.x >> 5; o < L.cout; o += blockDim.x >> 5) {
+      long long M = 0, B = 0;
+      const bool ok = fx_channel(L.mult[o], srt.zy, lo, S, M, B);
+      if ((threadIdx.x & 31) == 0) {
+        if (!ok) {
+          fx_ok = 0;
+        } else {
+          const long long cc = (long long)(int)((uint32_t)ep_cc[o] ^ 0x80000000u);
+          fx_b[o] = B + cc * M;                           // acc = v' + cc folded into the addend
+          fx_m[o] = (int)M;
+        }
+      }
+    }
+    __syncthreads();
+    if (fx_ok) {
+      // commit: the active SoA block now holds (B', M, zw) instead of (m, cc, zw)
+      long long* dst_b = reinterpret_cast<long long*>(L.ep);
+      int* dst_m = reinterpret_cast<int*>(dst_b + cs);
+      for (int o = threadIdx.x; o < cs; o += blockDim.x) {
+        dst_b[o] = o < L.cout ? fx_b[o] : 0;
+        dst_m[o] = o < L.cout ? fx_m[o] : 0;
+      }
+      if (threadIdx.x == 0) {
+        LayerRt r = srt;
+        r.fx = 1;
+        r.fx_s = S - 32;
+        r.fx_m0 = fx_m[0];
+        r.slow = 0;
+        srt = r;
+      }
+    }
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) *L.rt = srt;
   if (!L.addtab) return;
   __syncthreads();
   // fused residual add as a lookup table: row s (skip code as unsigned byte), column q + 128
@@ -311,8 +416,8 @@ __global__ void k_layer_params(const LayerSt* __restrict__ layers, const float* 
   }
 }
 void launch_layer_params(const LayerSt* d_layers, int n_layers, const float* act_scale,
-                         const int* act_zp, int wvar, cudaStream_t s) {
-  if (n_layers > 0) k_layer_params<<<n_layers, 256, 0, s>>>(d_layers, act_scale, act_zp, wvar);
+                         const int* act_zp, int wvar, int fx, cudaStream_t s) {
+  if (n_layers > 0) k_layer_params<<<n_layers, 512, 0, s>>>(d_layers, act_scale, act_zp, wvar, fx);
 }
 
 // ---------------------------------------------------------------- quantize / dequantize

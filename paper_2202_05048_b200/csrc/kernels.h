@@ -33,6 +33,13 @@ struct LayerRt {
   int uni;             // every channel has the same m and zw (per-tensor weights): m0 / zw0
   double m0;
   int zw0;
+  // exact fixed-point requant (k_layer_params, "FX"): code = (v'*M_c + B'_c) >> (32 + fx_s)
+  // reproduces clip(floor(fl(fl(acc*m_c) + 0.5)) + zy) for every int32 accumulator, with
+  // v' = dot - zw*rowsum (acc = v' + cc).  fx = 1 when every channel's (M_c, B'_c) was found;
+  // the EpiParam SoA then holds B'_c (int64) in the m slot and M_c in the cc slot.
+  int fx;
+  int fx_s;            // S - 32 (per layer)
+  int fx_m0;           // M of per-tensor layers (uni)
 };
 
 // per-config, per-output-channel epilogue constants of the tensor-core conv:
@@ -41,6 +48,8 @@ struct LayerRt {
 // (16 * cs bytes): m[cs] fp64 at byte 0, cc[cs] at byte 8*cs, zw[cs] at byte 12*cs.
 //   cc is cc + 2^31 (mod 2^32); valid when the layer's rt.slow == 0 (|cc| < 2^30, no int32
 //   clip possible).  The bias lets acc + 2^31 feed i2d directly.
+//   With rt.fx = 1 the same block holds the fixed-point constants instead: B'_c (int64) at
+//   byte 0, M_c (int32) at byte 8*cs, zw at 12*cs.
 struct alignas(16) EpiParam {
   double m;
   int cc;
@@ -107,8 +116,9 @@ void launch_weight_prepare8(const float* w, int cout, int64_t per_ch, bool depth
                             int fc_hw, int cin_p, int bn, int n_kiter, int64_t bytes_per_variant,
                             unsigned int* mnmx, float* scale, int* zp, int8_t* codes, int* wsum,
                             cudaStream_t s);
+// fx: 1 = also derive the exact fixed-point epilogue constants (LayerRt::fx), 0 = fp64 only
 void launch_layer_params(const LayerSt* d_layers, int n_layers, const float* act_scale,
-                         const int* act_zp, int wvar, cudaStream_t s);
+                         const int* act_zp, int wvar, int fx, cudaStream_t s);
 void launch_quant_input(const float* imgs_nchw, int64_t img0, View out, const float* act_scale,
                         const int* act_zp, int hist, cudaStream_t s);
 void launch_quant_input_s2d(const float* imgs_nchw, int64_t img0, int C0, View out,

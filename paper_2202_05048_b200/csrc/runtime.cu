@@ -183,6 +183,7 @@ struct ptq_ctx {
   // options
   int conv_ref = 0, fusion = 1, time_conv = 0, ablate = 0, tma = 1, subsample = 1;
   int dwconv_variant = 2, concat_v16 = 1, kwr = 0;   // A/B switches (per context)
+  int fx = 1;                            // exact fixed-point conv epilogue (0: fp64 epilogue)
   int64_t opt_chunk = 0;
   // stats
   int64_t launches = 0;
@@ -414,7 +415,8 @@ void import_graph(ptq_ctx* c, const ptq_graph_desc* g) {
     wd.mult = c->dalloc<double>(wd.cout);
     wd.biasq = c->dalloc<int>(wd.cout);
     wd.rt = c->dalloc<LayerRt>(1);
-    wd.ep = c->dalloc<EpiParam>(rup(wd.cout, 16));   // SoA block (kernels.h EpiParam)
+    // SoA block (kernels.h EpiParam) + the same again as k_layer_params' FX scratch
+    wd.ep = c->dalloc<EpiParam>(2 * rup(wd.cout, 16));
   }
 }
 
@@ -887,7 +889,7 @@ void eval_one(ptq_ctx* c, const ptq_config& cfg, unsigned long long* d_correct, 
   const int wv = cfg.scheme * 2 + cfg.granularity;
   const float* as = c->d_act_scale + (size_t)v * c->T;
   const int* az = c->d_act_zp + (size_t)v * c->T;
-  launch_layer_params(P.d_layers, (int)P.h_layers.size(), as, az, wv, c->st);
+  launch_layer_params(P.d_layers, (int)P.h_layers.size(), as, az, wv, c->fx, c->st);
   check_launch(c);
   const int N = (int)c->nodes.size();
   std::vector<int> alias(c->T);
@@ -1623,7 +1625,7 @@ int ptq_export_layer(ptq_ctx* c, const ptq_config* cfg, int32_t node, int8_t* co
     const int v = (cfg->cache * 4 + cfg->scheme) * 2 + cfg->clipping;
     // per-config layer constants (bias codes) exactly as an evaluation computes them
     launch_layer_params(P.d_layers, (int)P.h_layers.size(), c->d_act_scale + (size_t)v * c->T,
-                        c->d_act_zp + (size_t)v * c->T, wv, c->st);
+                        c->d_act_zp + (size_t)v * c->T, wv, c->fx, c->st);
     check_launch(c);
     CK(cudaMemcpyAsync(wscale, wd.scale + (size_t)wv * wd.cout, wd.cout * sizeof(float), cudaMemcpyDeviceToHost, c->st));
     CK(cudaMemcpyAsync(wzp, wd.zp + (size_t)wv * wd.cout, wd.cout * sizeof(int), cudaMemcpyDeviceToHost, c->st));
@@ -1697,6 +1699,7 @@ int ptq_set_option(ptq_ctx* c, const char* key, int64_t value) {
     else if (k == "dwconv_v4") c->dwconv_variant = (int)value;
     else if (k == "concat_v16") c->concat_v16 = (int)value;
     else if (k == "kwr") c->kwr = (int)value;
+    else if (k == "fx") c->fx = (int)value;
     else if (k == "time_conv") c->time_conv = (int)value;
     else if (k == "reset_stats") c->launches = 0;
     else if (k == "fusion") {
