@@ -206,6 +206,8 @@ struct EpiK {
   double m0;
   int zw0;
   int fxm0, fxs;       // FX: per-tensor M and the shift S - 32
+  int addfx, amc, ams, as;   // integer fused add (LayerRt::add_fx)
+  long long ab;
 };
 // 4-channel groups of a 16-channel chunk whose fused add runs on the fp64 pipe instead of
 // the shared-memory table: one group of four balances the L1 (table) and fp64 pipes (A/B
@@ -331,7 +333,12 @@ __device__ __forceinline__ int4 epi_chunk16_fx(const uint32_t (&v)[16], const ui
       q[j] = (int)(X >> 32) >> k.fxs;
       if (RELU || SKIP) q[j] = imax(q[j], k.lo_conv);
       if (SKIP) {
-        if ((PTQ_ADD_ALU_MASK >> g) & 1) {
+        if (k.addfx) {
+          // integer add (LayerRt::add_fx): low word of (xc Mc + xs Ms + B) >> S, S <= 31
+          const int skc = (int)(int8_t)(skw[g] >> (8 * j));   // (__byte_perm ignores the sign bit)
+          const long long X = (long long)imin(q[j], PTQ_QMAX) * k.amc + (long long)skc * k.ams + k.ab;
+          q[j] = imax(__funnelshift_r((uint32_t)X, (uint32_t)(X >> 32), k.as), k.lo_add);
+        } else if ((PTQ_ADD_ALU_MASK >> g) & 1) {
           const int skc = (int)(int8_t)(skw[g] >> (8 * j));
           const double t2 = __dadd_rn(__dmul_rn(b2d((uint32_t)imin(q[j], PTQ_QMAX) + k.zc_bias), k.rc),
                                       __dmul_rn(b2d((uint32_t)skc + k.zs_bias), k.rs));
@@ -341,9 +348,9 @@ __device__ __forceinline__ int4 epi_chunk16_fx(const uint32_t (&v)[16], const ui
         }
       }
     }
-    packed[g] = SKIP ? __byte_perm(__byte_perm((uint32_t)q[0], (uint32_t)q[1], 0x0040),
-                                   __byte_perm((uint32_t)q[2], (uint32_t)q[3], 0x0040), 0x5410)
-                     : pack4_sat(q[0], q[1], q[2], q[3]);
+    packed[g] = (SKIP && !k.addfx) ? __byte_perm(__byte_perm((uint32_t)q[0], (uint32_t)q[1], 0x0040),
+                                                 __byte_perm((uint32_t)q[2], (uint32_t)q[3], 0x0040), 0x5410)
+                                   : pack4_sat(q[0], q[1], q[2], q[3]);
   }
   return make_int4((int)packed[0], (int)packed[1], (int)packed[2], (int)packed[3]);
 }
@@ -851,6 +858,11 @@ __global__ void __launch_bounds__(TC_THREADS, 1) k_conv_tc(const __grid_constant
     k.zw0 = rt.zw0;
     k.fxm0 = rt.fx_m0;
     k.fxs = rt.fx_s;
+    k.addfx = rt.add_fx && a.add_int;
+    k.amc = rt.add_mc;
+    k.ams = rt.add_ms;
+    k.as = rt.add_s;
+    k.ab = rt.add_b;
     const EpiEnv e{tmem, tfull, tempty, rsfull, rsum, reinterpret_cast<const uint8_t*>(sparam), cs, stab_c,
                    q, grp, row, M, n_tiles, n_nt};
     // one persistent tile loop per epilogue variant: the per-chunk code carries no

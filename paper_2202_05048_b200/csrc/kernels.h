@@ -40,6 +40,12 @@ struct LayerRt {
   int fx;
   int fx_s;            // S - 32 (per layer)
   int fx_m0;           // M of per-tensor layers (uni)
+  // exact integer fused add: out = clip((xc*add_mc + xs*add_ms + add_b) >> add_s) over the
+  // clamped conv code xc and the skip code xs, verified against every entry of the fp64 add
+  // table (k_layer_params); add_fx = 0 keeps the table / fp64 lookup
+  int add_fx;
+  int add_mc, add_ms, add_s;
+  long long add_b;
 };
 
 // per-config, per-output-channel epilogue constants of the tensor-core conv:
@@ -207,6 +213,7 @@ struct ConvTcArgs {
   int flat;               // set by the launcher: GEMM row m is flat pixel m of the output (and of
                           // the add operand) -- halo-free TMA-mode layers skip the row geometry
   int kwr_mode;           // runtime option: -1 disables the kw-reuse slabs and the stem slab
+  int add_int;            // runtime option: integer fused add (LayerRt::add_fx) instead of the table
   int* acc_out;           // parity probe (ptq_probe_acc): when set, the epilogue stores the exact
                           // int32-clipped accumulator acc + bias (intexec.py:177-190) of every real
                           // output as [pixel][cout] int32 instead of requantized codes
