@@ -47,6 +47,7 @@ constexpr int TC_MAX_COUT = 2048;
 __constant__ EpiParam c_ep[TC_MAX_COUT];    // SoA image, see ep_soa() in kernels.h
 
 constexpr int TC_MAX_STAGES = 10;                 // smem pipeline depth cap (runtime depth: launcher)
+constexpr int TC_IO_NB = 2;                       // tile I/O buffers (tio)
 constexpr int TC_SMEM_MAX = 232448;                // 227 KB opt-in dynamic smem per CTA
 constexpr int TC_A_STAGE = TC_BM * 128;            // 16 KB: 8 chunks x 128 rows x 16 B
 #ifndef PTQ_EPI_GROUPS
@@ -54,7 +55,8 @@ constexpr int TC_A_STAGE = TC_BM * 128;            // 16 KB: 8 chunks x 128 rows
 #endif
 constexpr int TC_NG = PTQ_EPI_GROUPS;               // epilogue column groups per TMEM lane quarter
 constexpr int TC_EPI_WARPS = 4 * TC_NG;             // NG per SM sub-partition
-constexpr int TC_THREADS = (4 + TC_EPI_WARPS) * 32;    // + producer / MMA warps 0-3
+constexpr int TC_IO_WARP = 4 + TC_EPI_WARPS;         // tile I/O agent (after the epilogue warps)
+constexpr int TC_THREADS = (5 + TC_EPI_WARPS) * 32;    // + producer / MMA warps 0-3 + I/O agent
 
 
 __device__ __forceinline__ uint64_t umma_desc(uint32_t saddr, uint32_t lbo, uint32_t sbo) {
@@ -206,8 +208,6 @@ struct EpiK {
   double m0;
   int zw0;
   int fxm0, fxs;       // FX: per-tensor M and the shift S - 32
-  int addfx, amc, ams, as;   // integer fused add (LayerRt::add_fx)
-  long long ab;
 };
 // 4-channel groups of a 16-channel chunk whose fused add runs on the fp64 pipe instead of
 // the shared-memory table: one group of four balances the L1 (table) and fp64 pipes (A/B
@@ -333,12 +333,7 @@ __device__ __forceinline__ int4 epi_chunk16_fx(const uint32_t (&v)[16], const ui
       q[j] = (int)(X >> 32) >> k.fxs;
       if (RELU || SKIP) q[j] = imax(q[j], k.lo_conv);
       if (SKIP) {
-        if (k.addfx) {
-          // integer add (LayerRt::add_fx): low word of (xc Mc + xs Ms + B) >> S, S <= 31
-          const int skc = (int)(int8_t)(skw[g] >> (8 * j));   // (__byte_perm ignores the sign bit)
-          const long long X = (long long)imin(q[j], PTQ_QMAX) * k.amc + (long long)skc * k.ams + k.ab;
-          q[j] = imax(__funnelshift_r((uint32_t)X, (uint32_t)(X >> 32), k.as), k.lo_add);
-        } else if ((PTQ_ADD_ALU_MASK >> g) & 1) {
+        if ((PTQ_ADD_ALU_MASK >> g) & 1) {
           const int skc = (int)(int8_t)(skw[g] >> (8 * j));
           const double t2 = __dadd_rn(__dmul_rn(b2d((uint32_t)imin(q[j], PTQ_QMAX) + k.zc_bias), k.rc),
                                       __dmul_rn(b2d((uint32_t)skc + k.zs_bias), k.rs));
@@ -348,9 +343,9 @@ __device__ __forceinline__ int4 epi_chunk16_fx(const uint32_t (&v)[16], const ui
         }
       }
     }
-    packed[g] = (SKIP && !k.addfx) ? __byte_perm(__byte_perm((uint32_t)q[0], (uint32_t)q[1], 0x0040),
-                                                 __byte_perm((uint32_t)q[2], (uint32_t)q[3], 0x0040), 0x5410)
-                                   : pack4_sat(q[0], q[1], q[2], q[3]);
+    packed[g] = SKIP ? __byte_perm(__byte_perm((uint32_t)q[0], (uint32_t)q[1], 0x0040),
+                                   __byte_perm((uint32_t)q[2], (uint32_t)q[3], 0x0040), 0x5410)
+                     : pack4_sat(q[0], q[1], q[2], q[3]);
   }
   return make_int4((int)packed[0], (int)packed[1], (int)packed[2], (int)packed[3]);
 }
@@ -459,6 +454,8 @@ struct EpiEnv {
   int cs;                                            // SoA channel stride = roundup(Cout, 16)
   const int8_t* stab_c;
   int q, grp, row, M, n_tiles, n_nt;
+  uint8_t* sio;                                      // tile I/O buffers [TC_IO_NB][128][BN] (tio)
+  uint64_t *iofull, *ioempty, *ioready;
 };
 
 // persistent epilogue tile loop of one variant (GENERIC: runtime dispatch, slow layers and
@@ -506,11 +503,22 @@ __device__ __forceinline__ void epi_tiles(const ConvTcArgs& a, const LayerRt& rt
                       : pixel_rowsum(a, g.n, g.ih0, g.iw0);
     }
     const int zr = (FX && PT && WZP) ? k.zw0 * (int)rowsum : 0;   // per-tensor zw * rowsum
+    // tile I/O: this tile's shared buffer (the fused-add operand landed by TMA, or a buffer
+    // whose previous TMA store has finished reading it)
+    const uint32_t ib = lt % TC_IO_NB, iph = (lt / TC_IO_NB) & 1u;
+    uint8_t* io = e.sio + ib * (TC_BM * BN);
+    const int iow = a.io_w, iosh = a.io_w == 128 ? 3 : 2;   // box width in bytes, log2(16-byte units)
+    const int iorow = e.row * iow, ioswz = iow == 128 ? (e.row & 7) : ((e.row >> 1) & 3);
+    if (a.tio) {
+      if (has_skip) mbar_wait(&e.iofull[ib], iph);
+      else mbar_wait(&e.ioempty[ib], iph ^ 1u);
+    }
     // the residual operand does not depend on the accumulator: fetch it before the wait
     // and one chunk ahead inside the loop
     const int cb0 = nt * BN + first * 16;
     int4 sk_next = make_int4(0, 0, 0, 0);
-    if (has_skip && srow && first < NCH && cb0 < a.out.Cp) sk_next = __ldg(reinterpret_cast<const int4*>(srow + cb0));
+    if (has_skip && !a.tio && srow && first < NCH && cb0 < a.out.Cp)
+      sk_next = __ldg(reinterpret_cast<const int4*>(srow + cb0));
     mbar_wait(&e.tfull[buf], uph);
     tc_fence_after();
     const uint32_t tbase = e.tmem + ((uint32_t)(e.q * 32) << 16) + buf * BN;
@@ -527,10 +535,17 @@ __device__ __forceinline__ void epi_tiles(const ConvTcArgs& a, const LayerRt& rt
       tmem_ld16(tbase + (uint32_t)(c * 16), v);
       if (cb >= a.out.Cp) continue;                  // warp-uniform: the slow path re-reads TMEM
       int4 skv = make_int4(0, 0, 0, 0);
+      // swizzled slot of (row, chunk c) in the I/O tile: box c / iocpb, 16-byte unit XOR row phase
+      int4* ioslot = reinterpret_cast<int4*>(io + (c >> iosh) * (TC_BM * iow) + iorow +
+                                             (((c & ((1 << iosh) - 1)) ^ ioswz) << 4));
       if (has_skip) {
-        skv = sk_next;
-        if (srow && c + TC_NG < NCH && cb + 16 * TC_NG < a.out.Cp)
-          sk_next = __ldg(reinterpret_cast<const int4*>(srow + cb + 16 * TC_NG));
+        if (a.tio) {
+          skv = *ioslot;
+        } else {
+          skv = sk_next;
+          if (srow && c + TC_NG < NCH && cb + 16 * TC_NG < a.out.Cp)
+            sk_next = __ldg(reinterpret_cast<const int4*>(srow + cb + 16 * TC_NG));
+        }
       }
       int4 res;
       if (GENERIC && a.ablate == 1) {
@@ -542,10 +557,17 @@ __device__ __forceinline__ void epi_tiles(const ConvTcArgs& a, const LayerRt& rt
       } else {
         res = epi_slow_chunk(tbase + (uint32_t)(c * 16), cb, rowsum, a, rt, k.lo_conv, k.lo_add, skv);
       }
-      if (g.ok) *reinterpret_cast<int4*>(orow + cb) = res;
+      if (a.tio) *ioslot = res;
+      else if (g.ok) *reinterpret_cast<int4*>(orow + cb) = res;
     }
     tc_fence_before();
     mbar_arrive(&e.tempty[buf]);                     // accumulator buffer may be reused
+    if (a.tio) {
+      // this thread's codes are in the tile: hand them to the async proxy and tell the I/O
+      // agent (no CTA-wide barrier: the epilogue warps stay decoupled)
+      fence_proxy_async();
+      mbar_arrive(&e.ioready[ib]);
+    }
   }
 }
 
@@ -568,16 +590,20 @@ __global__ void __launch_bounds__(TC_THREADS, 1) k_conv_tc(const __grid_constant
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   // swizzled TMA tiles need 1024-byte aligned stages (the launcher reserves the slack)
   uint8_t* smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
-  uint8_t* sA = smem;
-  uint8_t* sB = smem + NS * TC_A_STAGE;             // B ring [NS][BN][128], or resident [n_kiter][BN][128]
+  uint8_t* sio = smem;                              // tile I/O buffers (tio), 1024-aligned boxes
+  uint8_t* sA = smem + (a.tio ? TC_IO_NB * TC_BM * BN : 0);
+  uint8_t* sB = sA + NS * TC_A_STAGE;               // B ring [NS][BN][128], or resident [n_kiter][BN][128]
   uint64_t* full = reinterpret_cast<uint64_t*>(sB + (a.b_res ? a.n_kiter : NS) * BN * 128);
   uint64_t* empty = full + NS;
   uint64_t* tfull = empty + NS;
   uint64_t* tempty = tfull + 2;
   uint64_t* rsfull = tempty + 2;                                 // row sums of tile buffer ready
   uint64_t* bfull = tempty + 4;                                  // resident B landed
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 5);
-  int* rsum = reinterpret_cast<int*>(tempty + 6);                // [2][128] A-row sums (tma_rowsum)
+  uint64_t* iofull = tempty + 5;                                 // [TC_IO_NB] operand tile landed
+  uint64_t* ioempty = iofull + TC_IO_NB;                         // [TC_IO_NB] tile buffer free
+  uint64_t* ioready = ioempty + TC_IO_NB;                        // [TC_IO_NB] epilogue wrote the tile
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(ioready + TC_IO_NB);
+  int* rsum = reinterpret_cast<int*>(ioready + TC_IO_NB + 1);    // [2][128] A-row sums (tma_rowsum)
   EpiParam* sparam = reinterpret_cast<EpiParam*>(rsum + 2 * TC_BM);   // [Cout] (no fused add)
   int8_t* stab = reinterpret_cast<int8_t*>(rsum + 2 * TC_BM);          // fused-add table
   constexpr uint32_t TMEM_COLS = (2 * BN) < 32 ? 32 : 2 * BN;
@@ -593,6 +619,11 @@ __global__ void __launch_bounds__(TC_THREADS, 1) k_conv_tc(const __grid_constant
       mbar_init(&empty[s], a.tma_rowsum ? 2 : 1);
     }
     mbar_init(bfull, 1);
+    for (int b = 0; b < TC_IO_NB; ++b) {
+      mbar_init(&iofull[b], 1);
+      mbar_init(&ioempty[b], 1);
+      mbar_init(&ioready[b], TC_EPI_WARPS * 32);
+    }
     for (int b = 0; b < 2; ++b) {
       mbar_init(&rsfull[b], 1);
       mbar_init(&tfull[b], 1);
@@ -825,6 +856,49 @@ __global__ void __launch_bounds__(TC_THREADS, 1) k_conv_tc(const __grid_constant
       }
     }
     __syncwarp();
+  } else if (warp == TC_IO_WARP) {
+    // ------------------------------------------------ tile I/O agent (tio)
+    // loads the fused-add operand of a tile into its buffer (TMA), and stores each tile the
+    // epilogue finished (TMA; rows past M and columns past Cp are clipped by the map); a buffer
+    // is reloaded / handed back once its store has finished reading it
+    if (a.tio && lane == 0) {
+      const bool skip = a.skip.p != nullptr;
+      const int iow = a.io_w;
+      if (skip) prefetch_tmap(&a.tmS);
+      prefetch_tmap(&a.tmO);
+      auto load = [&](int tile, uint32_t ib) {
+        const int mt = (int)a.div_nt.div((uint32_t)tile), nt = tile - mt * n_nt;
+        const int nbox = (imin(BN, a.skip.Cp - nt * BN) + iow - 1) / iow;
+        uint8_t* io = sio + ib * (TC_BM * BN);
+        mbar_arrive_expect_tx(&iofull[ib], (uint32_t)(nbox * TC_BM * iow));
+        for (int b = 0; b < nbox; ++b)
+          tma_load_2d(io + b * (TC_BM * iow), &a.tmS, nt * BN + b * iow, mt * TC_BM, &iofull[ib]);
+      };
+      if (skip)
+        for (int i = 0; i < TC_IO_NB && blockIdx.x + i * (int)gridDim.x < n_tiles; ++i)
+          load(blockIdx.x + i * gridDim.x, (uint32_t)i);
+      uint32_t lt = 0;
+      for (int tile = blockIdx.x; tile < n_tiles; tile += gridDim.x, ++lt) {
+        const uint32_t ib = lt % TC_IO_NB, iph = (lt / TC_IO_NB) & 1u;
+        const int mt = (int)a.div_nt.div((uint32_t)tile), nt = tile - mt * n_nt;
+        const int nbox = (imin(BN, a.out.Cp - nt * BN) + iow - 1) / iow;
+        uint8_t* io = sio + ib * (TC_BM * BN);
+        mbar_wait(&ioready[ib], iph);
+        for (int b = 0; b < nbox; ++b) tma_store_2d(&a.tmO, io + b * (TC_BM * iow), nt * BN + b * iow, mt * TC_BM);
+        bulk_commit();
+        if (skip) {
+          const int next = tile + TC_IO_NB * (int)gridDim.x;
+          if (next < n_tiles) {
+            bulk_wait_read<0>();
+            load(next, ib);
+          }
+        } else {
+          bulk_wait_read<1>();
+          if (lt > 0) mbar_arrive(&ioempty[(lt - 1) % TC_IO_NB]);
+        }
+      }
+      bulk_wait_all();
+    }
   } else {
     // ------------------------------------------------ epilogue warps
     // warp-uniform warp index (a shuffle from lane 0): q, grp, the chunk loop and the channel
@@ -858,13 +932,9 @@ __global__ void __launch_bounds__(TC_THREADS, 1) k_conv_tc(const __grid_constant
     k.zw0 = rt.zw0;
     k.fxm0 = rt.fx_m0;
     k.fxs = rt.fx_s;
-    k.addfx = rt.add_fx && a.add_int;
-    k.amc = rt.add_mc;
-    k.ams = rt.add_ms;
-    k.as = rt.add_s;
-    k.ab = rt.add_b;
+
     const EpiEnv e{tmem, tfull, tempty, rsfull, rsum, reinterpret_cast<const uint8_t*>(sparam), cs, stab_c,
-                   q, grp, row, M, n_tiles, n_nt};
+                   q, grp, row, M, n_tiles, n_nt, sio, iofull, ioempty, ioready};
     // one persistent tile loop per epilogue variant: the per-chunk code carries no
     // layer-level dispatch (that overhead was ~20% of the hot loop's instructions)
     const bool skip = a.skip.p != nullptr, wzp = a.has_wzp != 0, clamp = !rt.noclamp,
@@ -964,17 +1034,25 @@ static void launch_bn(const ConvTcArgs& a, cudaStream_t s) {
   const int n_nt = (a.L.cout + BN - 1) / BN;
   const size_t b_bytes = (size_t)a.n_kiter * BN * 128;
   const int b_res = n_nt == 1 && b_bytes <= 64 * 1024;
-  const size_t fixed = 1024 + (2 * TC_MAX_STAGES + 8) * 8 + 2 * TC_BM * 4 + 16 +
-                       (a.addtab ? PTQ_ADDTAB_BYTES : (size_t)((a.L.cout + 15) & ~15) * sizeof(EpiParam)) +
-                       (b_res ? b_bytes : 0);
-  const size_t per_stage = (size_t)TC_A_STAGE + (b_res ? 0 : (size_t)BN * 128);
-  int ns = (int)((TC_SMEM_MAX - fixed) / per_stage);
-  if (ns > TC_MAX_STAGES) ns = TC_MAX_STAGES;
-  if (ns < 2) ns = 2;                // does not fit: the launch fails loudly (check_launch)
   ConvTcArgs b = a;
+  size_t smem = 0;
+  int ns = 0;
+  // tile I/O takes TC_IO_NB [128][BN] buffers; without room for two pipeline stages beside
+  // them the layer keeps the direct global epilogue
+  for (int pass = 0; pass < 2; ++pass) {
+    const size_t fixed = 1024 + (2 * TC_MAX_STAGES + 8 + 3 * TC_IO_NB) * 8 + 2 * TC_BM * 4 + 16 +
+                         (a.addtab ? PTQ_ADDTAB_BYTES : (size_t)((a.L.cout + 15) & ~15) * sizeof(EpiParam)) +
+                         (b_res ? b_bytes : 0) + (b.tio ? (size_t)TC_IO_NB * TC_BM * BN : 0);
+    const size_t per_stage = (size_t)TC_A_STAGE + (b_res ? 0 : (size_t)BN * 128);
+    ns = fixed < TC_SMEM_MAX ? (int)((TC_SMEM_MAX - fixed) / per_stage) : 0;
+    if (ns < 2 && b.tio) { b.tio = 0; continue; }
+    if (ns > TC_MAX_STAGES) ns = TC_MAX_STAGES;
+    if (ns < 2) ns = 2;                // does not fit: the launch fails loudly (check_launch)
+    smem = (size_t)ns * per_stage + fixed;
+    break;
+  }
   b.n_stages = ns;
   b.b_res = b_res;
-  const size_t smem = (size_t)ns * per_stage + fixed;
   int dev = 0;
   cudaGetDevice(&dev);
   // the opt-in shared-memory limit is a per-device function attribute: raise it once per
@@ -1135,6 +1213,27 @@ static void plan_launch(ConvTcArgs& t, int bn) {
   // row sums (when needed) taken in-kernel
   t.flat = (t.tma_a == 64 || t.tma_a == 128) && t.in.halo == 0 && t.out.halo == 0 && t.OH == t.OHr &&
            t.OW == t.OWr && (!t.skip.p || t.skip.halo == 0) && (!t.has_wzp || t.tma_rowsum);
+  // tile I/O for flat layers: the output (and the fused-add operand) as 2-D [pixels][Cp] maps
+  // with boxes of 128 rows x io_w bytes, swizzled like the epilogue's shared tile
+  t.tio = 0;
+  if (t.flat && t.tio_mode && !t.acc_out && bn >= 64 && (t.out.Cp % 16) == 0) {
+    EncodeTiledFn fn = encode_tiled();
+    const int w = bn >= 128 ? 128 : 64;
+    const int64_t M = (int64_t)t.in.N * t.OH * t.OW;
+    auto enc = [&](CUtensorMap* m, const View& v) {
+      cuuint64_t gdim[2] = {(cuuint64_t)v.Cp, (cuuint64_t)M};
+      cuuint64_t gstride[1] = {(cuuint64_t)v.Cp};
+      cuuint32_t box[2] = {(cuuint32_t)w, (cuuint32_t)TC_BM};
+      cuuint32_t es[2] = {1, 1};
+      return fn && fn(m, CU_TENSOR_MAP_DATA_TYPE_UINT8, 2, (void*)v.p, gdim, gstride, box, es,
+                      CU_TENSOR_MAP_INTERLEAVE_NONE, w == 128 ? CU_TENSOR_MAP_SWIZZLE_128B : CU_TENSOR_MAP_SWIZZLE_64B,
+                      CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+    };
+    if (enc(&t.tmO, t.out) && (!t.skip.p || (t.skip.Cp == t.out.Cp && enc(&t.tmS, t.skip)))) {
+      t.tio = 1;
+      t.io_w = w;
+    }
+  }
 }
 
 bool conv_tc_tma_rowsum(const ConvTcArgs& a0, int bn) {

@@ -345,9 +345,6 @@ __global__ void __launch_bounds__(512) k_layer_params(const LayerSt* __restrict_
     r.fx = 0;
     r.fx_s = 0;
     r.fx_m0 = 0;
-    r.add_fx = 0;
-    r.add_mc = r.add_ms = r.add_s = 0;
-    r.add_b = 0;
     fx_S = 0;
     if (fx_enable && L.ep && !slow_base) {
       int e = 0;
@@ -406,30 +403,8 @@ __global__ void __launch_bounds__(512) k_layer_params(const LayerSt* __restrict_
   // channel) spread over the shared-memory banks.  Entry = clip(RHU(fl(fl((xa - za) * ra) +
   // fl((xb - zb) * rb))) + zo) with the add's relu floor (intexec.py:245-276 order); both
   // operands are int8 codes, so the table is exact.
-  //
-  // The same pass verifies the integer form of the add ("add-FX"): with S from max(rc, rs) and
-  // Mc = round(rc 2^S), Ms = round(rs 2^S), every entry T reachable by the conv (xc in
-  // [lo_conv, 127]) bounds B: T 2^S <= xc Mc + xs Ms + B < (T + 1) 2^S (one-sided at the clip
-  // levels lo / 127); the add runs as two IMAD.WIDE + a shift whenever the bounds intersect.
   const LayerRt r = srt;
   const int lo = r.add_relu_zp > PTQ_QMIN ? r.add_relu_zp : PTQ_QMIN;
-  const int lo_conv = r.relu_zp > PTQ_QMIN ? r.relu_zp : PTQ_QMIN;
-  const double rc = L.add_conv_is_a ? r.ra : r.rb, rs = L.add_conv_is_a ? r.rb : r.ra;
-  __shared__ long long b_lo, b_hi;
-  __shared__ int add_S;
-  if (threadIdx.x == 0) {
-    b_lo = LLONG_MIN;
-    b_hi = LLONG_MAX;
-    int e = 0;
-    frexp(fmax(rc, rs), &e);
-    // S <= 31: the kernel takes the low word of the 64-bit sum >> S with one funnel shift
-    add_S = min(31 - e, 31);
-    if (!(rc > 0.0 && rs > 0.0) || add_S < 1 || ldexp(fmax(rc, rs), add_S) >= 2147483647.0) add_S = 0;
-  }
-  __syncthreads();
-  const int S = add_S;
-  const long long Mc = S ? __double2ll_rn(ldexp(rc, S)) : 0, Ms = S ? __double2ll_rn(ldexp(rs, S)) : 0;
-  long long mylo = LLONG_MIN, myhi = LLONG_MAX;
   for (int idx = threadIdx.x; idx < PTQ_ADDTAB_BYTES; idx += blockDim.x) {
     const int row = idx / PTQ_ADDTAB_ROW, col = idx - row * PTQ_ADDTAB_ROW;
     if (col >= 256) { L.addtab[idx] = 0; continue; }
@@ -437,37 +412,7 @@ __global__ void __launch_bounds__(512) k_layer_params(const LayerSt* __restrict_
     const int xa = L.add_conv_is_a ? q : sk, xb = L.add_conv_is_a ? sk : q;
     const double v = __dadd_rn(__dmul_rn((double)(xa - r.za), r.ra), __dmul_rn((double)(xb - r.zb), r.rb));
     int code = clip8(rhu(v) + (double)r.zo);
-    code = code < lo ? lo : code;
-    L.addtab[idx] = (int8_t)code;
-    if (S && q >= lo_conv) {
-      const long long P = (long long)q * Mc + (long long)sk * Ms;
-      if (code > lo) mylo = max(mylo, ((long long)code << S) - P);
-      if (code < PTQ_QMAX) myhi = min(myhi, ((long long)(code + 1) << S) - P);
-    }
-  }
-  if (S) {
-    for (int o = 16; o; o >>= 1) {
-      mylo = max(mylo, (long long)__shfl_xor_sync(0xffffffffu, mylo, o));
-      myhi = min(myhi, (long long)__shfl_xor_sync(0xffffffffu, myhi, o));
-    }
-    if ((threadIdx.x & 31) == 0) {
-      atomicMax(&b_lo, mylo);
-      atomicMin(&b_hi, myhi);
-    }
-  }
-  __syncthreads();
-  if (threadIdx.x == 0) {
-    LayerRt w = srt;
-    w.add_fx = 0;
-    if (S && b_lo < b_hi) {
-      // any B in [b_lo, b_hi) reproduces the table; pick one away from the int64 extremes
-      w.add_fx = 1;
-      w.add_b = b_lo != LLONG_MIN ? b_lo : (b_hi != LLONG_MAX ? b_hi - 1 : 0);
-      w.add_mc = (int)Mc;
-      w.add_ms = (int)Ms;
-      w.add_s = S;
-    }
-    *L.rt = w;
+    L.addtab[idx] = (int8_t)(code < lo ? lo : code);
   }
 }
 void launch_layer_params(const LayerSt* d_layers, int n_layers, const float* act_scale,

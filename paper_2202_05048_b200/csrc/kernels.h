@@ -40,12 +40,6 @@ struct LayerRt {
   int fx;
   int fx_s;            // S - 32 (per layer)
   int fx_m0;           // M of per-tensor layers (uni)
-  // exact integer fused add: out = clip((xc*add_mc + xs*add_ms + add_b) >> add_s) over the
-  // clamped conv code xc and the skip code xs, verified against every entry of the fp64 add
-  // table (k_layer_params); add_fx = 0 keeps the table / fp64 lookup
-  int add_fx;
-  int add_mc, add_ms, add_s;
-  long long add_b;
 };
 
 // per-config, per-output-channel epilogue constants of the tensor-core conv:
@@ -181,6 +175,7 @@ void launch_im2col(View in, int k, int stride, int pad, int OH, int OW, int8_t* 
 
 struct ConvTcArgs {
   CUtensorMap tmA;        // TMA map of the A operand (tma_a != 0); 64-byte aligned first member
+  CUtensorMap tmO, tmS;   // tile I/O (tio): output / fused-add operand as [pixels][Cp] maps
   int tma_a;              // 0: cp.async implicit-im2col gather; 64 / 128: TMA tile loads of
                           // 128 flat padded pixels x 64 / 128 channel bytes (SWIZZLE_64B / 128B)
   int OHr, OWr;           // real output dims (TMA mode computes over the padded grid OH x OW)
@@ -213,7 +208,11 @@ struct ConvTcArgs {
   int flat;               // set by the launcher: GEMM row m is flat pixel m of the output (and of
                           // the add operand) -- halo-free TMA-mode layers skip the row geometry
   int kwr_mode;           // runtime option: -1 disables the kw-reuse slabs and the stem slab
-  int add_int;            // runtime option: integer fused add (LayerRt::add_fx) instead of the table
+  int tio_mode;           // runtime option: 0 disables tile I/O
+  int tio;                // set by the launcher (flat layers): the epilogue writes codes into a
+                          // swizzled shared tile stored by TMA, and reads the fused-add operand from
+                          // a tile a producer loads by TMA, instead of per-row 16-byte global accesses
+  int io_w;               // tile I/O box width in bytes (64 or 128 = the swizzle span)
   int* acc_out;           // parity probe (ptq_probe_acc): when set, the epilogue stores the exact
                           // int32-clipped accumulator acc + bias (intexec.py:177-190) of every real
                           // output as [pixel][cout] int32 instead of requantized codes

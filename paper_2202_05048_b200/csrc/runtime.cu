@@ -184,7 +184,7 @@ struct ptq_ctx {
   int conv_ref = 0, fusion = 1, time_conv = 0, ablate = 0, tma = 1, subsample = 1;
   int dwconv_variant = 2, concat_v16 = 1, kwr = 0;   // A/B switches (per context)
   int fx = 1;                            // exact fixed-point conv epilogue (0: fp64 epilogue)
-  int add_int = 0;                       // integer fused add instead of the table (A/B)
+  int tio = 1;                           // tile I/O through shared memory + TMA (flat conv layers)
   int64_t opt_chunk = 0;
   // stats
   int64_t launches = 0;
@@ -1044,7 +1044,7 @@ void eval_one(ptq_ctx* c, const ptq_config& cfg, unsigned long long* d_correct, 
           a.ablate = c->ablate;
           a.allow_tma = c->tma;
           a.kwr_mode = c->kwr;
-          a.add_int = c->add_int;
+          a.tio_mode = c->tio;
           if (a.has_wzp && !a.Rpix && (c->conv_ref || !conv_tc_tma_rowsum(a, wd.bn))) {
             launch_pixsum(vin, c->d_P, c->st);       // gather-mode convs sum input pixels first
             check_launch(c);
@@ -1702,7 +1702,7 @@ int ptq_set_option(ptq_ctx* c, const char* key, int64_t value) {
     else if (k == "concat_v16") c->concat_v16 = (int)value;
     else if (k == "kwr") c->kwr = (int)value;
     else if (k == "fx") c->fx = (int)value;
-    else if (k == "add_int") c->add_int = (int)value;
+    else if (k == "tio") c->tio = (int)value;
     else if (k == "time_conv") c->time_conv = (int)value;
     else if (k == "reset_stats") c->launches = 0;
     else if (k == "fusion") {
