@@ -406,6 +406,21 @@ void import_graph(ptq_ctx* c, const ptq_graph_desc* g) {
       wd.n_kiter = (wd.n_chunks + 7) / 8;
       REQ(wd.cout <= conv_tc_max_cout(), "conv / fc output channels exceed the tensor-core conv limit (2048)");
       wd.bn = conv_tc_bn_for(wd.cout);
+      // a conv whose residual add is fused into its epilogue (its output only feeds the add, and
+      // the add's other operand is produced earlier) keeps the 66 KB add table in shared memory;
+      // with B streamed (Cout > 256) BN = 128 leaves room for the tile-I/O buffers.  Only for
+      // K <= 512: deeper layers re-read A once per n-tile, which costs more than tile I/O saves
+      // (ResNet-50: poin37 0.39 -> 0.33 ms, conv102 K=1024 0.14 -> 0.17 ms)
+      const TensorI& ot = c->tens[n.out];
+      if (wd.bn == 256 && wd.cout > 256 && wd.n_kiter <= 4 && ot.consumers.size() == 1 &&
+          c->nodes[ot.consumers[0]].kind == PTQ_ADD) {
+        const NodeI& an = c->nodes[ot.consumers[0]];
+        const int other = an.in[0] == n.out ? an.in[1] : an.in[0];
+        int prod = -1;
+        for (int j = 0; j < g->n_nodes; ++j)
+          if (c->nodes[j].out == other) prod = j;
+        if (prod < i) wd.bn = 128;
+      }
       int ntiles = (wd.cout + wd.bn - 1) / wd.bn;
       wd.bytes_per_variant = (int64_t)ntiles * wd.n_kiter * 8 * wd.bn * 16;
     }
