@@ -394,7 +394,7 @@ def run_b200(args):
         best = int(np.argmax(counts))
         line = {"metric": metric_for(args.model), "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
                 "warmup": args.warmup, "ms_per_step": t_ms, "higher_is_better": True,
-                "scaling": "strong", "vs_baseline": None, "dtype": "int8 (s32 acc, fp64 requant)",
+                "scaling": "strong", "vs_baseline": None, "dtype": "int8 (s32 acc, exact int64 fixed-point requant of the fp64 reference)",
                 "data": f"synthetic (make_dataset seed 0, 224^2) + random-init {MODEL_LABEL.get(args.model, args.model)} IR (seed 0)",
                 "config": config_dict(args, world),
                 "roofline": roofline, "roofline_path": roofline_path, "cpu_baseline": cb,
