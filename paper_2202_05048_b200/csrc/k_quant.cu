@@ -262,7 +262,7 @@ __global__ void __launch_bounds__(512) k_layer_params(const LayerSt* __restrict_
   const double sx = (double)as[L.in_hist], sy = (double)as[L.out_hist];
   const float* ws = L.wscale + (int64_t)wvar * L.cout;
   const long long zx = az[L.in_hist];
-  __shared__ int slow, slow_base, zw_min, zw_max, fx_S, fx_ok;
+  __shared__ int slow, slow_base, zw_min, zw_max, fx_S;
   __shared__ unsigned long long m_max_bits, m_min_bits;   // m > 0: bit order == value order
   __shared__ LayerRt srt;
   if (threadIdx.x == 0) {
@@ -352,47 +352,12 @@ __global__ void __launch_bounds__(512) k_layer_params(const LayerSt* __restrict_
       const int S = 31 - e;
       if (S >= 32 && S <= 52) fx_S = S;
     }
-    fx_ok = fx_S != 0;
+    // candidate: k_layer_fx derives the per-channel constants, k_layer_fx_commit installs them
+    if (fx_S) {
+      r.fx = 2;
+      r.fx_s = fx_S - 32;
+    }
     srt = r;
-  }
-  __syncthreads();
-  if (fx_S) {
-    // per-channel (M, B') into the second half of the ep block (scratch), committed below
-    const int S = fx_S;
-    const int lo = srt.relu_zp > PTQ_QMIN ? srt.relu_zp : PTQ_QMIN;
-    long long* fx_b = reinterpret_cast<long long*>(L.ep + cs);
-    int* fx_m = reinterpret_cast<int*>(fx_b + cs);
-    for (int o = threadIdx.x >> 5; o < L.cout; o += blockDim.x >> 5) {
-      long long M = 0, B = 0;
-      const bool ok = fx_channel(L.mult[o], srt.zy, lo, S, M, B);
-      if ((threadIdx.x & 31) == 0) {
-        if (!ok) {
-          fx_ok = 0;
-        } else {
-          const long long cc = (long long)(int)((uint32_t)ep_cc[o] ^ 0x80000000u);
-          fx_b[o] = B + cc * M;                           // acc = v' + cc folded into the addend
-          fx_m[o] = (int)M;
-        }
-      }
-    }
-    __syncthreads();
-    if (fx_ok) {
-      // commit: the active SoA block now holds (B', M, zw) instead of (m, cc, zw)
-      long long* dst_b = reinterpret_cast<long long*>(L.ep);
-      int* dst_m = reinterpret_cast<int*>(dst_b + cs);
-      for (int o = threadIdx.x; o < cs; o += blockDim.x) {
-        dst_b[o] = o < L.cout ? fx_b[o] : 0;
-        dst_m[o] = o < L.cout ? fx_m[o] : 0;
-      }
-      if (threadIdx.x == 0) {
-        LayerRt r = srt;
-        r.fx = 1;
-        r.fx_s = S - 32;
-        r.fx_m0 = fx_m[0];
-        r.slow = 0;
-        srt = r;
-      }
-    }
   }
   __syncthreads();
   if (threadIdx.x == 0) *L.rt = srt;
@@ -415,9 +380,83 @@ __global__ void __launch_bounds__(512) k_layer_params(const LayerSt* __restrict_
     L.addtab[idx] = (int8_t)(code < lo ? lo : code);
   }
 }
+// FX constants of every channel of every candidate layer (rt.fx == 2): one warp per channel,
+// spread over FX_BLOCKS blocks per layer; a warp reuses its last channel's LP when the
+// multiplier repeats (per-tensor weights: one LP per warp).  Constants go to the scratch half of
+// the ep block; any channel without a solution clears the candidate (rt.fx = 0).
+constexpr int FX_BLOCKS = 8;
+__global__ void __launch_bounds__(256) k_layer_fx(const LayerSt* __restrict__ layers) {
+  const LayerSt L = layers[blockIdx.x];
+  if (!L.ep) return;
+  const LayerRt r = *L.rt;
+  if (r.fx != 2) return;
+  const int S = r.fx_s + 32;
+  const int lo = r.relu_zp > PTQ_QMIN ? r.relu_zp : PTQ_QMIN;
+  const int cs = (L.cout + 15) & ~15;
+  const int* ep_cc = reinterpret_cast<const int*>(reinterpret_cast<const double*>(L.ep) + cs);
+  long long* fx_b = reinterpret_cast<long long*>(L.ep + cs);
+  int* fx_m = reinterpret_cast<int*>(fx_b + cs);
+  const int wpb = blockDim.x >> 5, gw = blockIdx.y * wpb + (threadIdx.x >> 5), nw = gridDim.y * wpb;
+  double last_m = -1.0;
+  long long M = 0, B = 0;
+  bool ok = true;
+  for (int o = gw; o < L.cout; o += nw) {
+    const double m = L.mult[o];
+    if (m != last_m) {
+      ok = fx_channel(m, r.zy, lo, S, M, B);
+      last_m = m;
+    }
+    if (!ok) {
+      if ((threadIdx.x & 31) == 0) atomicExch(&L.rt->fx, 0);
+      return;
+    }
+    if ((threadIdx.x & 31) == 0) {
+      const long long cc = (long long)(int)((uint32_t)ep_cc[o] ^ 0x80000000u);
+      fx_b[o] = B + cc * M;                             // acc = v' + cc folded into the addend
+      fx_m[o] = (int)M;
+    }
+  }
+}
+// install the FX constants of layers whose every channel succeeded: the active SoA block now
+// holds (B', M, zw) instead of (m, cc, zw)
+__global__ void __launch_bounds__(256) k_layer_fx_commit(const LayerSt* __restrict__ layers) {
+  const LayerSt L = layers[blockIdx.x];
+  if (!L.ep || L.rt->fx != 2) return;
+  const int cs = (L.cout + 15) & ~15;
+  const long long* fx_b = reinterpret_cast<const long long*>(L.ep + cs);
+  const int* fx_m = reinterpret_cast<const int*>(fx_b + cs);
+  long long* dst_b = reinterpret_cast<long long*>(L.ep);
+  int* dst_m = reinterpret_cast<int*>(dst_b + cs);
+  for (int o = blockIdx.y * blockDim.x + threadIdx.x; o < cs; o += gridDim.y * blockDim.x) {
+    dst_b[o] = o < L.cout ? fx_b[o] : 0;
+    dst_m[o] = o < L.cout ? fx_m[o] : 0;
+  }
+}
+// the flag flips in its own launch: a block of k_layer_fx_commit that started after another
+// block had already set rt.fx = 1 would skip its share of the copy
+__global__ void k_layer_fx_done(const LayerSt* __restrict__ layers, int n_layers) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n_layers) return;
+  const LayerSt L = layers[i];
+  if (!L.ep) return;
+  LayerRt* rt = L.rt;
+  if (rt->fx == 2) {
+    const int cs = (L.cout + 15) & ~15;
+    rt->fx = 1;
+    rt->slow = 0;
+    rt->fx_m0 = reinterpret_cast<const int*>(reinterpret_cast<const long long*>(L.ep) + cs)[0];
+  } else {
+    rt->fx = 0;
+  }
+}
 void launch_layer_params(const LayerSt* d_layers, int n_layers, const float* act_scale,
                          const int* act_zp, int wvar, int fx, cudaStream_t s) {
-  if (n_layers > 0) k_layer_params<<<n_layers, 512, 0, s>>>(d_layers, act_scale, act_zp, wvar, fx);
+  if (n_layers <= 0) return;
+  k_layer_params<<<n_layers, 512, 0, s>>>(d_layers, act_scale, act_zp, wvar, fx);
+  if (!fx) return;
+  k_layer_fx<<<dim3(n_layers, FX_BLOCKS), 256, 0, s>>>(d_layers);
+  k_layer_fx_commit<<<dim3(n_layers, 2), 256, 0, s>>>(d_layers);
+  k_layer_fx_done<<<(n_layers + 127) / 128, 128, 0, s>>>(d_layers, n_layers);
 }
 
 // ---------------------------------------------------------------- quantize / dequantize
