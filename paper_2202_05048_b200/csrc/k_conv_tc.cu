@@ -213,7 +213,7 @@ struct EpiK {
 // the shared-memory table: one group of four balances the L1 (table) and fp64 pipes (A/B
 // on ResNet-50: 0x0 13.7 ms, 0x8 13.4 ms, 0xC 14.0 ms of conv per config)
 #ifndef PTQ_ADD_ALU_MASK
-#define PTQ_ADD_ALU_MASK 0x8
+#define PTQ_ADD_ALU_MASK 0x0
 #endif
 
 // RHU(acc*m) + zp (unclipped) on a biased accumulator: acc clamped to the layer's
