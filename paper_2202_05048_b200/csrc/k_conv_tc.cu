@@ -51,12 +51,11 @@ constexpr int TC_IO_NB = 2;                       // tile I/O buffers (tio)
 constexpr int TC_SMEM_MAX = 232448;                // 227 KB opt-in dynamic smem per CTA
 constexpr int TC_A_STAGE = TC_BM * 128;            // 16 KB: 8 chunks x 128 rows x 16 B
 #ifndef PTQ_EPI_GROUPS
-#define PTQ_EPI_GROUPS 3
+#define PTQ_EPI_GROUPS 4
 #endif
 constexpr int TC_NG = PTQ_EPI_GROUPS;               // epilogue column groups per TMEM lane quarter
 constexpr int TC_EPI_WARPS = 4 * TC_NG;             // NG per SM sub-partition
-constexpr int TC_IO_WARP = 4 + TC_EPI_WARPS;         // tile I/O agent (after the epilogue warps)
-constexpr int TC_THREADS = (5 + TC_EPI_WARPS) * 32;    // + producer / MMA warps 0-3 + I/O agent
+constexpr int TC_THREADS = (4 + TC_EPI_WARPS) * 32;    // + producer / MMA warps 0-3
 
 
 __device__ __forceinline__ uint64_t umma_desc(uint32_t saddr, uint32_t lbo, uint32_t sbo) {
@@ -799,6 +798,47 @@ __global__ void __launch_bounds__(TC_THREADS, 1) k_conv_tc(const __grid_constant
           if (++s == NS) { s = 0; ph ^= 1u; }
         }
       }
+    } else if (lane == 1 && a.tio) {
+      // ---------------------------------------------- tile I/O agent (tio), lane 1 of warp 2:
+      // loads the fused-add operand of a tile into its buffer (TMA), and stores each tile the
+      // epilogue finished (TMA; rows past M and columns past Cp are clipped by the map); a
+      // buffer is reloaded / handed back once its store has finished reading it
+      const bool skip = a.skip.p != nullptr;
+      const int iow = a.io_w;
+      if (skip) prefetch_tmap(&a.tmS);
+      prefetch_tmap(&a.tmO);
+      auto load = [&](int tile, uint32_t ib) {
+        const int mt = (int)a.div_nt.div((uint32_t)tile), nt = tile - mt * n_nt;
+        const int nbox = (imin(BN, a.skip.Cp - nt * BN) + iow - 1) / iow;
+        uint8_t* io = sio + ib * (TC_BM * BN);
+        mbar_arrive_expect_tx(&iofull[ib], (uint32_t)(nbox * TC_BM * iow));
+        for (int b = 0; b < nbox; ++b)
+          tma_load_2d(io + b * (TC_BM * iow), &a.tmS, nt * BN + b * iow, mt * TC_BM, &iofull[ib]);
+      };
+      if (skip)
+        for (int i = 0; i < TC_IO_NB && blockIdx.x + i * (int)gridDim.x < n_tiles; ++i)
+          load(blockIdx.x + i * gridDim.x, (uint32_t)i);
+      uint32_t lt = 0;
+      for (int tile = blockIdx.x; tile < n_tiles; tile += gridDim.x, ++lt) {
+        const uint32_t ib = lt % TC_IO_NB, iph = (lt / TC_IO_NB) & 1u;
+        const int mt = (int)a.div_nt.div((uint32_t)tile), nt = tile - mt * n_nt;
+        const int nbox = (imin(BN, a.out.Cp - nt * BN) + iow - 1) / iow;
+        uint8_t* io = sio + ib * (TC_BM * BN);
+        mbar_wait(&ioready[ib], iph);
+        for (int b = 0; b < nbox; ++b) tma_store_2d(&a.tmO, io + b * (TC_BM * iow), nt * BN + b * iow, mt * TC_BM);
+        bulk_commit();
+        if (skip) {
+          const int next = tile + TC_IO_NB * (int)gridDim.x;
+          if (next < n_tiles) {
+            bulk_wait_read<0>();
+            load(next, ib);
+          }
+        } else {
+          bulk_wait_read<1>();
+          if (lt > 0) mbar_arrive(&ioempty[(lt - 1) % TC_IO_NB]);
+        }
+      }
+      bulk_wait_all();
     }
   } else if (warp == 3) {
     // ------------------------------------------------ MMA issuer
@@ -856,49 +896,6 @@ __global__ void __launch_bounds__(TC_THREADS, 1) k_conv_tc(const __grid_constant
       }
     }
     __syncwarp();
-  } else if (warp == TC_IO_WARP) {
-    // ------------------------------------------------ tile I/O agent (tio)
-    // loads the fused-add operand of a tile into its buffer (TMA), and stores each tile the
-    // epilogue finished (TMA; rows past M and columns past Cp are clipped by the map); a buffer
-    // is reloaded / handed back once its store has finished reading it
-    if (a.tio && lane == 0) {
-      const bool skip = a.skip.p != nullptr;
-      const int iow = a.io_w;
-      if (skip) prefetch_tmap(&a.tmS);
-      prefetch_tmap(&a.tmO);
-      auto load = [&](int tile, uint32_t ib) {
-        const int mt = (int)a.div_nt.div((uint32_t)tile), nt = tile - mt * n_nt;
-        const int nbox = (imin(BN, a.skip.Cp - nt * BN) + iow - 1) / iow;
-        uint8_t* io = sio + ib * (TC_BM * BN);
-        mbar_arrive_expect_tx(&iofull[ib], (uint32_t)(nbox * TC_BM * iow));
-        for (int b = 0; b < nbox; ++b)
-          tma_load_2d(io + b * (TC_BM * iow), &a.tmS, nt * BN + b * iow, mt * TC_BM, &iofull[ib]);
-      };
-      if (skip)
-        for (int i = 0; i < TC_IO_NB && blockIdx.x + i * (int)gridDim.x < n_tiles; ++i)
-          load(blockIdx.x + i * gridDim.x, (uint32_t)i);
-      uint32_t lt = 0;
-      for (int tile = blockIdx.x; tile < n_tiles; tile += gridDim.x, ++lt) {
-        const uint32_t ib = lt % TC_IO_NB, iph = (lt / TC_IO_NB) & 1u;
-        const int mt = (int)a.div_nt.div((uint32_t)tile), nt = tile - mt * n_nt;
-        const int nbox = (imin(BN, a.out.Cp - nt * BN) + iow - 1) / iow;
-        uint8_t* io = sio + ib * (TC_BM * BN);
-        mbar_wait(&ioready[ib], iph);
-        for (int b = 0; b < nbox; ++b) tma_store_2d(&a.tmO, io + b * (TC_BM * iow), nt * BN + b * iow, mt * TC_BM);
-        bulk_commit();
-        if (skip) {
-          const int next = tile + TC_IO_NB * (int)gridDim.x;
-          if (next < n_tiles) {
-            bulk_wait_read<0>();
-            load(next, ib);
-          }
-        } else {
-          bulk_wait_read<1>();
-          if (lt > 0) mbar_arrive(&ioempty[(lt - 1) % TC_IO_NB]);
-        }
-      }
-      bulk_wait_all();
-    }
   } else {
     // ------------------------------------------------ epilogue warps
     // warp-uniform warp index (a shuffle from lane 0): q, grp, the chunk loop and the channel
