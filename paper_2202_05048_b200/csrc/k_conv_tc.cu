@@ -698,13 +698,37 @@ __global__ void __launch_bounds__(TC_THREADS, 1) k_conv_tc(const __grid_constant
       const int taps = a.k * a.k;
       int s = 0;
       uint32_t ph = 0, lt = 0;
+      const int iters = a.kwr ? a.a_iters : a.n_kiter;
       for (int tile = blockIdx.x; tile < n_tiles; tile += gridDim.x, ++lt) {
         const uint32_t buf = lt & 1u, uph = (lt >> 1) & 1u;
         int sum[4] = {0, 0, 0, 0};
-        for (int ki = 0; ki < a.n_kiter; ++ki) {
+        for (int ki = 0; ki < iters; ++ki) {
           mbar_wait(&full[s], ph);
           const uint8_t* st = sA + s * TC_A_STAGE;
-          if (a.tma_a == 128) {
+          if (a.kwr) {
+            // kw-reuse slab of one kernel row: 136 pixels x 64 channel bytes; GEMM row r takes
+            // pixels r, r + 1, r + 2 (the three kw taps).  Per-pixel sums px[i] of pixels
+            // lane + 32i, then the two right neighbours by shuffles
+            int px[5];
+#pragma unroll
+            for (int i = 0; i < 5; ++i) {
+              px[i] = 0;
+              const int j = lane + 32 * i;
+              if (j < TC_BM + 8)
+#pragma unroll
+                for (int q = 0; q < 4; ++q) {
+                  const int4 v = *reinterpret_cast<const int4*>(st + j * 64 + ((q + (lane >> 1)) & 3) * 16);
+                  px[i] = __dp4a(v.x, 0x01010101, __dp4a(v.y, 0x01010101, __dp4a(v.z, 0x01010101, __dp4a(v.w, 0x01010101, px[i]))));
+                }
+            }
+#pragma unroll
+            for (int i = 0; i < 4; ++i) {
+              const int a1 = __shfl_down_sync(0xffffffffu, px[i], 1), b1 = __shfl_sync(0xffffffffu, px[i + 1], 0);
+              const int a2 = __shfl_down_sync(0xffffffffu, px[i], 2);
+              const int b2 = __shfl_sync(0xffffffffu, px[i + 1], (lane + 2) & 31);
+              sum[i] += px[i] + (lane < 31 ? a1 : b1) + (lane < 30 ? a2 : b2);
+            }
+          } else if (a.tma_a == 128) {
 #pragma unroll
             for (int i = 0; i < 4; ++i)
 #pragma unroll
@@ -1205,7 +1229,7 @@ static void plan_launch(ConvTcArgs& t, int bn) {
       t.a_iters = 3;                                 // A stages per tile = kh rows
     }
   }
-  t.tma_rowsum = t.has_wzp && !t.Rpix && (t.tma_a == 64 || t.tma_a == 128) && !t.kwr;
+  t.tma_rowsum = t.has_wzp && !t.Rpix && (t.tma_a == 64 || t.tma_a == 128);
   // flat rows: halo-free input and output, no padded-grid rows, halo-free add operand, and
   // row sums (when needed) taken in-kernel
   t.flat = (t.tma_a == 64 || t.tma_a == 128) && t.in.halo == 0 && t.out.halo == 0 && t.OH == t.OHr &&
