@@ -83,6 +83,30 @@ __device__ __forceinline__ int quant1_f32g(float x, float r32, float zf, double 
   return q < PTQ_QMIN ? PTQ_QMIN : (q > PTQ_QMAX ? PTQ_QMAX : q);
 }
 
+// Four values through the fp32 quantizer with magic-number rounding (no conversion pipe):
+// t = fma(x, fl32(1/s), zp) is within 2^-23 (2|t| + |zp|) of the reference's fl(fl(x/s) + zp);
+// rm = t + 1.5*2^23 rounds to nearest (|t| < 2^22) and holds the integer in its low mantissa
+// bits.  Whenever t is farther than 2e-4 from a half-integer (|t| <= 600: the approximation error
+// is < 1.7e-4), round-to-nearest of t equals the reference's RHA of its own value; otherwise
+// `bad` is set and the caller recomputes the four values exactly (quant1_f32g).  Saturation is a
+// clamp of rm to [M - 128, M + 127]; the low bytes of the four words are the codes.
+__device__ __forceinline__ uint32_t quant4_magic(float x0, float x1, float x2, float x3, float r32, float zf,
+                                                 float lo, bool& bad) {
+  const float M = 12582912.0f;
+  const float xs[4] = {x0, x1, x2, x3};
+  uint32_t w[4];
+#pragma unroll
+  for (int j = 0; j < 4; ++j) {
+    const float t = __fmaf_rn(xs[j], r32, zf);
+    float rm = __fadd_rn(t, M);
+    const float d = fabsf(__fsub_rn(t, __fsub_rn(rm, M)));
+    bad |= !(d < 0.4998f) && !(fabsf(t) > 600.0f);   // far outside: saturates either way
+    rm = fminf(fmaxf(rm, M + lo), M + 127.0f);
+    w[j] = __float_as_uint(rm);
+  }
+  return __byte_perm(__byte_perm(w[0], w[1], 0x0040), __byte_perm(w[2], w[3], 0x0040), 0x5410);
+}
+
 // 4 int32 -> 4 saturated int8 codes in one word (byte j = x_j)
 __device__ __forceinline__ uint32_t pack4_sat(int x0, int x1, int x2, int x3) {
   uint32_t hi, out;

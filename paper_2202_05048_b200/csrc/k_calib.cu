@@ -121,18 +121,22 @@ __device__ __forceinline__ int np_bin_fast(double x, double lo, double hi, doubl
 // fp32 pre-filter: fe32 = fl32(fl32(x - lo) * fl32(2048 / (hi - lo))) is within
 // 3 * 2^-24 * 2048 = 3.7e-4 bins of the true position (three relative fp32 roundings on a
 // value <= 2048; numpy's own fp64 position and edges are 1e-12 away); when its fractional
-// part keeps a 5e-4 margin from both neighbouring integers the bin is settled on the fp32
-// pipe, otherwise np_bin_fast decides in fp64.
-__device__ __forceinline__ bool f32_bin_ok(float fe, int k) {
-  // |frac - 0.5| < 0.4995  <=>  5e-4 < frac < 0.9995 (frac = fe - k is exact).  k == 2048
-  // needs fe >= 2048, which for x <= hi is within 3.7e-4 of 2048 and fails the margin.
-  return fabsf(__fsub_rn(__fsub_rn(fe, (float)k), 0.5f)) < 0.4995f;
+// part keeps a 5e-4 margin from both neighbouring integers (|frac - 0.5| < 0.4995) the bin is
+// settled on the fp32 pipe, otherwise np_bin_fast decides in fp64.  A position at or past 2048
+// (x at hi) has frac ~ 0 and takes the fp64 path.
+// floor of the fp32 position without the conversion pipe: fe + 1.5*2^23 rounded down holds
+// floor(fe) in its low mantissa bits (-2^22 < fe < 2^22); the fractional part is exact
+__device__ __forceinline__ int f32_floor_frac(float fe, float& frac) {
+  const float rm = __fadd_rd(fe, 12582912.0f);
+  frac = __fsub_rn(fe, __fsub_rn(rm, 12582912.0f));
+  return (int)(__float_as_uint(rm) - 0x4B400000u);
 }
 __device__ __forceinline__ int np_bin_f32g(float x, float lo32, float rc32, double lo, double hi, double denom,
                                            double rc, double eps) {
   const float fe = __fmul_rn(__fsub_rn(x, lo32), rc32);
-  const int k = (int)fe;
-  if (f32_bin_ok(fe, k)) return k;
+  float frac;
+  const int k = f32_floor_frac(fe, frac);
+  if (fabsf(__fsub_rn(frac, 0.5f)) < 0.4995f) return k;
   return np_bin_fast((double)x, lo, hi, denom, rc, eps);
 }
 
@@ -209,8 +213,9 @@ __global__ void __launch_bounds__(256) k_histogram(const float* __restrict__ x, 
 #pragma unroll
       for (int e = 0; e < 16; ++e) {
         const float fe = __fmul_rn(__fsub_rn(v[e], lo32), rc32);
-        k[e] = (int)fe;
-        const bool ok = f32_bin_ok(fe, k[e]);
+        float frac;
+        k[e] = f32_floor_frac(fe, frac);
+        const bool ok = fabsf(__fsub_rn(frac, 0.5f)) < 0.4995f;
         const bool z = zero_in && v[e] == 0.0f;   // exact zeros: the zero bin, no fp64
         if (z) k[e] = z0;
         slow |= (unsigned)(!ok && !z) << e;
@@ -243,6 +248,119 @@ __global__ void __launch_bounds__(256) k_histogram(const float* __restrict__ x, 
 #pragma unroll
     for (int c = 0; c < HIST_COPIES; ++c) t += sh[c * PTQ_NBINS + i];
     if (t) atomicAdd(counts + i, (unsigned long long)t);
+  }
+}
+
+// ---------------------------------------------------------------- F1b, batched
+// All histograms of a calibration in one launch: the (cache, tensor) items are cut into
+// chunks of HIST_CHUNK values of their (image slot, element) space; a persistent grid walks the
+// chunk list, bins each chunk into the block's private shared sub-histograms and flushes them
+// to the item's int64 counts.  Small tensors no longer cost a launch each (366 launches per
+// calibration before), and every chunk keeps all SMs busy.
+constexpr int64_t HIST_CHUNK = 1 << 20;
+__global__ void __launch_bounds__(256) k_histogram_multi(const HistItem* __restrict__ items, int n_items,
+                                                         int64_t n_chunks) {
+  extern __shared__ unsigned int sh[];
+  unsigned int* my = sh + ((threadIdx.x >> 5) % HIST_COPIES) * PTQ_NBINS;
+  for (int64_t ch = blockIdx.x; ch < n_chunks; ch += gridDim.x) {
+    // item of this chunk: binary search over the chunk prefix
+    int lo_i = 0, hi_i = n_items - 1;
+    while (lo_i < hi_i) {
+      const int mid = (lo_i + hi_i + 1) >> 1;
+      if (items[mid].chunk0 <= ch) lo_i = mid; else hi_i = mid - 1;
+    }
+    const HistItem it = items[lo_i];
+    const int64_t total = it.elems * it.n_slots;
+    const int64_t f0 = (ch - it.chunk0) * HIST_CHUNK;
+    const int64_t f1 = f0 + HIST_CHUNK < total ? f0 + HIST_CHUNK : total;
+    const double lo = (double)it.range[0], hi = (double)it.range[1];
+    if (!(lo < hi)) {                                // lo == hi: every value lands in bin 0 (:86-87)
+      if (threadIdx.x == 0) atomicAdd(it.counts, (unsigned long long)(f1 - f0));
+      continue;
+    }
+    for (int i = threadIdx.x; i < HIST_COPIES * PTQ_NBINS; i += blockDim.x) sh[i] = 0;
+    __syncthreads();
+    const double denom = __dsub_rn(hi, lo);
+    const double rc = __ddiv_rn((double)PTQ_NBINS, denom);
+    const double mag = fmax(fabs(lo), fabs(hi));
+    const double eps = 16.0 * 2.220446049250313e-16 * mag * rc + 1e-9;
+    const int z0 = (lo <= 0.0 && 0.0 <= hi) ? np_bin(0.0, lo, hi, denom) : -1;
+    const float lo32 = it.range[0], rc32 = (float)rc;
+    unsigned int zc = 0;
+    auto put = [&](float v) {
+      if (v == 0.0f && z0 >= 0) ++zc;
+      else atomicAdd(&my[np_bin_f32g(v, lo32, rc32, lo, hi, denom, rc, eps)], 1u);
+    };
+    const bool vec = (it.elems & 3) == 0 && ((((uintptr_t)it.x) & 15) == 0);
+    if (vec) {
+      // float4 index u of the chunk -> (slot j, float4 r) cursors advanced by the block stride
+      const int64_t nv = it.elems >> 2;
+      const unsigned nvu = (unsigned)nv;
+      const int64_t u0 = (f0 >> 2) + threadIdx.x, u1 = f1 >> 2;
+      const int sj = (int)(blockDim.x / nv);
+      const unsigned sr = (unsigned)(blockDim.x % nv);
+      int j = (int)(u0 / nv);
+      unsigned r = (unsigned)(u0 % nv);
+      int64_t u = u0;
+      auto adv = [&](int& jj, unsigned& rr) {
+        rr += sr;
+        jj += sj;
+        if (rr >= nvu) { rr -= nvu; ++jj; }
+      };
+      auto at = [&](int jj, unsigned rr) -> float4 {
+        return __ldg(reinterpret_cast<const float4*>(it.x + (int64_t)__ldg(it.slots + jj) * it.elems) + rr);
+      };
+      const bool zero_in = z0 >= 0;
+      const int64_t st = blockDim.x;
+      for (; u + 3 * st < u1; u += 4 * st) {
+        int j1 = j, j2, j3;
+        unsigned r1 = r, r2, r3;
+        adv(j1, r1); j2 = j1; r2 = r1; adv(j2, r2); j3 = j2; r3 = r2; adv(j3, r3);
+        const float4 q0 = at(j, r), q1 = at(j1, r1), q2 = at(j2, r2), q3 = at(j3, r3);
+        j = j3; r = r3;
+        adv(j, r);
+        const float v[16] = {q0.x, q0.y, q0.z, q0.w, q1.x, q1.y, q1.z, q1.w,
+                             q2.x, q2.y, q2.z, q2.w, q3.x, q3.y, q3.z, q3.w};
+        int k[16];
+        unsigned slow = 0;
+#pragma unroll
+        for (int e = 0; e < 16; ++e) {
+          const float fe = __fmul_rn(__fsub_rn(v[e], lo32), rc32);
+          float frac;
+          k[e] = f32_floor_frac(fe, frac);
+          const bool ok = fabsf(__fsub_rn(frac, 0.5f)) < 0.4995f;
+          const bool z = zero_in && v[e] == 0.0f;
+          if (z) k[e] = z0;
+          slow |= (unsigned)(!ok && !z) << e;
+        }
+        if (slow) {
+#pragma unroll
+          for (int e = 0; e < 16; ++e)
+            if (slow & (1u << e)) k[e] = np_bin_fast((double)v[e], lo, hi, denom, rc, eps);
+        }
+#pragma unroll
+        for (int e = 0; e < 16; ++e) atomicAdd(&my[k[e]], 1u);
+      }
+      for (; u < u1; u += st, adv(j, r)) {
+        const float4 v = at(j, r);
+        put(v.x); put(v.y); put(v.z); put(v.w);
+      }
+    } else {
+      for (int64_t i = f0 + threadIdx.x; i < f1; i += blockDim.x) {
+        const int jj = (int)(i / it.elems);
+        put(__ldg(it.x + (int64_t)it.slots[jj] * it.elems + (i - (int64_t)jj * it.elems)));
+      }
+    }
+    for (int d = 16; d; d >>= 1) zc += __shfl_xor_sync(0xffffffffu, zc, d);
+    if ((threadIdx.x & 31) == 0 && zc) atomicAdd(&sh[z0], zc);
+    __syncthreads();
+    for (int i = threadIdx.x; i < PTQ_NBINS; i += blockDim.x) {
+      unsigned int t = 0;
+#pragma unroll
+      for (int c = 0; c < HIST_COPIES; ++c) t += sh[c * PTQ_NBINS + i];
+      if (t) atomicAdd(it.counts + i, (unsigned long long)t);
+    }
+    __syncthreads();
   }
 }
 
@@ -446,6 +564,27 @@ void launch_histogram(const float* x, int64_t elems, const int* slots, int n_slo
     attr.fetch_or(bit);
   k_histogram<<<nblocks(total, 256, 148 * HIST_BLOCKS_PER_SM), 256, smem, s>>>(x, elems, slots, n_slots, range,
                                                                                counts);
+}
+int64_t hist_items_chunk0(HistItem* items, int n) {
+  int64_t c = 0;
+  for (int i = 0; i < n; ++i) {
+    items[i].chunk0 = c;
+    c += (items[i].elems * items[i].n_slots + HIST_CHUNK - 1) / HIST_CHUNK;
+  }
+  return c;
+}
+void launch_histogram_multi(const HistItem* d_items, int n_items, int64_t n_chunks, cudaStream_t s) {
+  if (n_items <= 0 || n_chunks <= 0) return;
+  constexpr int smem = HIST_COPIES * PTQ_NBINS * 4;
+  static std::atomic<uint64_t> attr{0};
+  int dev = 0;
+  cudaGetDevice(&dev);
+  const uint64_t bit = 1ull << (dev & 63);
+  if (!(attr.load() & bit) &&
+      cudaFuncSetAttribute(k_histogram_multi, cudaFuncAttributeMaxDynamicSharedMemorySize, smem) == cudaSuccess)
+    attr.fetch_or(bit);
+  const int grid = (int)(n_chunks < 148 * HIST_BLOCKS_PER_SM ? n_chunks : 148 * HIST_BLOCKS_PER_SM);
+  k_histogram_multi<<<grid, 256, smem, s>>>(d_items, n_items, n_chunks);
 }
 // ---------------------------------------------------------------- F2b: percentile clipping
 // Extension (not in the reference, which rejects "Percentile": clipping.py:91-92): the

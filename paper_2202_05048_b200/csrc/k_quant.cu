@@ -495,32 +495,62 @@ void launch_quant_input(const float* imgs, int64_t img0, View out, const float* 
 // the stride-2 stem: s2d pixel (R, Q) holds x[c][2R+a][2Q+b] at byte (2a+b)*C0 + c, so the
 // stride-2 kxk conv becomes a stride-1 k'xk' conv (k' = (k+1)/2) whose 16-byte pixels are
 // TMA-loadable.  Same per-element quantizer as k_quant_input.  grid.x = (n, R) row.
-__global__ void k_quant_input_s2d(const float* __restrict__ imgs, int64_t img0, int C0, View out,
-                                  const float* __restrict__ as, const int* __restrict__ az, int hist) {
+__global__ void __launch_bounds__(256) k_quant_input_s2d(const float* __restrict__ imgs, int64_t img0, int C0,
+                                                         View out, const float* __restrict__ as,
+                                                         const int* __restrict__ az, int hist) {
   const double s = (double)as[hist], z = (double)az[hist];
   const double rs = __ddiv_rn(1.0, s);
   const float rs32 = (float)rs, zf = (float)z;
-  const int n = blockIdx.x / out.H, R = blockIdx.x - (blockIdx.x / out.H) * out.H;
   const int W0 = 2 * out.W;
   const int64_t plane = (int64_t)(2 * out.H) * W0;
-  for (int Q = blockIdx.y * blockDim.x + threadIdx.x; Q < out.W; Q += gridDim.y * blockDim.x) {
-    uint32_t pk[4] = {0u, 0u, 0u, 0u};
+  const int64_t total = (int64_t)out.N * out.H * out.W;
+  const int nv = 4 * C0;                              // real bytes of the 16-byte pixel
+  // one s2d pixel per thread (grid-stride over every (n, R, Q)): 2 x 2 x C0 fp32 values from
+  // C0 x 2 coalesced float2 loads, quantized four at a time with the magic-number quantizer
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < total; i += (int64_t)gridDim.x * blockDim.x) {
+    const int Q = (int)(i % out.W);
+    const int64_t t = i / out.W;
+    const int R = (int)(t % out.H), n = (int)(t / out.H);
+    const float* src = imgs + (img0 + n) * C0 * plane + (int64_t)(2 * R) * W0 + 2 * Q;
+    float v[16];
+#pragma unroll
+    for (int j = 0; j < 16; ++j) v[j] = 0.0f;
 #pragma unroll
     for (int a = 0; a < 2; ++a)
-      for (int c = 0; c < C0; ++c) {
-        const float2 v = __ldg(reinterpret_cast<const float2*>(imgs + (img0 + n) * C0 * plane + (int64_t)c * plane +
-                                                               (int64_t)(2 * R + a) * W0 + 2 * Q));
-        const int j0 = (2 * a) * C0 + c, j1 = (2 * a + 1) * C0 + c;
-        pk[j0 >> 2] |= ((uint32_t)quant1_f32g(v.x, rs32, zf, rs, s, z) & 0xffu) << (8 * (j0 & 3));
-        pk[j1 >> 2] |= ((uint32_t)quant1_f32g(v.y, rs32, zf, rs, s, z) & 0xffu) << (8 * (j1 & 3));
+#pragma unroll
+      for (int c = 0; c < 4; ++c)
+        if (c < C0) {
+          const float2 f = __ldg(reinterpret_cast<const float2*>(src + (int64_t)c * plane + a * W0));
+          v[(2 * a) * C0 + c] = f.x;
+          v[(2 * a + 1) * C0 + c] = f.y;
+        }
+    bool bad = false;
+    uint32_t pk[4];
+#pragma unroll
+    for (int g = 0; g < 4; ++g) pk[g] = quant4_magic(v[4 * g], v[4 * g + 1], v[4 * g + 2], v[4 * g + 3], rs32, zf, -128.0f, bad);
+    if (bad) {
+#pragma unroll
+      for (int g = 0; g < 4; ++g) {
+        int q[4];
+#pragma unroll
+        for (int j = 0; j < 4; ++j) q[j] = quant1_f32g(v[4 * g + j], rs32, zf, rs, s, z);
+        pk[g] = pack4_sat(q[0], q[1], q[2], q[3]);
       }
+    }
+    // pad bytes (beyond 4 * C0) are 0: zero quantized values are zp, so mask them explicitly
+#pragma unroll
+    for (int g = 0; g < 4; ++g) {
+      const int keep = nv - 4 * g;
+      if (keep <= 0) pk[g] = 0u;
+      else if (keep < 4) pk[g] &= 0xffffffffu >> (8 * (4 - keep));
+    }
     *reinterpret_cast<int4*>(out.p + voff(out, n, R, Q)) = make_int4((int)pk[0], (int)pk[1], (int)pk[2], (int)pk[3]);
   }
 }
 void launch_quant_input_s2d(const float* imgs, int64_t img0, int C0, View out, const float* as,
                             const int* az, int hist, cudaStream_t s) {
-  dim3 g(out.N * out.H, (out.W + 127) / 128);
-  k_quant_input_s2d<<<g, 128, 0, s>>>(imgs, img0, C0, out, as, az, hist);
+  const int64_t total = (int64_t)out.N * out.H * out.W;
+  k_quant_input_s2d<<<nblk(total, 256, 148 * 16), 256, 0, s>>>(imgs, img0, C0, out, as, az, hist);
 }
 
 // per-output-pixel sum of the input codes under the stem's real kxk window (halo taps hold
@@ -605,6 +635,7 @@ __global__ void k_quant_nhwc4(const float* __restrict__ x, View out, const float
   const double rs = __ddiv_rn(1.0, s);
   const float rs32 = (float)rs, zf = (float)z;
   const int rz = relu_hist >= 0 ? az[relu_hist] : INT_MIN;
+  const int lo = rz > PTQ_QMIN ? (rz > PTQ_QMAX ? PTQ_QMAX : rz) : PTQ_QMIN;   // relu floor of the codes
   const int qp = out.Cp >> 2, qc = out.C >> 2;                // channel quads per pixel
   const int n = blockIdx.x / out.H, h = blockIdx.x - n * out.H;   // one (image, row) per block
   const float4* src = reinterpret_cast<const float4*>(x + ((int64_t)n * out.H + h) * out.W * out.C);
@@ -615,8 +646,11 @@ __global__ void k_quant_nhwc4(const float* __restrict__ x, View out, const float
     uint32_t pk = 0u;
     if (cq < qc) {
       const float4 v = __ldg(src + w * qc + cq);
-      pk = pack4_sat(max(quant1_f32g_raw(v.x, rs32, zf, rs, s, z), rz), max(quant1_f32g_raw(v.y, rs32, zf, rs, s, z), rz),
-                     max(quant1_f32g_raw(v.z, rs32, zf, rs, s, z), rz), max(quant1_f32g_raw(v.w, rs32, zf, rs, s, z), rz));
+      bool bad = false;
+      pk = quant4_magic(v.x, v.y, v.z, v.w, rs32, zf, (float)lo, bad);
+      if (bad)
+        pk = pack4_sat(max(quant1_f32g_raw(v.x, rs32, zf, rs, s, z), rz), max(quant1_f32g_raw(v.y, rs32, zf, rs, s, z), rz),
+                       max(quant1_f32g_raw(v.z, rs32, zf, rs, s, z), rz), max(quant1_f32g_raw(v.w, rs32, zf, rs, s, z), rz));
     }
     *reinterpret_cast<uint32_t*>(dst + (int64_t)w * out.Cp + cq * 4) = pk;
   }

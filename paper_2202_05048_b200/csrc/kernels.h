@@ -85,6 +85,18 @@ void launch_minmax_reduce_cache(const unsigned int* per_img, int n_tensors, int 
                                 const int* slots, int n_slots, float* ranges, cudaStream_t s);
 void launch_histogram(const float* x, int64_t elems, const int* slots, int n_slots,
                       const float* range, unsigned long long* counts, cudaStream_t s);
+// one histogram of the batched launch: values x[slots[j]][e], range (lo, hi), 2048 int64 counts
+struct HistItem {
+  const float* x;
+  int64_t elems;
+  const int* slots;
+  int n_slots;
+  const float* range;
+  unsigned long long* counts;
+  int64_t chunk0;          // first chunk index of this item (hist_items_chunk0)
+};
+int64_t hist_items_chunk0(HistItem* items, int n);      // fills chunk0, returns the chunk count
+void launch_histogram_multi(const HistItem* d_items, int n_items, int64_t n_chunks, cudaStream_t s);
 void launch_percentile(const long long* counts, const float* ranges, int n_hist, double q, double* out,
                        cudaStream_t s);
 void launch_kl_sweep(const long long* counts, const float* ranges, int n_hist, double* cum,

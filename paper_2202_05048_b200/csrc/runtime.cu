@@ -185,6 +185,7 @@ struct ptq_ctx {
   int dwconv_variant = 2, concat_v16 = 1, kwr = 0;   // A/B switches (per context)
   int fx = 1;                            // exact fixed-point conv epilogue (0: fp64 epilogue)
   int tio = 1;                           // tile I/O through shared memory + TMA (flat conv layers)
+  int hist_multi = 1;                    // batched histogram launch (0: one launch per histogram, A/B)
   int64_t opt_chunk = 0;
   // stats
   int64_t launches = 0;
@@ -1339,12 +1340,23 @@ int ptq_calib_histogram(ptq_ctx* c, const float* ranges, int64_t* counts) {
     unsigned long long* d_cnt = c->dalloc<unsigned long long>((size_t)nk * T * PTQ_NBINS);
     CK(cudaMemcpyAsync(d_rng, ranges, (size_t)nk * T * 2 * sizeof(float), cudaMemcpyHostToDevice, c->st));
     CK(cudaMemsetAsync(d_cnt, 0, (size_t)nk * T * PTQ_NBINS * 8, c->st));
+    // F1b: every histogram (cache k, tensor t) with the cache's global (lo, hi), one batched launch
+    std::vector<HistItem> items;
     for (int k = 0; k < nk; ++k) {
       if (c->cal_sizes[k] == 0) continue;
-      // F1b: histograms with the cache's global (lo, hi)
-      for (int t = 0; t < T; ++t) {
-        launch_histogram(c->cal_bufs[t], c->tens[t].elems, c->cal_slots[k], c->cal_sizes[k],
-                         d_rng + ((size_t)k * T + t) * 2, d_cnt + ((size_t)k * T + t) * PTQ_NBINS, c->st);
+      for (int t = 0; t < T; ++t)
+        items.push_back(HistItem{c->cal_bufs[t], c->tens[t].elems, c->cal_slots[k], c->cal_sizes[k],
+                                 d_rng + ((size_t)k * T + t) * 2, d_cnt + ((size_t)k * T + t) * PTQ_NBINS, 0});
+    }
+    const int64_t n_chunks = hist_items_chunk0(items.data(), (int)items.size());
+    HistItem* d_items = c->dalloc<HistItem>(items.size() ? items.size() : 1);
+    if (c->hist_multi) {
+      CK(cudaMemcpyAsync(d_items, items.data(), items.size() * sizeof(HistItem), cudaMemcpyHostToDevice, c->st));
+      launch_histogram_multi(d_items, (int)items.size(), n_chunks, c->st);
+      check_launch(c);
+    } else {
+      for (const HistItem& it : items) {
+        launch_histogram(it.x, it.elems, it.slots, it.n_slots, it.range, it.counts, c->st);
         check_launch(c);
       }
     }
@@ -1357,6 +1369,7 @@ int ptq_calib_histogram(ptq_ctx* c, const float* ranges, int64_t* counts) {
     c->cal_sizes.clear();
     c->dfree(d_rng);
     c->dfree(d_cnt);
+    c->dfree(d_items);
   });
 }
 
@@ -1718,6 +1731,7 @@ int ptq_set_option(ptq_ctx* c, const char* key, int64_t value) {
     else if (k == "kwr") c->kwr = (int)value;
     else if (k == "fx") c->fx = (int)value;
     else if (k == "tio") c->tio = (int)value;
+    else if (k == "hist_multi") c->hist_multi = (int)value;
     else if (k == "time_conv") c->time_conv = (int)value;
     else if (k == "reset_stats") c->launches = 0;
     else if (k == "fusion") {

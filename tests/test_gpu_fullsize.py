@@ -38,6 +38,27 @@ def test_histogram_count_conservation(ev224):
     assert np.all(lo <= hi)
 
 
+def test_batched_histograms_equal_per_tensor_launches(ev224):
+    """The batched work-list histogram launch (k_histogram_multi, chunks of 2^20 values over
+    every cache/tensor) bins every calibration value exactly like one k_histogram launch per
+    histogram (the per-tensor kernel is pinned bin-exact against np.histogram in
+    test_gpu_parity.py)."""
+    from paper_2202_05048_b200 import dist
+    from paper_2202_05048_b200.config import CACHE_SIZES, select_images
+    ids = [select_images(ev224.n_calib, sc, 0) for sc in CACHE_SIZES]
+    sizes = np.asarray([len(i) for i in ids], dtype=np.int32)
+    flat = np.concatenate(ids).astype(np.int64)
+    got = {}
+    for mode in (1, 0):
+        ev224.set_option("hist_multi", mode)
+        ranges = ev224.forward_minmax(sizes, flat)
+        got[mode] = ev224.histogram(ranges)
+    ev224.set_option("hist_multi", 1)
+    assert np.array_equal(got[0], got[1])
+    assert np.array_equal(got[1], ev224.cache_counts)
+    del dist
+
+
 def test_fast_paths_equal_plain_path(ev224):
     space = enumerate_space(GENERIC)
     picks = [space[i] for i in (0, 2, 12, 20, 45, 54, 67, 90)]   # Off + FirstLastFp32, zw = 0 / != 0
