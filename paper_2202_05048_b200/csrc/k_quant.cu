@@ -286,8 +286,10 @@ __global__ void __launch_bounds__(512) k_layer_params(const LayerSt* __restrict_
     L.biasq[o] = bq;
     if (L.ep) {
       const long long zw = L.wzp8[(int64_t)wvar * L.cout + o];
-      const long long sw8 = L.wsum8[(int64_t)wvar * L.cout + o];
-      const long long cc = (long long)bq - zx * sw8 + (long long)L.kreal * zx * zw;
+      // depthwise layers sum (x - zx)(w - zw) themselves: only the bias code is constant
+      const long long cc = L.dw ? (long long)bq
+                                : (long long)bq - zx * (long long)L.wsum8[(int64_t)wvar * L.cout + o] +
+                                      (long long)L.kreal * zx * zw;
       const bool big = cc >= (1LL << 30) || cc <= -(1LL << 30);
       if (big) atomicOr(&slow, 1);
       ep_m[o] = m;
@@ -1157,8 +1159,131 @@ __global__ void k_dwconv_i8_k(View in, View out, const int8_t* __restrict__ w,
   }
 }
 
+// 3x3 depthwise, four channels x PX consecutive output pixels per thread, on the dot-product
+// units: the 4 channels' tap words of a 4-tap group are byte-transposed (8 PRMT) into one word
+// per channel holding its 4 taps, so each dp4a does 4 of the channel's MACs against its packed
+// s8 weights; the ninth tap is one IMAD.  With acc = sum (x - zx)(w - zw)
+//   = sum x w - zw sum x - zx (sum w - 9 zw)
+// the raw s8 codes feed dp4a and sum x (only when zw != 0) is a dp4a against 0x01010101.  The
+// input columns of the PX outputs are loaded once ((PX - 1) S + 3 per kernel row).  Requant by
+// the exact fixed-point constants (rt.fx: code = hi32(acc M + B') >> s, B' folding the bias
+// code), else the fp64 requant1.  Bit-identical to k_dwconv_i8 (same int32 sum, exact requant).
+__device__ __forceinline__ void transpose4x4(uint32_t t0, uint32_t t1, uint32_t t2, uint32_t t3, uint32_t (&c)[4]) {
+  const uint32_t p0 = __byte_perm(t0, t1, 0x5140), p1 = __byte_perm(t0, t1, 0x7362);
+  const uint32_t p2 = __byte_perm(t2, t3, 0x5140), p3 = __byte_perm(t2, t3, 0x7362);
+  c[0] = __byte_perm(p0, p2, 0x5410);
+  c[1] = __byte_perm(p0, p2, 0x7632);
+  c[2] = __byte_perm(p1, p3, 0x5410);
+  c[3] = __byte_perm(p1, p3, 0x7632);
+}
+template <int S, bool WZP>
+__global__ void __launch_bounds__(256) k_dwconv3_dp4(View in, View out, const int8_t* __restrict__ w,
+                                                     const int* __restrict__ wzp, int pad, LayerSt L,
+                                                     int* __restrict__ acc_out) {
+  constexpr int PX = 4, NCOL = (PX - 1) * S + 3;
+  const LayerRt r = *L.rt;
+  const int cq = out.Cp >> 2, owq = (out.W + PX - 1) / PX;
+  const int64_t rowp = (int64_t)(in.W + 2 * in.halo) * in.Cp;
+  const int64_t total = (int64_t)out.N * out.H * owq * cq;
+  const int cs = (L.cout + 15) & ~15;
+  const long long* fxb = reinterpret_cast<const long long*>(L.ep);
+  const int* fxm = reinterpret_cast<const int*>(fxb + cs);
+  const int lo = r.relu_zp > PTQ_QMIN ? r.relu_zp : PTQ_QMIN;
+  // a thread keeps one channel quad (its packed weights in registers) and strides over pixel
+  // groups; consecutive threads take consecutive quads of the same pixels (coalesced)
+  const int64_t nthr = (int64_t)gridDim.x * blockDim.x, tid = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  const int64_t per_q = nthr / cq;                    // threads per channel quad
+  if (tid >= per_q * cq) return;
+  const int c0 = (int)(tid % cq) * 4;
+  const int64_t npg = total / cq;                     // pixel groups (PX outputs of one row)
+  // packed weights per channel: taps 0-3, taps 4-7 (s8 bytes), tap 8; zero past Cout
+  uint32_t wa[4], wb[4];
+  int w8[4], kc[4], zw[4];
+#pragma unroll
+  for (int j = 0; j < 4; ++j) {
+      const bool ok = c0 + j < out.C;
+      const int8_t* wc = w + (c0 + j) * 9;
+      uint32_t a = 0, b = 0;
+      int sw = 0;
+#pragma unroll
+      for (int tap = 0; tap < 9; ++tap) {
+        const int v = ok ? (int)__ldg(wc + tap) : 0;
+        sw += v;
+        if (tap < 4) a |= ((uint32_t)v & 0xffu) << (8 * tap);
+        else if (tap < 8) b |= ((uint32_t)v & 0xffu) << (8 * (tap - 4));
+        else w8[j] = v;
+      }
+      wa[j] = a;
+      wb[j] = b;
+      zw[j] = (WZP && ok) ? __ldg(wzp + c0 + j) : 0;
+      kc[j] = -r.zx * (sw - 9 * zw[j]);
+  }
+  long long fb[4];
+  int fm[4];
+#pragma unroll
+  for (int j = 0; j < 4; ++j) {
+    const bool ok = r.fx && c0 + j < out.C;
+    fb[j] = ok ? fxb[c0 + j] : 0;
+    fm[j] = ok ? fxm[c0 + j] : 0;
+  }
+  for (int64_t p = tid / cq; p < npg; p += per_q) {
+    const int ow0 = (int)(p % owq) * PX, t = (int)(p / owq);
+    const int oh = t % out.H, n = t / out.H;
+    const int nvalid = out.W - ow0 < PX ? out.W - ow0 : PX;
+    const int8_t* base = in.p + voff(in, n, oh * S - pad, ow0 * S - pad) + c0;
+    uint32_t col[3][NCOL];
+    const int ncol = (nvalid - 1) * S + 3;
+#pragma unroll
+    for (int kh = 0; kh < 3; ++kh)
+#pragma unroll
+      for (int j = 0; j < NCOL; ++j)
+        col[kh][j] = j < ncol ? __ldg(reinterpret_cast<const uint32_t*>(base + kh * rowp + (int64_t)j * in.Cp)) : 0u;
+    int8_t* obase = out.p + voff(out, n, oh, ow0) + c0;
+#pragma unroll
+    for (int px = 0; px < PX; ++px) {
+      if (px >= nvalid) break;
+      uint32_t ca[4], cb[4];
+      transpose4x4(col[0][px * S], col[0][px * S + 1], col[0][px * S + 2], col[1][px * S], ca);
+      transpose4x4(col[1][px * S + 1], col[1][px * S + 2], col[2][px * S], col[2][px * S + 1], cb);
+      const uint32_t t8 = col[2][px * S + 2];
+      int q[4];
+#pragma unroll
+      for (int j = 0; j < 4; ++j) {
+        const int x8 = (int)(int8_t)(t8 >> (8 * j));
+        int acc = __dp4a((int)ca[j], (int)wa[j], __dp4a((int)cb[j], (int)wb[j], x8 * w8[j])) + kc[j];
+        if (WZP) acc -= zw[j] * __dp4a((int)ca[j], 0x01010101, __dp4a((int)cb[j], 0x01010101, x8));
+        const int c = c0 + j;
+        if (c < out.C) {
+          if (acc_out)
+            acc_out[((int64_t)(n * out.H + oh) * out.W + ow0 + px) * out.C + c] =
+                (int)clip32((long long)acc + L.biasq[c]);
+          if (r.fx) q[j] = (int)(((long long)acc * fm[j] + fb[j]) >> 32) >> r.fx_s;
+          else q[j] = requant1(clip32((long long)acc + L.biasq[c]), L.mult[c], r.zy);
+          q[j] = q[j] < lo ? lo : q[j];
+        } else {
+          q[j] = 0;
+        }
+      }
+      *reinterpret_cast<uint32_t*>(obase + (int64_t)px * out.Cp) = pack4_sat(q[0], q[1], q[2], q[3]);
+    }
+  }
+}
+
 void launch_dwconv_i8(View in, View out, const int8_t* w, const int* wzp, int k, int stride, int pad,
                       LayerSt L, cudaStream_t s, int* acc_out, int variant) {
+  if (k == 3 && (stride == 1 || stride == 2) && in.Cp % 4 == 0 && out.Cp % 4 == 0 && variant == 3) {
+    constexpr int PX = 4;
+    const int64_t total = (int64_t)out.N * out.H * ((out.W + PX - 1) / PX) * (out.Cp / 4);
+    const bool wz = wzp != nullptr;
+    if (stride == 1) {
+      if (wz) k_dwconv3_dp4<1, true><<<nblk(total), 256, 0, s>>>(in, out, w, wzp, pad, L, acc_out);
+      else k_dwconv3_dp4<1, false><<<nblk(total), 256, 0, s>>>(in, out, w, wzp, pad, L, acc_out);
+    } else {
+      if (wz) k_dwconv3_dp4<2, true><<<nblk(total), 256, 0, s>>>(in, out, w, wzp, pad, L, acc_out);
+      else k_dwconv3_dp4<2, false><<<nblk(total), 256, 0, s>>>(in, out, w, wzp, pad, L, acc_out);
+    }
+    return;
+  }
   if (k == 3 && in.Cp % 4 == 0 && out.Cp % 4 == 0 && variant == 2) {
     constexpr int PX = 4;
     const int64_t total = (int64_t)out.N * out.H * ((out.W + PX - 1) / PX) * (out.Cp / 4);

@@ -75,6 +75,7 @@ struct LayerSt {
   int8_t* addtab;               // fused residual add: [256 skip codes][260: conv code + 128]
                                 // -> add output code (out, per config), or nullptr
   int add_conv_is_a;            // 1 if the conv output is operand 0 of the fused add
+  int dw;                       // depthwise layer: cc = bias code only (the kernel sums the rest)
 };
 
 // ---------------------------------------------------------------- F1 / F2 (k_calib.cu)

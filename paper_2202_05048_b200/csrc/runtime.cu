@@ -182,7 +182,7 @@ struct ptq_ctx {
   std::vector<int> cal_sizes;
   // options
   int conv_ref = 0, fusion = 1, time_conv = 0, ablate = 0, tma = 1, subsample = 1;
-  int dwconv_variant = 2, concat_v16 = 1, kwr = 0;   // A/B switches (per context)
+  int dwconv_variant = 3, concat_v16 = 1, kwr = 0;   // A/B switches (per context)
   int fx = 1;                            // exact fixed-point conv epilogue (0: fp64 epilogue)
   int tio = 1;                           // tile I/O through shared memory + TMA (flat conv layers)
   int hist_multi = 1;                    // batched histogram launch (0: one launch per histogram, A/B)
@@ -606,10 +606,11 @@ void build_plan(ptq_ctx* c, int mixed) {
     L.wzp8 = wd.zp;
     L.wsum8 = wd.wsum;
     L.kreal = wd.kreal;
-    L.ep = n.kind == PTQ_DWCONV ? nullptr : wd.ep;
+    L.ep = wd.ep;
+    L.dw = n.kind == PTQ_DWCONV;
     L.addtab = nullptr;
     L.add_conv_is_a = P.add_is_a[i];
-    if (P.add_node[i] >= 0 && L.ep) {
+    if (P.add_node[i] >= 0 && L.ep && !L.dw) {
       if (!wd.addtab) wd.addtab = c->dalloc<int8_t>(PTQ_ADDTAB_BYTES);
       L.addtab = wd.addtab;
     }
@@ -1011,9 +1012,11 @@ void eval_one(ptq_ctx* c, const ptq_config& cfg, unsigned long long* d_correct, 
         const bool acc_probe = pr && pr->acc_node == i && !sel.empty();
         int* d_acc = acc_probe ? c->dalloc<int>((size_t)B * yo.elems) : nullptr;
         if (n.kind == PTQ_DWCONV) {
+          // the dp4a kernel takes the weight zero points only when this variant has any
+          const bool dp4 = c->dwconv_variant == 3;
           launch_dwconv_i8(V(tin), V(tout), wd.codes + (size_t)wv * wd.bytes_per_variant,
-                           wd.zp + (size_t)wv * wd.cout, n.k, n.stride, n.pad, L, c->st, d_acc,
-                           c->dwconv_variant);
+                           (dp4 && !wd.has_wzp[wv]) ? nullptr : wd.zp + (size_t)wv * wd.cout, n.k, n.stride,
+                           n.pad, L, c->st, d_acc, c->dwconv_variant);
           check_launch(c);
         } else {
           ConvTcArgs a{};
