@@ -1226,18 +1226,31 @@ __global__ void __launch_bounds__(256) k_dwconv3_dp4(View in, View out, const in
     fb[j] = ok ? fxb[c0 + j] : 0;
     fm[j] = ok ? fxm[c0 + j] : 0;
   }
-  for (int64_t p = tid / cq; p < npg; p += per_q) {
-    const int ow0 = (int)(p % owq) * PX, t = (int)(p / owq);
-    const int oh = t % out.H, n = t / out.H;
+  // this thread's contiguous run of pixel groups, walked with incremental (n, oh, ow0)
+  const int64_t g = tid / cq, run = (npg + per_q - 1) / per_q;
+  const int pg0 = (int)(g * run), pg1 = (int)(g * run + run < npg ? g * run + run : npg);
+  if (pg0 >= pg1) return;
+  int ow0 = (pg0 % owq) * PX, t0 = pg0 / owq;
+  int oh = t0 % out.H, n = t0 / out.H;
+  const int cp = in.Cp;
+  for (int pg = pg0; pg < pg1; ++pg) {
     const int nvalid = out.W - ow0 < PX ? out.W - ow0 : PX;
     const int8_t* base = in.p + voff(in, n, oh * S - pad, ow0 * S - pad) + c0;
     uint32_t col[3][NCOL];
-    const int ncol = (nvalid - 1) * S + 3;
+    if (nvalid == PX) {
 #pragma unroll
-    for (int kh = 0; kh < 3; ++kh)
+      for (int kh = 0; kh < 3; ++kh)
 #pragma unroll
-      for (int j = 0; j < NCOL; ++j)
-        col[kh][j] = j < ncol ? __ldg(reinterpret_cast<const uint32_t*>(base + kh * rowp + (int64_t)j * in.Cp)) : 0u;
+        for (int j = 0; j < NCOL; ++j)
+          col[kh][j] = __ldg(reinterpret_cast<const uint32_t*>(base + kh * rowp + j * cp));
+    } else {
+      const int ncol = (nvalid - 1) * S + 3;
+#pragma unroll
+      for (int kh = 0; kh < 3; ++kh)
+#pragma unroll
+        for (int j = 0; j < NCOL; ++j)
+          col[kh][j] = j < ncol ? __ldg(reinterpret_cast<const uint32_t*>(base + kh * rowp + j * cp)) : 0u;
+    }
     int8_t* obase = out.p + voff(out, n, oh, ow0) + c0;
 #pragma unroll
     for (int px = 0; px < PX; ++px) {
@@ -1265,6 +1278,11 @@ __global__ void __launch_bounds__(256) k_dwconv3_dp4(View in, View out, const in
         }
       }
       *reinterpret_cast<uint32_t*>(obase + (int64_t)px * out.Cp) = pack4_sat(q[0], q[1], q[2], q[3]);
+    }
+    ow0 += PX;
+    if (ow0 >= out.W) {
+      ow0 = 0;
+      if (++oh == out.H) { oh = 0; ++n; }
     }
   }
 }
