@@ -365,22 +365,47 @@ __global__ void __launch_bounds__(256) k_histogram_multi(const HistItem* __restr
 }
 
 // ---------------------------------------------------------------- F2: KL sweep
-// Per histogram h we precompute (k_kl_prep): cum[j] = sum counts[0..j] (fp64, exact
-// integers), nzc[j] = #(counts[0..j] > 0), logc[j] = log(counts[j]) (0 where empty).
-__global__ void k_kl_prep(const long long* __restrict__ counts, int n_hist,
-                          double* __restrict__ cum, int* __restrict__ nzc, double* __restrict__ logc) {
-  int h = blockIdx.x;
-  if (h >= n_hist || threadIdx.x != 0) return;
+// Per histogram h we precompute (k_kl_prep): cum[j] = sum counts[0..j] (fp64 of exact
+// integers: any summation order gives the same value below 2^53), nzc[j] = #(counts[0..j] > 0),
+// logc[j] = log(counts[j]) (0 where empty).  One 256-thread block per histogram: 8 bins per
+// thread, a block scan of the per-thread sums, logs in parallel.
+__global__ void __launch_bounds__(256) k_kl_prep(const long long* __restrict__ counts, int n_hist,
+                                                 double* __restrict__ cum, int* __restrict__ nzc,
+                                                 double* __restrict__ logc) {
+  const int h = blockIdx.x, t = threadIdx.x;
+  if (h >= n_hist) return;
+  __shared__ long long ps[256];
+  __shared__ int pz[256];
   const long long* c = counts + (int64_t)h * PTQ_NBINS;
-  double acc = 0.0;
-  int nz = 0;
-  for (int j = 0; j < PTQ_NBINS; ++j) {
-    double v = (double)c[j];
-    acc = __dadd_rn(acc, v);
-    nz += (c[j] > 0);
-    cum[(int64_t)h * PTQ_NBINS + j] = acc;
-    nzc[(int64_t)h * PTQ_NBINS + j] = nz;
-    logc[(int64_t)h * PTQ_NBINS + j] = c[j] > 0 ? log(v) : 0.0;
+  long long v[8], s = 0;
+  int z = 0;
+#pragma unroll
+  for (int j = 0; j < 8; ++j) {
+    v[j] = c[t * 8 + j];
+    s += v[j];
+    z += v[j] > 0;
+  }
+  ps[t] = s;
+  pz[t] = z;
+  __syncthreads();
+  for (int d = 1; d < 256; d <<= 1) {                 // inclusive Hillis-Steele scan
+    const long long a = t >= d ? ps[t - d] : 0;
+    const int b = t >= d ? pz[t - d] : 0;
+    __syncthreads();
+    ps[t] += a;
+    pz[t] += b;
+    __syncthreads();
+  }
+  long long run = ps[t] - s;
+  int nz = pz[t] - z;
+#pragma unroll
+  for (int j = 0; j < 8; ++j) {
+    const int k = t * 8 + j;
+    run += v[j];
+    nz += v[j] > 0;
+    cum[(int64_t)h * PTQ_NBINS + k] = (double)run;
+    nzc[(int64_t)h * PTQ_NBINS + k] = nz;
+    logc[(int64_t)h * PTQ_NBINS + k] = v[j] > 0 ? log((double)v[j]) : 0.0;
   }
 }
 
@@ -443,7 +468,7 @@ __global__ void __launch_bounds__(128) k_kl_sweep(const long long* __restrict__ 
   __shared__ int gcount[PTQ_LEVELS + 1];
   __shared__ double leafsum[40];
   __shared__ int lstart[40], llen[40], nleaves;
-  __shared__ int infeasible;
+  __shared__ int infeasible, wtot[4];
 
   const int w = blockIdx.x, h = blockIdx.y, g = threadIdx.x;
   const int i = w + PTQ_LEVELS;                    // window width in bins
@@ -493,10 +518,21 @@ __global__ void __launch_bounds__(128) k_kl_sweep(const long long* __restrict__ 
   gcount[g + 1] = gnz;
   __syncthreads();
   if (gnz > 0 && gsum == 0.0) infeasible = 1;      // Q = 0 under P > 0 -> inf (:49-50)
-  // exclusive scan of gnz over groups (128 entries, one thread)
-  if (g == 0) {
-    gcount[0] = 0;
-    for (int k = 1; k <= PTQ_LEVELS; ++k) gcount[k] += gcount[k - 1];
+  // exclusive scan of gnz over the 128 groups: warp shuffle scans + the 4 warp totals
+  {
+    const int lane = g & 31, wi = g >> 5;
+    int x = gnz;
+#pragma unroll
+    for (int d = 1; d < 32; d <<= 1) {
+      const int y = __shfl_up_sync(0xffffffffu, x, d);
+      if (lane >= d) x += y;
+    }
+    if (lane == 31) wtot[wi] = x;
+    __syncthreads();
+    int off = 0;
+    for (int w2 = 0; w2 < wi; ++w2) off += wtot[w2];
+    gcount[g + 1] = x + off;                         // inclusive prefix at g + 1
+    if (g == 0) gcount[0] = 0;
   }
   __syncthreads();
   if (infeasible) {
@@ -647,7 +683,7 @@ void launch_percentile(const long long* counts, const float* ranges, int n_hist,
 void launch_kl_sweep(const long long* counts, const float* ranges, int n_hist, double* cum,
                      int* nzc, double* logc, double* kl_out, cudaStream_t s) {
   if (n_hist <= 0) return;
-  k_kl_prep<<<n_hist, 32, 0, s>>>(counts, n_hist, cum, nzc, logc);
+  k_kl_prep<<<n_hist, 256, 0, s>>>(counts, n_hist, cum, nzc, logc);
   dim3 g(PTQ_NWIN, n_hist);
   k_kl_sweep<<<g, 128, 0, s>>>(counts, ranges, cum, nzc, logc, kl_out);
 }
