@@ -459,10 +459,9 @@ struct EpiEnv {
 
 // persistent epilogue tile loop of one variant (GENERIC: runtime dispatch, slow layers and
 // the profiling ablation).  q / grp come from a warp-uniform (shuffled) warp index, so the
-// chunk loop and the channel base cb are uniform: the per-channel constants c_ep[cb + j] are
-// loaded into uniform registers through the constant cache (LDCU) and used as operands
-// directly -- no shared-memory loads (each broadcast LDS.128 costs 4 L1 wavefronts per warp,
-// which saturated the L1 data pipe) and no vector registers.
+// chunk loop and the channel base cb are warp-uniform: every lane of a warp loads the same
+// per-channel constants (broadcast shared-memory loads, or for the fused-add layers indexed
+// LDC from __constant__ c_ep, which keeps them off the L1 data pipe the add table uses).
 template <int BN, bool WZP, bool SKIP, bool CLAMP, bool RELU, bool GENERIC, bool ACC = false, bool PT = false,
           bool FX = false>
 __device__ __forceinline__ void epi_tiles(const ConvTcArgs& a, const LayerRt& rt, const EpiK& k, const EpiEnv& e) {

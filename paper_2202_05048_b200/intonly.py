@@ -7,10 +7,14 @@ the GPU evaluator's device state (codes of the graph output over its eval images
 
 What the device executes: every shift of the integer program is a requantization
 by m = 2^-s with s an integer (all scales are powers of two, checked below).
-The conv epilogue evaluates floor(acc * m + 0.5) in fp64 with acc < 2^31, which is
-exact and therefore identical to (acc + 2^(s-1)) >> s; the residual add
-xs*2^(ka-ko) + ys*2^(kb-ko) is exact in fp64 for the same reason and equals the
-reference's (xs << (ka-kmin)) + (ys << (kb-kmin)) shifted by ko-kmin.  The codes
+The conv epilogue is the exact fixed-point requant of k_conv_tc (LayerRt::fx):
+code = hi32(acc * M + B) >> (S - 32), integer multiply-add and shift only; for
+m = 2^-s the solved M is a power of two and B the rounding constant, i.e. the
+reference's (acc + 2^(s-1)) >> s.  (Layers whose constants cannot be solved fall back
+to floor(acc * m + 0.5) in fp64, also exact for m = 2^-s and |acc| < 2^31.)  The
+residual add goes through the per-config add table, whose entries
+xs*2^(ka-ko) + ys*2^(kb-ko) are exact in fp64 and equal the reference's
+(xs << (ka-kmin)) + (ys << (kb-kmin)) shifted by ko-kmin.  The codes
 are therefore bit-identical to run_integer_only (tests/test_intonly.py checks
 them against the reference's own output).  The ``OpTrace`` returned here is the
 trace of the integer PROGRAM (the reference's categories, derived from the executed
