@@ -29,6 +29,8 @@ def main() -> int:
     ap.add_argument("--models", nargs="+", default=["squeezenet", "resnet18"])
     ap.add_argument("--n-eval", type=int, default=1000)
     ap.add_argument("--budget", type=int, default=96)
+    ap.add_argument("--cpu-samples", type=int, default=2, help="reference CPU samples per model (0: skip)")
+    ap.add_argument("--cpu-imgs", type=int, default=8)
     args = ap.parse_args()
 
     import ptqtune as R                                   # the reference driver
@@ -60,6 +62,7 @@ def main() -> int:
             # measure_many's thread pool (tuner.py:192-203): concurrent calls coalesce
             "grid-workers8": lambda: RT.tune_grid(None, space, timed, budget=args.budget, workers=8),
         }
+        trials = {}
         for strat, fn in runs.items():
             stamps.clear()
             t0 = time.perf_counter()
@@ -74,7 +77,32 @@ def main() -> int:
                               "best_config": res.best_config.to_dict(),
                               "evaluator": "paper_2202_05048_b200 GPU (tcgen05 int8)",
                               "driver": "ptqtune.tuner (reference, baseline/_ref)"}), flush=True)
+            trials[strat] = (res.trials_to_best, t_all)
         ev.close()
+        if args.cpu_samples:
+            # the same searches with the reference's own CPU evaluator: the trajectory is the
+            # same (identical accuracies), so time-to-best = trials_to_best x the reference's
+            # per-config cost (calibration + KL reported separately, as for the GPU lines), measured on a bounded sample (bench.py's sampler:
+            # calibrate() of 2 images, clip_range_kl of 1 histogram, quantize_model of 1 config and
+            # run_quantized of `cpu_imgs` eval images per sample) and extrapolated linearly
+            from bench import ReferenceSampler
+            smp = ReferenceSampler(g, d, args.cpu_imgs)
+            for _ in range(args.cpu_samples):
+                smp.step()
+            T = len(g.nodes) + 1
+            t_cal_cpu = smp.n_union() * smp.t_cal / smp.n_cal + 3 * T * smp.t_kl / smp.n_kl
+            t_cfg_cpu = smp.t_q / smp.n_q + args.n_eval * smp.t_ev / smp.n_ev
+            for strat in ("grid", "xgb"):
+                n_best = trials[strat][0]
+                print(json.dumps({"model": name, "strategy": strat, "n_eval": args.n_eval, "budget": args.budget,
+                                  "evaluator": f"reference ptqtune CPU ({smp.kind}, {os.cpu_count()} threads), "
+                                               "extrapolated from a bounded sample",
+                                  "calibrate_s": round(t_cal_cpu, 1), "per_config_s": round(t_cfg_cpu, 2),
+                                  "trials_to_best": n_best,
+                                  "time_to_best_s": round(n_best * t_cfg_cpu, 1),
+                                  "search_s": round(args.budget * t_cfg_cpu, 1),
+                                  "sample": f"{smp.calls} samples: {smp.n_cal} calibration images, {smp.n_kl} KL "
+                                            f"sweeps, {smp.n_q} quantize_model, {smp.n_ev} eval images"}), flush=True)
     return 0
 
 
