@@ -199,21 +199,13 @@ __device__ __forceinline__ double b2d(uint32_t accb) {
 struct EpiK {
   uint32_t clo, chi;   // biased acc clamp bounds 2^31 -/+ aclamp
   int lo_conv, lo_add;
-  // fused add on the fp64 pipe: conv / skip operand (zero point as a 2^31 bias, ratio)
-  uint32_t zc_bias, zs_bias;
-  double rc, rs;
   // per-tensor weight granularity (rt.uni): the requant multiplier and the weight zero point
   // are the same for every channel and live in registers; only cc is loaded per channel
   double m0;
   int zw0;
   int fxm0, fxs;       // FX: per-tensor M and the shift S - 32
 };
-// 4-channel groups of a 16-channel chunk whose fused add runs on the fp64 pipe instead of
-// the shared-memory table: one group of four balances the L1 (table) and fp64 pipes (A/B
-// on ResNet-50: 0x0 13.7 ms, 0x8 13.4 ms, 0xC 14.0 ms of conv per config)
-#ifndef PTQ_ADD_ALU_MASK
-#define PTQ_ADD_ALU_MASK 0x0
-#endif
+
 
 // RHU(acc*m) + zp (unclipped) on a biased accumulator: acc clamped to the layer's
 // saturation margin, then fl(fl(acc*m) + 0.5) exactly as the reference, floor and +zp in
@@ -276,16 +268,7 @@ __device__ __forceinline__ int4 epi_chunk16(const uint32_t (&v)[16], const uint8
       q[j] = requant_raw<CLAMP>(accb, mv[j], rt, k);
       if (RELU || SKIP) q[j] = imax(q[j], k.lo_conv);
       if (SKIP) {
-        if ((PTQ_ADD_ALU_MASK >> g) & 1) {
-          // the table entry computed in place: fl(fl((xc - zc) rc) + fl((xs - zs) rs)) (the sum
-          // is commutative, so the operand order needs no branch), RHU + zo, clip, relu floor
-          const int skc = (int)(int8_t)(skw[g] >> (8 * j));
-          const double t2 = __dadd_rn(__dmul_rn(b2d((uint32_t)imin(q[j], PTQ_QMAX) + k.zc_bias), k.rc),
-                                      __dmul_rn(b2d((uint32_t)skc + k.zs_bias), k.rs));
-          q[j] = imin(imax(__double2loint(__dadd_rd(__dadd_rn(t2, 0.5), rt.mg_zo)), k.lo_add), PTQ_QMAX);
-        } else {
-          q[j] = stab[(int)__byte_perm(skw[g], 0u, 0x4440u + j) * PTQ_ADDTAB_ROW + imin(q[j], PTQ_QMAX)];
-        }
+        q[j] = stab[(int)__byte_perm(skw[g], 0u, 0x4440u + j) * PTQ_ADDTAB_ROW + imin(q[j], PTQ_QMAX)];
       }
     }
     packed[g] = SKIP ? __byte_perm(__byte_perm((uint32_t)q[0], (uint32_t)q[1], 0x0040),
@@ -332,14 +315,7 @@ __device__ __forceinline__ int4 epi_chunk16_fx(const uint32_t (&v)[16], const ui
       q[j] = (int)(X >> 32) >> k.fxs;
       if (RELU || SKIP) q[j] = imax(q[j], k.lo_conv);
       if (SKIP) {
-        if ((PTQ_ADD_ALU_MASK >> g) & 1) {
-          const int skc = (int)(int8_t)(skw[g] >> (8 * j));
-          const double t2 = __dadd_rn(__dmul_rn(b2d((uint32_t)imin(q[j], PTQ_QMAX) + k.zc_bias), k.rc),
-                                      __dmul_rn(b2d((uint32_t)skc + k.zs_bias), k.rs));
-          q[j] = imin(imax(__double2loint(__dadd_rd(__dadd_rn(t2, 0.5), rt.mg_zo)), k.lo_add), PTQ_QMAX);
-        } else {
-          q[j] = stab[(int)__byte_perm(skw[g], 0u, 0x4440u + j) * PTQ_ADDTAB_ROW + imin(q[j], PTQ_QMAX)];
-        }
+        q[j] = stab[(int)__byte_perm(skw[g], 0u, 0x4440u + j) * PTQ_ADDTAB_ROW + imin(q[j], PTQ_QMAX)];
       }
     }
     packed[g] = SKIP ? __byte_perm(__byte_perm((uint32_t)q[0], (uint32_t)q[1], 0x0040),
@@ -933,10 +909,6 @@ __global__ void __launch_bounds__(TC_THREADS, 1) k_conv_tc(const __grid_constant
     k.lo_add = rt.add_relu_zp > PTQ_QMIN ? rt.add_relu_zp : PTQ_QMIN;
     k.clo = 0x80000000u - (uint32_t)rt.aclamp;
     k.chi = 0x80000000u + (uint32_t)rt.aclamp;
-    k.zc_bias = 0x80000000u - (uint32_t)(a.conv_is_a ? rt.za : rt.zb);
-    k.zs_bias = 0x80000000u - (uint32_t)(a.conv_is_a ? rt.zb : rt.za);
-    k.rc = a.conv_is_a ? rt.ra : rt.rb;
-    k.rs = a.conv_is_a ? rt.rb : rt.ra;
     const int Cout = a.L.cout;
     // stage the fused-add table (or the per-channel constants) in shared memory, then sync
     // the epilogue warps only (add layers read their constants from __constant__ c_ep)
