@@ -721,6 +721,49 @@ __global__ void k_halo_fill(View v, const int* __restrict__ az, int hist) {
     *reinterpret_cast<int4*>(d) = make_int4((int)pk[0], (int)pk[1], (int)pk[2], (int)pk[3]);
   }
 }
+// every halo of a config in one launch: items in a by-value parameter block, each thread
+// block walks the flattened (item, halo pixel, 16-channel chunk) space
+__global__ void k_halo_fill_multi(const __grid_constant__ HaloBatch hb, const int* __restrict__ az) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < hb.total;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    int it = 0;
+    while (it + 1 < hb.n && hb.unit0[it + 1] <= i) ++it;
+    const View v = hb.v[it];
+    const int64_t u = i - hb.unit0[it];
+    const int8_t z = (int8_t)az[hb.hist[it]];
+    const int Hp = v.H + 2 * v.halo, Wp = v.W + 2 * v.halo;
+    const int rows = 2 * v.halo * Wp, per_img = rows + 2 * v.halo * v.H;
+    const int nch = v.Cp >> 4;
+    const int c0 = (int)(u % nch) * 16;
+    const int64_t q = u / nch;
+    const int n = (int)(q / per_img), k = (int)(q - (int64_t)n * per_img);
+    int h, w;
+    if (k < rows) {
+      const int r = k / Wp;
+      h = r < v.halo ? r : v.H + r;
+      w = k - r * Wp;
+    } else {
+      const int k2 = k - rows, r = k2 / (2 * v.halo), cc = k2 - r * 2 * v.halo;
+      h = v.halo + r;
+      w = cc < v.halo ? cc : v.W + cc;
+    }
+    int8_t* d = v.p + (((int64_t)n * Hp + h) * Wp + w) * v.Cp + c0;
+    uint32_t pk[4] = {0u, 0u, 0u, 0u};
+#pragma unroll
+    for (int j = 0; j < 16; ++j)
+      if (c0 + j < v.C) pk[j >> 2] |= ((uint32_t)(uint8_t)z) << (8 * (j & 3));
+    *reinterpret_cast<int4*>(d) = make_int4((int)pk[0], (int)pk[1], (int)pk[2], (int)pk[3]);
+  }
+}
+void launch_halo_fill_multi(HaloBatch& hb, const int* az, cudaStream_t s) {
+  hb.total = 0;
+  for (int i = 0; i < hb.n; ++i) {
+    const View& v = hb.v[i];
+    hb.unit0[i] = hb.total;
+    hb.total += (int64_t)v.N * (2 * v.halo * (v.W + 2 * v.halo) + 2 * v.halo * v.H) * (v.Cp >> 4);
+  }
+  if (hb.total > 0) k_halo_fill_multi<<<nblk(hb.total), 256, 0, s>>>(hb, az);
+}
 void launch_halo_fill(View v, const int* az, int hist, cudaStream_t s) {
   if (v.halo <= 0) return;
   const int Wp = v.W + 2 * v.halo;

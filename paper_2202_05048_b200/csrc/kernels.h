@@ -142,6 +142,15 @@ void launch_quant_nhwc(const float* x, View out, const float* act_scale, const i
 void launch_dequant(View in, const float* act_scale, const int* act_zp, int hist, float* y,
                     cudaStream_t s);
 void launch_halo_fill(View v, const int* act_zp, int hist, cudaStream_t s);
+// the halos of up to 48 tensors with their zero-point codes act_zp[hist[i]], one launch
+struct HaloBatch {
+  int n;
+  View v[48];
+  int hist[48];
+  int64_t unit0[48];
+  int64_t total;
+};
+void launch_halo_fill_multi(HaloBatch& hb, const int* act_zp, cudaStream_t s);
 void launch_relu_codes(View in, View out, const int* act_zp, int hist, cudaStream_t s);
 void launch_pool_codes(View in, View out, int k, int stride, int mode, const int* act_zp,
                        int hist, cudaStream_t s);

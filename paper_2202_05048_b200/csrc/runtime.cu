@@ -22,6 +22,7 @@
 #include <set>
 #include <stdexcept>
 #include <string>
+#include <array>
 #include <vector>
 
 #include "kernels.h"
@@ -164,6 +165,8 @@ struct ptq_ctx {
   // eval buffers
   int64_t chunk = 0;
   std::vector<int8_t*> d_codes;          // per tensor int8 view buffer (or null)
+  // (variant, act_gen, zero-point source, first image, images) each halo was last filled with
+  std::vector<std::array<int64_t, 5>> halo_key;
   std::vector<int> halo, cpad;
   std::vector<float*> d_f32;             // per tensor fp32 eval buffer (mixed tail)
   float* d_prefix = nullptr;             // mixed: fp32 output of the first compute node, all eval imgs
@@ -660,6 +663,7 @@ void ensure_eval_buffers(ptq_ctx* c) {
   for (const NodeI& n : c->nodes)
     if (n.kind == PTQ_FC) REQ(c->halo[n.in[0]] == 0, "fc input also feeds a padded conv");
   c->d_codes.assign(T, nullptr);
+  c->halo_key.clear();
   c->d_f32.assign(T, nullptr);
   std::set<int> need8, need32;
   for (int m = 0; m < 2; ++m) {
@@ -948,13 +952,29 @@ void eval_one(ptq_ctx* c, const ptq_config& cfg, unsigned long long* d_correct, 
       const int64_t per_img = (int64_t)(x.h + 2 * pv.halo) * (x.w + 2 * pv.halo) * pv.Cp;
       copy_nchw<int8_t>(c, pv.p, per_img, x.h, x.w, x.c, 0, pv.halo, pv.Cp, sel, out);
     };
-    auto halo_fill = [&](int t) {
-      View vv = V(t);
-      if (vv.halo > 0) {
-        launch_halo_fill(vv, az, P.psrc[t], c->st);
+    // every int8 tensor buffer is dedicated and no producer writes its halo, so all halos of
+    // this config are filled up front in one launch -- and only those whose zero point (or
+    // image range) changed since they were last filled
+    {
+      HaloBatch hb{};
+      if (c->halo_key.size() != (size_t)c->T) c->halo_key.assign(c->T, std::array<int64_t, 5>{-1, -1, -1, -1, -1});
+      for (int t = 0; t < c->T && hb.n < 48; ++t) {
+        if (!c->d_codes[t] || P.psrc[t] < 0) continue;
+        const View vv = V(t);
+        if (vv.halo <= 0 || vv.p == nullptr) continue;
+        const std::array<int64_t, 5> key = {(int64_t)v, (int64_t)c->act_gen, (int64_t)P.psrc[t], img0, (int64_t)B};
+        if (c->halo_key[t] == key) continue;
+        c->halo_key[t] = key;
+        hb.v[hb.n] = vv;
+        hb.hist[hb.n] = P.psrc[t];
+        ++hb.n;
+      }
+      if (hb.n) {
+        launch_halo_fill_multi(hb, az, c->st);
         check_launch(c);
       }
-    };
+    }
+    auto halo_fill = [&](int t) { (void)t; };
     // graph input / mixed prefix
     int start = 0;
     if (!cfg.mixed) {
@@ -1743,6 +1763,7 @@ int ptq_set_option(ptq_ctx* c, const char* key, int64_t value) {
         for (auto& P : c->plans) { if (P.d_layers) c->dfree(P.d_layers); P = Plan{}; }
         for (auto p : c->d_codes) c->dfree(p);
         c->d_codes.clear();
+        c->halo_key.clear();
         c->static_ready = false;
         c->prepared = false;
       }
