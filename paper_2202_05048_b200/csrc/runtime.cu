@@ -23,6 +23,7 @@
 #include <stdexcept>
 #include <string>
 #include <array>
+#include <atomic>
 #include <vector>
 
 #include "kernels.h"
@@ -226,13 +227,41 @@ void check_launch(ptq_ctx* c) {
   if (e != cudaSuccess) throw Err{PTQ_ECUDA, std::string("kernel launch: ") + cudaGetErrorString(e)};
 }
 
+// A device fault (illegal address, trap, ...) leaves the CUDA context of the process unusable:
+// every later call would fail with the same error or, worse, appear to work on garbage.  The
+// first such fault poisons the library; from then on every entry point fails fast with
+// PTQ_ECUDA and the original message, so each later trial is reported as failed (the
+// reference's _safe_eval records it, tuner.py:173-177) instead of returning wrong accuracies.
+// Recovery needs a new process (an in-process device reset would destroy every other context
+// of the process, e.g. PyTorch's).
+static std::atomic<int> g_poisoned{0};
+static std::string g_poison_msg;
+static bool sticky_cuda_error(cudaError_t e) {
+  switch (e) {
+    case cudaErrorIllegalAddress: case cudaErrorLaunchFailure: case cudaErrorHardwareStackError:
+    case cudaErrorIllegalInstruction: case cudaErrorMisalignedAddress: case cudaErrorInvalidAddressSpace:
+    case cudaErrorInvalidPc: case cudaErrorLaunchTimeout: case cudaErrorAssert: case cudaErrorECCUncorrectable:
+      return true;
+    default:
+      return false;
+  }
+}
 template <typename F>
 int guarded(F&& f) {
+  if (g_poisoned.load()) {
+    g_err = "CUDA context unusable after an earlier device fault (" + g_poison_msg +
+            "); start a new process";
+    return PTQ_ECUDA;
+  }
   try {
     f();
     return PTQ_OK;
   } catch (const Err& e) {
     g_err = e.msg;
+    if (e.code == PTQ_ECUDA && sticky_cuda_error(cudaGetLastError())) {
+      g_poison_msg = e.msg;
+      g_poisoned.store(1);
+    }
     return e.code;
   } catch (const std::exception& e) {
     g_err = e.what();

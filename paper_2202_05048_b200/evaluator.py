@@ -302,10 +302,26 @@ class GpuEvaluator:
             chosen = np.zeros((3 * T, 2), dtype=np.float64)
             self.kl_reranked = 0
             with _trace("choose_kl_ranges"):
-                for h in range(lo, hi):
-                    (a, b), nr = choose_kl_range(flat_c[h], flat_r[h, 0], flat_r[h, 1], kl[h])
-                    chosen[h] = (a, b)
-                    self.kl_reranked += nr
+                # vectorised first pass: histograms whose best window is unique within the tie
+                # band (and finite) need no numpy re-rank; only the rest go through
+                # choose_kl_range one by one
+                if hi > lo:
+                    sub = kl[lo:hi]
+                    best = sub.argmin(axis=1)
+                    kb = sub[np.arange(hi - lo), best]
+                    band = (sub <= (kb + np.abs(kb) * TIE_BAND)[:, None]).sum(axis=1)
+                    lo_r, hi_r = flat_r[lo:hi, 0].astype(np.float64), flat_r[lo:hi, 1].astype(np.float64)
+                    simple = np.isfinite(kb) & (band == 1) & (lo_r < hi_r) & (flat_c[lo:hi].sum(axis=1) > 0)
+                    for k in range(hi - lo):
+                        h = lo + k
+                        if simple[k]:
+                            start, end = kl_window_bounds(float(lo_r[k]), float(hi_r[k]), int(best[k]) + 128)
+                            chosen[h] = (_linspace_edge(float(lo_r[k]), float(hi_r[k]), start),
+                                         _linspace_edge(float(lo_r[k]), float(hi_r[k]), end))
+                        else:
+                            (a, b), nr = choose_kl_range(flat_c[h], flat_r[h, 0], flat_r[h, 1], kl[h])
+                            chosen[h] = (a, b)
+                            self.kl_reranked += nr
             kl_ranges = dist.allreduce(chosen, "sum") if world > 1 else chosen
         self.kl_ranges = np.ascontiguousarray(kl_ranges, dtype=np.float64).reshape(3, T, 2)
         for k in range(3):
