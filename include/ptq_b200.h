@@ -83,7 +83,10 @@ int ptq_version(void);
 
 /* Upload graph, images (N, C, H, W fp32, calibration pool first) and the eval
  * labels (n_images - n_calib int64) to device `device`.  Replaces the state the
- * reference builds inside make_accuracy_evaluator (tuner.py:434-438). */
+ * reference builds inside make_accuracy_evaluator (tuner.py:434-438).
+ * Returns once the calibration images are resident; the evaluation images keep
+ * uploading in the background (overlapping calibration), so `images` must stay
+ * valid until ptq_destroy (the first call that needs them waits for the copy). */
 int ptq_create(ptq_ctx** out, int device, const ptq_graph_desc* g, const float* images,
                const int64_t* eval_labels, int64_t n_images, int64_t n_calib);
 int ptq_destroy(ptq_ctx* ctx);

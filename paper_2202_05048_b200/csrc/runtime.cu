@@ -23,6 +23,7 @@
 #include <stdexcept>
 #include <string>
 #include <array>
+#include <thread>
 #include <atomic>
 #include <vector>
 
@@ -165,6 +166,12 @@ struct ptq_ctx {
   int* h_zp = nullptr;                   // pinned [sum of 8*cout] weight zero points
   // eval buffers
   int64_t chunk = 0;
+  // evaluation images upload in the background while calibration runs (ptq_create returns
+  // once the calibration images are resident); ensure_upload() joins it before first use
+  std::thread up_thread;
+  cudaStream_t st_up = nullptr;
+  cudaEvent_t ev_up = nullptr;
+  std::string up_err;
   std::vector<int8_t*> d_codes;          // per tensor int8 view buffer (or null)
   // (variant, act_gen, zero-point source, first image, images) each halo was last filled with
   std::vector<std::array<int64_t, 5>> halo_key;
@@ -1244,6 +1251,16 @@ void eval_one(ptq_ctx* c, const ptq_config& cfg, unsigned long long* d_correct, 
 extern "C" {
 
 const char* ptq_last_error(void) { return g_err.c_str(); }
+// the background upload of the evaluation images has landed (and the host buffer is no
+// longer read); the context stream waits for it
+static void ensure_upload(ptq_ctx* c) {
+  if (c->up_thread.joinable()) {
+    c->up_thread.join();
+    if (!c->up_err.empty()) throw Err{PTQ_ECUDA, "evaluation image upload: " + c->up_err};
+    CK(cudaStreamWaitEvent(c->st, c->ev_up, 0));
+  }
+}
+
 int ptq_version(void) { return 1; }
 
 int ptq_create(ptq_ctx** out, int device, const ptq_graph_desc* g, const float* images,
@@ -1271,8 +1288,25 @@ int ptq_create(ptq_ctx** out, int device, const ptq_graph_desc* g, const float* 
     c->n_eval = n_images - n_calib;
     const TensorI& in = c->tens[0];
     c->d_imgs = c->dalloc<float>((size_t)n_images * in.elems);
-    CK(cudaMemcpyAsync(c->d_imgs, images, (size_t)n_images * in.elems * sizeof(float),
+    // calibration pool now; the evaluation images (3.4x the bytes at 300/1000) stream in a
+    // background thread on their own stream while the calibration forward runs
+    CK(cudaMemcpyAsync(c->d_imgs, images, (size_t)n_calib * in.elems * sizeof(float),
                        cudaMemcpyHostToDevice, c->st));
+    if (n_images > n_calib) {
+      CK(cudaStreamSynchronize(c->st));          // d_imgs allocated (stream-ordered) before the copy
+      CK(cudaStreamCreateWithFlags(&c->st_up, cudaStreamNonBlocking));
+      CK(cudaEventCreateWithFlags(&c->ev_up, cudaEventDisableTiming));
+      float* dst = c->d_imgs + (size_t)n_calib * in.elems;
+      const float* src = images + (size_t)n_calib * in.elems;
+      const size_t bytes = (size_t)(n_images - n_calib) * in.elems * sizeof(float);
+      c->up_thread = std::thread([c, dst, src, bytes] {
+        cudaError_t e = cudaSetDevice(c->dev);
+        if (e == cudaSuccess) e = cudaMemcpyAsync(dst, src, bytes, cudaMemcpyHostToDevice, c->st_up);
+        if (e == cudaSuccess) e = cudaEventRecord(c->ev_up, c->st_up);
+        if (e == cudaSuccess) e = cudaStreamSynchronize(c->st_up);
+        if (e != cudaSuccess) c->up_err = cudaGetErrorString(e);
+      });
+    }
     c->d_labels = c->dalloc<long long>(std::max<int64_t>(c->n_eval, 1));
     if (c->n_eval > 0 && eval_labels)
       CK(cudaMemcpyAsync(c->d_labels, eval_labels, c->n_eval * sizeof(long long),
@@ -1284,6 +1318,7 @@ int ptq_create(ptq_ctx** out, int device, const ptq_graph_desc* g, const float* 
     *out = c;
   });
   if (rc != PTQ_OK) {
+    if (c->up_thread.joinable()) c->up_thread.join();
     for (void* p : c->allocs) cudaFreeAsync(p, c->st);
     if (c->st) cudaStreamSynchronize(c->st);
     if (c->st) cudaStreamDestroy(c->st);
@@ -1294,6 +1329,7 @@ int ptq_create(ptq_ctx** out, int device, const ptq_graph_desc* g, const float* 
 
 int ptq_destroy(ptq_ctx* c) {
   if (!c) return PTQ_OK;
+  if (c->up_thread.joinable()) c->up_thread.join();
   cudaSetDevice(c->dev);
   if (c->st) cudaStreamSynchronize(c->st);
   for (void* p : c->allocs) cudaFreeAsync(p, c->st);
@@ -1301,6 +1337,8 @@ int ptq_destroy(ptq_ctx* c) {
   for (auto e : c->ev_pool) cudaEventDestroy(e);
   if (c->h_zp) cudaFreeHost(c->h_zp);
   if (c->st) cudaStreamDestroy(c->st);
+  if (c->st_up) cudaStreamDestroy(c->st_up);
+  if (c->ev_up) cudaEventDestroy(c->ev_up);
   delete c;
   return PTQ_OK;
 }
@@ -1501,6 +1539,7 @@ int ptq_set_clip_ranges(ptq_ctx* c, int32_t cache, int32_t clipping, const doubl
 
 int ptq_prepare(ptq_ctx* c) {
   return guarded([&] {
+    if (c) ensure_upload(c);
     REQ(c, "null context");
     CK(cudaSetDevice(c->dev));
     prepare(c);
@@ -1509,6 +1548,7 @@ int ptq_prepare(ptq_ctx* c) {
 
 int ptq_eval_configs(ptq_ctx* c, const ptq_config* cfgs, int32_t n_cfg, int64_t* correct) {
   return guarded([&] {
+    if (c) ensure_upload(c);
     Trace tr("eval_configs");
     REQ(c && cfgs && correct && n_cfg >= 0, "null argument");
     CK(cudaSetDevice(c->dev));
@@ -1550,6 +1590,7 @@ int ptq_eval_configs(ptq_ctx* c, const ptq_config* cfgs, int32_t n_cfg, int64_t*
 
 int ptq_probe_codes(ptq_ctx* c, const ptq_config* cfg, int32_t tensor, int8_t* out, int64_t* n_out) {
   return guarded([&] {
+    if (c) ensure_upload(c);
     REQ(c && cfg && tensor >= 0 && tensor < c->T, "bad argument");
     const int64_t n = c->n_eval * c->tens[tensor].elems;
     if (n_out) *n_out = n;
@@ -1582,6 +1623,7 @@ static void probe_images(ptq_ctx* c, ProbeReq& pr, int32_t n_imgs, const int64_t
 int ptq_probe_tensors(ptq_ctx* c, const ptq_config* cfg, int32_t n_tensors, const int32_t* tensors,
                       int32_t n_imgs, const int64_t* imgs, int8_t* out, int32_t* found) {
   return guarded([&] {
+    if (c) ensure_upload(c);
     REQ(c && cfg && tensors && out && found && n_tensors > 0, "null argument");
     CK(cudaSetDevice(c->dev));
     prepare(c);
@@ -1606,6 +1648,7 @@ int ptq_probe_tensors(ptq_ctx* c, const ptq_config* cfg, int32_t n_tensors, cons
 int ptq_probe_acc(ptq_ctx* c, const ptq_config* cfg, int32_t node, int32_t n_imgs, const int64_t* imgs,
                   int32_t* out) {
   return guarded([&] {
+    if (c) ensure_upload(c);
     REQ(c && cfg && out, "null argument");
     REQ(node >= 0 && node < (int)c->nodes.size() && is_compute(c->nodes[node].kind), "not a compute node");
     CK(cudaSetDevice(c->dev));
@@ -1625,6 +1668,7 @@ int ptq_probe_acc(ptq_ctx* c, const ptq_config* cfg, int32_t node, int32_t n_img
 
 int ptq_probe_output(ptq_ctx* c, const ptq_config* cfg, int32_t n_imgs, const int64_t* imgs, float* out) {
   return guarded([&] {
+    if (c) ensure_upload(c);
     REQ(c && cfg && out, "null argument");
     CK(cudaSetDevice(c->dev));
     prepare(c);
@@ -1641,6 +1685,7 @@ int ptq_probe_output(ptq_ctx* c, const ptq_config* cfg, int32_t n_imgs, const in
 int ptq_probe_f32(ptq_ctx* c, const ptq_config* cfg, int32_t tensor, int32_t n_imgs, const int64_t* imgs,
                   float* out) {
   return guarded([&] {
+    if (c) ensure_upload(c);
     REQ(c && cfg && out && tensor >= 0 && tensor < c->T, "bad argument");
     CK(cudaSetDevice(c->dev));
     prepare(c);
@@ -1695,6 +1740,7 @@ int ptq_probe_act_params(ptq_ctx* c, int32_t cache, int32_t scheme, int32_t clip
 int ptq_export_layer(ptq_ctx* c, const ptq_config* cfg, int32_t node, int8_t* codes, float* wscale,
                      int32_t* wzp, int32_t* bias) {
   return guarded([&] {
+    if (c) ensure_upload(c);
     REQ(c && cfg && codes && wscale && wzp, "null argument");
     REQ(node >= 0 && node < (int)c->nodes.size() && is_compute(c->nodes[node].kind), "not a compute node");
     CK(cudaSetDevice(c->dev));

@@ -235,6 +235,9 @@ class GpuEvaluator:
         self._ctx = C.c_void_p()
         _lib.check(self.lib.ptq_create(C.byref(self._ctx), device, C.byref(self.lowered.desc),
                                        _lib.ptr(imgs), _lib.ptr(labels), len(imgs), self.n_calib))
+        # ptq_create returns once the calibration images are resident; the evaluation images keep
+        # uploading from this buffer while calibration runs, so it must outlive the context
+        self._host_imgs = imgs
         if eval_chunk:
             self.set_option("eval_chunk", int(eval_chunk))
         self.kl_reranked = 0
@@ -549,6 +552,7 @@ class GpuEvaluator:
         if getattr(self, "_ctx", None) and self._ctx.value:
             self.lib.ptq_destroy(self._ctx)
             self._ctx = C.c_void_p()
+        self._host_imgs = None
 
     def __del__(self):
         try:
