@@ -736,46 +736,100 @@ __global__ void __launch_bounds__(TC_THREADS, 1) k_conv_tc(const __grid_constant
     }
   } else if (warp < 2) {
     // ------------------------------------------------ A producers (implicit im2col gather)
-    // 64 threads, two GEMM rows (output pixels) each: r and r + 64
-    const int r = threadIdx.x;
-    const int Cp = a.in.Cp, cpc = Cp >> 4;
-    const int Wp = a.in.W + 2 * a.in.halo, Hp = a.in.H + 2 * a.in.halo;
-    int s = 0;
-    uint32_t ph = 0;
-    for (int tile = blockIdx.x; tile < n_tiles; tile += gridDim.x) {
-      const int mt = (int)a.div_nt.div((uint32_t)tile);
-      const RowGeo g0 = row_geo(a, mt * TC_BM + r, M);
-      const RowGeo g1 = row_geo(a, mt * TC_BM + r + 64, M);
-      const int8_t* base0 = a.in.p + (((int64_t)g0.n * Hp + g0.ih0) * Wp + g0.iw0) * Cp;
-      const int8_t* base1 = a.in.p + (((int64_t)g1.n * Hp + g1.ih0) * Wp + g1.iw0) * Cp;
-      if (a.skip.p) {
-        // the fused add's operand rows for this tile: pull them into L2 now, a few tiles
-        // before the epilogue reads them 16 bytes at a time
-        const int nt = tile - mt * n_nt;
-        const int c0 = nt * BN;
-        const uint32_t bytes = (uint32_t)(a.skip.Cp - c0 < BN ? a.skip.Cp - c0 : BN);
-        if (g0.ok) bulk_prefetch_l2(a.skip.p + vpix(a.skip, g0.n, g0.oh, g0.ow) * a.skip.Cp + c0, bytes);
-        if (g1.ok) bulk_prefetch_l2(a.skip.p + vpix(a.skip, g1.n, g1.oh, g1.ow) * a.skip.Cp + c0, bytes);
-      }
-      int kh = 0, kw = 0, ch = 0, kk = 0;
-      for (int ki = 0; ki < a.n_kiter; ++ki) {
-        mbar_wait(&empty[s], ph ^ 1u);
-        uint8_t* dst = sA + s * TC_A_STAGE + r * 16;
+    if (a.in.Cp & 16) {
+      // odd chunks per tap: the chunk pairs below would straddle taps (two pixels), so one GEMM
+      // row per lane: 64 threads, rows r and r + 64, 16-byte chunks of one row in sequence
+      const int r = threadIdx.x;
+      const int Cp = a.in.Cp, cpc = Cp >> 4;
+      const int Wp = a.in.W + 2 * a.in.halo, Hp = a.in.H + 2 * a.in.halo;
+      int s = 0;
+      uint32_t ph = 0;
+      for (int tile = blockIdx.x; tile < n_tiles; tile += gridDim.x) {
+        const int mt = (int)a.div_nt.div((uint32_t)tile);
+        const RowGeo g0 = row_geo(a, mt * TC_BM + r, M);
+        const RowGeo g1 = row_geo(a, mt * TC_BM + r + 64, M);
+        const int8_t* base0 = a.in.p + (((int64_t)g0.n * Hp + g0.ih0) * Wp + g0.iw0) * Cp;
+        const int8_t* base1 = a.in.p + (((int64_t)g1.n * Hp + g1.ih0) * Wp + g1.iw0) * Cp;
+        if (a.skip.p) {
+          const int nt = tile - mt * n_nt;
+          const int c0 = nt * BN;
+          const uint32_t bytes = (uint32_t)(a.skip.Cp - c0 < BN ? a.skip.Cp - c0 : BN);
+          if (g0.ok) bulk_prefetch_l2(a.skip.p + vpix(a.skip, g0.n, g0.oh, g0.ow) * a.skip.Cp + c0, bytes);
+          if (g1.ok) bulk_prefetch_l2(a.skip.p + vpix(a.skip, g1.n, g1.oh, g1.ow) * a.skip.Cp + c0, bytes);
+        }
+        int kh = 0, kw = 0, ch = 0, kk = 0;
+        for (int ki = 0; ki < a.n_kiter; ++ki) {
+          mbar_wait(&empty[s], ph ^ 1u);
+          uint8_t* dst = sA + s * TC_A_STAGE + r * 16;
 #pragma unroll
-        for (int j = 0; j < 8; ++j) {
-          const bool kin = kk < a.n_chunks && a.ablate != 2;
-          const int64_t off = ((int64_t)kh * Wp + kw) * Cp + ch * 16;
-          const bool v0 = g0.ok && kin, v1 = g1.ok && kin;
-          cp_async16(dst + j * (TC_BM * 16), v0 ? base0 + off : a.in.p, v0 ? 16u : 0u);
-          cp_async16(dst + j * (TC_BM * 16) + 64 * 16, v1 ? base1 + off : a.in.p, v1 ? 16u : 0u);
-          ++kk;
-          if (++ch == cpc) {
-            ch = 0;
-            if (++kw == a.k) { kw = 0; ++kh; }
+          for (int j = 0; j < 8; ++j) {
+            const bool kin = kk < a.n_chunks && a.ablate != 2;
+            const int64_t off = ((int64_t)kh * Wp + kw) * Cp + ch * 16;
+            const bool v0 = g0.ok && kin, v1 = g1.ok && kin;
+            cp_async16(dst + j * (TC_BM * 16), v0 ? base0 + off : a.in.p, v0 ? 16u : 0u);
+            cp_async16(dst + j * (TC_BM * 16) + 64 * 16, v1 ? base1 + off : a.in.p, v1 ? 16u : 0u);
+            ++kk;
+            if (++ch == cpc) {
+              ch = 0;
+              if (++kw == a.k) { kw = 0; ++kh; }
+            }
+          }
+          cp_async_mbar_arrive_noinc(&full[s]);
+          if (++s == NS) { s = 0; ph ^= 1u; }
+        }
+      }
+    } else {
+      // 64 threads; a warp instruction covers 16 GEMM rows x 2 adjacent 16-byte K chunks, so the
+      // two lanes of a row fill one 32-byte sector (one L2 request instead of two half-used ones;
+      // the 2-way shared-memory write conflict between the two chunk planes is cheaper).  Lane l of
+      // warp w: rows w*64 + 16g + l/2 (g = 0..3), chunks of parity l & 1
+      const int lane2 = threadIdx.x & 31, par = lane2 & 1;
+      const int rbase = (threadIdx.x >> 5) * 64 + (lane2 >> 1);
+      const int Cp = a.in.Cp, cpc = Cp >> 4;
+      const int Wp = a.in.W + 2 * a.in.halo, Hp = a.in.H + 2 * a.in.halo;
+      int s = 0;
+      uint32_t ph = 0;
+      for (int tile = blockIdx.x; tile < n_tiles; tile += gridDim.x) {
+        const int mt = (int)a.div_nt.div((uint32_t)tile);
+        const int8_t* base[4];
+        bool rok[4];
+  #pragma unroll
+        for (int gi = 0; gi < 4; ++gi) {
+          const RowGeo gg = row_geo(a, mt * TC_BM + rbase + 16 * gi, M);
+          rok[gi] = gg.ok;
+          base[gi] = a.in.p + (((int64_t)gg.n * Hp + gg.ih0) * Wp + gg.iw0) * Cp;
+          if (a.skip.p && par == 0 && gg.ok) {
+            // the fused add's operand rows for this tile: pull them into L2 now, a few tiles
+            // before the epilogue reads them 16 bytes at a time
+            const int nt = tile - mt * n_nt;
+            const int c0 = nt * BN;
+            const uint32_t bytes = (uint32_t)(a.skip.Cp - c0 < BN ? a.skip.Cp - c0 : BN);
+            bulk_prefetch_l2(a.skip.p + vpix(a.skip, gg.n, gg.oh, gg.ow) * a.skip.Cp + c0, bytes);
           }
         }
-        cp_async_mbar_arrive_noinc(&full[s]);
-        if (++s == NS) { s = 0; ph ^= 1u; }
+        // this lane's K chunks: kk = par, par + 2, ... walked as (kh, kw, ch)
+        int kh = 0, kw = 0, ch = par, kk = par;
+        while (ch >= cpc) { ch -= cpc; if (++kw == a.k) { kw = 0; ++kh; } }
+        for (int ki = 0; ki < a.n_kiter; ++ki) {
+          mbar_wait(&empty[s], ph ^ 1u);
+          uint8_t* dst = sA + s * TC_A_STAGE + rbase * 16;
+  #pragma unroll
+          for (int q = 0; q < 4; ++q) {
+            const bool kin = kk < a.n_chunks && a.ablate != 2;
+            const int64_t off = ((int64_t)kh * Wp + kw) * Cp + ch * 16;
+            uint8_t* d = dst + (2 * q + par) * (TC_BM * 16);
+  #pragma unroll
+            for (int gi = 0; gi < 4; ++gi) {
+              const bool v = rok[gi] && kin;
+              cp_async16(d + gi * (16 * 16), v ? base[gi] + off : a.in.p, v ? 16u : 0u);
+            }
+            kk += 2;
+            ch += 2;
+            while (ch >= cpc) { ch -= cpc; if (++kw == a.k) { kw = 0; ++kh; } }
+          }
+          cp_async_mbar_arrive_noinc(&full[s]);
+          if (++s == NS) { s = 0; ph ^= 1u; }
+        }
       }
     }
   } else if (warp == 2) {
