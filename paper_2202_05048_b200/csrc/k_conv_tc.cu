@@ -80,10 +80,10 @@ __device__ __forceinline__ uint64_t umma_desc_sw(uint32_t saddr, int swz, uint32
   return d;
 }
 
-// instruction descriptor: D=s32, A=s8, B=s8, both K-major, N=BN, M=128
-template <int BN>
+// instruction descriptor: D=s32, A=s8, B=s8, both K-major, N (multiple of 16, <= 256), M=128
+template <int N>
 __device__ __forceinline__ uint32_t idesc_i8() {
-  return (2u << 4) | (1u << 7) | (1u << 10) | ((uint32_t)(BN >> 3) << 17) |
+  return (2u << 4) | (1u << 7) | (1u << 10) | ((uint32_t)(N >> 3) << 17) |
          ((uint32_t)(TC_BM >> 4) << 24);
 }
 
@@ -469,14 +469,15 @@ __device__ __forceinline__ void epi_tiles(const ConvTcArgs& a, const LayerRt& rt
       srow = (g.ok && has_skip) ? a.skip.p + vpix(a.skip, g.n, g.oh, g.ow) * a.skip.Cp : nullptr;
     }
     long long rowsum = 0;
-    if ((GENERIC || WZP) && a.tma_rowsum) {
+    if ((GENERIC || WZP) && a.rs_mma) {
+      // read below from the accumulator's indicator columns
+    } else if ((GENERIC || WZP) && a.tma_rowsum) {
       mbar_wait(&e.rsfull[buf], uph);
       rowsum = e.rsum[buf * TC_BM + e.row];
     } else if ((GENERIC || WZP) && g.ok && first < NCH) {
       rowsum = a.Rpix ? (long long)a.Rpix[((int64_t)g.n * a.OHr + g.oh) * a.OWr + g.ow]
                       : pixel_rowsum(a, g.n, g.ih0, g.iw0);
     }
-    const int zr = (FX && PT && WZP) ? k.zw0 * (int)rowsum : 0;   // per-tensor zw * rowsum
     // tile I/O: this tile's shared buffer (the fused-add operand landed by TMA, or a buffer
     // whose previous TMA store has finished reading it)
     const uint32_t ib = lt % TC_IO_NB, iph = (lt / TC_IO_NB) & 1u;
@@ -495,7 +496,9 @@ __device__ __forceinline__ void epi_tiles(const ConvTcArgs& a, const LayerRt& rt
       sk_next = __ldg(reinterpret_cast<const int4*>(srow + cb0));
     mbar_wait(&e.tfull[buf], uph);
     tc_fence_after();
-    const uint32_t tbase = e.tmem + ((uint32_t)(e.q * 32) << 16) + buf * BN;
+    const uint32_t tbase = e.tmem + ((uint32_t)(e.q * 32) << 16) + buf * (uint32_t)a.b_rows;
+    if ((GENERIC || WZP) && a.rs_mma) rowsum = (int)tmem_ld1(tbase + BN);   // sum_k x[row][k]
+    const int zr = (FX && PT && WZP) ? k.zw0 * (int)rowsum : 0;   // per-tensor zw * rowsum
 #pragma unroll 1
     for (int c = first; c < NCH; c += TC_NG) {
       const int cb = nt * BN + c * 16;
@@ -558,7 +561,9 @@ __device__ __forceinline__ void epi_fx(const ConvTcArgs& a, const LayerRt& rt, c
   else epi_tiles<BN, WZP, SKIP, false, RELU, false, false, false, true>(a, rt, k, e);
 }
 
-template <int BN>
+// BR = B rows per tile (a.b_rows): BN, or BN + 16 K-indicator rows (the MMA then runs over
+// N = BR and accumulator columns BN..BN+15 are the A-row sums, rs_mma)
+template <int BN, int BR>
 __global__ void __launch_bounds__(TC_THREADS, 1) k_conv_tc(const __grid_constant__ ConvTcArgs a) {
   const int NS = a.n_stages;
   extern __shared__ __align__(1024) uint8_t smem_raw[];
@@ -567,7 +572,7 @@ __global__ void __launch_bounds__(TC_THREADS, 1) k_conv_tc(const __grid_constant
   uint8_t* sio = smem;                              // tile I/O buffers (tio), 1024-aligned boxes
   uint8_t* sA = smem + (a.tio ? TC_IO_NB * TC_BM * BN : 0);
   uint8_t* sB = sA + NS * TC_A_STAGE;               // B ring [NS][BN][128], or resident [n_kiter][BN][128]
-  uint64_t* full = reinterpret_cast<uint64_t*>(sB + (a.b_res ? a.n_kiter : NS) * BN * 128);
+  uint64_t* full = reinterpret_cast<uint64_t*>(sB + (a.b_res ? a.n_kiter : NS) * BR * 128);
   uint64_t* empty = full + NS;
   uint64_t* tfull = empty + NS;
   uint64_t* tempty = tfull + 2;
@@ -580,7 +585,8 @@ __global__ void __launch_bounds__(TC_THREADS, 1) k_conv_tc(const __grid_constant
   int* rsum = reinterpret_cast<int*>(ioready + TC_IO_NB + 1);    // [2][128] A-row sums (tma_rowsum)
   EpiParam* sparam = reinterpret_cast<EpiParam*>(rsum + 2 * TC_BM);   // [Cout] (no fused add)
   int8_t* stab = reinterpret_cast<int8_t*>(rsum + 2 * TC_BM);          // fused-add table
-  constexpr uint32_t TMEM_COLS = (2 * BN) < 32 ? 32 : 2 * BN;
+  // two accumulator buffers of BR columns (power-of-two allocation, at least 32)
+  constexpr uint32_t TMEM_COLS = 2 * BR <= 32 ? 32u : 2 * BR <= 64 ? 64u : 2 * BR <= 128 ? 128u : 2 * BR <= 256 ? 256u : 512u;
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int M = a.in.N * a.OH * a.OW;
@@ -835,19 +841,19 @@ __global__ void __launch_bounds__(TC_THREADS, 1) k_conv_tc(const __grid_constant
   } else if (warp == 2) {
     // ------------------------------------------------ B producer (bulk copies of pre-tiled weights)
     if (lane == 0 && a.b_res) {                     // one n-tile: load every K stage once
-      mbar_arrive_expect_tx(bfull, (uint32_t)(a.n_kiter * BN * 128));
+      mbar_arrive_expect_tx(bfull, (uint32_t)(a.n_kiter * BR * 128));
       for (int ki = 0; ki < a.n_kiter; ++ki)
-        bulk_g2s(sB + ki * BN * 128, a.wB + (int64_t)ki * BN * 128, BN * 128, bfull);
+        bulk_g2s(sB + ki * BR * 128, a.wB + (int64_t)ki * BR * 128, BR * 128, bfull);
     } else if (lane == 0) {
       int s = 0;
       uint32_t ph = 0;
       for (int tile = blockIdx.x; tile < n_tiles; tile += gridDim.x) {
         const int nt = tile - (int)a.div_nt.div((uint32_t)tile) * n_nt;
-        const int8_t* gB = a.wB + (int64_t)nt * a.n_kiter * BN * 128;
+        const int8_t* gB = a.wB + (int64_t)nt * a.n_kiter * BR * 128;
         for (int ki = 0; ki < a.n_kiter; ++ki) {
           mbar_wait(&empty[s], ph ^ 1u);
-          mbar_arrive_expect_tx(&full[s], BN * 128);
-          bulk_g2s(sB + s * BN * 128, gB + (int64_t)ki * BN * 128, BN * 128, &full[s]);
+          mbar_arrive_expect_tx(&full[s], BR * 128);
+          bulk_g2s(sB + s * BR * 128, gB + (int64_t)ki * BR * 128, BR * 128, &full[s]);
           if (++s == NS) { s = 0; ph ^= 1u; }
         }
       }
@@ -905,7 +911,9 @@ __global__ void __launch_bounds__(TC_THREADS, 1) k_conv_tc(const __grid_constant
     //   kw-reuse: A slab shifted by kw rows (4 units per kw), B resident chunk-major
     // B: no swizzle, LBO = one K plane of BN rows; K=32 step = 2 planes = 2*BN units.
     {
-      const uint32_t idesc = idesc_i8<BN>();
+      // BR > BN: the MMA also covers the 16 K-indicator rows, so accumulator columns BN..BN+15
+      // of every row hold that A row's sum
+      const uint32_t idesc = idesc_i8<BR>();
       const int mode = a.tma_a;
       const uint32_t sa = smem_u32(sA), sb = smem_u32(sB);
       const bool nosw = mode == 0 || mode == 65;
@@ -913,14 +921,14 @@ __global__ void __launch_bounds__(TC_THREADS, 1) k_conv_tc(const __grid_constant
                            : nosw ? umma_desc(0, TC_BM * 16, 128)
                            : mode == 67 ? umma_desc(0, 16, 128)
                            : mode == 128 ? umma_desc_sw(0, 128) : umma_desc_sw(0, 64);
-      const uint64_t bdt = umma_desc(0, BN * 16, 128);
+      const uint64_t bdt = umma_desc(0, BR * 16, 128);
       const int Wp = a.in.W + 2 * a.in.halo;
       uint64_t a1, a2, a3;
       if (nosw) { a1 = 256; a2 = 512; a3 = 768; }
       else if (mode == 67) { a1 = 2; a2 = (uint64_t)Wp; a3 = (uint64_t)Wp + 2; }
       else if (mode == 128) { a1 = 2; a2 = 4; a3 = 6; }
       else { a1 = 2; a2 = 512; a3 = 514; }
-      const uint64_t bstep = 2 * BN;
+      const uint64_t bstep = 2 * BR;
       if (a.b_res) mbar_wait(bfull, 0);
       int s = 0;
       uint32_t ph = 0, lt = 0;
@@ -928,7 +936,7 @@ __global__ void __launch_bounds__(TC_THREADS, 1) k_conv_tc(const __grid_constant
         const uint32_t buf = lt & 1u, uph = (lt >> 1) & 1u;
         mbar_wait(&tempty[buf], uph ^ 1u);           // epilogue drained this accumulator
         tc_fence_after();
-        const uint32_t d = tmem + buf * BN;
+        const uint32_t d = tmem + buf * (uint32_t)BR;
         for (int ki = 0; ki < a.a_iters; ++ki) {
           mbar_wait(&full[s], ph);
           tc_fence_after();
@@ -938,9 +946,9 @@ __global__ void __launch_bounds__(TC_THREADS, 1) k_conv_tc(const __grid_constant
           if (a.kwr) {
             // slab = input rows p0 + ki*Wp + [0, 136); tap (ki, kw) = the slab shifted by kw
             // rows (A: +4 units per kw, +2 per K half); B chunk ki*12 + kw*4 + 2*ks2
-            mma6_commit(d, ad, bdt + (sb >> 4) + (uint64_t)(ki * 12 * BN), 2, bstep, idesc, ki != 0, bar);
+            mma6_commit(d, ad, bdt + (sb >> 4) + (uint64_t)(ki * 12 * BR), 2, bstep, idesc, ki != 0, bar);
           } else {
-            const uint64_t bd = bdt + ((sb + (uint32_t)((a.b_res ? ki : s) * BN * 128)) >> 4);
+            const uint64_t bd = bdt + ((sb + (uint32_t)((a.b_res ? ki : s) * BR * 128)) >> 4);
             mma4_commit(d, ad, bd, a1, a2, a3, bstep, idesc, ki != 0, mode != 67 || 2 * ki + 1 < a.k, bar);
           }
           if (++s == NS) { s = 0; ph ^= 1u; }
@@ -1044,7 +1052,7 @@ __global__ void k_conv_i8_ref(const ConvTcArgs a) {
       const int tap = kk / cpc, ch = kk % cpc;
       const int kh = tap / a.k, kw = tap % a.k;
       const int8_t* xs = a.in.p + (((int64_t)g.n * Hp + g.ih0 + kh) * Wp + g.iw0 + kw) * a.in.Cp + ch * 16;
-      const int8_t* ws = a.wB + (((int64_t)ntile * a.n_kiter + kk / 8) * 8 + kk % 8) * BN * 16 + row * 16;
+      const int8_t* ws = a.wB + (((int64_t)ntile * a.n_kiter + kk / 8) * 8 + kk % 8) * a.b_rows * 16 + row * 16;
       for (int b = 0; b < 16; ++b) dot += (long long)xs[b] * ws[b];
     }
     const long long rowsum = a.Rpix ? (long long)a.Rpix[((int64_t)g.n * a.OHr + g.oh) * a.OWr + g.ow]
@@ -1073,12 +1081,12 @@ int conv_tc_bn_for(int cout) {
 }
 
 
-template <int BN>
+template <int BN, int BR>
 static void launch_bn(const ConvTcArgs& a, cudaStream_t s) {
   // fixed part: barriers, TMEM slot, optional add table, resident B; the rest of the 227 KB
   // goes to pipeline stages (deeper for narrow tiles, at least 2)
   const int n_nt = (a.L.cout + BN - 1) / BN;
-  const size_t b_bytes = (size_t)a.n_kiter * BN * 128;
+  const size_t b_bytes = (size_t)a.n_kiter * a.b_rows * 128;
   const int b_res = n_nt == 1 && b_bytes <= 64 * 1024;
   ConvTcArgs b = a;
   size_t smem = 0;
@@ -1089,7 +1097,7 @@ static void launch_bn(const ConvTcArgs& a, cudaStream_t s) {
     const size_t fixed = 1024 + (2 * TC_MAX_STAGES + 8 + 3 * TC_IO_NB) * 8 + 2 * TC_BM * 4 + 16 +
                          (a.addtab ? PTQ_ADDTAB_BYTES : (size_t)((a.L.cout + 15) & ~15) * sizeof(EpiParam)) +
                          (b_res ? b_bytes : 0) + (b.tio ? (size_t)TC_IO_NB * TC_BM * BN : 0);
-    const size_t per_stage = (size_t)TC_A_STAGE + (b_res ? 0 : (size_t)BN * 128);
+    const size_t per_stage = (size_t)TC_A_STAGE + (b_res ? 0 : (size_t)a.b_rows * 128);
     ns = fixed < TC_SMEM_MAX ? (int)((TC_SMEM_MAX - fixed) / per_stage) : 0;
     if (ns < 2 && b.tio) { b.tio = 0; continue; }
     if (ns > TC_MAX_STAGES) ns = TC_MAX_STAGES;
@@ -1106,7 +1114,7 @@ static void launch_bn(const ConvTcArgs& a, cudaStream_t s) {
   static std::atomic<uint64_t> configured{0};
   const uint64_t bit = 1ull << (dev & 63);
   if (!(configured.load() & bit) &&
-      cudaFuncSetAttribute(k_conv_tc<BN>, cudaFuncAttributeMaxDynamicSharedMemorySize, TC_SMEM_MAX) == cudaSuccess)
+      cudaFuncSetAttribute(k_conv_tc<BN, BR>, cudaFuncAttributeMaxDynamicSharedMemorySize, TC_SMEM_MAX) == cudaSuccess)
     configured.fetch_or(bit);
   int num_sms = 0;
   cudaDeviceGetAttribute(&num_sms, cudaDevAttrMultiProcessorCount, dev);
@@ -1128,7 +1136,7 @@ static void launch_bn(const ConvTcArgs& a, cudaStream_t s) {
   if (a.addtab)
     cudaMemcpyToSymbolAsync(c_ep, a.L.ep, (size_t)((a.L.cout + 15) & ~15) * sizeof(EpiParam), 0,
                             cudaMemcpyDeviceToDevice, s);
-  k_conv_tc<BN><<<grid, TC_THREADS, smem, s>>>(b);
+  k_conv_tc<BN, BR><<<grid, TC_THREADS, smem, s>>>(b);
   cudaEventRecord(last[d], s);
   last_stream[d] = s;
 }
@@ -1254,11 +1262,12 @@ static void plan_launch(ConvTcArgs& t, int bn) {
       t.a_iters = 3;                                 // A stages per tile = kh rows
     }
   }
-  t.tma_rowsum = t.has_wzp && !t.Rpix && (t.tma_a == 64 || t.tma_a == 128);
+  t.tma_rowsum = t.has_wzp && !t.rs_mma && !t.Rpix && (t.tma_a == 64 || t.tma_a == 128);
   // flat rows: halo-free input and output, no padded-grid rows, halo-free add operand, and
   // row sums (when needed) taken in-kernel
   t.flat = (t.tma_a == 64 || t.tma_a == 128) && t.in.halo == 0 && t.out.halo == 0 && t.OH == t.OHr &&
-           t.OW == t.OWr && (!t.skip.p || t.skip.halo == 0) && (!t.has_wzp || t.tma_rowsum);
+           t.OW == t.OWr && (!t.skip.p || t.skip.halo == 0) &&
+           (!t.has_wzp || t.tma_rowsum || t.rs_mma);
   // tile I/O for flat layers: the output (and the fused-add operand) as 2-D [pixels][Cp] maps
   // with boxes of 128 rows x io_w bytes, swizzled like the epilogue's shared tile
   t.tio = 0;
@@ -1292,12 +1301,13 @@ void launch_conv_tc(const ConvTcArgs& a0, int bn, cudaStream_t s) {
   ConvTcArgs t = a0;
   plan_launch(t, bn);
   const ConvTcArgs a = with_divs(t, bn);
+  const bool ind = a.b_rows > bn;                   // tiles carry the K-indicator rows
   switch (bn) {
-    case 16: launch_bn<16>(a, s); break;
-    case 32: launch_bn<32>(a, s); break;
-    case 64: launch_bn<64>(a, s); break;
-    case 128: launch_bn<128>(a, s); break;
-    default: launch_bn<256>(a, s); break;
+    case 16: ind ? launch_bn<16, 32>(a, s) : launch_bn<16, 16>(a, s); break;
+    case 32: ind ? launch_bn<32, 48>(a, s) : launch_bn<32, 32>(a, s); break;
+    case 64: ind ? launch_bn<64, 80>(a, s) : launch_bn<64, 64>(a, s); break;
+    case 128: ind ? launch_bn<128, 144>(a, s) : launch_bn<128, 128>(a, s); break;
+    default: launch_bn<256, 256>(a, s); break;
   }
 }
 

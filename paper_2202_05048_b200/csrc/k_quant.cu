@@ -140,16 +140,23 @@ __global__ void k_weight_params8(const unsigned int* __restrict__ mnmx, int cout
 }
 __global__ void k_weight_quant_tc8(const float* __restrict__ w, int cout, int cin, int k, int fc_hw,
                                    int cin_p, const float* __restrict__ scale, const int* __restrict__ zp,
-                                   int bn, int n_kiter, int8_t* __restrict__ out, int64_t per_variant) {
+                                   int bn, int rows_mask, int n_kiter, int8_t* __restrict__ out) {
+  // variant wv: tiles of brows rows (bn, + 16 K-indicator rows when bit wv of rows_mask is set),
+  // variants stored back to back
   const int wv = blockIdx.y;
+  const int ntiles = (cout + bn - 1) / bn;
+  int64_t off = 0;
+  for (int v = 0; v < wv; ++v) off += (int64_t)ntiles * n_kiter * 8 * ((rows_mask >> v & 1) ? bn + 16 : bn) * 16;
+  const int brows = (rows_mask >> wv & 1) ? bn + 16 : bn;
+  const int64_t per_variant = (int64_t)ntiles * n_kiter * 8 * brows * 16;
   const float* sc = scale + (int64_t)wv * cout;
   const int* z = zp + (int64_t)wv * cout;
-  int8_t* o8 = out + (int64_t)wv * per_variant;
+  int8_t* o8 = out + off;
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < per_variant;
        i += (int64_t)gridDim.x * blockDim.x) {
     int b = (int)(i & 15);
     int64_t r = i >> 4;
-    int row = (int)(r % bn); r /= bn;
+    int row = (int)(r % brows); r /= brows;
     int j = (int)(r & 7); r >>= 3;
     int it = (int)(r % n_kiter);
     int nt = (int)(r / n_kiter);
@@ -157,7 +164,9 @@ __global__ void k_weight_quant_tc8(const float* __restrict__ w, int cout, int ci
     int64_t kb = ((int64_t)it * 8 + j) * 16 + b;
     int8_t code = 0;
     int64_t si;
-    if (o < cout && wsrc(o, kb, cin, k, fc_hw, cin_p, &si))
+    if (row >= bn)                       // K-indicator rows: the MMA's A-row sums (rs_mma)
+      code = wsrc(0, kb, cin, k, fc_hw, cin_p, &si) ? 1 : 0;
+    else if (o < cout && wsrc(o, kb, cin, k, fc_hw, cin_p, &si))
       code = (int8_t)quant1(__ldg(w + si), (double)sc[o], (double)z[o]);
     o8[i] = code;
   }
@@ -188,7 +197,7 @@ __global__ void k_weight_quant_dw8(const float* __restrict__ w, int c, int kk, c
       (int8_t)quant1(__ldg(w + i), (double)scale[(int64_t)wv * c + ch], (double)zp[(int64_t)wv * c + ch]);
 }
 void launch_weight_prepare8(const float* w, int cout, int64_t per_ch, bool depthwise, int cin, int k,
-                            int fc_hw, int cin_p, int bn, int n_kiter, int64_t bytes_per_variant,
+                            int fc_hw, int cin_p, int bn, int rows_mask, int n_kiter, int64_t bytes_per_variant,
                             unsigned int* mnmx /*[2*(cout+1)]*/, float* scale, int* zp, int8_t* codes,
                             int* wsum, cudaStream_t s) {
   k_init_minmax<<<(cout + 255) / 256, 256, 0, s>>>(mnmx, cout);
@@ -199,7 +208,7 @@ void launch_weight_prepare8(const float* w, int cout, int64_t per_ch, bool depth
     k_weight_quant_dw8<<<dim3((unsigned)((cout * k * k + 255) / 256), 8), 256, 0, s>>>(w, cout, k * k, scale, zp, codes);
   } else {
     k_weight_quant_tc8<<<dim3(nblk(bytes_per_variant, 256, 148 * 4), 8), 256, 0, s>>>(
-        w, cout, cin, k, fc_hw, cin_p, scale, zp, bn, n_kiter, codes, bytes_per_variant);
+        w, cout, cin, k, fc_hw, cin_p, scale, zp, bn, rows_mask, n_kiter, codes);
     k_weight_sum8<<<dim3(cout, 8), 128, 0, s>>>(w, per_ch, cout, scale, zp, wsum);
   }
 }

@@ -126,7 +126,7 @@ void launch_act_params(const double* ranges /*[n_var][T][2]*/, const int* var_sc
                        int T, float* scale, int* zp, cudaStream_t s);
 // all 8 (scheme, granularity) variants of one weight tensor: params, codes, code sums
 void launch_weight_prepare8(const float* w, int cout, int64_t per_ch, bool depthwise, int cin, int k,
-                            int fc_hw, int cin_p, int bn, int n_kiter, int64_t bytes_per_variant,
+                            int fc_hw, int cin_p, int bn, int rows_mask, int n_kiter, int64_t bytes_per_variant,
                             unsigned int* mnmx, float* scale, int* zp, int8_t* codes, int* wsum,
                             cudaStream_t s);
 // fx: 1 = also derive the exact fixed-point epilogue constants (LayerRt::fx), 0 = fp64 only
@@ -204,7 +204,12 @@ struct ConvTcArgs {
   int allow_tma;          // runtime option: TMA A loads for eligible layers
   View in, out;
   int k, stride, pad, OH, OW;
-  const int8_t* wB;       // tiled weights [n_tiles][n_kiter][8][BN][16]
+  const int8_t* wB;       // tiled weights [n_tiles][n_kiter][8][b_rows][16]
+  int b_rows;             // B rows per tile: BN, or BN + 16 when the tiles carry the 16 K-indicator
+                          // rows (1 at every real K position) used by rs_mma
+  int rs_mma;             // set by the runtime (has_wzp, b_rows > BN): the MMA runs over N = BN + 16
+                          // and the extra accumulator columns are the A-row sums sum_k x[row][k]
+                          // (no row-sum warp, pixel-sum pass or stem window-sum pass)
   int n_kiter;            // K stages of 128 bytes
   int n_chunks;           // real 16-byte K chunks = k*k*Cp/16
   const int* wzp;         // [cout] weight zero points (variant)

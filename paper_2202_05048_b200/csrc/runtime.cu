@@ -94,14 +94,17 @@ bool is_tc(int k) { return k == PTQ_CONV || k == PTQ_PWCONV || k == PTQ_FC; }
 struct WeightsDev {
   int cout = 0, cin = 0, k = 1, fc_hw = 0, cin_p = 0;
   int bn = 0, n_kiter = 0, n_chunks = 0, kreal = 0;
+  int brows_mask = 0;           // variants whose B tiles carry 16 K-indicator rows (rs_mma)
+  int var_rows[8] = {};         // B rows per tile of each variant (bn, or bn + 16)
+  int64_t var_off[9] = {};      // byte offset of each variant's codes (var_off[8] = total)
   bool im2col = false;          // few-channel conv: packed im2col + 1x1 tensor-core GEMM
   bool sub1x1 = false;          // strided 1x1 conv: subsampled input + stride-1 pointwise GEMM
   int im_cp = 0;                // im2col row pitch (k*k*Cin rounded up to 16)
   int q_cin_p = 0, q_k = 1, q_fc_hw = 0;   // weight-quantizer view of the K layout
   float* f32_gemm = nullptr;    // [K][cout] fp32 (NHWC K order) for the fp32 path, or dw [C][k*k]
   float* f32_bias = nullptr;
-  int8_t* codes = nullptr;      // [8 variants][bytes_per_variant]
-  int64_t bytes_per_variant = 0;
+  int8_t* codes = nullptr;      // 8 variants back to back (var_off)
+  int64_t bytes_per_variant = 0;  // largest variant (dw: every variant)
   float* scale = nullptr;       // [8][cout]
   int* zp = nullptr;            // [8][cout]
   int* wsum = nullptr;          // [8][cout]
@@ -196,6 +199,7 @@ struct ptq_ctx {
   int dwconv_variant = 3, concat_v16 = 1, kwr = 0;   // A/B switches (per context)
   int fx = 1;                            // exact fixed-point conv epilogue (0: fp64 epilogue)
   int tio = 1;                           // tile I/O through shared memory + TMA (flat conv layers)
+  int rs_mma = 1;                        // A-row sums for weight zero points from the MMA (bn <= 128)
   int hist_multi = 1;                    // batched histogram launch (0: one launch per histogram, A/B)
   int64_t opt_chunk = 0;
   // stats
@@ -461,10 +465,25 @@ void import_graph(ptq_ctx* c, const ptq_graph_desc* g) {
           if (c->nodes[j].out == other) prod = j;
         if (prod < i) wd.bn = 128;
       }
+      // narrow tiles of the variants with weight zero points (scheme 0 = Asymmetric, both
+      // granularities) carry 16 K-indicator rows: the MMA also yields the A-row sums (N = bn + 16
+      // <= 144; bn = 256 tiles fill TMEM and keep the row-sum warp).  The other variants keep
+      // bn-row tiles (no extra B bytes or MMA columns)
+      wd.brows_mask = wd.bn <= 128 ? 0x3 : 0;
       int ntiles = (wd.cout + wd.bn - 1) / wd.bn;
-      wd.bytes_per_variant = (int64_t)ntiles * wd.n_kiter * 8 * wd.bn * 16;
+      for (int v = 0; v < 8; ++v) {
+        wd.var_rows[v] = (wd.brows_mask >> v & 1) ? wd.bn + 16 : wd.bn;
+        const int64_t vb = (int64_t)ntiles * wd.n_kiter * 8 * wd.var_rows[v] * 16;
+        wd.var_off[v + 1] = wd.var_off[v] + vb;
+        wd.bytes_per_variant = std::max(wd.bytes_per_variant, vb);
+      }
     }
-    wd.codes = c->dalloc<int8_t>(8 * wd.bytes_per_variant);
+    if (n.kind == PTQ_DWCONV)
+      for (int v = 0; v < 8; ++v) {
+        wd.var_rows[v] = 0;
+        wd.var_off[v + 1] = wd.var_off[v] + wd.bytes_per_variant;
+      }
+    wd.codes = c->dalloc<int8_t>(wd.var_off[8]);
     wd.scale = c->dalloc<float>(8 * wd.cout);
     wd.zp = c->dalloc<int>(8 * wd.cout);
     wd.wsum = c->dalloc<int>(8 * wd.cout);
@@ -820,7 +839,7 @@ void prepare_static(ptq_ctx* c) {
     int64_t per_ch = 1;
     for (size_t d = 1; d < c->wshape[n.weight].size(); ++d) per_ch *= c->wshape[n.weight][d];
     launch_weight_prepare8(w, wd.cout, per_ch, n.kind == PTQ_DWCONV, wd.cin, n.kind == PTQ_DWCONV ? wd.k : wd.q_k,
-                           wd.q_fc_hw, wd.q_cin_p, wd.bn, wd.n_kiter, wd.bytes_per_variant, d_mm, wd.scale,
+                           wd.q_fc_hw, wd.q_cin_p, wd.bn, wd.brows_mask, wd.n_kiter, wd.bytes_per_variant, d_mm, wd.scale,
                            wd.zp, wd.codes, wd.wsum, c->st);
     check_launch(c);
   }
@@ -1070,7 +1089,7 @@ void eval_one(ptq_ctx* c, const ptq_config& cfg, unsigned long long* d_correct, 
         if (n.kind == PTQ_DWCONV) {
           // the dp4a kernel takes the weight zero points only when this variant has any
           const bool dp4 = c->dwconv_variant == 3;
-          launch_dwconv_i8(V(tin), V(tout), wd.codes + (size_t)wv * wd.bytes_per_variant,
+          launch_dwconv_i8(V(tin), V(tout), wd.codes + wd.var_off[wv],
                            (dp4 && !wd.has_wzp[wv]) ? nullptr : wd.zp + (size_t)wv * wd.cout, n.k, n.stride,
                            n.pad, L, c->st, d_acc, c->dwconv_variant);
           check_launch(c);
@@ -1096,14 +1115,16 @@ void eval_one(ptq_ctx* c, const ptq_config& cfg, unsigned long long* d_correct, 
           }
           a.in = vin;
           a.out = V(tout);
-          a.wB = wd.codes + (size_t)wv * wd.bytes_per_variant;
+          a.wB = wd.codes + wd.var_off[wv];
+          a.b_rows = wd.var_rows[wv];
           a.n_kiter = wd.n_kiter;
           a.n_chunks = wd.n_chunks;
           a.wzp = wd.zp + (size_t)wv * wd.cout;
           a.wsum = wd.wsum + (size_t)wv * wd.cout;
           a.kreal = wd.kreal;
           a.has_wzp = wd.has_wzp[wv];
-          if (a.has_wzp && i == c->s2d_node) {
+          a.rs_mma = a.has_wzp && c->rs_mma && a.b_rows > wd.bn && !c->conv_ref;
+          if (a.has_wzp && !a.rs_mma && i == c->s2d_node) {
             REQ((int64_t)B * a.OH * a.OW <= c->P_cap, "stem rowsum buffer too small");
             launch_stem_rowsum(vin, n.k, c->tens[0].c, a.OH, a.OW, c->d_P, c->st);
             check_launch(c);
@@ -1120,7 +1141,7 @@ void eval_one(ptq_ctx* c, const ptq_config& cfg, unsigned long long* d_correct, 
           a.allow_tma = c->tma;
           a.kwr_mode = c->kwr;
           a.tio_mode = c->tio;
-          if (a.has_wzp && !a.Rpix && (c->conv_ref || !conv_tc_tma_rowsum(a, wd.bn))) {
+          if (a.has_wzp && !a.rs_mma && !a.Rpix && (c->conv_ref || !conv_tc_tma_rowsum(a, wd.bn))) {
             launch_pixsum(vin, c->d_P, c->st);       // gather-mode convs sum input pixels first
             check_launch(c);
             a.P = c->d_P;
@@ -1759,8 +1780,8 @@ int ptq_export_layer(ptq_ctx* c, const ptq_config* cfg, int32_t node, int8_t* co
     CK(cudaMemcpyAsync(wzp, wd.zp + (size_t)wv * wd.cout, wd.cout * sizeof(int), cudaMemcpyDeviceToHost, c->st));
     if (bias && wd.f32_bias)
       CK(cudaMemcpyAsync(bias, wd.biasq, wd.cout * sizeof(int), cudaMemcpyDeviceToHost, c->st));
-    std::vector<int8_t> tiled((size_t)wd.bytes_per_variant);
-    CK(cudaMemcpyAsync(tiled.data(), wd.codes + (size_t)wv * wd.bytes_per_variant, tiled.size(),
+    std::vector<int8_t> tiled((size_t)(wd.var_off[wv + 1] - wd.var_off[wv]));
+    CK(cudaMemcpyAsync(tiled.data(), wd.codes + wd.var_off[wv], tiled.size(),
                        cudaMemcpyDeviceToHost, c->st));
     CK(cudaStreamSynchronize(c->st));
     if (n.kind == PTQ_DWCONV) {                      // [C][k*k], stored as is
@@ -1789,7 +1810,7 @@ int ptq_export_layer(ptq_ctx* c, const ptq_config* cfg, int32_t node, int8_t* co
         }
         const int nt = o / wd.bn, row = o % wd.bn;
         const int64_t it = kb >> 7, j = (kb >> 4) & 7, b = kb & 15;
-        codes[(int64_t)o * per_o + e] = tiled[(size_t)((((int64_t)nt * wd.n_kiter + it) * 8 + j) * wd.bn + row) * 16 + b];
+        codes[(int64_t)o * per_o + e] = tiled[(size_t)((((int64_t)nt * wd.n_kiter + it) * 8 + j) * wd.var_rows[wv] + row) * 16 + b];
       }
   });
 }
@@ -1828,6 +1849,7 @@ int ptq_set_option(ptq_ctx* c, const char* key, int64_t value) {
     else if (k == "concat_v16") c->concat_v16 = (int)value;
     else if (k == "kwr") c->kwr = (int)value;
     else if (k == "fx") c->fx = (int)value;
+    else if (k == "rs_mma") c->rs_mma = (int)value;
     else if (k == "tio") c->tio = (int)value;
     else if (k == "hist_multi") c->hist_multi = (int)value;
     else if (k == "time_conv") c->time_conv = (int)value;
