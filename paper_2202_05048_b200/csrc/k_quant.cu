@@ -506,22 +506,27 @@ void launch_quant_input(const float* imgs, int64_t img0, View out, const float* 
 // the stride-2 stem: s2d pixel (R, Q) holds x[c][2R+a][2Q+b] at byte (2a+b)*C0 + c, so the
 // stride-2 kxk conv becomes a stride-1 k'xk' conv (k' = (k+1)/2) whose 16-byte pixels are
 // TMA-loadable.  Same per-element quantizer as k_quant_input.  grid.x = (n, R) row.
-__global__ void __launch_bounds__(256) k_quant_input_s2d(const float* __restrict__ imgs, int64_t img0, int C0,
+template <int C0>
+__global__ void __launch_bounds__(256) k_quant_input_s2d(const float* __restrict__ imgs, int64_t img0,
                                                          View out, const float* __restrict__ as,
-                                                         const int* __restrict__ az, int hist) {
+                                                         const int* __restrict__ az, int hist,
+                                                         FastDiv fw, FastDiv fh) {
   const double s = (double)as[hist], z = (double)az[hist];
   const double rs = __ddiv_rn(1.0, s);
   const float rs32 = (float)rs, zf = (float)z;
   const int W0 = 2 * out.W;
   const int64_t plane = (int64_t)(2 * out.H) * W0;
-  const int64_t total = (int64_t)out.N * out.H * out.W;
-  const int nv = 4 * C0;                              // real bytes of the 16-byte pixel
+  const uint32_t total = (uint32_t)out.N * out.H * out.W;   // < 2^31 (launcher)
+  constexpr int nv = 4 * C0;                          // real bytes of the 16-byte pixel
   // one s2d pixel per thread (grid-stride over every (n, R, Q)): 2 x 2 x C0 fp32 values from
-  // C0 x 2 coalesced float2 loads, quantized four at a time with the magic-number quantizer
-  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < total; i += (int64_t)gridDim.x * blockDim.x) {
-    const int Q = (int)(i % out.W);
-    const int64_t t = i / out.W;
-    const int R = (int)(t % out.H), n = (int)(t / out.H);
+  // C0 x 2 coalesced float2 loads (C0 compile-time: all issued before the first use),
+  // quantized four at a time with the magic-number quantizer; (n, R, Q) by multiply-high
+  // divisions
+  for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < total; i += gridDim.x * blockDim.x) {
+    const uint32_t t = fw.div(i);
+    const int Q = (int)(i - t * (uint32_t)out.W);
+    const uint32_t nn = fh.div(t);
+    const int R = (int)(t - nn * (uint32_t)out.H), n = (int)nn;
     const float* src = imgs + (img0 + n) * C0 * plane + (int64_t)(2 * R) * W0 + 2 * Q;
     float v[16];
 #pragma unroll
@@ -561,7 +566,16 @@ __global__ void __launch_bounds__(256) k_quant_input_s2d(const float* __restrict
 void launch_quant_input_s2d(const float* imgs, int64_t img0, int C0, View out, const float* as,
                             const int* az, int hist, cudaStream_t s) {
   const int64_t total = (int64_t)out.N * out.H * out.W;
-  k_quant_input_s2d<<<nblk(total, 256, 148 * 16), 256, 0, s>>>(imgs, img0, C0, out, as, az, hist);
+  // 32-bit pixel index: a larger view (not reachable: N <= the eval chunk) launches an empty
+  // grid, which fails loudly as an invalid configuration in check_launch
+  const unsigned grid = total < (1LL << 31) ? (unsigned)nblk(total, 256, 148 * 16) : 0u;
+  const FastDiv fw = FastDiv::make((uint32_t)out.W), fh = FastDiv::make((uint32_t)out.H);
+  switch (C0) {
+    case 1: k_quant_input_s2d<1><<<grid, 256, 0, s>>>(imgs, img0, out, as, az, hist, fw, fh); break;
+    case 2: k_quant_input_s2d<2><<<grid, 256, 0, s>>>(imgs, img0, out, as, az, hist, fw, fh); break;
+    case 3: k_quant_input_s2d<3><<<grid, 256, 0, s>>>(imgs, img0, out, as, az, hist, fw, fh); break;
+    default: k_quant_input_s2d<4><<<grid, 256, 0, s>>>(imgs, img0, out, as, az, hist, fw, fh); break;
+  }
 }
 
 // per-output-pixel sum of the input codes under the stem's real kxk window (halo taps hold

@@ -115,3 +115,41 @@ def test_strided_1x1_subsample_codes_bit_exact(ev224):
                     ev224.set_option("subsample", 1)
                     ev224.set_option("fusion", 1)
                 assert np.array_equal(fast, plain), (ci, n.id, fusion)
+
+
+def test_mma_row_sums_equal_row_sum_warp(ev224):
+    """Asymmetric weights: the row sums Σx the tensor core computes through the K-indicator
+    rows of the bn <= 128 weight tiles (rs_mma) must give the same int32 accumulators and
+    codes as the row-sum warp / pixel-sum / stem window-sum sources (rs_mma=0), on every
+    A-operand mode the bench runs (s2d stem slab, kw-reuse 3x3, TMA 1x1, strided gather)."""
+    space = enumerate_space(GENERIC)
+    g = ev224.graph
+    comp = [n for n in g.nodes if n.kind in ("conv2d", "pointwise_conv2d")]
+    by_id = {n.id: n for n in comp}
+    probe = [nid for nid in ("conv0", "conv5", "poin25", "conv27", "poin33") if nid in by_id]
+    assert len(probe) == 5
+    imgs = np.array([0, 137, 421, 999], dtype=np.int32)
+
+    def materialised(t):                         # a relu-fused conv output: probe the relu
+        relu = [m for m in g.nodes if m.kind == "relu" and m.inputs[0] == t]
+        return relu[0].output if relu else t
+    outs = [materialised(by_id[nid].output) for nid in probe]
+    for ci in (0, 2):                            # Asymmetric per-tensor / per-channel, Mixed=Off
+        cfg = space[ci]
+        assert cfg.to_dict()["scheme"] == "Asymmetric"
+        got = {}
+        for mode in (1, 0):
+            ev224.set_option("rs_mma", mode)
+            try:
+                acc = {nid: ev224.probe_acc(cfg, nid, imgs) for nid in probe}
+                codes = ev224.probe_tensors(cfg, outs, imgs)
+                counts = ev224.correct_counts([cfg])
+            finally:
+                ev224.set_option("rs_mma", 1)
+            got[mode] = (acc, codes, counts)
+        for nid in probe:
+            assert np.array_equal(got[1][0][nid], got[0][0][nid]), (ci, nid)
+        assert set(got[1][1]) == set(got[0][1]) and len(got[1][1]) >= 3, sorted(got[1][1])
+        for t in got[1][1]:
+            assert np.array_equal(got[1][1][t], got[0][1][t]), (ci, t)
+        assert np.array_equal(np.asarray(got[1][2]), np.asarray(got[0][2])), ci
