@@ -439,10 +439,13 @@ struct EpiEnv {
 // per-channel constants (broadcast shared-memory loads, or for the fused-add layers indexed
 // LDC from __constant__ c_ep, which keeps them off the L1 data pipe the add table uses).
 template <int BN, bool WZP, bool SKIP, bool CLAMP, bool RELU, bool GENERIC, bool ACC = false, bool PT = false,
-          bool FX = false>
+          bool FX = false, int TIOM = -1>
 __device__ __forceinline__ void epi_tiles(const ConvTcArgs& a, const LayerRt& rt, const EpiK& k, const EpiEnv& e) {
   constexpr int NCH = BN / 16;                       // 16-column chunks per tile
   const int Cout = a.L.cout;
+  // tile I/O: a compile-time choice for the FX variants (TIOM 0 / 1), so the tile-I/O loop
+  // carries no direct-store / residual-load code and keeps its slot address in registers
+  const bool tio = TIOM < 0 ? a.tio != 0 : TIOM == 1;
   const bool has_skip = GENERIC ? a.skip.p != nullptr : SKIP;
   uint32_t lt = 0;
   int rot = 0;                                       // lt % TC_NG
@@ -483,17 +486,14 @@ __device__ __forceinline__ void epi_tiles(const ConvTcArgs& a, const LayerRt& rt
     const uint32_t ib = lt % TC_IO_NB, iph = (lt / TC_IO_NB) & 1u;
     uint8_t* io = e.sio + ib * (TC_BM * BN);
     const int iow = a.io_w, iosh = a.io_w == 128 ? 3 : 2;   // box width in bytes, log2(16-byte units)
-    const int iorow = e.row * iow, ioswz = iow == 128 ? (e.row & 7) : ((e.row >> 1) & 3);
-    if (a.tio) {
+    // this row's slot base (shared address) and 16-byte-unit swizzle, once per tile: per chunk
+    // only the uniform box / unit offset is added and the unit XORed with the row phase
+    const uint32_t io_row = smem_u32(io) + (uint32_t)(e.row * iow);
+    const uint32_t io_x = (uint32_t)(iow == 128 ? (e.row & 7) : ((e.row >> 1) & 3)) << 4;
+    if (tio) {
       if (has_skip) mbar_wait(&e.iofull[ib], iph);
       else mbar_wait(&e.ioempty[ib], iph ^ 1u);
     }
-    // the residual operand does not depend on the accumulator: fetch it before the wait
-    // and one chunk ahead inside the loop
-    const int cb0 = nt * BN + first * 16;
-    int4 sk_next = make_int4(0, 0, 0, 0);
-    if (has_skip && !a.tio && srow && first < NCH && cb0 < a.out.Cp)
-      sk_next = __ldg(reinterpret_cast<const int4*>(srow + cb0));
     mbar_wait(&e.tfull[buf], uph);
     tc_fence_after();
     const uint32_t tbase = e.tmem + ((uint32_t)(e.q * 32) << 16) + buf * (uint32_t)a.b_rows;
@@ -508,22 +508,18 @@ __device__ __forceinline__ void epi_tiles(const ConvTcArgs& a, const LayerRt& rt
         epi_acc_chunk(tbase + (uint32_t)(c * 16), cb, rowsum, a, rt, g.ok ? a.acc_out + pix * Cout : nullptr);
         continue;
       }
+      // residual operand without tile I/O (non-flat layers): a direct 16-byte load issued
+      // ahead of the TMEM load it overlaps with (no cross-chunk prefetch state: those register
+      // moves cost every chunk of the tile-I/O layers an extra 8 instructions)
+      int4 skv = make_int4(0, 0, 0, 0);
+      if (has_skip && !tio && srow && cb < a.out.Cp) skv = __ldg(reinterpret_cast<const int4*>(srow + cb));
       uint32_t v[16];
       tmem_ld16(tbase + (uint32_t)(c * 16), v);
       if (cb >= a.out.Cp) continue;                  // warp-uniform: the slow path re-reads TMEM
-      int4 skv = make_int4(0, 0, 0, 0);
       // swizzled slot of (row, chunk c) in the I/O tile: box c / iocpb, 16-byte unit XOR row phase
-      int4* ioslot = reinterpret_cast<int4*>(io + (c >> iosh) * (TC_BM * iow) + iorow +
-                                             (((c & ((1 << iosh) - 1)) ^ ioswz) << 4));
-      if (has_skip) {
-        if (a.tio) {
-          skv = *ioslot;
-        } else {
-          skv = sk_next;
-          if (srow && c + TC_NG < NCH && cb + 16 * TC_NG < a.out.Cp)
-            sk_next = __ldg(reinterpret_cast<const int4*>(srow + cb + 16 * TC_NG));
-        }
-      }
+      const uint32_t ioslot = io_row + (uint32_t)((c >> iosh) * (TC_BM * iow)) +
+                              (((uint32_t)(c & ((1 << iosh) - 1)) << 4) ^ io_x);
+      if (has_skip && tio) skv = lds128(ioslot);
       int4 res;
       if (GENERIC && a.ablate == 1) {
         res = make_int4((int)v[0], (int)v[1], (int)v[2], (int)v[3]);
@@ -534,12 +530,12 @@ __device__ __forceinline__ void epi_tiles(const ConvTcArgs& a, const LayerRt& rt
       } else {
         res = epi_slow_chunk(tbase + (uint32_t)(c * 16), cb, rowsum, a, rt, k.lo_conv, k.lo_add, skv);
       }
-      if (a.tio) *ioslot = res;
+      if (tio) sts128(ioslot, res);
       else if (g.ok) *reinterpret_cast<int4*>(orow + cb) = res;
     }
     tc_fence_before();
     mbar_arrive(&e.tempty[buf]);                     // accumulator buffer may be reused
-    if (a.tio) {
+    if (tio) {
       // this thread's codes are in the tile: hand them to the async proxy and tell the I/O
       // agent (no CTA-wide barrier: the epilogue warps stay decoupled)
       fence_proxy_async();
@@ -557,8 +553,13 @@ __device__ __forceinline__ void epi_pt(const ConvTcArgs& a, const LayerRt& rt, c
 }
 template <int BN, bool WZP, bool SKIP, bool RELU>
 __device__ __forceinline__ void epi_fx(const ConvTcArgs& a, const LayerRt& rt, const EpiK& k, const EpiEnv& e) {
-  if (rt.uni) epi_tiles<BN, WZP, SKIP, false, RELU, false, false, true, true>(a, rt, k, e);
-  else epi_tiles<BN, WZP, SKIP, false, RELU, false, false, false, true>(a, rt, k, e);
+  if (a.tio) {
+    if (rt.uni) epi_tiles<BN, WZP, SKIP, false, RELU, false, false, true, true, 1>(a, rt, k, e);
+    else epi_tiles<BN, WZP, SKIP, false, RELU, false, false, false, true, 1>(a, rt, k, e);
+  } else {
+    if (rt.uni) epi_tiles<BN, WZP, SKIP, false, RELU, false, false, true, true, 0>(a, rt, k, e);
+    else epi_tiles<BN, WZP, SKIP, false, RELU, false, false, false, true, 0>(a, rt, k, e);
+  }
 }
 
 // BR = B rows per tile (a.b_rows): BN, or BN + 16 K-indicator rows (the MMA then runs over
