@@ -56,6 +56,18 @@ constexpr int TC_A_STAGE = TC_BM * 128;            // 16 KB: 8 chunks x 128 rows
 constexpr int TC_NG = PTQ_EPI_GROUPS;               // epilogue column groups per TMEM lane quarter
 constexpr int TC_EPI_WARPS = 4 * TC_NG;             // NG per SM sub-partition
 constexpr int TC_THREADS = (4 + TC_EPI_WARPS) * 32;    // + producer / MMA warps 0-3
+// Narrow tiles (BN <= 64: at most 4 chunks of 16 columns) would give each epilogue warp one
+// chunk per tile, so the per-tile work (barrier waits, row geometry, arrivals) would cost as
+// much as the chunk.  There the 4 column groups take whole tiles in turn instead (group g:
+// the CTA's tiles lt = g mod 4, all chunks), each with its own accumulator buffer (4 TMEM
+// buffers) and, with tile I/O, its own shared tile.
+template <int BN> struct TcGeom {
+  static constexpr bool GROUPED = BN <= 64;
+  static constexpr int NACC = GROUPED ? 4 : 2;                  // accumulator buffers
+  static constexpr int NIO = GROUPED ? 4 : TC_IO_NB;           // tile I/O buffers
+  static constexpr int ARRIVE = (GROUPED ? 4 : TC_EPI_WARPS) * 32;   // epilogue threads per tile
+};
+constexpr int TC_MAX_BUF = 4;                      // barrier slots per buffer kind
 
 
 __device__ __forceinline__ uint64_t umma_desc(uint32_t saddr, uint32_t lbo, uint32_t sbo) {
@@ -429,7 +441,7 @@ struct EpiEnv {
   int cs;                                            // SoA channel stride = roundup(Cout, 16)
   const int8_t* stab_c;
   int q, grp, row, M, n_tiles, n_nt;
-  uint8_t* sio;                                      // tile I/O buffers [TC_IO_NB][128][BN] (tio)
+  uint8_t* sio;                                      // tile I/O buffers [NIO][128][BN] (tio)
   uint64_t *iofull, *ioempty, *ioready;
 };
 
@@ -447,17 +459,20 @@ __device__ __forceinline__ void epi_tiles(const ConvTcArgs& a, const LayerRt& rt
   // carries no direct-store / residual-load code and keeps its slot address in registers
   const bool tio = TIOM < 0 ? a.tio != 0 : TIOM == 1;
   const bool has_skip = GENERIC ? a.skip.p != nullptr : SKIP;
+  using G = TcGeom<BN>;
   uint32_t lt = 0;
   int rot = 0;                                       // lt % TC_NG
   for (int tile = blockIdx.x; tile < e.n_tiles; tile += gridDim.x, ++lt, rot = rot == TC_NG - 1 ? 0 : rot + 1) {
-    const uint32_t buf = lt & 1u, uph = (lt >> 1) & 1u;
+    if (G::GROUPED && rot != e.grp) continue;        // warp-uniform: another group's tile
+    const uint32_t buf = lt % G::NACC, uph = (lt / G::NACC) & 1u;
     const int mt = (int)a.div_nt.div((uint32_t)tile);
     // n-tile (warp-uniform; the shuffle lets ptxas keep it, and every channel index derived
     // from it, in uniform registers)
     const int nt = __shfl_sync(0xffffffffu, tile - mt * e.n_nt, 0);
     // chunks c = first, first+3, ...: the assignment rotates with the tile so the three
     // column groups share BN/16 chunks evenly over consecutive tiles
-    const int first = e.grp >= rot ? e.grp - rot : e.grp - rot + TC_NG;
+    const int first = G::GROUPED ? 0 : e.grp >= rot ? e.grp - rot : e.grp - rot + TC_NG;
+    constexpr int CSTEP = G::GROUPED ? 1 : TC_NG;
     const int m = mt * TC_BM + e.row;
     RowGeo g;
     int8_t* orow;
@@ -483,7 +498,7 @@ __device__ __forceinline__ void epi_tiles(const ConvTcArgs& a, const LayerRt& rt
     }
     // tile I/O: this tile's shared buffer (the fused-add operand landed by TMA, or a buffer
     // whose previous TMA store has finished reading it)
-    const uint32_t ib = lt % TC_IO_NB, iph = (lt / TC_IO_NB) & 1u;
+    const uint32_t ib = lt % G::NIO, iph = (lt / G::NIO) & 1u;
     uint8_t* io = e.sio + ib * (TC_BM * BN);
     const int iow = a.io_w, iosh = a.io_w == 128 ? 3 : 2;   // box width in bytes, log2(16-byte units)
     // this row's slot base (shared address) and 16-byte-unit swizzle, once per tile: per chunk
@@ -500,7 +515,7 @@ __device__ __forceinline__ void epi_tiles(const ConvTcArgs& a, const LayerRt& rt
     if ((GENERIC || WZP) && a.rs_mma) rowsum = (int)tmem_ld1(tbase + BN);   // sum_k x[row][k]
     const int zr = (FX && PT && WZP) ? k.zw0 * (int)rowsum : 0;   // per-tensor zw * rowsum
 #pragma unroll 1
-    for (int c = first; c < NCH; c += TC_NG) {
+    for (int c = first; c < NCH; c += CSTEP) {
       const int cb = nt * BN + c * 16;
       if (ACC) {
         if (cb >= Cout) continue;                    // warp-uniform
@@ -571,23 +586,27 @@ __global__ void __launch_bounds__(TC_THREADS, 1) k_conv_tc(const __grid_constant
   // swizzled TMA tiles need 1024-byte aligned stages (the launcher reserves the slack)
   uint8_t* smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
   uint8_t* sio = smem;                              // tile I/O buffers (tio), 1024-aligned boxes
-  uint8_t* sA = smem + (a.tio ? TC_IO_NB * TC_BM * BN : 0);
+  using G = TcGeom<BN>;
+  uint8_t* sA = smem + (a.tio ? G::NIO * TC_BM * BN : 0);
   uint8_t* sB = sA + NS * TC_A_STAGE;               // B ring [NS][BN][128], or resident [n_kiter][BN][128]
   uint64_t* full = reinterpret_cast<uint64_t*>(sB + (a.b_res ? a.n_kiter : NS) * BR * 128);
   uint64_t* empty = full + NS;
-  uint64_t* tfull = empty + NS;
-  uint64_t* tempty = tfull + 2;
-  uint64_t* rsfull = tempty + 2;                                 // row sums of tile buffer ready
-  uint64_t* bfull = tempty + 4;                                  // resident B landed
-  uint64_t* iofull = tempty + 5;                                 // [TC_IO_NB] operand tile landed
-  uint64_t* ioempty = iofull + TC_IO_NB;                         // [TC_IO_NB] tile buffer free
-  uint64_t* ioready = ioempty + TC_IO_NB;                        // [TC_IO_NB] epilogue wrote the tile
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(ioready + TC_IO_NB);
-  int* rsum = reinterpret_cast<int*>(ioready + TC_IO_NB + 1);    // [2][128] A-row sums (tma_rowsum)
-  EpiParam* sparam = reinterpret_cast<EpiParam*>(rsum + 2 * TC_BM);   // [Cout] (no fused add)
-  int8_t* stab = reinterpret_cast<int8_t*>(rsum + 2 * TC_BM);          // fused-add table
-  // two accumulator buffers of BR columns (power-of-two allocation, at least 32)
-  constexpr uint32_t TMEM_COLS = 2 * BR <= 32 ? 32u : 2 * BR <= 64 ? 64u : 2 * BR <= 128 ? 128u : 2 * BR <= 256 ? 256u : 512u;
+  uint64_t* tfull = empty + NS;                                  // [NACC] accumulator ready
+  uint64_t* tempty = tfull + TC_MAX_BUF;                         // [NACC] accumulator drained
+  uint64_t* rsfull = tempty + TC_MAX_BUF;                        // [NACC] row sums of tile buffer ready
+  uint64_t* bfull = rsfull + TC_MAX_BUF;                         // resident B landed
+  uint64_t* iofull = bfull + 1;                                  // [NIO] operand tile landed
+  uint64_t* ioempty = iofull + TC_MAX_BUF;                       // [NIO] tile buffer free
+  uint64_t* ioready = ioempty + TC_MAX_BUF;                      // [NIO] epilogue wrote the tile
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(ioready + TC_MAX_BUF);
+  int* rsum = reinterpret_cast<int*>(ioready + TC_MAX_BUF + 1);  // [NACC][128] A-row sums (tma_rowsum)
+  EpiParam* sparam = reinterpret_cast<EpiParam*>(rsum + TC_MAX_BUF * TC_BM);   // [Cout] (no fused add)
+  int8_t* stab = reinterpret_cast<int8_t*>(rsum + TC_MAX_BUF * TC_BM);          // fused-add table
+  // NACC accumulator buffers of BR columns (power-of-two allocation, at least 32)
+  constexpr uint32_t TMEM_NEED = G::NACC * BR;
+  constexpr uint32_t TMEM_COLS = TMEM_NEED <= 32 ? 32u : TMEM_NEED <= 64 ? 64u : TMEM_NEED <= 128 ? 128u
+                                 : TMEM_NEED <= 256 ? 256u : 512u;
+  static_assert(TMEM_NEED <= 512, "accumulator buffers exceed TMEM");
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int M = a.in.N * a.OH * a.OW;
@@ -600,15 +619,15 @@ __global__ void __launch_bounds__(TC_THREADS, 1) k_conv_tc(const __grid_constant
       mbar_init(&empty[s], a.tma_rowsum ? 2 : 1);
     }
     mbar_init(bfull, 1);
-    for (int b = 0; b < TC_IO_NB; ++b) {
+    for (int b = 0; b < G::NIO; ++b) {
       mbar_init(&iofull[b], 1);
       mbar_init(&ioempty[b], 1);
-      mbar_init(&ioready[b], TC_EPI_WARPS * 32);
+      mbar_init(&ioready[b], G::ARRIVE);
     }
-    for (int b = 0; b < 2; ++b) {
+    for (int b = 0; b < G::NACC; ++b) {
       mbar_init(&rsfull[b], 1);
       mbar_init(&tfull[b], 1);
-      mbar_init(&tempty[b], TC_EPI_WARPS * 32);
+      mbar_init(&tempty[b], G::ARRIVE);
     }
     fence_mbar_init();
   }
@@ -682,7 +701,7 @@ __global__ void __launch_bounds__(TC_THREADS, 1) k_conv_tc(const __grid_constant
       uint32_t ph = 0, lt = 0;
       const int iters = a.kwr ? a.a_iters : a.n_kiter;
       for (int tile = blockIdx.x; tile < n_tiles; tile += gridDim.x, ++lt) {
-        const uint32_t buf = lt & 1u, uph = (lt >> 1) & 1u;
+        const uint32_t buf = lt % G::NACC, uph = (lt / G::NACC) & 1u;
         int sum[4] = {0, 0, 0, 0};
         for (int ki = 0; ki < iters; ++ki) {
           mbar_wait(&full[s], ph);
@@ -876,11 +895,11 @@ __global__ void __launch_bounds__(TC_THREADS, 1) k_conv_tc(const __grid_constant
           tma_load_2d(io + b * (TC_BM * iow), &a.tmS, nt * BN + b * iow, mt * TC_BM, &iofull[ib]);
       };
       if (skip)
-        for (int i = 0; i < TC_IO_NB && blockIdx.x + i * (int)gridDim.x < n_tiles; ++i)
+        for (int i = 0; i < G::NIO && blockIdx.x + i * (int)gridDim.x < n_tiles; ++i)
           load(blockIdx.x + i * gridDim.x, (uint32_t)i);
       uint32_t lt = 0;
       for (int tile = blockIdx.x; tile < n_tiles; tile += gridDim.x, ++lt) {
-        const uint32_t ib = lt % TC_IO_NB, iph = (lt / TC_IO_NB) & 1u;
+        const uint32_t ib = lt % G::NIO, iph = (lt / G::NIO) & 1u;
         const int mt = (int)a.div_nt.div((uint32_t)tile), nt = tile - mt * n_nt;
         const int nbox = (imin(BN, a.out.Cp - nt * BN) + iow - 1) / iow;
         uint8_t* io = sio + ib * (TC_BM * BN);
@@ -888,14 +907,14 @@ __global__ void __launch_bounds__(TC_THREADS, 1) k_conv_tc(const __grid_constant
         for (int b = 0; b < nbox; ++b) tma_store_2d(&a.tmO, io + b * (TC_BM * iow), nt * BN + b * iow, mt * TC_BM);
         bulk_commit();
         if (skip) {
-          const int next = tile + TC_IO_NB * (int)gridDim.x;
+          const int next = tile + G::NIO * (int)gridDim.x;
           if (next < n_tiles) {
             bulk_wait_read<0>();
             load(next, ib);
           }
         } else {
           bulk_wait_read<1>();
-          if (lt > 0) mbar_arrive(&ioempty[(lt - 1) % TC_IO_NB]);
+          if (lt > 0) mbar_arrive(&ioempty[(lt - 1) % G::NIO]);
         }
       }
       bulk_wait_all();
@@ -934,7 +953,7 @@ __global__ void __launch_bounds__(TC_THREADS, 1) k_conv_tc(const __grid_constant
       int s = 0;
       uint32_t ph = 0, lt = 0;
       for (int tile = blockIdx.x; tile < n_tiles; tile += gridDim.x, ++lt) {
-        const uint32_t buf = lt & 1u, uph = (lt >> 1) & 1u;
+        const uint32_t buf = lt % G::NACC, uph = (lt / G::NACC) & 1u;
         mbar_wait(&tempty[buf], uph ^ 1u);           // epilogue drained this accumulator
         tc_fence_after();
         const uint32_t d = tmem + buf * (uint32_t)BR;
@@ -1092,12 +1111,12 @@ static void launch_bn(const ConvTcArgs& a, cudaStream_t s) {
   ConvTcArgs b = a;
   size_t smem = 0;
   int ns = 0;
-  // tile I/O takes TC_IO_NB [128][BN] buffers; without room for two pipeline stages beside
+  // tile I/O takes NIO [128][BN] buffers; without room for two pipeline stages beside
   // them the layer keeps the direct global epilogue
   for (int pass = 0; pass < 2; ++pass) {
-    const size_t fixed = 1024 + (2 * TC_MAX_STAGES + 8 + 3 * TC_IO_NB) * 8 + 2 * TC_BM * 4 + 16 +
+    const size_t fixed = 1024 + (2 * TC_MAX_STAGES + 2 + 6 * TC_MAX_BUF) * 8 + TC_MAX_BUF * TC_BM * 4 + 16 +
                          (a.addtab ? PTQ_ADDTAB_BYTES : (size_t)((a.L.cout + 15) & ~15) * sizeof(EpiParam)) +
-                         (b_res ? b_bytes : 0) + (b.tio ? (size_t)TC_IO_NB * TC_BM * BN : 0);
+                         (b_res ? b_bytes : 0) + (b.tio ? (size_t)TcGeom<BN>::NIO * TC_BM * BN : 0);
     const size_t per_stage = (size_t)TC_A_STAGE + (b_res ? 0 : (size_t)a.b_rows * 128);
     ns = fixed < TC_SMEM_MAX ? (int)((TC_SMEM_MAX - fixed) / per_stage) : 0;
     if (ns < 2 && b.tio) { b.tio = 0; continue; }
