@@ -56,16 +56,20 @@ constexpr int TC_A_STAGE = TC_BM * 128;            // 16 KB: 8 chunks x 128 rows
 constexpr int TC_NG = PTQ_EPI_GROUPS;               // epilogue column groups per TMEM lane quarter
 constexpr int TC_EPI_WARPS = 4 * TC_NG;             // NG per SM sub-partition
 constexpr int TC_THREADS = (4 + TC_EPI_WARPS) * 32;    // + producer / MMA warps 0-3
-// Narrow tiles (BN <= 64: at most 4 chunks of 16 columns) would give each epilogue warp one
-// chunk per tile, so the per-tile work (barrier waits, row geometry, arrivals) would cost as
-// much as the chunk.  There the 4 column groups take whole tiles in turn instead (group g:
-// the CTA's tiles lt = g mod 4, all chunks), each with its own accumulator buffer (4 TMEM
-// buffers) and, with tile I/O, its own shared tile.
+// How the 4 epilogue column groups share tiles.  Splitting every tile over all 4 groups
+// gives each warp BN/64 chunks of 16 columns per tile, so for narrow tiles the per-tile work
+// (barrier waits, row geometry, arrivals) costs as much as the chunks.  Instead GPT groups
+// drain one tile (BN/(16*GPT) = 4 chunks per warp whenever BN >= 64) and the 4/GPT group sets
+// take the CTA's tiles in turn (slot = lt mod SLOTS), each tile in its own TMEM accumulator
+// (NACC >= SLOTS + 1 buffers where TMEM allows, so the MMA can fill one ahead) and, with tile
+// I/O, its own shared tile (NIO).
 template <int BN> struct TcGeom {
-  static constexpr bool GROUPED = BN <= 64;
-  static constexpr int NACC = GROUPED ? 4 : 2;                  // accumulator buffers
-  static constexpr int NIO = GROUPED ? 4 : TC_IO_NB;           // tile I/O buffers
-  static constexpr int ARRIVE = (GROUPED ? 4 : TC_EPI_WARPS) * 32;   // epilogue threads per tile
+  static constexpr int GPT = BN <= 64 ? 1 : BN == 128 ? 2 : 4;   // column groups per tile
+  static constexpr int SLOTS = TC_NG / GPT;                      // tiles drained at once
+  static constexpr bool GROUPED = SLOTS > 1;
+  static constexpr int NACC = BN <= 64 ? 4 : BN == 128 ? 3 : 2;  // accumulator buffers
+  static constexpr int NIO = BN <= 64 ? 4 : BN == 128 ? 3 : TC_IO_NB;   // tile I/O buffers
+  static constexpr int ARRIVE = GPT * 4 * 32;                    // epilogue threads per tile
 };
 constexpr int TC_MAX_BUF = 4;                      // barrier slots per buffer kind
 
@@ -461,18 +465,18 @@ __device__ __forceinline__ void epi_tiles(const ConvTcArgs& a, const LayerRt& rt
   const bool has_skip = GENERIC ? a.skip.p != nullptr : SKIP;
   using G = TcGeom<BN>;
   uint32_t lt = 0;
-  int rot = 0;                                       // lt % TC_NG
-  for (int tile = blockIdx.x; tile < e.n_tiles; tile += gridDim.x, ++lt, rot = rot == TC_NG - 1 ? 0 : rot + 1) {
-    if (G::GROUPED && rot != e.grp) continue;        // warp-uniform: another group's tile
+  int slot = 0;                                      // lt % SLOTS
+  const int my_slot = e.grp / G::GPT;                // this group's tiles: slot == my_slot
+  for (int tile = blockIdx.x; tile < e.n_tiles; tile += gridDim.x, ++lt, slot = slot == G::SLOTS - 1 ? 0 : slot + 1) {
+    if (G::GROUPED && slot != my_slot) continue;     // warp-uniform: another group set's tile
     const uint32_t buf = lt % G::NACC, uph = (lt / G::NACC) & 1u;
     const int mt = (int)a.div_nt.div((uint32_t)tile);
     // n-tile (warp-uniform; the shuffle lets ptxas keep it, and every channel index derived
     // from it, in uniform registers)
     const int nt = __shfl_sync(0xffffffffu, tile - mt * e.n_nt, 0);
-    // chunks c = first, first+3, ...: the assignment rotates with the tile so the three
-    // column groups share BN/16 chunks evenly over consecutive tiles
-    const int first = G::GROUPED ? 0 : e.grp >= rot ? e.grp - rot : e.grp - rot + TC_NG;
-    constexpr int CSTEP = G::GROUPED ? 1 : TC_NG;
+    // chunks c = first, first + GPT, ... (BN / (16 GPT) per warp: an even split)
+    const int first = e.grp % G::GPT;
+    constexpr int CSTEP = G::GPT;
     const int m = mt * TC_BM + e.row;
     RowGeo g;
     int8_t* orow;
