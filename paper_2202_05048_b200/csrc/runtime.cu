@@ -456,15 +456,21 @@ void import_graph(ptq_ctx* c, const ptq_graph_desc* g) {
       // K <= 512: deeper layers re-read A once per n-tile, which costs more than tile I/O saves
       // (ResNet-50: poin37 0.39 -> 0.33 ms, conv102 K=1024 0.14 -> 0.17 ms)
       const TensorI& ot = c->tens[n.out];
-      if (wd.bn == 256 && wd.cout > 256 && wd.n_kiter <= 4 && ot.consumers.size() == 1 &&
-          c->nodes[ot.consumers[0]].kind == PTQ_ADD) {
+      bool fused_add = false;
+      if (ot.consumers.size() == 1 && c->nodes[ot.consumers[0]].kind == PTQ_ADD) {
         const NodeI& an = c->nodes[ot.consumers[0]];
         const int other = an.in[0] == n.out ? an.in[1] : an.in[0];
         int prod = -1;
         for (int j = 0; j < g->n_nodes; ++j)
           if (c->nodes[j].out == other) prod = j;
-        if (prod < i) wd.bn = 128;
+        fused_add = prod < i;
       }
+      if (wd.bn == 256 && wd.cout > 256 && wd.n_kiter <= 4 && fused_add) wd.bn = 128;
+      // shallow (K <= 128) wide layers without a fused add: 128-wide tiles (3 accumulators in
+      // flight, group pairs) drain faster and the second A pass is one stage per row
+      // (ResNet-50 poin7 0.300 -> 0.287, poin29 0.158 -> 0.148 ms; with a fused add the 256-wide
+      // tile stays faster: poin8 0.461 vs 0.484)
+      if (wd.bn == 256 && wd.n_kiter <= 1 && !fused_add) wd.bn = 128;
       // narrow tiles of the variants with weight zero points (scheme 0 = Asymmetric, both
       // granularities) carry 16 K-indicator rows: the MMA also yields the A-row sums (N = bn + 16
       // <= 144; bn = 256 tiles fill TMEM and keep the row-sum warp).  The other variants keep
