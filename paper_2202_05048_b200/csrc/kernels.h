@@ -236,6 +236,7 @@ struct ConvTcArgs {
                           // the add operand) -- halo-free TMA-mode layers skip the row geometry
   int kwr_mode;           // runtime option: -1 disables the kw-reuse slabs and the stem slab
   int tio_mode;           // runtime option: 0 disables tile I/O
+  int skip_pf;            // runtime option: L2 prefetch of the fused-add operand tiles (tile I/O)
   int tio;                // set by the launcher (flat layers): the epilogue writes codes into a
                           // swizzled shared tile stored by TMA, and reads the fused-add operand from
                           // a tile a producer loads by TMA, instead of per-row 16-byte global accesses

@@ -200,6 +200,7 @@ struct ptq_ctx {
   int fx = 1;                            // exact fixed-point conv epilogue (0: fp64 epilogue)
   int tio = 1;                           // tile I/O through shared memory + TMA (flat conv layers)
   int rs_mma = 1;                        // A-row sums for weight zero points from the MMA (bn <= 128)
+  int skip_pf = 1;                       // L2 prefetch of the fused-add operand tiles
   int hist_multi = 1;                    // batched histogram launch (0: one launch per histogram, A/B)
   int64_t opt_chunk = 0;
   // stats
@@ -1147,6 +1148,7 @@ void eval_one(ptq_ctx* c, const ptq_config& cfg, unsigned long long* d_correct, 
           a.allow_tma = c->tma;
           a.kwr_mode = c->kwr;
           a.tio_mode = c->tio;
+          a.skip_pf = c->skip_pf;
           if (a.has_wzp && !a.rs_mma && !a.Rpix && (c->conv_ref || !conv_tc_tma_rowsum(a, wd.bn))) {
             launch_pixsum(vin, c->d_P, c->st);       // gather-mode convs sum input pixels first
             check_launch(c);
@@ -1856,6 +1858,7 @@ int ptq_set_option(ptq_ctx* c, const char* key, int64_t value) {
     else if (k == "kwr") c->kwr = (int)value;
     else if (k == "fx") c->fx = (int)value;
     else if (k == "rs_mma") c->rs_mma = (int)value;
+    else if (k == "skip_pf") c->skip_pf = (int)value;
     else if (k == "tio") c->tio = (int)value;
     else if (k == "hist_multi") c->hist_multi = (int)value;
     else if (k == "time_conv") c->time_conv = (int)value;
