@@ -467,11 +467,13 @@ void import_graph(ptq_ctx* c, const ptq_graph_desc* g) {
         fused_add = prod < i;
       }
       if (wd.bn == 256 && wd.cout > 256 && wd.n_kiter <= 4 && fused_add) wd.bn = 128;
-      // shallow (K <= 128) wide layers without a fused add: 128-wide tiles (3 accumulators in
-      // flight, group pairs) drain faster and the second A pass is one stage per row
-      // (ResNet-50 poin7 0.300 -> 0.287, poin29 0.158 -> 0.148 ms; with a fused add the 256-wide
-      // tile stays faster: poin8 0.461 vs 0.484)
-      if (wd.bn == 256 && wd.n_kiter <= 1 && !fused_add) wd.bn = 128;
+      // shallow (K <= 128) wide layers without a fused add whose width is a multiple of 128:
+      // 128-wide tiles (3 accumulators in flight, group pairs) drain faster and the second A
+      // pass is one stage per row (ResNet-50 poin7 0.300 -> 0.287, poin29 0.158 -> 0.148 ms,
+      // MobileNet-v2 384-wide 0.060 -> 0.048).  A partial last 128-wide tile costs more than it
+      // saves (MobileNet-v2 144 / 192 / 576-wide: 0.29 -> 0.49, 0.093 -> 0.131, 0.072 -> 0.085),
+      // and with a fused add the 256-wide tile stays faster (poin8 0.461 vs 0.484)
+      if (wd.bn == 256 && wd.n_kiter <= 1 && !fused_add && wd.cout % 128 == 0) wd.bn = 128;
       // narrow tiles of the variants with weight zero points (scheme 0 = Asymmetric, both
       // granularities) carry 16 K-indicator rows: the MMA also yields the A-row sums (N = bn + 16
       // <= 144; bn = 256 tiles fill TMEM and keep the row-sum warp).  The other variants keep
