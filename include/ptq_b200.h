@@ -193,7 +193,12 @@ int ptq_histogram_host(ptq_ctx* ctx, const float* x, int64_t n, float lo, float 
  * "reset_stats" (zero the cumulative kernel-launch counter).  A/B switches for tests, each
  * path bit-identical to its fallback: "tma" (0 = gather A operand), "kwr" (kw-reuse slabs),
  * "subsample" (0 = strided 1x1 convs gather directly), "dwconv_v4" (2 register-tap 3x3,
- * 1 four-channel, 0 scalar depthwise), "concat_v16" (0 = per-byte concat requant). */
+ * 1 four-channel, 0 scalar depthwise), "concat_v16" (0 = per-byte concat requant),
+ * "fx" (0 = fp64 requant epilogue instead of the exact fixed-point one), "tio" (0 = direct
+ * global epilogue stores instead of shared tiles + TMA), "hist_multi" (0 = one histogram
+ * launch per tensor), "rs_mma" (0 = weight-zero-point row sums from the row-sum warp /
+ * pixel-sum passes instead of the MMA's K-indicator columns), "skip_pf" (0 = no L2 prefetch
+ * of the fused-add operand tiles). */
 int ptq_set_option(ptq_ctx* ctx, const char* key, int64_t value);
 /* Statistics: cumulative kernel launches (option "reset_stats" zeroes it) and, for the
  * last ptq_eval_configs call, the summed CUDA-event time of the int8 conv launches of
